@@ -1,0 +1,149 @@
+// Context: shards, streams, communicator (local fixed-order device sums or
+// NCCL allreduce over NVLink), and the row partition used for SNP sharding.
+#include <algorithm>
+#include <cstring>
+
+#include "host.hpp"
+
+namespace gkb {
+
+namespace {
+void check_nccl(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(GKB_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+}  // namespace
+
+void Shard::ensure_partial(int64_t doubles) {
+  if (rs.cap >= doubles) return;
+  GKB_CUDA(cudaSetDevice(dev));
+  if (rs.partial) GKB_CUDA(cudaFree(rs.partial));
+  const int64_t cap = std::max<int64_t>(doubles, 1 << 16);
+  GKB_CUDA(cudaMalloc(&rs.partial, sizeof(double) * (size_t)cap));
+  rs.cap = cap;
+}
+
+static void init_shard(Shard& s, int index, int dev) {
+  s.index = index;
+  s.dev = dev;
+  GKB_CUDA(cudaSetDevice(dev));
+  GKB_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+  GKB_CUDA(cudaMalloc(&s.dres, sizeof(double) * kResCap));
+  GKB_CUDA(cudaMallocHost(&s.hres, sizeof(double) * kResCap));
+  GKB_CUDA(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+  s.ensure_partial(1 << 16);
+}
+
+void Context::init_local(const std::vector<int>& devices) {
+  if (devices.empty() || devices.size() > 16) fail(GKB_EINVAL, "gkb_init: need 1..16 shards");
+  int ndev = 0;
+  GKB_CUDA(cudaGetDeviceCount(&ndev));
+  shards.resize(devices.size());
+  for (size_t i = 0; i < devices.size(); ++i) {
+    if (devices[i] < 0 || devices[i] >= ndev) fail(GKB_EINVAL, "gkb_init: bad device ordinal");
+    init_shard(shards[i], (int)i, devices[i]);
+  }
+  nshards_total = (int)devices.size();
+  first_shard = 0;
+  use_nccl = false;
+}
+
+void Context::init_nccl(int device, const ncclUniqueId& id, int nranks, int rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(GKB_EINVAL, "gkb_init_nccl: bad rank");
+  shards.resize(1);
+  init_shard(shards[0], rank, device);
+  nshards_total = nranks;
+  first_shard = rank;
+  use_nccl = true;
+  GKB_CUDA(cudaSetDevice(device));
+  check_nccl(ncclCommInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
+}
+
+Context::~Context() {
+  for (auto& s : shards) {
+    cudaSetDevice(s.dev);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    if (s.rs.partial) cudaFree(s.rs.partial);
+    if (s.dres) cudaFree(s.dres);
+    if (s.hres) cudaFreeHost(s.hres);
+    if (s.flush_buf) cudaFree(s.flush_buf);
+    if (s.ev) cudaEventDestroy(s.ev);
+    if (s.stream) cudaStreamDestroy(s.stream);
+  }
+  if (stage && !shards.empty()) {
+    cudaSetDevice(shards[0].dev);
+    cudaFree(stage);
+  }
+  if (comm) ncclCommDestroy(comm);
+}
+
+void Context::set_device(int i) const { GKB_CUDA(cudaSetDevice(shards[i].dev)); }
+
+void Context::sync_all() {
+  for (auto& s : shards) {
+    GKB_CUDA(cudaSetDevice(s.dev));
+    GKB_CUDA(cudaStreamSynchronize(s.stream));
+  }
+}
+
+void Context::allreduce(const std::vector<double*>& bufs, int64_t count) {
+  if (count == 0) return;
+  if (use_nccl) {
+    if (nshards_total == 1) return;
+    Shard& s = shards[0];
+    GKB_CUDA(cudaSetDevice(s.dev));
+    check_nccl(ncclAllReduce(bufs[0], bufs[0], (size_t)count, ncclDouble, ncclSum, comm, s.stream),
+               "ncclAllReduce");
+    return;
+  }
+  const int G = (int)shards.size();
+  if (G == 1) return;
+  // Gather every shard's buffer on shard 0's device, sum in shard order,
+  // scatter the identical result back.
+  Shard& s0 = shards[0];
+  GKB_CUDA(cudaSetDevice(s0.dev));
+  if (stage_cap < count * G) {
+    if (stage) GKB_CUDA(cudaFree(stage));
+    stage_cap = std::max<int64_t>(count * G, 1 << 16);
+    GKB_CUDA(cudaMalloc(&stage, sizeof(double) * (size_t)stage_cap));
+  }
+  for (int i = 1; i < G; ++i) {
+    GKB_CUDA(cudaSetDevice(shards[i].dev));
+    GKB_CUDA(cudaEventRecord(shards[i].ev, shards[i].stream));
+    GKB_CUDA(cudaSetDevice(s0.dev));
+    GKB_CUDA(cudaStreamWaitEvent(s0.stream, shards[i].ev, 0));
+  }
+  GKB_CUDA(cudaSetDevice(s0.dev));
+  std::vector<const double*> srcs(G);
+  for (int i = 0; i < G; ++i) {
+    double* dst = stage + (int64_t)i * count;
+    GKB_CUDA(cudaMemcpyPeerAsync(dst, s0.dev, bufs[i], shards[i].dev, sizeof(double) * (size_t)count,
+                                 s0.stream));
+    srcs[i] = dst;
+  }
+  dev::sum_buffers(srcs.data(), G, bufs[0], count, s0.stream);
+  GKB_LAUNCH_CHECK();
+  for (int i = 1; i < G; ++i)
+    GKB_CUDA(cudaMemcpyPeerAsync(bufs[i], shards[i].dev, bufs[0], s0.dev,
+                                 sizeof(double) * (size_t)count, s0.stream));
+  GKB_CUDA(cudaEventRecord(s0.ev, s0.stream));
+  for (int i = 1; i < G; ++i) {
+    GKB_CUDA(cudaSetDevice(shards[i].dev));
+    GKB_CUDA(cudaStreamWaitEvent(shards[i].stream, s0.ev, 0));
+  }
+  GKB_CUDA(cudaSetDevice(s0.dev));
+}
+
+std::vector<int64_t> partition_rows(int64_t m, int nparts) {
+  if (nparts < 1) fail(GKB_EINVAL, "partition_rows: nparts < 1");
+  if (m < 0) fail(GKB_EINVAL, "partition_rows: negative size");
+  std::vector<int64_t> st(nparts + 1);
+  const int64_t quads = (m + 3) / 4;
+  for (int i = 0; i <= nparts; ++i) {
+    int64_t q = quads * i / nparts;
+    st[i] = std::min<int64_t>(m, 4 * q);
+  }
+  st[nparts] = m;
+  return st;
+}
+
+}  // namespace gkb

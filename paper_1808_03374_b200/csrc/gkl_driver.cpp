@@ -1,0 +1,800 @@
+// GKL driver (reference gkl.hpp / gkl.cpp) with device-resident Krylov
+// bases: U (reference left basis, SNP side, length m) is sharded by rows like
+// the operator, V (sample side, length n, plus the pending vector) is
+// replicated on every shard. B, the couplings, the omega rows, Ritz
+// extraction and the small SVD stay on the host; every host decision reads
+// device scalars (norms) after a fixed-order device reduction, all of which
+// are identical on every shard/rank.
+//
+// Control flow, constants and update order follow gkl.cpp line by line; the
+// line references below are to /root/reference/proj/src/gkl.cpp.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "host.hpp"
+
+namespace gkb {
+
+namespace {
+
+const double kEps = std::numeric_limits<double>::epsilon();
+const double kBreakdownFactor = std::pow(kEps, 2.0 / 3.0);  // gkl.cpp:19
+const double kOneSidedGuard = 1.0 / std::sqrt(kEps);        // gkl.cpp:21
+const double kCgs2Eta = 0.70710678118654752440;             // orth.hpp:11
+
+double eps_level(int64_t m, int64_t n) {  // gkl.cpp:23-25
+  return kEps * std::sqrt(static_cast<double>(std::max(m, n)));
+}
+
+bool monitors_side(bool left, int64_t m, int64_t n, const Options& o, double norm_scale) {
+  if (!o.one_sided || norm_scale > kOneSidedGuard) return true;  // gkl.cpp:27-33
+  return left ? m <= n : n < m;
+}
+
+}  // namespace
+
+Options options_from(const gkb_gkl_options* o) {
+  Options r;
+  if (!o) return r;
+  r.k = o->k;
+  r.tol = o->tol;
+  r.max_mvps = o->max_mvps;
+  r.full = o->reorth == 0;
+  r.omega = o->omega;
+  r.one_sided = o->one_sided != 0;
+  r.thick = o->restart == 1;
+  r.max_subspace = o->max_subspace;
+  r.keep = o->keep;
+  r.seed = o->seed;
+  r.record_history = o->record_history != 0;
+  r.omega_recurrence = o->omega_recurrence;
+  return r;
+}
+
+// GklOptions::validate (gkl.cpp:53-73), same messages.
+void validate_options(const Options& o, int64_t m, int64_t n) {
+  const int64_t minmn = std::min(m, n);
+  if (m <= 0 || n <= 0) fail(GKB_EINVAL, "svdl: operator has an empty dimension");
+  if (o.k < 1 || o.k > minmn) fail(GKB_EINVAL, "svdl: k must lie in [1, min(m, n)]");
+  if (!(o.tol > 0.0)) fail(GKB_EINVAL, "svdl: tol must be positive");
+  if (o.max_mvps < 2) fail(GKB_EINVAL, "svdl: max_mvps must allow at least one step");
+  if (!o.full && !(o.omega > 0.0)) fail(GKB_EINVAL, "svdl: omega must be positive");
+  if (o.thick) {
+    if (o.keep < o.k) fail(GKB_EINVAL, "svdl: keep must be at least k");
+    if (o.keep >= o.max_subspace) fail(GKB_EINVAL, "svdl: keep must be below max_subspace");
+    if (o.max_subspace > minmn) fail(GKB_EINVAL, "svdl: max_subspace cannot exceed min(m, n)");
+  }
+}
+
+// ---------------------------------------------------------------- Lanczos
+// LanczosFactorization ctor (gkl.cpp:75-98)
+Lanczos::Lanczos(DevOp* op, int64_t capacity, const double* start, uint64_t rng_seed)
+    : rng(rng_seed), op_(op), ctx_(op->ctx), m_(op->m), n_(op->n) {
+  if (m_ <= 0 || n_ <= 0) fail(GKB_EINVAL, "LanczosFactorization: empty dimensions");
+  cap_ = std::min(capacity, std::min(m_, n_));
+  if (cap_ < 1) fail(GKB_EINVAL, "LanczosFactorization: capacity < 1");
+  double nrm = 0.0;
+  for (int64_t i = 0; i < n_; ++i) nrm += start[i] * start[i];
+  nrm = std::sqrt(nrm);
+  if (!(nrm > 0.0)) fail(GKB_EINVAL, "LanczosFactorization: zero start vector");
+  const int L = (int)ctx_->shards.size();
+  U_.assign(L, nullptr);
+  U2_.assign(L, nullptr);
+  V_.assign(L, nullptr);
+  V2_.assign(L, nullptr);
+  w_.assign(L, nullptr);
+  z_.assign(L, nullptr);
+  cbuf_.assign(L, nullptr);
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    const size_t r = (size_t)std::max<int64_t>(op_->rows(i), 1);
+    GKB_CUDA(cudaMalloc(&U_[i], sizeof(double) * r * (size_t)cap_));
+    GKB_CUDA(cudaMalloc(&U2_[i], sizeof(double) * r * (size_t)cap_));
+    GKB_CUDA(cudaMalloc(&V_[i], sizeof(double) * (size_t)n_ * (size_t)(cap_ + 1)));
+    GKB_CUDA(cudaMalloc(&V2_[i], sizeof(double) * (size_t)n_ * (size_t)(cap_ + 1)));
+    GKB_CUDA(cudaMalloc(&w_[i], sizeof(double) * r));
+    GKB_CUDA(cudaMalloc(&z_[i], sizeof(double) * (size_t)n_));
+    GKB_CUDA(cudaMalloc(&cbuf_[i], sizeof(double) * (size_t)(cap_ + 2)));
+    const int64_t need = dev::red_blocks(std::max<int64_t>(op_->rows(i), n_)) * (cap_ + 4) + 64;
+    ctx_->shards[i].ensure_partial(need);
+  }
+  B_.assign((size_t)(cap_ * cap_), 0.0);
+  coupling_.assign((size_t)cap_, 0.0);
+  mu_.assign((size_t)(cap_ + 2), 0.0);
+  mu_next_.assign((size_t)(cap_ + 2), 0.0);
+  nu_.assign((size_t)(cap_ + 1), 0.0);
+  nu_next_.assign((size_t)(cap_ + 1), 0.0);
+  std::vector<double> v0(start, start + n_);
+  for (auto& x : v0) x /= nrm;
+  host_to_all(v0.data(), n_, V_);
+  mu_[0] = 1.0;
+  ctx_->sync_all();
+}
+
+Lanczos::~Lanczos() {
+  for (size_t i = 0; i < U_.size(); ++i) {
+    cudaSetDevice(ctx_->shards[i].dev);
+    cudaStreamSynchronize(ctx_->shards[i].stream);
+    for (double* p : {U_[i], U2_[i], V_[i], V2_[i], w_[i], z_[i], cbuf_[i]})
+      if (p) cudaFree(p);
+    if (i < tmp_small_.size() && tmp_small_[i]) cudaFree(tmp_small_[i]);
+  }
+  if (pinned_) cudaFreeHost(pinned_);
+}
+
+void Lanczos::host_to_all(const double* h, int64_t count, std::vector<double*>& dst) {
+  if (count == 0) return;
+  if (pinned_cap_ < count) {
+    if (pinned_) {
+      ctx_->sync_all();
+      GKB_CUDA(cudaFreeHost(pinned_));
+    }
+    pinned_cap_ = std::max<int64_t>(count, 1 << 12);
+    GKB_CUDA(cudaMallocHost(&pinned_, sizeof(double) * (size_t)pinned_cap_));
+  } else {
+    ctx_->sync_all();  // previous uploads from the staging buffer have completed
+  }
+  std::memcpy(pinned_, h, sizeof(double) * (size_t)count);
+  for (size_t i = 0; i < dst.size(); ++i) {
+    ctx_->set_device((int)i);
+    GKB_CUDA(cudaMemcpyAsync(dst[i], pinned_, sizeof(double) * (size_t)count,
+                             cudaMemcpyHostToDevice, ctx_->shards[i].stream));
+  }
+}
+
+void Lanczos::upload_small(const std::vector<double>& W, std::vector<double*>& dst) {
+  const int64_t need = (int64_t)W.size();
+  const int L = (int)ctx_->shards.size();
+  if (tmp_small_.size() != (size_t)L) tmp_small_.assign(L, nullptr);
+  if (tmp_cap_ < need) {
+    ctx_->sync_all();
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      if (tmp_small_[i]) GKB_CUDA(cudaFree(tmp_small_[i]));
+      GKB_CUDA(cudaMalloc(&tmp_small_[i], sizeof(double) * (size_t)std::max<int64_t>(need, 1024)));
+    }
+    tmp_cap_ = std::max<int64_t>(need, 1024);
+  }
+  host_to_all(W.data(), need, tmp_small_);
+  dst = tmp_small_;
+}
+
+void Lanczos::read(int64_t count) {
+  Shard& s = ctx_->shards[0];
+  ctx_->set_device(0);
+  GKB_CUDA(cudaMemcpyAsync(s.hres, s.dres, sizeof(double) * (size_t)count, cudaMemcpyDeviceToHost,
+                           s.stream));
+  GKB_CUDA(cudaStreamSynchronize(s.stream));
+  ++host_syncs;
+}
+
+// cgs2 (orth.hpp:19-44) on device vectors. Left side (sharded rows):
+// partial dot products are summed across shards before use.
+double Lanczos::cgs2(Side side, int64_t ncols, const std::vector<double*>& vec) {
+  const int L = (int)ctx_->shards.size();
+  const auto& Q = basis(side);
+  std::vector<double*> dres(L);
+  for (int i = 0; i < L; ++i) dres[i] = ctx_->shards[i].dres;
+  auto reduce = [&](int64_t off, int64_t cnt) {
+    if (side != kLeft) return;
+    std::vector<double*> b(L);
+    for (int i = 0; i < L; ++i) b[i] = dres[i] + off;
+    ctx_->allreduce(b, cnt);
+  };
+  if (ncols == 0) {
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      dev::nrm2sq(vec[i], len(side, i), ctx_->shards[i].rs, dres[i], ctx_->shards[i].stream);
+    }
+    reduce(0, 1);
+    read(1);
+    return std::sqrt(ctx_->shards[0].hres[0]);
+  }
+  // pass 1: c = Q^T v and ||v||^2 in one sweep, then v -= Q c with ||v||^2
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    Shard& s = ctx_->shards[i];
+    dev::gemv_t(Q[i], ld(side, i), len(side, i), ncols, vec[i], true, s.rs, dres[i], s.stream);
+  }
+  reduce(0, ncols + 1);
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    Shard& s = ctx_->shards[i];
+    dev::gemv_n(Q[i], ld(side, i), len(side, i), ncols, dres[i], vec[i], 1.0, -1.0, true, s.rs,
+                dres[i] + ncols + 1, s.stream);
+  }
+  reduce(ncols + 1, 2);
+  read(ncols + 3);
+  const double norm_before = std::sqrt(ctx_->shards[0].hres[ncols]);
+  double norm_after = std::sqrt(ctx_->shards[0].hres[ncols + 2]);
+  if (norm_after < kCgs2Eta * norm_before) {
+    const int64_t o = ncols + 3;
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      Shard& s = ctx_->shards[i];
+      dev::gemv_t(Q[i], ld(side, i), len(side, i), ncols, vec[i], false, s.rs, dres[i] + o, s.stream);
+    }
+    reduce(o, ncols);
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      Shard& s = ctx_->shards[i];
+      dev::gemv_n(Q[i], ld(side, i), len(side, i), ncols, dres[i] + o, vec[i], 1.0, -1.0, true, s.rs,
+                  dres[i] + o + ncols, s.stream);
+    }
+    reduce(o + ncols, 2);
+    read(o + ncols + 2);
+    norm_after = std::sqrt(ctx_->shards[0].hres[o + ncols + 1]);
+  }
+  return norm_after;
+}
+
+// partial_reorth_update (gkl.cpp:112-176): omega recurrences on the host,
+// device cgs2 when the estimate crosses omega.
+bool Lanczos::partial_reorth_update(Side side, const std::vector<double*>& cand, double cand_coeff,
+                                    const Options& o, double norm_scale) {
+  const int64_t j = j_;
+  const double lvl = eps_level(m_, n_);
+  const double tau = 2.0 * lvl * norm_scale + lvl;
+  const double denom = std::max(cand_coeff, tau + kEps);
+  double worst = 0.0;
+  if (side == kLeft) {
+    for (int64_t i = 0; i < j; ++i) {
+      double acc = 0.0;
+      for (int64_t c = i; c < j; ++c) acc += std::abs(Bc(i, c)) * mu_[c];
+      if (o.omega_recurrence == 1) {
+        // alpha u_new = X v - sum_c coupling_c u_c: the u_i component of each
+        // subtracted coupling_c u_c (c != i) is bounded by |coupling_c| * nu,
+        // nu being the committed level of the newest u (or the restart carry).
+        for (int64_t c = 0; c < j; ++c)
+          if (c != i && coupling_[c] != 0.0) acc += std::abs(coupling_[c]) * nu_[std::min(c, i)];
+      }
+      const double est = std::min(1.0, (acc + tau) / denom);
+      nu_next_[i] = est;
+      worst = std::max(worst, est);
+    }
+    nu_next_[j] = 1.0;
+    if (worst > o.omega && monitors_side(true, m_, n_, o, norm_scale)) {
+      cgs2(kLeft, j, cand);
+      for (int64_t i = 0; i < j; ++i) nu_next_[i] = lvl;
+      return true;
+    }
+    return false;
+  }
+  const double alpha_last = Bc(j - 1, j - 1);
+  for (int64_t i = 0; i < j; ++i) {
+    double acc = 0.0;
+    if (i == j - 1) {
+      for (int64_t r = 0; r + 1 < j; ++r) acc += std::abs(Bc(r, i)) * nu_[r];
+    } else {
+      for (int64_t r = 0; r <= i; ++r) acc += std::abs(Bc(r, i)) * nu_[r];
+      acc += alpha_last * mu_[i];
+    }
+    const double est = std::min(1.0, (acc + tau) / denom);
+    mu_next_[i] = est;
+    worst = std::max(worst, est);
+  }
+  mu_next_[j] = 1.0;
+  if (worst > o.omega && monitors_side(false, m_, n_, o, norm_scale)) {
+    cgs2(kRight, j, cand);
+    for (int64_t i = 0; i < j; ++i) mu_next_[i] = lvl;
+    return true;
+  }
+  return false;
+}
+
+// deflate_right (gkl.cpp:178-204)
+void Lanczos::deflate_right() {
+  const int64_t j = j_;
+  const double lvl = eps_level(m_, n_);
+  const int L = (int)ctx_->shards.size();
+  std::fill(coupling_.begin(), coupling_.begin() + j, 0.0);
+  if (j < n_) {
+    std::vector<double> v((size_t)n_);
+    for (int attempt = 0; attempt < 4; ++attempt) {
+      for (int64_t i = 0; i < n_; ++i) v[i] = rng.uniform_symmetric();
+      host_to_all(v.data(), n_, z_);
+      const double nrm = cgs2(kRight, j, z_);
+      if (nrm > 1e-3 * std::sqrt(static_cast<double>(n_))) {
+        for (int i = 0; i < L; ++i) {
+          ctx_->set_device(i);
+          dev::div_copy(z_[i], nrm, V_[i] + j * n_, n_, ctx_->shards[i].stream);
+        }
+        std::fill(mu_.begin(), mu_.begin() + j, lvl);
+        mu_[j] = 1.0;
+        right_exhausted_ = false;
+        return;
+      }
+    }
+  }
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    GKB_CUDA(cudaMemsetAsync(V_[i] + j * n_, 0, sizeof(double) * (size_t)n_, ctx_->shards[i].stream));
+  }
+  std::fill(mu_.begin(), mu_.begin() + j + 1, lvl);
+  right_exhausted_ = true;
+}
+
+// bidiag_step (gkl.cpp:206-312)
+StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter) {
+  const int64_t s = j_;
+  if (s >= cap_ || s >= std::min(m_, n_))
+    fail(GKB_ELOGIC, "bidiag_step: factorization cannot grow further");
+  if (right_exhausted_) fail(GKB_ELOGIC, "bidiag_step: right side exhausted");
+  const int L = (int)ctx_->shards.size();
+  StepInfo info;
+  const double breakdown_tol = kBreakdownFactor * norm_scale;
+  const double lvl = eps_level(m_, n_);
+  const bool full = o.full;
+  std::vector<double*> dres(L);
+  for (int i = 0; i < L; ++i) dres[i] = ctx_->shards[i].dres;
+  auto reduce_left = [&](int64_t off, int64_t cnt) {
+    std::vector<double*> b(L);
+    for (int i = 0; i < L; ++i) b[i] = dres[i] + off;
+    ctx_->allreduce(b, cnt);
+  };
+
+  // Left half-step: alpha u_{s+1} = X v_pending - U coupling.
+  {
+    std::vector<const double*> vin(L);
+    for (int i = 0; i < L; ++i) vin[i] = V_[i] + s * n_;
+    op_->apply_dev(vin, w_);
+    if (mvp_counter) ++*mvp_counter;
+  }
+  double alpha;
+  if (full) {
+    alpha = cgs2(kLeft, s, w_);
+  } else {
+    int64_t lo = -1, hi = -1;
+    for (int64_t i = 0; i < s; ++i)
+      if (coupling_[i] != 0.0) {
+        if (lo < 0) lo = i;
+        hi = i;
+      }
+    double w_norm0, alpha_cand;
+    if (lo < 0) {
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        dev::nrm2sq(w_[i], op_->rows(i), ctx_->shards[i].rs, dres[i], ctx_->shards[i].stream);
+      }
+      reduce_left(0, 1);
+      read(1);
+      w_norm0 = alpha_cand = std::sqrt(ctx_->shards[0].hres[0]);
+    } else {
+      std::vector<double> cf(coupling_.begin() + lo, coupling_.begin() + hi + 1);
+      host_to_all(cf.data(), hi - lo + 1, cbuf_);
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        Shard& sh = ctx_->shards[i];
+        const int64_t r = op_->rows(i);
+        dev::gemv_n(U_[i] + lo * r, r, r, hi - lo + 1, cbuf_[i], w_[i], 1.0, -1.0, true, sh.rs,
+                    dres[i], sh.stream);
+      }
+      reduce_left(0, 2);
+      read(2);
+      w_norm0 = std::sqrt(ctx_->shards[0].hres[0]);
+      alpha_cand = std::sqrt(ctx_->shards[0].hres[1]);
+    }
+    if (alpha_cand < kCgs2Eta * w_norm0) {
+      // Local (modified) second pass over the structural pattern.
+      for (int64_t c = 0; c < s; ++c) {
+        if (coupling_[c] == 0.0) continue;
+        for (int i = 0; i < L; ++i) {
+          ctx_->set_device(i);
+          Shard& sh = ctx_->shards[i];
+          const int64_t r = op_->rows(i);
+          dev::dot(U_[i] + c * r, w_[i], r, sh.rs, dres[i] + 8, sh.stream);
+        }
+        reduce_left(8, 1);
+        for (int i = 0; i < L; ++i) {
+          ctx_->set_device(i);
+          const int64_t r = op_->rows(i);
+          dev::axpy_dev(dres[i] + 8, U_[i] + c * r, w_[i], r, ctx_->shards[i].stream);
+        }
+      }
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        dev::nrm2sq(w_[i], op_->rows(i), ctx_->shards[i].rs, dres[i], ctx_->shards[i].stream);
+      }
+      reduce_left(0, 1);
+      read(1);
+      alpha_cand = std::sqrt(ctx_->shards[0].hres[0]);
+    }
+    if (partial_reorth_update(kLeft, w_, alpha_cand, o, norm_scale)) {
+      info.reorth_left = true;
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        dev::nrm2sq(w_[i], op_->rows(i), ctx_->shards[i].rs, dres[i], ctx_->shards[i].stream);
+      }
+      reduce_left(0, 1);
+      read(1);
+      alpha_cand = std::sqrt(ctx_->shards[0].hres[0]);
+    }
+    alpha = alpha_cand;
+  }
+  if (!(alpha > breakdown_tol)) {
+    info.status = 1;
+    return info;  // nothing appended
+  }
+  info.alpha = alpha;
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    const int64_t r = op_->rows(i);
+    dev::div_copy(w_[i], alpha, U_[i] + s * r, r, ctx_->shards[i].stream);
+  }
+  for (int64_t i = 0; i < s; ++i) B(i, s) = coupling_[i];
+  B(s, s) = alpha;
+  if (full) {
+    std::fill(nu_.begin(), nu_.begin() + s, lvl);
+    nu_[s] = 1.0;
+  } else {
+    std::copy(nu_next_.begin(), nu_next_.begin() + s + 1, nu_.begin());
+  }
+  j_ = s + 1;
+
+  // Right half-step: beta v_new = X^T u_{s+1} - alpha v_pending.
+  {
+    std::vector<const double*> uin(L);
+    for (int i = 0; i < L; ++i) uin[i] = U_[i] + s * op_->rows(i);
+    op_->adjoint_dev(uin, z_);
+    if (mvp_counter) ++*mvp_counter;
+  }
+  double beta;
+  if (full) {
+    beta = cgs2(kRight, s + 1, z_);
+  } else {
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      Shard& sh = ctx_->shards[i];
+      dev::axpy_norms(alpha, V_[i] + s * n_, z_[i], n_, sh.rs, dres[i], sh.stream);
+    }
+    read(2);
+    const double z_norm0 = std::sqrt(ctx_->shards[0].hres[0]);
+    double beta_cand = std::sqrt(ctx_->shards[0].hres[1]);
+    if (beta_cand < kCgs2Eta * z_norm0) {
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        Shard& sh = ctx_->shards[i];
+        dev::dot(V_[i] + s * n_, z_[i], n_, sh.rs, dres[i] + 8, sh.stream);
+        dev::axpy_dev(dres[i] + 8, V_[i] + s * n_, z_[i], n_, sh.stream);
+        dev::nrm2sq(z_[i], n_, sh.rs, dres[i], sh.stream);
+      }
+      read(1);
+      beta_cand = std::sqrt(ctx_->shards[0].hres[0]);
+    }
+    if (partial_reorth_update(kRight, z_, beta_cand, o, norm_scale)) {
+      info.reorth_right = true;
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        dev::nrm2sq(z_[i], n_, ctx_->shards[i].rs, dres[i], ctx_->shards[i].stream);
+      }
+      read(1);
+      beta_cand = std::sqrt(ctx_->shards[0].hres[0]);
+    }
+    beta = beta_cand;
+  }
+  std::fill(coupling_.begin(), coupling_.begin() + s + 1, 0.0);
+  if (!(beta > breakdown_tol)) {
+    info.status = 2;
+    deflate_right();
+    return info;
+  }
+  info.beta = beta;
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    dev::div_copy(z_[i], beta, V_[i] + (s + 1) * n_, n_, ctx_->shards[i].stream);
+  }
+  coupling_[s] = beta;
+  if (full) {
+    std::fill(mu_.begin(), mu_.begin() + s + 1, lvl);
+    mu_[s + 1] = 1.0;
+  } else {
+    std::copy(mu_next_.begin(), mu_next_.begin() + s + 2, mu_.begin());
+  }
+  return info;
+}
+
+// ritz_extract (gkl.cpp:314-339)
+Ritz Lanczos::ritz_extract(double tol) const {
+  Ritz out;
+  const int64_t j = j_;
+  out.j = j;
+  if (j == 0) return out;
+  std::vector<double> Bj((size_t)(j * j));
+  for (int64_t c = 0; c < j; ++c)
+    for (int64_t r = 0; r < j; ++r) Bj[r + c * j] = Bc(r, c);
+  out.values.assign((size_t)j, 0.0);
+  out.WL.assign((size_t)(j * j), 0.0);
+  out.WR.assign((size_t)(j * j), 0.0);
+  svd_small(Bj.data(), j, j, out.WL.data(), out.values.data(), out.WR.data());
+  out.err_crude.assign((size_t)j, 0.0);
+  for (int64_t i = 0; i < j; ++i) {
+    double acc = 0.0;
+    for (int64_t r = 0; r < j; ++r) acc += out.WL[r + i * j] * coupling_[r];
+    out.err_crude[i] = std::abs(acc);
+  }
+  out.err = out.err_crude;
+  for (int64_t i = 0; i < j; ++i) {
+    double gap = std::numeric_limits<double>::infinity();
+    for (int64_t l = 0; l < j; ++l)
+      if (l != i) gap = std::min(gap, std::abs(out.values[l] - out.values[i]));
+    if (j > 1 && gap > 10.0 * out.err_crude[i] && gap > 0.0) {
+      const double refined = out.err_crude[i] * out.err_crude[i] / gap;
+      out.err[i] = std::min(out.err_crude[i], refined);
+    }
+  }
+  const double theta_max = out.values[0];
+  out.converged.assign((size_t)j, 0);
+  for (int64_t i = 0; i < j; ++i) out.converged[i] = out.err[i] <= tol * theta_max;
+  return out;
+}
+
+// thick_restart (gkl.cpp:341-378)
+void Lanczos::thick_restart(int64_t keep) {
+  const int64_t j = j_;
+  if (keep < 1 || keep >= j) fail(GKB_EINVAL, "thick_restart: need 1 <= keep < steps");
+  const int L = (int)ctx_->shards.size();
+  const Ritz ritz = ritz_extract(0.0);
+  std::vector<double> rho((size_t)keep);
+  for (int64_t i = 0; i < keep; ++i) {
+    double acc = 0.0;
+    for (int64_t r = 0; r < j; ++r) acc += ritz.WL[r + i * j] * coupling_[r];
+    rho[i] = acc;
+  }
+  // W = [W_L[:, :keep] | W_R[:, :keep]] uploaded once
+  std::vector<double> Wup((size_t)(2 * j * keep));
+  std::copy(ritz.WL.begin(), ritz.WL.begin() + j * keep, Wup.begin());
+  std::copy(ritz.WR.begin(), ritz.WR.begin() + j * keep, Wup.begin() + j * keep);
+  std::vector<double*> Wd;
+  upload_small(Wup, Wd);
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    cudaStream_t st = ctx_->shards[i].stream;
+    const int64_t r = op_->rows(i);
+    dev::gemm_small(U_[i], r, r, j, Wd[i], j, keep, U2_[i], r, st);
+    dev::gemm_small(V_[i], n_, n_, j, Wd[i] + j * keep, j, keep, V2_[i], n_, st);
+    GKB_CUDA(cudaMemcpyAsync(V2_[i] + keep * n_, V_[i] + j * n_, sizeof(double) * (size_t)n_,
+                             cudaMemcpyDeviceToDevice, st));
+    std::swap(U_[i], U2_[i]);
+    std::swap(V_[i], V2_[i]);
+  }
+  std::fill(B_.begin(), B_.end(), 0.0);
+  for (int64_t i = 0; i < keep; ++i) B(i, i) = ritz.values[i];
+  std::fill(coupling_.begin(), coupling_.end(), 0.0);
+  for (int64_t i = 0; i < keep; ++i) coupling_[i] = rho[i];
+  j_ = keep;
+  const double lvl = eps_level(m_, n_);
+  const double scale = std::sqrt(static_cast<double>(j));
+  const double mmax = *std::max_element(mu_.begin(), mu_.begin() + j);
+  const double nmax = *std::max_element(nu_.begin(), nu_.begin() + j);
+  const double mu_carry = std::min(1.0, scale * mmax + lvl);
+  const double nu_carry = std::min(1.0, scale * nmax + lvl);
+  std::fill(mu_.begin(), mu_.begin() + keep, mu_carry);
+  mu_[keep] = 1.0;
+  std::fill(nu_.begin(), nu_.begin() + keep, nu_carry);
+}
+
+// compress_exhausted (gkl.cpp:380-409)
+void Lanczos::compress_exhausted() {
+  const int64_t j = j_;
+  if (j == 0) return;
+  const int L = (int)ctx_->shards.size();
+  std::vector<double> aug((size_t)(j * (j + 1)));
+  for (int64_t c = 0; c < j; ++c)
+    for (int64_t r = 0; r < j; ++r) aug[r + c * j] = Bc(r, c);
+  for (int64_t r = 0; r < j; ++r) aug[r + j * j] = coupling_[r];
+  std::vector<double> SU((size_t)(j * j)), Ss((size_t)j), SV((size_t)((j + 1) * j));
+  svd_small(aug.data(), j, j + 1, SU.data(), Ss.data(), SV.data());
+  std::vector<double> Wup(SU);
+  Wup.insert(Wup.end(), SV.begin(), SV.end());
+  std::vector<double*> Wd;
+  upload_small(Wup, Wd);
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    cudaStream_t st = ctx_->shards[i].stream;
+    const int64_t r = op_->rows(i);
+    dev::gemm_small(U_[i], r, r, j, Wd[i], j, j, U2_[i], r, st);
+    dev::gemm_small(V_[i], n_, n_, j + 1, Wd[i] + j * j, j + 1, j, V2_[i], n_, st);
+    GKB_CUDA(cudaMemsetAsync(V2_[i] + j * n_, 0, sizeof(double) * (size_t)n_, st));
+    std::swap(U_[i], U2_[i]);
+    std::swap(V_[i], V2_[i]);
+  }
+  std::fill(B_.begin(), B_.end(), 0.0);
+  for (int64_t i = 0; i < j; ++i) B(i, i) = Ss[i];
+  std::fill(coupling_.begin(), coupling_.end(), 0.0);
+  right_exhausted_ = true;
+  const double lvl = eps_level(m_, n_);
+  std::fill(mu_.begin(), mu_.begin() + j + 1, lvl);
+  std::fill(nu_.begin(), nu_.begin() + j, lvl);
+}
+
+// Gathers a left-side (sharded rows) block of `ncols` columns, ld = rows(i),
+// into host column-major m x ncols.
+static void gather_left(Context* ctx, DevOp* op, const std::vector<double*>& src, int64_t ncols,
+                        double* host) {
+  const int L = (int)ctx->shards.size();
+  const int64_t m = op->m;
+  if (ncols == 0) return;
+  if (ctx->use_nccl && ctx->nshards_total > 1) {
+    ctx->set_device(0);
+    Shard& s = ctx->shards[0];
+    double* full = nullptr;
+    GKB_CUDA(cudaMalloc(&full, sizeof(double) * (size_t)(m * ncols)));
+    GKB_CUDA(cudaMemsetAsync(full, 0, sizeof(double) * (size_t)(m * ncols), s.stream));
+    const int64_t r = op->rows(0);
+    if (r > 0)
+      GKB_CUDA(cudaMemcpy2DAsync(full + op->row0(0), sizeof(double) * (size_t)m, src[0],
+                                 sizeof(double) * (size_t)r, sizeof(double) * (size_t)r,
+                                 (size_t)ncols, cudaMemcpyDeviceToDevice, s.stream));
+    ctx->allreduce({full}, m * ncols);
+    GKB_CUDA(cudaMemcpyAsync(host, full, sizeof(double) * (size_t)(m * ncols),
+                             cudaMemcpyDeviceToHost, s.stream));
+    GKB_CUDA(cudaStreamSynchronize(s.stream));
+    cudaFree(full);
+    return;
+  }
+  for (int i = 0; i < L; ++i) {
+    ctx->set_device(i);
+    const int64_t r = op->rows(i);
+    if (r == 0) continue;
+    GKB_CUDA(cudaMemcpy2DAsync(host + op->row0(i), sizeof(double) * (size_t)m, src[i],
+                               sizeof(double) * (size_t)r, sizeof(double) * (size_t)r,
+                               (size_t)ncols, cudaMemcpyDeviceToHost, ctx->shards[i].stream));
+  }
+  ctx->sync_all();
+}
+
+void Lanczos::get(double* U, double* V, double* B, double* coupling, double* om_left,
+                  double* om_right) {
+  ctx_->sync_all();
+  const int64_t j = j_;
+  if (U) gather_left(ctx_, op_, U_, j, U);
+  if (V) {
+    ctx_->set_device(0);
+    GKB_CUDA(cudaMemcpy(V, V_[0], sizeof(double) * (size_t)(n_ * (j + 1)), cudaMemcpyDeviceToHost));
+  }
+  if (B)
+    for (int64_t c = 0; c < j; ++c)
+      for (int64_t r = 0; r < j; ++r) B[r + c * j] = Bc(r, c);
+  if (coupling) std::copy(coupling_.begin(), coupling_.begin() + j, coupling);
+  if (om_left) std::copy(nu_.begin(), nu_.begin() + j, om_left);
+  if (om_right) std::copy(mu_.begin(), mu_.begin() + j + 1, om_right);
+}
+
+void Lanczos::ritz_vectors(const Ritz& r, int64_t kc, double* outU, double* outV) {
+  const int64_t j = j_;
+  if (kc == 0 || j == 0) return;
+  const int L = (int)ctx_->shards.size();
+  std::vector<double> Wup((size_t)(2 * j * kc));
+  std::copy(r.WL.begin(), r.WL.begin() + j * kc, Wup.begin());
+  std::copy(r.WR.begin(), r.WR.begin() + j * kc, Wup.begin() + j * kc);
+  std::vector<double*> Wd;
+  upload_small(Wup, Wd);
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    cudaStream_t st = ctx_->shards[i].stream;
+    const int64_t rr = op_->rows(i);
+    dev::gemm_small(U_[i], rr, rr, j, Wd[i], j, kc, U2_[i], rr, st);
+    dev::gemm_small(V_[i], n_, n_, j, Wd[i] + j * kc, j, kc, V2_[i], n_, st);
+  }
+  ctx_->sync_all();
+  if (outU) gather_left(ctx_, op_, U2_, kc, outU);
+  if (outV) {
+    ctx_->set_device(0);
+    GKB_CUDA(cudaMemcpy(outV, V2_[0], sizeof(double) * (size_t)(n_ * kc), cudaMemcpyDeviceToHost));
+  }
+}
+
+// ---------------------------------------------------------------- svdl
+// svdl (gkl.cpp:416-514)
+SvdlOutput svdl(DevOp* op, const Options& o) {
+  const auto t_start = std::chrono::steady_clock::now();
+  const int64_t m = op->m, n = op->n;
+  validate_options(o, m, n);
+  const int64_t minmn = std::min(m, n);
+  const int64_t cap = o.thick ? o.max_subspace : minmn;
+
+  int64_t mvps = 0;
+  Rng start_rng(o.seed);
+  std::vector<double> v0((size_t)n);
+  for (int64_t i = 0; i < n; ++i) v0[i] = start_rng.uniform_symmetric();
+  // The deflation draws continue the same stream (gkl.cpp:427-430, :189).
+  Lanczos f(op, cap, v0.data(), 0);
+  f.rng = start_rng;
+
+  Context* ctx = op->ctx;
+  cudaEvent_t e0, e1;
+  ctx->set_device(0);
+  GKB_CUDA(cudaEventCreate(&e0));
+  GKB_CUDA(cudaEventCreate(&e1));
+  GKB_CUDA(cudaEventRecord(e0, ctx->shards[0].stream));
+
+  SvdlOutput out;
+  double norm_scale = 0.0;
+  Ritz ritz;
+  int consecutive_breakdowns = 0;
+  auto extract = [&]() {
+    ritz = f.ritz_extract(o.tol);
+    if (!ritz.values.empty()) norm_scale = std::max(norm_scale, ritz.values[0]);
+    if (o.record_history) {
+      for (int64_t i = 0; i < o.k; ++i) {
+        out.ritz_history.push_back(i < ritz.j ? ritz.values[i] : std::nan(""));
+        out.err_history.push_back(i < ritz.j ? ritz.err[i] : std::nan(""));
+      }
+      ++out.history_len;
+    }
+  };
+  auto top_k_converged = [&]() {
+    if (f.steps() < o.k || ritz.j < o.k) return false;
+    for (int64_t i = 0; i < o.k; ++i)
+      if (!ritz.converged[i]) return false;
+    return true;
+  };
+
+  while (true) {
+    if (f.steps() >= minmn) break;  // factorization complete
+    if (mvps + 2 > o.max_mvps) break;
+    if (f.right_exhausted()) break;
+    const StepInfo step = f.step(o, norm_scale, &mvps);
+    if (step.status == 1) {
+      ++out.deflations;
+      ++consecutive_breakdowns;
+      f.compress_exhausted();
+      extract();
+      if (top_k_converged() || consecutive_breakdowns > 3) break;
+      f.deflate_right();
+      continue;
+    }
+    ++out.steps;
+    if (step.reorth_left) ++out.reorth_count;
+    if (step.reorth_right) ++out.reorth_count;
+    norm_scale = std::max(norm_scale, std::hypot(step.alpha, step.beta));
+    if (step.status == 2) {
+      ++out.deflations;
+      ++consecutive_breakdowns;
+    } else {
+      consecutive_breakdowns = 0;
+    }
+    if (!o.thick) {
+      extract();
+      if (top_k_converged()) break;
+    } else if (f.steps() == o.max_subspace) {
+      extract();
+      if (top_k_converged()) break;
+      if (mvps + 2 > o.max_mvps) break;
+      f.thick_restart(o.keep);
+      ++out.restarts;
+    }
+  }
+
+  extract();
+  const int64_t j = f.steps();
+  const int64_t count = std::min<int64_t>(o.k, j);
+  out.count = count;
+  out.singvals.assign(ritz.values.begin(), ritz.values.begin() + count);
+  out.err.assign(ritz.err.begin(), ritz.err.begin() + count);
+  out.converged.assign(ritz.converged.begin(), ritz.converged.begin() + count);
+  out.U.assign((size_t)(m * count), 0.0);
+  out.V.assign((size_t)(n * count), 0.0);
+  // Ritz vectors U W_L, V W_R, returned as-is (gkl.cpp:500-507).
+  f.ritz_vectors(ritz, count, out.U.data(), out.V.data());
+  out.all_converged = count == o.k && top_k_converged();
+  out.mvps = mvps;
+  ctx->set_device(0);
+  GKB_CUDA(cudaEventRecord(e1, ctx->shards[0].stream));
+  GKB_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  GKB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  out.device_seconds = ms * 1e-3;
+  out.host_syncs = f.host_syncs;
+  op->mvps += mvps;
+  out.wall_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  return out;
+}
+
+}  // namespace gkb

@@ -1,0 +1,238 @@
+// Host-side structures of the B200 GKL library: context (shards, streams,
+// communicator), device operators (packed genotype, dense) and the GKL
+// driver with device-resident Krylov bases.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "gkb_common.hpp"
+#include "kernels.hpp"
+
+namespace gkb {
+
+// Rng (rng.hpp:17-62): std::mt19937_64 with the reference's draw algorithms.
+class Rng {
+ public:
+  explicit Rng(uint64_t seed) : engine_(seed) {}
+  uint64_t bits() { return engine_(); }
+  double uniform() { return static_cast<double>(engine_() >> 11) * 0x1.0p-53; }
+  double uniform_symmetric() { return 2.0 * uniform() - 1.0; }
+
+ private:
+  std::mt19937_64 engine_;
+};
+
+// One SNP shard: a device, a stream, scratch for fixed-order reductions and
+// pinned staging for scalar read-backs.
+struct Shard {
+  int index = 0;  // global shard index (rank in SPMD mode)
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  dev::RedScratch rs{nullptr, 0};
+  double* dres = nullptr;  // device results (kResCap doubles)
+  double* hres = nullptr;  // pinned host mirror
+  void* flush_buf = nullptr;
+  size_t flush_bytes = 0;
+  cudaEvent_t ev = nullptr;
+  void ensure_partial(int64_t doubles);
+};
+
+constexpr int64_t kResCap = 1 << 16;
+
+struct Context {
+  std::vector<Shard> shards;
+  int nshards_total = 1;
+  int first_shard = 0;
+  bool use_nccl = false;
+  ncclComm_t comm = nullptr;
+  // local-mode allreduce staging on shard 0's device
+  double* stage = nullptr;
+  int64_t stage_cap = 0;
+
+  ~Context();
+  void init_local(const std::vector<int>& devices);
+  void init_nccl(int device, const ncclUniqueId& id, int nranks, int rank);
+  // In-place sum over all shards (all processes). bufs: one device pointer per
+  // local shard. Result identical on every shard.
+  void allreduce(const std::vector<double*>& bufs, int64_t count);
+  void sync_all();
+  void set_device(int i) const;
+};
+
+// Contiguous row partition; interior boundaries multiples of 4.
+std::vector<int64_t> partition_rows(int64_t m, int nparts);
+
+// Device linear operator (LinearOperator, linop.hpp:13-39) with rows
+// (reference m = SNPs) sharded and columns (samples) replicated.
+struct DevOp {
+  Context* ctx = nullptr;
+  int64_t m = 0, n = 0;
+  std::vector<int64_t> starts;  // global partition, nshards_total + 1
+  int64_t mvps = 0;
+  // host-API staging buffers per local shard
+  std::vector<double*> xbuf, ybuf, zbuf, yfull;
+
+  virtual ~DevOp();
+  int64_t row0(int i) const { return starts[ctx->shards[i].index]; }
+  int64_t rows(int i) const { return starts[ctx->shards[i].index + 1] - starts[ctx->shards[i].index]; }
+  // y_i (rows(i)) = X_i x_i ; x_i replicated (n). Stream-ordered on shard streams.
+  virtual void apply_dev(const std::vector<const double*>& x, const std::vector<double*>& y) = 0;
+  // z (n) = sum_i X_i^T y_i, allreduced so every shard holds the full z.
+  virtual void adjoint_dev(const std::vector<const double*>& y, const std::vector<double*>& z) = 0;
+  void alloc_host_api_buffers();
+  void apply_host(const double* x, double* y);
+  void adjoint_host(const double* y, double* z);
+};
+
+struct GenoShard {
+  int64_t p_loc = 0, n = 0, W = 0, P4 = 0;
+  uint4* layA = nullptr;
+  uint4* layB = nullptr;
+  double* mu = nullptr;
+  double* inv_s = nullptr;
+  int64_t* counts = nullptr;  // device p_loc*4
+  int64_t nmissing = 0;
+  int64_t* row_ptr = nullptr;
+  int32_t* row_idx = nullptr;
+  int64_t* col_ptr = nullptr;
+  int32_t* col_idx = nullptr;
+  dev::K1Plan k1{};
+  dev::K2Plan k2{};
+  double* ypart = nullptr;
+  double* xsum = nullptr;
+  double* zpart = nullptr;
+  double* kpart = nullptr;
+  double* cmiss = nullptr;
+  dev::GenoView view() const;
+};
+
+struct GenoOp : DevOp {
+  std::vector<GenoShard> gs;
+  std::vector<int64_t> counts_host;  // p*4 (local rows only in SPMD mode, zero elsewhere)
+  bool scaled = false;
+  ~GenoOp() override;
+  void build_from_payload(const uint8_t* payload, int64_t p, int64_t n);
+  void build_from_synth(const dev::SynthDev& spec_host_ptrs, const gkb_synth_spec* spec);
+  void finish_build();  // counts, missing lists, plans, scratch
+  void set_scaling(const double* mu, const double* inv_s);  // global p arrays
+  void get_scaling(double* mu, double* inv_s);
+  void apply_dev(const std::vector<const double*>& x, const std::vector<double*>& y) override;
+  void adjoint_dev(const std::vector<const double*>& y, const std::vector<double*>& z) override;
+  int64_t packed_bytes() const;
+  int64_t device_bytes() const;
+  void read_bed(int64_t row0, int64_t nrows, uint8_t* out);
+
+ private:
+  void alloc_shard(int i, int64_t p_loc, int64_t n);
+};
+
+struct DenseOp : DevOp {
+  std::vector<double*> X;  // per shard rows(i) x n, ld = rows(i)
+  ~DenseOp() override;
+  void build(const double* Xh, int64_t m, int64_t n);
+  void apply_dev(const std::vector<const double*>& x, const std::vector<double*>& y) override;
+  void adjoint_dev(const std::vector<const double*>& y, const std::vector<double*>& z) override;
+};
+
+// Marker scaling from counts (genio.cpp:150-185 restated on counts).
+void marker_scaling(const int64_t* counts, int64_t p, int64_t n, int scheme, double* mu, double* inv_s);
+
+// svd_small (small_svd.cpp:14-28) -- host one-sided Jacobi.
+void svd_small(const double* M, int64_t r, int64_t c, double* U, double* s, double* V);
+
+// ---- GKL (gkl.hpp / gkl.cpp) ----------------------------------------------
+struct Options {
+  int64_t k = 10;
+  double tol = 1e-8;
+  int64_t max_mvps = 1000000;
+  bool full = false;  // reorth == kFull
+  double omega = 1e-8;
+  bool one_sided = false;
+  bool thick = false;  // restart == kThick
+  int64_t max_subspace = 40;
+  int64_t keep = 20;
+  uint64_t seed = 0;
+  bool record_history = false;
+  int omega_recurrence = 1;
+};
+Options options_from(const gkb_gkl_options* o);
+void validate_options(const Options& o, int64_t m, int64_t n);  // throws GKB_EINVAL
+
+struct Ritz {
+  int64_t j = 0;
+  std::vector<double> values, WL, WR, err, err_crude;
+  std::vector<int32_t> converged;
+};
+
+struct StepInfo {
+  int status = 0;  // 0 ok, 1 alpha breakdown, 2 beta breakdown
+  bool reorth_left = false, reorth_right = false;
+  double alpha = 0.0, beta = 0.0;
+};
+
+class Lanczos {
+ public:
+  Lanczos(DevOp* op, int64_t capacity, const double* start_host, uint64_t rng_seed);
+  ~Lanczos();
+  int64_t steps() const { return j_; }
+  int64_t capacity() const { return cap_; }
+  bool right_exhausted() const { return right_exhausted_; }
+  StepInfo step(const Options& o, double norm_scale, int64_t* mvp_counter);
+  Ritz ritz_extract(double tol) const;
+  void thick_restart(int64_t keep);
+  void compress_exhausted();
+  void deflate_right();
+  // downloads (host arrays sized by the caller)
+  void get(double* U, double* V, double* B, double* coupling, double* om_left, double* om_right);
+  // out_U (m x kc) = U[:, :j] W_L[:, :kc], out_V (n x kc) = V[:, :j] W_R[:, :kc]
+  void ritz_vectors(const Ritz& r, int64_t kc, double* outU, double* outV);
+  double cgs2_right_host(int64_t ncols);  // test hook
+  int64_t host_syncs = 0;
+  Rng rng;
+
+ private:
+  enum Side { kLeft = 0, kRight = 1 };
+  DevOp* op_;
+  Context* ctx_;
+  int64_t m_, n_, cap_, j_ = 0;
+  std::vector<double*> U_, V_, U2_, V2_, w_, z_, cbuf_;
+  std::vector<double> B_, coupling_, mu_, nu_, mu_next_, nu_next_;
+  bool right_exhausted_ = false;
+
+  double& B(int64_t i, int64_t c) { return B_[i + c * cap_]; }
+  double Bc(int64_t i, int64_t c) const { return B_[i + c * cap_]; }
+  int64_t len(Side s, int i) const { return s == kLeft ? op_->rows(i) : n_; }
+  const std::vector<double*>& basis(Side s) const { return s == kLeft ? U_ : V_; }
+  int64_t ld(Side s, int i) const { return s == kLeft ? op_->rows(i) : n_; }
+  void read(int64_t count);  // D2H shard-0 dres[0..count) -> hres, sync
+  double cgs2(Side side, int64_t ncols, const std::vector<double*>& vec);
+  bool partial_reorth_update(Side side, const std::vector<double*>& cand, double cand_coeff,
+                             const Options& o, double norm_scale);
+  void upload_small(const std::vector<double>& W, std::vector<double*>& dst);
+  std::vector<double*> tmp_small_;
+  int64_t tmp_cap_ = 0;
+  double* pinned_ = nullptr;
+  int64_t pinned_cap_ = 0;
+  void host_to_all(const double* h, int64_t count, std::vector<double*>& dst);
+};
+
+struct SvdlOutput {
+  std::vector<double> singvals, U, V, err;
+  std::vector<int32_t> converged;
+  int64_t count = 0, mvps = 0, steps = 0;
+  int restarts = 0, reorth_count = 0, deflations = 0;
+  bool all_converged = false;
+  double wall_seconds = 0.0, device_seconds = 0.0;
+  int64_t host_syncs = 0;
+  std::vector<double> ritz_history, err_history;
+  int64_t history_len = 0;
+};
+SvdlOutput svdl(DevOp* op, const Options& o);
+
+}  // namespace gkb

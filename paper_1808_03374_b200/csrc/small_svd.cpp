@@ -1,0 +1,112 @@
+// svd_small (small_svd.cpp:14-28 of the reference): the projected problem
+// stays on the host (BASELINE north star item 3). SPEC.md's design decision
+// names one-sided Jacobi "for accuracy on small projected matrices"; this is
+// Hestenes' cyclic method with accumulated right rotations, singular values
+// sorted descending, and an orthonormal completion for numerically null
+// directions so both factors always have orthonormal columns.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <numeric>
+#include <vector>
+
+#include "host.hpp"
+
+namespace gkb {
+
+namespace {
+
+// A (r x c, r >= c) -> U (r x c), s (c), V (c x c)
+void jacobi_tall(const double* M, int64_t r, int64_t c, double* U, double* s, double* V) {
+  std::vector<double> A(M, M + r * c), R((size_t)(c * c), 0.0);
+  for (int64_t i = 0; i < c; ++i) R[i + i * c] = 1.0;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    bool rotated = false;
+    for (int64_t p = 0; p + 1 < c; ++p) {
+      for (int64_t q = p + 1; q < c; ++q) {
+        double* ap = A.data() + p * r;
+        double* aq = A.data() + q * r;
+        double alpha = 0.0, beta = 0.0, gamma = 0.0;
+        for (int64_t i = 0; i < r; ++i) {
+          alpha += ap[i] * ap[i];
+          beta += aq[i] * aq[i];
+          gamma += ap[i] * aq[i];
+        }
+        if (gamma == 0.0 || std::fabs(gamma) <= DBL_EPSILON * std::sqrt(alpha) * std::sqrt(beta))
+          continue;
+        rotated = true;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::hypot(1.0, zeta));
+        const double cs = 1.0 / std::sqrt(1.0 + t * t);
+        const double sn = cs * t;
+        for (int64_t i = 0; i < r; ++i) {
+          const double x = ap[i], y = aq[i];
+          ap[i] = cs * x - sn * y;
+          aq[i] = sn * x + cs * y;
+        }
+        double* rp = R.data() + p * c;
+        double* rq = R.data() + q * c;
+        for (int64_t i = 0; i < c; ++i) {
+          const double x = rp[i], y = rq[i];
+          rp[i] = cs * x - sn * y;
+          rq[i] = sn * x + cs * y;
+        }
+      }
+    }
+    if (!rotated) break;
+  }
+  std::vector<double> sv((size_t)c);
+  for (int64_t i = 0; i < c; ++i) {
+    double t = 0.0;
+    for (int64_t k = 0; k < r; ++k) t += A[i * r + k] * A[i * r + k];
+    sv[i] = std::sqrt(t);
+  }
+  std::vector<int64_t> order((size_t)c);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sv[a] > sv[b]; });
+  const double smax = c > 0 ? sv[order[0]] : 0.0;
+  const double zero_tol = smax * DBL_EPSILON * (double)std::max(r, c);
+  for (int64_t i = 0; i < c; ++i) {
+    const int64_t src = order[i];
+    s[i] = sv[src];
+    std::copy(R.begin() + src * c, R.begin() + (src + 1) * c, V + i * c);
+    double* u = U + i * r;
+    if (sv[src] > zero_tol && sv[src] > 0.0) {
+      for (int64_t k = 0; k < r; ++k) u[k] = A[src * r + k] / sv[src];
+      continue;
+    }
+    for (int64_t e = 0; e < r; ++e) {
+      for (int64_t k = 0; k < r; ++k) u[k] = (k == e) ? 1.0 : 0.0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int64_t l = 0; l < i; ++l) {
+          const double* ul = U + l * r;
+          double d = 0.0;
+          for (int64_t k = 0; k < r; ++k) d += ul[k] * u[k];
+          for (int64_t k = 0; k < r; ++k) u[k] -= d * ul[k];
+        }
+      double nn = 0.0;
+      for (int64_t k = 0; k < r; ++k) nn += u[k] * u[k];
+      nn = std::sqrt(nn);
+      if (nn > 0.5) {
+        for (int64_t k = 0; k < r; ++k) u[k] /= nn;
+        break;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void svd_small(const double* M, int64_t r, int64_t c, double* U, double* s, double* V) {
+  if (r <= 0 || c <= 0) return;
+  if (r >= c) {
+    jacobi_tall(M, r, c, U, s, V);
+    return;
+  }
+  std::vector<double> T((size_t)(r * c));
+  for (int64_t i = 0; i < r; ++i)
+    for (int64_t j = 0; j < c; ++j) T[j + i * c] = M[i + j * r];
+  jacobi_tall(T.data(), c, r, V, s, U);
+}
+
+}  // namespace gkb

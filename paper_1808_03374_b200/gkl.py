@@ -1,0 +1,538 @@
+"""Host-side mirror of the reference's solver and operator API.
+
+Python twin of ``gkpca::GklOptions``, ``svdl``, ``LinearOperator`` /
+``DenseOperator`` and the ``LanczosFactorization`` step functions
+(/root/reference/proj/include/gkpca/gkl.hpp:17-196, linop.hpp:13-64), bound
+through the C ABI of libgkb.so. Same names, argument meaning and error
+behaviour (ValueError for std::invalid_argument, LogicError for
+std::logic_error), so the parity tests read like the reference's own tests.
+
+Orientation follows the reference: an operator is m x n with
+``apply(x) = X x`` and ``apply_adjoint(y) = X^T y``; a genotype operator is
+markers x samples (m = p SNPs, n individuals).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+__all__ = [
+    "ReorthMode", "RestartMode", "ScalingScheme", "GklOptions", "SvdlStats", "SvdlResult",
+    "Context", "LinearOperator", "DenseOperator", "GenotypeOperator", "LanczosFactorization",
+    "StepInfo", "StepStatus", "RitzSet", "svdl", "cgs2", "svd_small", "rng_uniform_symmetric",
+    "partition_rows", "marker_scaling", "error_metric_l1",
+]
+
+
+def _pd(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _f64(a, n: Optional[int] = None) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if n is not None and a.size != n:
+        raise ValueError(f"length mismatch: expected {n}, got {a.size}")
+    return a
+
+
+class ReorthMode(enum.IntEnum):  # gkl.hpp:12
+    kFull = 0
+    kPartial = 1
+
+
+class RestartMode(enum.IntEnum):  # gkl.hpp:13
+    kNone = 0
+    kThick = 1
+
+
+class ScalingScheme(enum.IntEnum):  # genio.hpp:58-62 (+ BASELINE's hwe)
+    kUnitVariance = 0
+    kBinomial = 1
+    kHwe = 2  # (g - 2f)/sqrt(2f(1-f)), BASELINE.json config standardization
+    kNone = 3
+
+
+class StepStatus(enum.IntEnum):  # gkl.hpp:111-116
+    kOk = 0
+    kBreakdownAlpha = 1
+    kBreakdownBeta = 2
+
+
+@dataclass
+class GklOptions:
+    """GklOptions (gkl.hpp:17-33); same field names and defaults."""
+    k: int = 10
+    tol: float = 1e-8
+    max_mvps: int = 1000000
+    reorth: ReorthMode = ReorthMode.kPartial
+    omega: float = 1e-8
+    one_sided: bool = False
+    restart: RestartMode = RestartMode.kNone
+    max_subspace: int = 40
+    keep: int = 20
+    seed: int = 0
+    record_history: bool = False
+    # 1: complete left omega recurrence (default); 0: gkl.cpp:127-136 as written
+    omega_recurrence: int = 1
+
+    def _c(self) -> _lib.gkb_gkl_options:
+        o = _lib.gkb_gkl_options()
+        o.k = int(self.k)
+        o.tol = float(self.tol)
+        o.max_mvps = int(self.max_mvps)
+        o.reorth = int(self.reorth)
+        o.omega = float(self.omega)
+        o.one_sided = int(bool(self.one_sided))
+        o.restart = int(self.restart)
+        o.max_subspace = int(self.max_subspace)
+        o.keep = int(self.keep)
+        o.seed = int(self.seed) & 0xFFFFFFFFFFFFFFFF
+        o.record_history = int(bool(self.record_history))
+        o.omega_recurrence = int(self.omega_recurrence)
+        return o
+
+    def validate(self, m: int, n: int) -> None:
+        """GklOptions::validate (gkl.cpp:53-73): raises ValueError."""
+        o = self._c()
+        check(lib.gkb_gkl_options_validate(C.byref(o), int(m), int(n)))
+
+
+@dataclass
+class SvdlStats:  # gkl.hpp:170-180
+    mvps: int = 0
+    steps: int = 0
+    restarts: int = 0
+    reorth_count: int = 0
+    deflations: int = 0
+    converged: bool = False
+    wall_seconds: float = 0.0
+    ritz_history: List[np.ndarray] = field(default_factory=list)
+    err_history: List[np.ndarray] = field(default_factory=list)
+    device_seconds: float = 0.0
+    host_syncs: int = 0
+
+
+@dataclass
+class SvdlResult:  # gkl.hpp:182-189
+    singvals: np.ndarray
+    U: np.ndarray
+    V: np.ndarray
+    err_estimates: np.ndarray
+    converged: np.ndarray
+    stats: SvdlStats
+
+
+class Context:
+    """Device context: shards + communicator (gkb_init / gkb_init_nccl)."""
+
+    def __init__(self, devices: Sequence[int] = (0,), *, nccl: Optional[tuple] = None):
+        self._h = C.c_void_p()
+        if nccl is not None:
+            device, uid, nranks, rank = nccl
+            buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
+            check(lib.gkb_init_nccl(int(device), buf, int(nranks), int(rank), C.byref(self._h)))
+        else:
+            devs = (C.c_int * len(devices))(*devices)
+            check(lib.gkb_init(len(devices), devs, C.byref(self._h)))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib.gkb_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def info(self):
+        a, b, c = C.c_int(), C.c_int(), C.c_int()
+        check(lib.gkb_ctx_info(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def synchronize(self):
+        check(lib.gkb_synchronize(self._h))
+
+    def close(self):
+        if self._h:
+            check(lib.gkb_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context((0,))
+    return _default_ctx
+
+
+class LinearOperator:
+    """LinearOperator (linop.hpp:13-39) backed by a device operator handle."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p):
+        self.ctx = ctx
+        self._h = handle
+        m, n = C.c_int64(), C.c_int64()
+        check(lib.gkb_op_shape(self._h, C.byref(m), C.byref(n)))
+        self._m, self._n = m.value, n.value
+
+    def rows(self) -> int:
+        return self._m
+
+    def cols(self) -> int:
+        return self._n
+
+    @property
+    def shape(self):
+        return (self._m, self._n)
+
+    def apply(self, x) -> np.ndarray:
+        """y = X x (linop.hpp:20-22); raises ValueError on length mismatch."""
+        x = _f64(x, self._n)
+        y = np.empty(self._m)
+        check(lib.gkb_op_apply(self._h, _pd(x), _pd(y)))
+        return y
+
+    def apply_adjoint(self, x) -> np.ndarray:
+        """y = X^T x (linop.hpp:24-26)."""
+        x = _f64(x, self._m)
+        y = np.empty(self._n)
+        check(lib.gkb_op_apply_adjoint(self._h, _pd(x), _pd(y)))
+        return y
+
+    def mvps(self) -> int:
+        return int(lib.gkb_op_mvps(self._h))
+
+    def bench(self, which: int, iters: int, flush_l2: bool = True):
+        ms, main_ms, launches = C.c_double(), C.c_double(), C.c_int()
+        check(lib.gkb_op_bench(self._h, int(which), int(iters), int(bool(flush_l2)), C.byref(ms),
+                               C.byref(main_ms), C.byref(launches)))
+        return ms.value, main_ms.value, launches.value
+
+    def close(self):
+        if self._h:
+            check(lib.gkb_op_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DenseOperator(LinearOperator):
+    """DenseOperator (linop.hpp:43-64) on the device (column-major copy)."""
+
+    def __init__(self, X, ctx: Optional[Context] = None):
+        ctx = ctx or default_context()
+        X = np.asfortranarray(np.asarray(X, dtype=np.float64))
+        if X.ndim != 2:
+            raise ValueError("DenseOperator: 2-D matrix required")
+        h = C.c_void_p()
+        check(lib.gkb_dense_create(ctx._h, X.ctypes.data_as(C.POINTER(C.c_double)), X.shape[0],
+                                   X.shape[1], C.byref(h)))
+        super().__init__(ctx, h)
+
+
+class GenotypeOperator(LinearOperator):
+    """Packed 2-bit genotype operator in HBM (p markers x n samples).
+
+    Entry (j, s) = (d_js - mu_j) * inv_s_j for an observed dosage, 0 for a
+    missing one: impute_mean + standardize (genio.cpp:124-185) applied
+    implicitly, never densified (load_matrix, gkpca.cpp:89-108, is replaced).
+    """
+
+    def __init__(self, ctx: Context, handle: C.c_void_p, p: int, n: int):
+        super().__init__(ctx, handle)
+        self.p, self.n = p, n
+
+    @classmethod
+    def from_bed_payload(cls, payload, p: int, n: int, ctx: Optional[Context] = None,
+                         scheme: Optional[ScalingScheme] = ScalingScheme.kHwe):
+        ctx = ctx or default_context()
+        buf = np.ascontiguousarray(np.frombuffer(payload, dtype=np.uint8)
+                                   if isinstance(payload, (bytes, bytearray, memoryview))
+                                   else np.asarray(payload, dtype=np.uint8))
+        stride = (n + 3) // 4
+        if buf.size != p * stride:
+            raise _lib.FormatError(
+                f"payload size mismatch (expected {p * stride} bytes, found {buf.size})")
+        h = C.c_void_p()
+        check(lib.gkb_geno_from_bed(ctx._h, buf.ctypes.data_as(C.POINTER(C.c_uint8)), p, n,
+                                    C.byref(h)))
+        op = cls(ctx, h, p, n)
+        if scheme is not None:
+            op.standardize(scheme)
+        return op
+
+    @classmethod
+    def from_synth(cls, spec, ctx: Optional[Context] = None,
+                   scheme: Optional[ScalingScheme] = ScalingScheme.kHwe):
+        """Genotypes generated on the device (see synth.py)."""
+        ctx = ctx or default_context()
+        cs, keep = spec.to_c()
+        h = C.c_void_p()
+        check(lib.gkb_geno_from_synth(ctx._h, C.byref(cs), C.byref(h)))
+        del keep
+        op = cls(ctx, h, spec.p, spec.n)
+        if scheme is not None:
+            op.standardize(scheme)
+        return op
+
+    def counts(self) -> np.ndarray:
+        """Per-marker [n0, n1, n2, nmissing] counted on the device."""
+        out = np.zeros((self.p, 4), dtype=np.int64)
+        check(lib.gkb_geno_counts(self._h, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out
+
+    def standardize(self, scheme: ScalingScheme) -> None:
+        check(lib.gkb_geno_standardize(self._h, int(scheme)))
+
+    def set_scaling(self, mu, inv_s) -> None:
+        mu, inv_s = _f64(mu, self.p), _f64(inv_s, self.p)
+        check(lib.gkb_geno_set_scaling(self._h, _pd(mu), _pd(inv_s)))
+
+    def scaling(self):
+        mu, inv_s = np.empty(self.p), np.empty(self.p)
+        check(lib.gkb_geno_get_scaling(self._h, _pd(mu), _pd(inv_s)))
+        return mu, inv_s
+
+    def read_bed(self, row0: int = 0, nrows: Optional[int] = None) -> np.ndarray:
+        nrows = self.p - row0 if nrows is None else nrows
+        out = np.empty(nrows * ((self.n + 3) // 4), dtype=np.uint8)
+        check(lib.gkb_geno_read_bed(self._h, row0, nrows, out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out
+
+    def info(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.gkb_geno_info(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"nmissing": a.value, "packed_bytes": b.value, "device_bytes": c.value}
+
+
+def svdl(op: LinearOperator, opts: GklOptions) -> SvdlResult:
+    """svdl (gkl.hpp:196, gkl.cpp:416-514)."""
+    o = opts._c()
+    res = C.POINTER(_lib.gkb_svdl_result)()
+    check(lib.gkb_svdl(op._h, C.byref(o), C.byref(res)))
+    try:
+        r = res.contents
+        cnt, m, n = r.count, r.m, r.n
+
+        def arr(p, k):
+            return np.ctypeslib.as_array(p, shape=(k,)).copy() if k > 0 else np.zeros(0)
+
+        singvals = arr(r.singvals, cnt)
+        U = arr(r.U, m * cnt).reshape((cnt, m)).T.copy() if cnt else np.zeros((m, 0))
+        V = arr(r.V, n * cnt).reshape((cnt, n)).T.copy() if cnt else np.zeros((n, 0))
+        err = arr(r.err_estimates, cnt)
+        conv = (np.ctypeslib.as_array(r.converged, shape=(cnt,)).astype(bool).copy()
+                if cnt else np.zeros(0, dtype=bool))
+        st = SvdlStats(mvps=r.mvps, steps=r.steps, restarts=r.restarts,
+                       reorth_count=r.reorth_count, deflations=r.deflations,
+                       converged=bool(r.all_converged), wall_seconds=r.wall_seconds,
+                       device_seconds=r.device_seconds, host_syncs=r.host_syncs)
+        if r.history_len > 0:
+            k = int(opts.k)
+            h = arr(r.ritz_history, r.history_len * k).reshape(r.history_len, k)
+            e = arr(r.err_history, r.history_len * k).reshape(r.history_len, k)
+            st.ritz_history = [row[~np.isnan(row)] for row in h]
+            st.err_history = [row[~np.isnan(row)] for row in e]
+        return SvdlResult(singvals, U, V, err, conv, st)
+    finally:
+        check(lib.gkb_svdl_result_free(res))
+
+
+@dataclass
+class StepInfo:  # gkl.hpp:118-125
+    status: StepStatus
+    reorthogonalized_left: bool
+    reorthogonalized_right: bool
+    alpha: float
+    beta: float
+
+
+@dataclass
+class RitzSet:  # gkl.hpp:39-46
+    values: np.ndarray
+    left_coeffs: np.ndarray
+    right_coeffs: np.ndarray
+    err_estimates: np.ndarray
+    err_crude: np.ndarray
+    converged: np.ndarray
+
+
+class LanczosFactorization:
+    """LanczosFactorization (gkl.hpp:59-109) with device-resident bases.
+
+    The Rng used for deflation vectors is owned here (seed ``rng_seed``),
+    standing in for the ``Rng&`` argument of bidiag_step.
+    """
+
+    def __init__(self, op: LinearOperator, capacity: int, start, rng_seed: int = 1):
+        start = _f64(start, op.cols())
+        self.op = op
+        self._h = C.c_void_p()
+        check(lib.gkb_lanczos_create(op._h, int(capacity), _pd(start), int(rng_seed),
+                                     C.byref(self._h)))
+
+    def _info(self):
+        s, c, r = C.c_int64(), C.c_int64(), C.c_int()
+        check(lib.gkb_lanczos_info(self._h, C.byref(s), C.byref(c), C.byref(r)))
+        return s.value, c.value, bool(r.value)
+
+    def rows(self):
+        return self.op.rows()
+
+    def cols(self):
+        return self.op.cols()
+
+    def steps(self) -> int:
+        return self._info()[0]
+
+    def capacity(self) -> int:
+        return self._info()[1]
+
+    def right_exhausted(self) -> bool:
+        return self._info()[2]
+
+    def _get(self):
+        j = self.steps()
+        m, n = self.rows(), self.cols()
+        U = np.empty(m * j)
+        V = np.empty(n * (j + 1))
+        B = np.empty(j * j)
+        cp = np.empty(j)
+        ol = np.empty(j)
+        orr = np.empty(j + 1)
+        check(lib.gkb_lanczos_get(self._h, _pd(U), _pd(V), _pd(B), _pd(cp), _pd(ol), _pd(orr)))
+        return (U.reshape(j, m).T, V.reshape(j + 1, n).T, B.reshape(j, j).T, cp, ol, orr)
+
+    def left_basis(self):
+        return self._get()[0]
+
+    def right_basis(self):
+        return self._get()[1]
+
+    def projected(self):
+        return self._get()[2]
+
+    def residual_coupling(self):
+        return self._get()[3]
+
+    def omega_left(self):
+        return self._get()[4]
+
+    def omega_right(self):
+        return self._get()[5]
+
+    def alphas(self):
+        return np.diag(self.projected()).copy()
+
+    def betas(self):  # gkl.cpp:100-106
+        B = self.projected()
+        j = B.shape[0]
+        out = np.empty(j)
+        for i in range(j - 1):
+            out[i] = B[i, i + 1]
+        if j:
+            out[j - 1] = np.linalg.norm(self.residual_coupling())
+        return out
+
+    def bidiag_step(self, opts: GklOptions, norm_scale: float) -> StepInfo:
+        o = opts._c()
+        st, rl, rr = C.c_int(), C.c_int(), C.c_int()
+        a, b = C.c_double(), C.c_double()
+        check(lib.gkb_bidiag_step(self._h, C.byref(o), float(norm_scale), C.byref(st),
+                                  C.byref(rl), C.byref(rr), C.byref(a), C.byref(b)))
+        return StepInfo(StepStatus(st.value), bool(rl.value), bool(rr.value), a.value, b.value)
+
+    def ritz_extract(self, tol: float) -> RitzSet:
+        j = self.steps()
+        vals, wl, wr = np.empty(j), np.empty(j * j), np.empty(j * j)
+        err, crude = np.empty(j), np.empty(j)
+        conv = np.empty(j, dtype=np.int32)
+        check(lib.gkb_ritz_extract(self._h, float(tol), _pd(vals), _pd(wl), _pd(wr), _pd(err),
+                                   _pd(crude), conv.ctypes.data_as(C.POINTER(C.c_int32))))
+        return RitzSet(vals, wl.reshape(j, j).T, wr.reshape(j, j).T, err, crude, conv.astype(bool))
+
+    def thick_restart(self, keep: int) -> None:
+        check(lib.gkb_thick_restart(self._h, int(keep)))
+
+    def compress_exhausted(self) -> None:
+        check(lib.gkb_compress_exhausted(self._h))
+
+    def close(self):
+        if self._h:
+            check(lib.gkb_lanczos_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def error_metric_l1(ritz: RitzSet, k: int) -> float:  # gkl.cpp:411-414
+    return float(np.sum(ritz.err_crude[: min(k, ritz.err_crude.size)]))
+
+
+def cgs2(basis, v, coeffs=None, ctx: Optional[Context] = None):
+    """cgs2 (orth.hpp:19-44) on the device; returns (norm_after, v)."""
+    ctx = ctx or default_context()
+    Q = np.asfortranarray(np.asarray(basis, dtype=np.float64))
+    v = _f64(v).copy()
+    if Q.ndim != 2 or Q.shape[0] != v.size:
+        raise ValueError("cgs2: basis rows must match the vector length")
+    cf = np.zeros(Q.shape[1]) if coeffs is None else _f64(coeffs, Q.shape[1])
+    na = C.c_double()
+    check(lib.gkb_cgs2(ctx._h, Q.ctypes.data_as(C.POINTER(C.c_double)), Q.shape[0], Q.shape[1],
+                       _pd(v), _pd(cf), C.byref(na)))
+    if coeffs is not None:
+        coeffs[...] = cf
+    return na.value, v
+
+
+def svd_small(M):
+    """svd_small (small_svd.cpp:14-28): (U, s, V) with s descending."""
+    M = np.asfortranarray(np.asarray(M, dtype=np.float64))
+    r, c = M.shape
+    k = min(r, c)
+    U, s, V = np.empty(r * k), np.empty(k), np.empty(c * k)
+    check(lib.gkb_svd_small(M.ctypes.data_as(C.POINTER(C.c_double)), r, c, _pd(U), _pd(s), _pd(V)))
+    return U.reshape(k, r).T, s, V.reshape(k, c).T
+
+
+def rng_uniform_symmetric(seed: int, n: int) -> np.ndarray:
+    """Rng(seed).uniform_symmetric() x n (rng.hpp:27; gkl.cpp:428-429)."""
+    out = np.empty(n)
+    check(lib.gkb_rng_fill_symmetric(int(seed) & 0xFFFFFFFFFFFFFFFF, n, _pd(out)))
+    return out
+
+
+def partition_rows(m: int, nparts: int) -> np.ndarray:
+    out = np.empty(nparts + 1, dtype=np.int64)
+    check(lib.gkb_partition_rows(int(m), int(nparts), out.ctypes.data_as(C.POINTER(C.c_int64))))
+    return out
+
+
+def marker_scaling(counts, n: int, scheme: ScalingScheme):
+    counts = np.ascontiguousarray(np.asarray(counts, dtype=np.int64).reshape(-1, 4))
+    p = counts.shape[0]
+    mu, inv_s = np.empty(p), np.empty(p)
+    check(lib.gkb_marker_scaling(counts.ctypes.data_as(C.POINTER(C.c_int64)), p, int(n),
+                                 int(scheme), _pd(mu), _pd(inv_s)))
+    return mu, inv_s

@@ -1,0 +1,138 @@
+"""Packed genotype operator on the B200 vs the CPU oracle (through the C ABI).
+
+Covers: layout round trip (.bed bytes back from HBM), device marker counts
+and (mu, 1/s) bit-exact against the oracle, K1 (apply, X x) and K2
+(apply_adjoint, X^T y) against the oracle's packed operator on ragged
+shapes, missing entries, all-missing and zero-variance markers, adjoint
+consistency (linop.cpp:30-39), sharded == unsharded, and the device
+generator's bytes == the CPU generator's bytes.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def random_payload(p, n, seed, missing=0.02, special_rows=True):
+    rng = np.random.default_rng(seed)
+    d = rng.integers(0, 3, size=(p, n)).astype(np.uint8)
+    d[rng.random((p, n)) < missing] = 3
+    if special_rows and p >= 4:
+        d[0, :] = 3                 # all missing
+        d[1, :] = 2                 # zero variance
+        d[2, :] = np.where(rng.random(n) < 0.5, 1, 3)  # one observed dosage + missing
+    from paper_1808_03374_b200 import genio
+    return genio.encode(d), d
+
+
+SHAPES = [(1, 1), (4, 16), (5, 17), (7, 3), (33, 100), (130, 257), (257, 1000), (1031, 2049),
+          (64, 4099)]
+
+
+@pytest.mark.parametrize("p,n", SHAPES)
+def test_layout_roundtrip_and_counts(gkb, orc, p, n):
+    payload, d = random_payload(p, n, seed=p * 1000 + n)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=None)
+    back = op.read_bed()
+    assert np.array_equal(back, payload)
+    assert np.array_equal(op.counts(), orc.marker_counts(payload, p, n))
+
+
+@pytest.mark.parametrize("scheme", [0, 1, 2, 3])
+def test_scaling_bit_exact(gkb, orc, scheme):
+    p, n = 300, 517
+    payload, _ = random_payload(p, n, seed=11)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme(scheme))
+    mu, inv_s = op.scaling()
+    mu_o, is_o = orc.marker_scaling(orc.marker_counts(payload, p, n), n, scheme)
+    assert np.array_equal(mu, mu_o)
+    assert np.array_equal(inv_s, is_o)
+
+
+@pytest.mark.parametrize("p,n", SHAPES)
+@pytest.mark.parametrize("missing", [0.0, 0.05])
+def test_apply_and_adjoint_vs_oracle(gkb, orc, p, n, missing):
+    payload, _ = random_payload(p, n, seed=7 + p + n, missing=missing)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
+    mu, inv_s = op.scaling()
+    ref = orc.GenoOracle(payload, p, n, mu, inv_s)
+    rng = np.random.default_rng(3)
+    for scale in (1.0, 1e-200, 1e150):
+        x = rng.standard_normal(n) * scale
+        y = rng.standard_normal(p) * scale
+        ya, yo = op.apply(x), ref.apply(x)
+        za, zo = op.apply_adjoint(y), ref.apply_adjoint(y)
+        # fp64 summation-order differences only (tolerance relative to the
+        # magnitude of the summed terms, ~ sqrt(n) * eps * |x|_inf * max|entry|)
+        assert np.max(np.abs(ya - yo)) <= 1e-12 * max(1e-300, np.max(np.abs(yo))) + \
+            1e-13 * scale * np.sqrt(n) * (np.max(inv_s) * 2.0 + 1.0)
+        assert np.max(np.abs(za - zo)) <= 1e-12 * max(1e-300, np.max(np.abs(zo))) + \
+            1e-13 * scale * np.sqrt(p) * (np.max(inv_s) * 2.0 + 1.0)
+
+
+def test_edge_rows_are_zero(gkb, orc):
+    p, n = 9, 50
+    payload, d = random_payload(p, n, seed=5)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kUnitVariance)
+    mu, inv_s = op.scaling()
+    assert inv_s[0] == 0.0 and mu[0] == 0.0     # all missing: mean 0, flagged
+    assert inv_s[1] == 0.0 and mu[1] == 2.0     # constant marker zeroed (genio.cpp:167-171)
+    assert inv_s[2] == 0.0 and mu[2] == 1.0
+    y = op.apply(np.ones(n))
+    assert y[0] == 0.0 and y[1] == 0.0 and y[2] == 0.0
+
+
+def test_adjoint_consistency(gkb):
+    p, n = 211, 389
+    payload, _ = random_payload(p, n, seed=9)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n)
+    rng = np.random.default_rng(1)
+    u, v = rng.standard_normal(p), rng.standard_normal(n)
+    mis = abs(u @ op.apply(v) - op.apply_adjoint(u) @ v) / (np.linalg.norm(u) * np.linalg.norm(v))
+    assert mis <= 1e-12
+
+
+@pytest.mark.parametrize("nshards", [2, 3, 5])
+def test_sharded_equals_unsharded(gkb, orc, nshards):
+    p, n = 1003, 777
+    payload, _ = random_payload(p, n, seed=21)
+    one = gkb.GenotypeOperator.from_bed_payload(payload, p, n)
+    ctx = gkb.Context([0] * nshards)
+    sh = gkb.GenotypeOperator.from_bed_payload(payload, p, n, ctx=ctx)
+    assert np.array_equal(sh.read_bed(), payload)
+    assert np.array_equal(sh.counts(), one.counts())
+    rng = np.random.default_rng(2)
+    x, y = rng.standard_normal(n), rng.standard_normal(p)
+    # apply is shard-local: identical bytes per row
+    assert np.array_equal(sh.apply(x), one.apply(x))
+    # adjoint sums shard partials: fp64 reassociation only
+    assert rel_err(sh.apply_adjoint(y), one.apply_adjoint(y)) <= 1e-13
+
+
+def test_mvp_counter(gkb):
+    payload, _ = random_payload(8, 40, seed=1)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, 8, 40)
+    op.apply(np.ones(40))
+    op.apply_adjoint(np.ones(8))
+    op.apply(np.ones(40))
+    assert op.mvps() == 3
+    with pytest.raises(ValueError):
+        op.apply(np.ones(8))
+
+
+def test_synth_bytes_match_cpu_generator(gkb, orc):
+    from paper_1808_03374_b200 import synth
+    for cfg in (1, 2, 3, 4):
+        spec = synth.config_spec(cfg, scale=0.02)
+        op = gkb.GenotypeOperator.from_synth(spec, scheme=None)
+        cpu = orc.synth_bed(spec)
+        assert np.array_equal(op.read_bed(), cpu), cfg
+
+
+def test_format_errors(gkb):
+    with pytest.raises(gkb.FormatError):
+        gkb.GenotypeOperator.from_bed_payload(np.zeros(10, np.uint8), 3, 16)
+    with pytest.raises(ValueError):
+        gkb.GenotypeOperator.from_bed_payload(np.zeros(0, np.uint8), 0, 16)
