@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -33,6 +34,8 @@ namespace {
 
 constexpr int kS = 1000;  // coefficient scale exponent (see header comment)
 constexpr int kThreads = 256;
+constexpr int kDepth = 4;  // 16-byte loads in flight per thread in the main loops
+constexpr int kSubQ = 64;  // SNP quads per pair-table sub-chunk in k2_main_h (8 KB of tables)
 
 __device__ __forceinline__ double fld(uint32_t w, int k) {
   return __hiloint2double(0, (int)(w & (3u << (2 * k))));
@@ -272,7 +275,37 @@ __global__ void k_layout_to_bed(const uint4* __restrict__ layA, int64_t P4, int6
 }
 
 // ---------------------------------------------------------------- K1 apply
-// grid (ceil(P4/256), ntiles). Thread = SNP quad q (4 SNPs), loops over the
+// One 16-byte chunk: 4 SNP words x 16 samples against the 16 (scaled) sample
+// coefficients of that word position.
+__device__ __forceinline__ void k1_word(const uint4 c, const double2* __restrict__ cf, double& a0,
+                                        double& a1, double& a2, double& a3) {
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const double2 xx = cf[kk];
+    a0 = fma(fld(c.x, 2 * kk), xx.x, a0);
+    a1 = fma(fld(c.y, 2 * kk), xx.x, a1);
+    a2 = fma(fld(c.z, 2 * kk), xx.x, a2);
+    a3 = fma(fld(c.w, 2 * kk), xx.x, a3);
+    a0 = fma(fld(c.x, 2 * kk + 1), xx.y, a0);
+    a1 = fma(fld(c.y, 2 * kk + 1), xx.y, a1);
+    a2 = fma(fld(c.z, 2 * kk + 1), xx.y, a2);
+    a3 = fma(fld(c.w, 2 * kk + 1), xx.y, a3);
+  }
+}
+
+// One 16-byte chunk of layout A: 4 SNP words x the lane's 16 samples.
+__device__ __forceinline__ void k2_quad(const uint4 c, const double2 ca, const double2 cb,
+                                        double (&acc)[16]) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = fma(fld(c.x, k), ca.x, acc[k]);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = fma(fld(c.y, k), ca.y, acc[k]);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = fma(fld(c.z, k), cb.x, acc[k]);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = fma(fld(c.w, k), cb.y, acc[k]);
+}
+// grid (ceil(P4/32), ntiles). Lane = SNP quad q (4 SNPs), loops over the
 // tile's word positions; lanes read 32 consecutive 16-byte chunks (512 B).
 __global__ void __launch_bounds__(kThreads) k1_main(const uint4* __restrict__ layB, int64_t P4,
                                                     int64_t W, const double* __restrict__ x,
@@ -304,34 +337,54 @@ __global__ void __launch_bounds__(kThreads) k1_main(const uint4* __restrict__ la
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) xsum[tile] = tsum;
 
-  const int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (q >= P4) return;
+  // Lane = SNP quad (32 consecutive quads per CTA, 512-B coalesced rows of
+  // layout B); warp w takes the w-th eighth of the tile's word positions, and
+  // the 8 warp partials are added in warp order through shared memory.
+  __shared__ double wsum[8][4][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * 32 + lane;
+  const int sub = (nw + 7) / 8;
+  const int wa = min(nw, warp * sub), we = min(nw, wa + sub);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  const uint4* src = layB + w0 * P4 + q;
-  uint4 cn = ld_stream(src);
-  for (int w = 0; w < nw; ++w) {
-    const uint4 c = cn;
-    if (w + 1 < nw) cn = ld_stream(src + (int64_t)(w + 1) * P4);
-    const double2* cf = xp2 + 8 * w;
+  if (q < P4 && wa < we) {
+    const uint4* src = layB + w0 * P4 + q;
+    const uint4 Z = make_uint4(0, 0, 0, 0);
+    // four 16-byte loads in flight per thread; each slot is refilled right
+    // after it is consumed (no dynamic indexing, no early exits)
+    uint4 c0 = ld_stream(src + (int64_t)wa * P4);
+    uint4 c1 = wa + 1 < we ? ld_stream(src + (int64_t)(wa + 1) * P4) : Z;
+    uint4 c2 = wa + 2 < we ? ld_stream(src + (int64_t)(wa + 2) * P4) : Z;
+    uint4 c3 = wa + 3 < we ? ld_stream(src + (int64_t)(wa + 3) * P4) : Z;
+    int w = wa;
+    for (; w + 4 <= we; w += 4) {
+      k1_word(c0, xp2 + 8 * w, a0, a1, a2, a3);
+      c0 = w + 4 < we ? ld_stream(src + (int64_t)(w + 4) * P4) : Z;
+      k1_word(c1, xp2 + 8 * (w + 1), a0, a1, a2, a3);
+      c1 = w + 5 < we ? ld_stream(src + (int64_t)(w + 5) * P4) : Z;
+      k1_word(c2, xp2 + 8 * (w + 2), a0, a1, a2, a3);
+      c2 = w + 6 < we ? ld_stream(src + (int64_t)(w + 6) * P4) : Z;
+      k1_word(c3, xp2 + 8 * (w + 3), a0, a1, a2, a3);
+      c3 = w + 7 < we ? ld_stream(src + (int64_t)(w + 7) * P4) : Z;
+    }
+    if (w < we) k1_word(c0, xp2 + 8 * w, a0, a1, a2, a3);
+    if (w + 1 < we) k1_word(c1, xp2 + 8 * (w + 1), a0, a1, a2, a3);
+    if (w + 2 < we) k1_word(c2, xp2 + 8 * (w + 2), a0, a1, a2, a3);
+  }
+  wsum[warp][0][lane] = a0;
+  wsum[warp][1][lane] = a1;
+  wsum[warp][2][lane] = a2;
+  wsum[warp][3][lane] = a3;
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    const int i = threadIdx.x >> 5;  // SNP within the quad
+    const int64_t qq = (int64_t)blockIdx.x * 32 + lane;
+    if (qq < P4) {
+      double t = 0.0;
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const double2 xx = cf[kk];
-      a0 = fma(fld(c.x, 2 * kk), xx.x, a0);
-      a1 = fma(fld(c.y, 2 * kk), xx.x, a1);
-      a2 = fma(fld(c.z, 2 * kk), xx.x, a2);
-      a3 = fma(fld(c.w, 2 * kk), xx.x, a3);
-      a0 = fma(fld(c.x, 2 * kk + 1), xx.y, a0);
-      a1 = fma(fld(c.y, 2 * kk + 1), xx.y, a1);
-      a2 = fma(fld(c.z, 2 * kk + 1), xx.y, a2);
-      a3 = fma(fld(c.w, 2 * kk + 1), xx.y, a3);
+      for (int w = 0; w < 8; ++w) t += wsum[w][i][lane];
+      ypart[(int64_t)tile * 4 * P4 + 4 * qq + i] = scalbn(t, 1074 - kS + E);
     }
   }
-  const int un = 1074 - kS + E;
-  double* out = ypart + (int64_t)tile * 4 * P4 + 4 * q;
-  out[0] = scalbn(a0, un);
-  out[1] = scalbn(a1, un);
-  out[2] = scalbn(a2, un);
-  out[3] = scalbn(a3, un);
 }
 
 // y_j = inv_s_j * (sum_t ypart - mu_j X_tot - (3 - mu_j) S_miss_j)
@@ -351,6 +404,7 @@ __global__ void k1_reduce(const double* __restrict__ ypart, const double* __rest
     double acc = 0.0, sm = 0.0;
     for (int t = lane; t < ntiles; t += 32) acc += ypart[(int64_t)t * 4 * P4 + j];
     if (row_ptr)
+#pragma unroll 4
       for (int64_t e = row_ptr[j] + lane; e < row_ptr[j + 1]; e += 32) sm += x[row_idx[e]];
     for (int o = 16; o > 0; o >>= 1) {
       acc += __shfl_down_sync(0xffffffffu, acc, o);
@@ -364,10 +418,10 @@ __global__ void k1_reduce(const double* __restrict__ ypart, const double* __rest
 }
 
 // ---------------------------------------------------------------- K2 adjoint
-// grid (ceil(W/256), nchunks). Thread = word position w (16 samples, 16
+// grid (ceil(W/32), nchunks). Lane = word position w (16 samples, 16
 // accumulators); loops over the chunk's SNP quads; lanes read 32 consecutive
 // 16-byte chunks of one quad row (512 B).
-__global__ void __launch_bounds__(kThreads) k2_main(const uint4* __restrict__ layA, int64_t P4,
+__global__ void __launch_bounds__(kThreads, 4) k2_main(const uint4* __restrict__ layA, int64_t P4,
                                                     int64_t W, const double* __restrict__ y,
                                                     const double* __restrict__ mu,
                                                     const double* __restrict__ inv_s,
@@ -402,31 +456,191 @@ __global__ void __launch_bounds__(kThreads) k2_main(const uint4* __restrict__ la
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) kpart[chunk] = ksum;
 
-  const int64_t w = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (w >= W) return;
+  // Lane = word position (32 consecutive words, 512-B coalesced rows of
+  // layout A); warp w takes the w-th eighth of the chunk's SNP quads; the 8
+  // warp partials are added in warp order through shared memory.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t w = (int64_t)blockIdx.x * 32 + lane;
+  const int sub = (nq + 7) / 8;
+  const int qa = min(nq, warp * sub), qe = min(nq, qa + sub);
   double acc[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.0;
-  const uint4* src = layA + q0 * W + w;
-  uint4 cn = ld_stream(src);
-  for (int qq = 0; qq < nq; ++qq) {
-    const uint4 c = cn;
-    if (qq + 1 < nq) cn = ld_stream(src + (int64_t)(qq + 1) * W);
-    const double2 ca = cs2[2 * qq], cb = cs2[2 * qq + 1];
+  if (w < W && qa < qe) {
+    const uint4* src = layA + q0 * W + w;
+    const uint4 Z = make_uint4(0, 0, 0, 0);
+    uint4 c0 = ld_stream(src + (int64_t)qa * W);
+    uint4 c1 = qa + 1 < qe ? ld_stream(src + (int64_t)(qa + 1) * W) : Z;
+    uint4 c2 = qa + 2 < qe ? ld_stream(src + (int64_t)(qa + 2) * W) : Z;
+    uint4 c3 = qa + 3 < qe ? ld_stream(src + (int64_t)(qa + 3) * W) : Z;
+    int qq = qa;
+    for (; qq + 4 <= qe; qq += 4) {
+      k2_quad(c0, cs2[2 * qq], cs2[2 * qq + 1], acc);
+      c0 = qq + 4 < qe ? ld_stream(src + (int64_t)(qq + 4) * W) : Z;
+      k2_quad(c1, cs2[2 * qq + 2], cs2[2 * qq + 3], acc);
+      c1 = qq + 5 < qe ? ld_stream(src + (int64_t)(qq + 5) * W) : Z;
+      k2_quad(c2, cs2[2 * qq + 4], cs2[2 * qq + 5], acc);
+      c2 = qq + 6 < qe ? ld_stream(src + (int64_t)(qq + 6) * W) : Z;
+      k2_quad(c3, cs2[2 * qq + 6], cs2[2 * qq + 7], acc);
+      c3 = qq + 7 < qe ? ld_stream(src + (int64_t)(qq + 7) * W) : Z;
+    }
+    if (qq < qe) k2_quad(c0, cs2[2 * qq], cs2[2 * qq + 1], acc);
+    if (qq + 1 < qe) k2_quad(c1, cs2[2 * qq + 2], cs2[2 * qq + 3], acc);
+    if (qq + 2 < qe) k2_quad(c2, cs2[2 * qq + 4], cs2[2 * qq + 5], acc);
+  }
+  // cross-warp combine in two halves of 8 fields (16 KB of the coefficient
+  // region, which is sized >= 2048 doubles)
+  double* part = cs;
+  const int k_out = threadIdx.x >> 5;  // field within the half, 0..7
+  const int64_t w_out = (int64_t)blockIdx.x * 32 + lane;
+  double* out = zpart + (int64_t)chunk * 16 * W;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      acc[k] = fma(fld(c.x, k), ca.x, acc[k]);
-      acc[k] = fma(fld(c.y, k), ca.y, acc[k]);
-      acc[k] = fma(fld(c.z, k), cb.x, acc[k]);
-      acc[k] = fma(fld(c.w, k), cb.y, acc[k]);
+  for (int h = 0; h < 2; ++h) {
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) part[(warp * 8 + k) * 32 + lane] = acc[8 * h + k];
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) t += part[(ww * 8 + k_out) * 32 + lane];
+    const int field = 8 * h + k_out;
+    if (w_out < W) out[16 * w_out + field] = scalbn(t, 1074 - kS + E - 2 * field);
+  }
+}
+
+// ---------------------------------------------------------------- K2 hybrid
+// Same contract as k2_main, but the work of every SNP quad is split across
+// two pipes: SNPs (4q, 4q+1) go through a 16-entry fp64 pair table in shared
+// memory -- T_q[r_a | r_b << 2] = v_a(r_a) + v_b(r_b), v_j(r) = c_j (r - mu_j)
+// for r <= 2 and 0 for a missing entry -- so each lookup (one PRMT address
+// op, one LDS.64, one DADD) covers two genotypes on the LSU pipe; SNPs
+// (4q+2, 4q+3) go through the denormal-injection DFMA path on the FP64 pipe.
+// Table-path SNPs need no missing correction (cmiss = 0) and no mu term.
+// Lane = half a word (8 samples): lanes 2i, 2i+1 share word w0 + i.
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));  // tables are read-only after setup
+  return v;
+}
+
+__global__ void __launch_bounds__(kThreads) k2_main_h(const uint4* __restrict__ layA, int64_t P4,
+                                                      int64_t W, const double* __restrict__ y,
+                                                      const double* __restrict__ mu,
+                                                      const double* __restrict__ inv_s,
+                                                      int64_t p_loc, int qc,
+                                                      double* __restrict__ zpart,
+                                                      double* __restrict__ kpart,
+                                                      double* __restrict__ cmiss) {
+  extern __shared__ __align__(16) double sm_raw[];
+  // tables start on a 256-byte boundary: table qq is at byte (qq>>1)*256 + (qq&1)*128
+  const uint32_t raw_addr = (uint32_t)__cvta_generic_to_shared(sm_raw);
+  double* sm2 = sm_raw + (((raw_addr + 255u) & ~255u) - raw_addr) / 8;
+  double* tabs = sm2;                                            // kSubQ * 16 (128 B per quad)
+  double2* csd = reinterpret_cast<double2*>(sm2 + 16 * kSubQ);   // qc scaled (c_{4q+2}, c_{4q+3})
+  __shared__ double red[33];
+  __shared__ int redi[33];
+  const int chunk = blockIdx.y;
+  const int64_t q0 = (int64_t)chunk * qc;
+  const int64_t q1 = min(P4, q0 + qc);
+  const int nq = (int)(q1 - q0);
+
+  // DFMA-path coefficients (SNPs 4q+2, 4q+3) of the whole chunk: exponent,
+  // mu term and missing corrections
+  int emax = -1100;
+  double kp = 0.0;
+  for (int t = threadIdx.x; t < 2 * nq; t += kThreads) {
+    const int64_t j = 4 * (q0 + (t >> 1)) + 2 + (t & 1);
+    const double c = j < p_loc ? inv_s[j] * y[j] : 0.0;
+    emax = max(emax, exp_of(c));
+    if (j < p_loc) kp += c * mu[j];
+    reinterpret_cast<double*>(csd)[t] = c;
+  }
+  if (cmiss && blockIdx.x == 0)
+    for (int t = threadIdx.x; t < 4 * nq; t += kThreads) {
+      const int64_t j = 4 * q0 + t;
+      if (j < p_loc) cmiss[j] = (t & 2) ? inv_s[j] * y[j] * (3.0 - mu[j]) : 0.0;
+    }
+  const int E = block_max_int(emax, redi);
+  const double ksum = block_sum(kp, red);
+  for (int t = threadIdx.x; t < 2 * nq; t += kThreads)
+    reinterpret_cast<double*>(csd)[t] = scalbn(reinterpret_cast<double*>(csd)[t], kS - E);
+  if (blockIdx.x == 0 && threadIdx.x == 0) kpart[chunk] = ksum;
+
+  // Warps split the CTA's 128 word positions (16 per warp, two lanes per
+  // word); every warp walks all quads of the chunk, kSubQ at a time, against
+  // pair tables shared by the whole CTA.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int half = lane & 1;
+  const int64_t w = (int64_t)blockIdx.x * 128 + warp * 16 + (lane >> 1);
+  const bool active = w < W;
+  const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tabs);
+  const uint32_t sel_h = half ? 0x00007632u : 0x00005410u;  // bytes (2h, 2h+1) of te | to
+  const int sh = 16 * half;
+  const uint4* src = layA + q0 * W + (active ? w : 0);
+  double at[8], ad[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    at[k] = 0.0;
+    ad[k] = 0.0;
+  }
+  for (int s0 = 0; s0 < nq; s0 += kSubQ) {
+    const int s1 = min(nq, s0 + kSubQ);
+    __syncthreads();  // previous sub-chunk's tables fully consumed (and csd visible)
+    // pair tables for SNPs (4q, 4q+1) of quads [s0, s1)
+    for (int e = threadIdx.x; e < 16 * (s1 - s0); e += kThreads) {
+      const int qq = e >> 4, n = e & 15, ra = n & 3, rb = n >> 2;
+      const int64_t ja = 4 * (q0 + s0 + qq), jb = ja + 1;
+      double va = 0.0, vb = 0.0;
+      if (ra != 3 && ja < p_loc) va = inv_s[ja] * y[ja] * ((double)ra - mu[ja]);
+      if (rb != 3 && jb < p_loc) vb = inv_s[jb] * y[jb] * ((double)rb - mu[jb]);
+      tabs[e] = va + vb;
+    }
+    __syncthreads();
+    if (!active) continue;
+    const uint4 Z = make_uint4(0, 0, 0, 0);
+    uint4 n0 = ld_stream(src + (int64_t)s0 * W);
+    uint4 n1 = s0 + 1 < s1 ? ld_stream(src + (int64_t)(s0 + 1) * W) : Z;
+    uint4 n2 = s0 + 2 < s1 ? ld_stream(src + (int64_t)(s0 + 2) * W) : Z;
+    for (int qq = s0; qq < s1; ++qq) {
+      const uint4 c = n0;
+      n0 = n1;
+      n1 = n2;
+      n2 = qq + 3 < s1 ? ld_stream(src + (int64_t)(qq + 3) * W) : Z;
+      // ---- table path: nibble (r_x | r_y << 2) per sample
+      const uint32_t te = (c.x & 0x33333333u) | ((c.y << 2) & 0xCCCCCCCCu);  // fields 0,2,..,14
+      const uint32_t to = ((c.x >> 2) & 0x33333333u) | (c.y & 0xCCCCCCCCu);  // fields 1,3,..,15
+      // this lane's 8 fields: nibbles n0..n3 = fields 8h+{0,2,4,6}, n4..n7 = 8h+{1,3,5,7}
+      const uint32_t tt = __byte_perm(te, to, sel_h);
+      const uint32_t par = (qq & 1) ? 0x80808080u : 0u;
+      const uint32_t u0 = ((tt << 3) & 0x78787878u) | par;  // n0,n2,n4,n6 -> fields 0,4,1,5
+      const uint32_t u1 = ((tt >> 1) & 0x78787878u) | par;  // n1,n3,n5,n7 -> fields 2,6,3,7
+      const uint32_t base = tab_addr + (uint32_t)((qq - s0) >> 1) * 256u;
+      // address = table base (bytes 1..3, byte 0 == 0) with byte 0 = nibble*8 | parity*128
+      at[0] += lds_f64(__byte_perm(u0, base, 0x7650u));
+      at[4] += lds_f64(__byte_perm(u0, base, 0x7651u));
+      at[1] += lds_f64(__byte_perm(u0, base, 0x7652u));
+      at[5] += lds_f64(__byte_perm(u0, base, 0x7653u));
+      at[2] += lds_f64(__byte_perm(u1, base, 0x7650u));
+      at[6] += lds_f64(__byte_perm(u1, base, 0x7651u));
+      at[3] += lds_f64(__byte_perm(u1, base, 0x7652u));
+      at[7] += lds_f64(__byte_perm(u1, base, 0x7653u));
+      // ---- DFMA path for SNPs 4q+2, 4q+3 on this lane's 8 fields
+      const double2 cc = csd[qq];
+      const uint32_t zz = c.z >> sh, ww = c.w >> sh;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ad[k] = fma(fld(zz, k), cc.x, ad[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ad[k] = fma(fld(ww, k), cc.y, ad[k]);
     }
   }
-  double* out = zpart + (int64_t)chunk * 16 * W + 16 * w;
+  // lane's field f (0..7) = sample 16w + 8h + f: at[f] plain, ad[f] scaled by
+  // 2^(2f + kS - E - 1074)
+  if (active) {
+    double2* out = reinterpret_cast<double2*>(zpart + (int64_t)chunk * 16 * W + 16 * w + 8 * half);
 #pragma unroll
-  for (int k = 0; k < 16; k += 2) {
-    const double2 v = make_double2(scalbn(acc[k], 1074 - kS + E - 2 * k),
-                                   scalbn(acc[k + 1], 1074 - kS + E - 2 * (k + 1)));
-    reinterpret_cast<double2*>(out)[k / 2] = v;
+    for (int f = 0; f < 8; f += 2)
+      out[f / 2] = make_double2(at[f] + scalbn(ad[f], 1074 - kS + E - 2 * f),
+                                at[f + 1] + scalbn(ad[f + 1], 1074 - kS + E - 2 * (f + 1)));
   }
 }
 
@@ -451,6 +665,7 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ zpar
   const int64_t s = s0 + lane;
   double acc = 0.0;
   if (s < n)
+#pragma unroll 4
     for (int c = warp; c < nchunks; c += 8) acc += zpart[(int64_t)c * 16 * W + s];
   part[warp][lane] = acc;
   for (int t = 0; t < 4; ++t) {
@@ -458,6 +673,7 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ zpar
     const int64_t ss = s0 + li;
     double cs = 0.0;
     if (col_ptr && ss < n)
+#pragma unroll 4
       for (int64_t e = col_ptr[ss] + lane; e < col_ptr[ss + 1]; e += 32) cs += cmiss[col_idx[e]];
     for (int o = 16; o > 0; o >>= 1) cs += __shfl_down_sync(0xffffffffu, cs, o);
     if (lane == 0) corr[li] = cs;
@@ -528,12 +744,13 @@ void layout_to_bed(const uint4* layA, int64_t P4, int64_t W, int64_t n, int64_t 
 
 K1Plan k1_plan(int64_t W, int64_t P4) {
   K1Plan pl;
-  // A sample tile of 128 words (2048 samples): 16 KB of coefficients per CTA,
-  // partial traffic 8 B per SNP per tile (1/64 of the 512 packed bytes).
-  pl.tileW = (int)(W < 128 ? (W > 0 ? W : 1) : 128);
+  // CTA = 32 SNP quads x a sample tile of 256 words (4096 samples; 32 KB of
+  // coefficients), each warp 32 words. Partial traffic: 8 B per SNP per tile
+  // (1/128 of the 1 KB of packed bytes per SNP and tile).
+  pl.tileW = (int)(W < 256 ? (W > 0 ? W : 1) : 256);
   pl.ntiles = (int)((W + pl.tileW - 1) / pl.tileW);
   if (pl.ntiles < 1) pl.ntiles = 1;
-  pl.grid_x = (P4 + kThreads - 1) / kThreads;
+  pl.grid_x = (P4 + 31) / 32;
   if (pl.grid_x < 1) pl.grid_x = 1;
   pl.smem = (size_t)pl.tileW * 16 * sizeof(double);
   return pl;
@@ -541,18 +758,41 @@ K1Plan k1_plan(int64_t W, int64_t P4) {
 
 K2Plan k2_plan(int64_t W, int64_t P4) {
   K2Plan pl;
-  pl.grid_x = (W + kThreads - 1) / kThreads;
+  // GKB_K2=hybrid selects the pair-table + DFMA split (k2_main_h); measured
+  // slower than the DFMA-only kernel so far, so off by default.
+  const char* env = getenv("GKB_K2");
+  pl.hybrid = env && env[0] == 'h';
+  if (pl.hybrid) {
+    // CTA = 128 word positions (2048 samples; 8 warps x 16 words, two lanes
+    // per word) x a chunk of up to 512 SNP quads walked in sub-chunks of
+    // kSubQ quads (8 KB of pair tables). The chunk shrinks (down to kSubQ)
+    // until there are >= 4 CTAs per SM; partial traffic is 8 B per sample per
+    // chunk (1/64 of the packed bytes at 512 quads).
+    pl.grid_x = (W + 127) / 128;
+    if (pl.grid_x < 1) pl.grid_x = 1;
+    int64_t want = (148 * 4 + pl.grid_x - 1) / pl.grid_x;
+    int64_t qc = (P4 + want - 1) / (want > 0 ? want : 1);
+    qc = ((qc + kSubQ - 1) / kSubQ) * kSubQ;
+    if (qc > 512) qc = 512;
+    if (qc < kSubQ) qc = kSubQ;
+    pl.qc = (int)qc;
+    pl.nchunks = (int)((P4 + qc - 1) / qc);
+    if (pl.nchunks < 1) pl.nchunks = 1;
+    pl.smem = (size_t)(16 * kSubQ + 2 * qc) * sizeof(double) + 256;
+    return pl;
+  }
+  // CTA = 32 word positions (512 samples) x a chunk of up to 512 SNP quads
+  // (2048 SNPs), each warp 64 quads. Partial traffic: 8 B per sample per
+  // chunk (1/64 of the 512 packed bytes per sample and chunk).
+  pl.grid_x = (W + 31) / 32;
   if (pl.grid_x < 1) pl.grid_x = 1;
-  // Aim for >= ~4 CTAs per SM (148 SMs) while keeping chunks >= 64 quads.
-  int64_t want_chunks = (148 * 4 + pl.grid_x - 1) / pl.grid_x;
-  int64_t qc = (P4 + want_chunks - 1) / (want_chunks > 0 ? want_chunks : 1);
-  if (qc < 64) qc = 64;
-  if (qc > 1024) qc = 1024;
-  if (qc > P4) qc = P4 > 0 ? P4 : 1;
+  int64_t qc = 512;
+  const int64_t p4r = ((P4 + 7) / 8) * 8;
+  if (qc > p4r) qc = p4r > 0 ? p4r : 8;
   pl.qc = (int)qc;
   pl.nchunks = (int)((P4 + qc - 1) / qc);
   if (pl.nchunks < 1) pl.nchunks = 1;
-  pl.smem = (size_t)qc * 4 * sizeof(double);
+  pl.smem = (size_t)(qc * 4 > 2048 ? qc * 4 : 2048) * sizeof(double);
   return pl;
 }
 
@@ -574,8 +814,12 @@ void k1_apply(const GenoView& g, const K1Plan& pl, const double* x, double* ypar
 void k2_main_only(const GenoView& g, const K2Plan& pl, const double* y, double* zpart,
                   double* kpart, cudaStream_t s) {
   dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nchunks);
-  k2_main<<<grid, kThreads, pl.smem, s>>>(g.layA, g.P4, g.W, y, g.mu, g.inv_s, g.p_loc, pl.qc,
-                                          zpart, kpart, g.nmissing ? g.cmiss : nullptr);
+  if (pl.hybrid)
+    k2_main_h<<<grid, kThreads, pl.smem, s>>>(g.layA, g.P4, g.W, y, g.mu, g.inv_s, g.p_loc, pl.qc,
+                                              zpart, kpart, g.nmissing ? g.cmiss : nullptr);
+  else
+    k2_main<<<grid, kThreads, pl.smem, s>>>(g.layA, g.P4, g.W, y, g.mu, g.inv_s, g.p_loc, pl.qc,
+                                            zpart, kpart, g.nmissing ? g.cmiss : nullptr);
 }
 
 void k2_adjoint(const GenoView& g, const K2Plan& pl, const double* y, double* zpart, double* kpart,

@@ -67,6 +67,7 @@ struct K2Plan {
   int nchunks;
   int64_t grid_x;
   size_t smem;
+  int hybrid;    // 1: pair-table (LSU) + DFMA split (k2_main_h); 0: DFMA only (k2_main)
 };
 K2Plan k2_plan(int64_t W, int64_t P4);
 // K2 apply_adjoint (reference X^T*y, per-sample sum) over the local SNPs.
