@@ -403,9 +403,11 @@ __global__ void k1_reduce(const double* __restrict__ ypart, const double* __rest
   for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < p_loc; j += nwarps) {
     double acc = 0.0, sm = 0.0;
     for (int t = lane; t < ntiles; t += 32) acc += ypart[(int64_t)t * 4 * P4 + j];
-    if (row_ptr)
-#pragma unroll 4
-      for (int64_t e = row_ptr[j] + lane; e < row_ptr[j + 1]; e += 32) sm += x[row_idx[e]];
+    if (row_ptr) {
+      const int64_t e0 = row_ptr[j], e1 = row_ptr[j + 1];
+#pragma unroll 8
+      for (int64_t e = e0 + lane; e < e1; e += 32) sm += x[row_idx[e]];
+    }
     for (int o = 16; o > 0; o >>= 1) {
       acc += __shfl_down_sync(0xffffffffu, acc, o);
       sm += __shfl_down_sync(0xffffffffu, sm, o);
@@ -650,14 +652,18 @@ __global__ void __launch_bounds__(kThreads) k2_main_h(const uint4* __restrict__ 
 // with lanes on consecutive samples (coalesced), then the 8 partials are
 // added in warp order; each warp walks 4 samples' missing lists with lanes
 // striding the entries. Fixed trees -> deterministic.
-__global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ zpart,
-                                                 const double* __restrict__ kpart, int nchunks,
-                                                 int64_t W, int64_t n,
-                                                 const double* __restrict__ cmiss,
-                                                 const int64_t* __restrict__ col_ptr,
-                                                 const int32_t* __restrict__ col_idx,
-                                                 double* __restrict__ z) {
-  __shared__ double part[8][32];
+__global__ void __launch_bounds__(1024) k2_reduce(const double* __restrict__ zpart,
+                                                  const double* __restrict__ kpart, int nchunks,
+                                                  int64_t W, int64_t n,
+                                                  const double* __restrict__ cmiss,
+                                                  const int64_t* __restrict__ col_ptr,
+                                                  const int32_t* __restrict__ col_idx,
+                                                  double* __restrict__ z) {
+  // Block = 32 warps x 32 consecutive samples. Warp w sums chunks c = w (mod
+  // 32) with lanes on consecutive samples (coalesced), and walks sample
+  // s0 + w's missing list with lanes striding the entries. Partials are added
+  // in warp order -> deterministic.
+  __shared__ double part[32][33];
   __shared__ double corr[32];
   __shared__ double kt_s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -666,27 +672,29 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ zpar
   double acc = 0.0;
   if (s < n)
 #pragma unroll 4
-    for (int c = warp; c < nchunks; c += 8) acc += zpart[(int64_t)c * 16 * W + s];
+    for (int c = warp; c < nchunks; c += 32) acc += zpart[(int64_t)c * 16 * W + s];
   part[warp][lane] = acc;
-  for (int t = 0; t < 4; ++t) {
-    const int li = warp * 4 + t;
-    const int64_t ss = s0 + li;
+  {
+    const int64_t ss = s0 + warp;
     double cs = 0.0;
-    if (col_ptr && ss < n)
-#pragma unroll 4
-      for (int64_t e = col_ptr[ss] + lane; e < col_ptr[ss + 1]; e += 32) cs += cmiss[col_idx[e]];
+    if (col_ptr && ss < n) {
+      const int64_t e0 = col_ptr[ss], e1 = col_ptr[ss + 1];
+#pragma unroll 8
+      for (int64_t e = e0 + lane; e < e1; e += 32) cs += cmiss[col_idx[e]];
+    }
     for (int o = 16; o > 0; o >>= 1) cs += __shfl_down_sync(0xffffffffu, cs, o);
-    if (lane == 0) corr[li] = cs;
+    if (lane == 0) corr[warp] = cs;
   }
-  if (threadIdx.x == 0) {
+  if (warp == 1) {
     double kt = 0.0;
-    for (int c = 0; c < nchunks; ++c) kt += kpart[c];
-    kt_s = kt;
+    for (int c = lane; c < nchunks; c += 32) kt += kpart[c];
+    for (int o = 16; o > 0; o >>= 1) kt += __shfl_down_sync(0xffffffffu, kt, o);
+    if (lane == 0) kt_s = kt;
   }
   __syncthreads();
   if (warp == 0 && s < n) {
     double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    for (int w = 0; w < 32; ++w) t += part[w][lane];
     z[s] = t - kt_s - corr[lane];
   }
 }
@@ -830,7 +838,7 @@ void k2_adjoint(const GenoView& g, const K2Plan& pl, const double* y, double* zp
     return;
   }
   k2_main_only(g, pl, y, zpart, kpart, s);
-  k2_reduce<<<(unsigned)((g.n + 31) / 32), 256, 0, s>>>(
+  k2_reduce<<<(unsigned)((g.n + 31) / 32), 1024, 0, s>>>(
       zpart, kpart, pl.nchunks, g.W, g.n, g.cmiss, g.nmissing ? g.miss_col_ptr : nullptr,
       g.miss_col_idx, z);
 }
