@@ -18,8 +18,10 @@
 // fixed order.
 //
 // Missing entries are stored as r = 3 in the layouts (so the layouts retain
-// the full .bed information); their 3*coef contribution is removed exactly
-// by sparse corrections over sorted missing lists in the reduce kernels.
+// the full .bed information); their 3*coef contribution is removed exactly in
+// the main kernels' epilogues, each CTA walking its own block's sorted
+// missing list (16-bit local indices into its shared-memory coefficients).
+// The reduce kernels are plain fixed-order sums of the per-CTA partials.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -35,7 +37,6 @@ namespace {
 constexpr int kS = 1000;  // coefficient scale exponent (see header comment)
 constexpr int kThreads = 256;
 constexpr int kDepth = 4;  // 16-byte loads in flight per thread in the main loops
-constexpr int kSubQ = 64;  // SNP quads per pair-table sub-chunk in k2_main_h (8 KB of tables)
 
 __device__ __forceinline__ double fld(uint32_t w, int k) {
   return __hiloint2double(0, (int)(w & (3u << (2 * k))));
@@ -168,89 +169,103 @@ __global__ void k_marker_counts(const uint4* __restrict__ layA, int64_t P4, int6
   }
 }
 
-// thread per word position: counts missing per sample over all local SNPs
-__global__ void k_sample_missing_counts(const uint4* __restrict__ layA, int64_t P4, int64_t W,
-                                        int64_t p_loc, int64_t n, int64_t* __restrict__ col_counts) {
-  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= W) return;
-  int cnt[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) cnt[k] = 0;
-  for (int64_t q = 0; q < P4; ++q) {
-    const uint4 v = layA[q * W + w];
-    const uint32_t m = missing_mask(v.x) | (missing_mask(v.y) << 1);
-    const uint32_t m2 = missing_mask(v.z) | (missing_mask(v.w) << 1);
-    if ((m | m2) == 0) continue;
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      cnt[k] += ((m >> (2 * k)) & 1u) + ((m >> (2 * k + 1)) & 1u) + ((m2 >> (2 * k)) & 1u) +
-                ((m2 >> (2 * k + 1)) & 1u);
-  }
-  (void)p_loc;  // pad SNP rows are r = 0, never missing
-#pragma unroll
-  for (int k = 0; k < 16; ++k)
-    if (16 * w + k < n) col_counts[16 * w + k] = cnt[k];
+// ---------------------------------------------------------------- missing lists
+// Per-CTA missing lists. The missing entries of one
+// main-kernel CTA's block are stored in that block's own segment, grouped by
+// the output the owning thread writes and sorted ascending, as 16-bit local
+// indices:
+//   K1 block (qb, tile): 128 SNP rows 4*lane+i, entries = sample offset in the tile (< 4096)
+//   K2 block (wb, chunk): 512 samples 16*lane+k, entries = SNP offset in the chunk (< 2048)
+// Block b's row r owns ent[base[b] + off[b*(span+1)+r] .. base[b] + off[b*(span+1)+r+1]).
+// Count pass (kFill = false) writes cnt[b*span + r]; fill pass writes ent.
+template <bool kFill>
+__global__ void __launch_bounds__(128) k_miss_k1(const uint4* __restrict__ layA, int64_t P4,
+                                                 int64_t W, int tileW, uint32_t* __restrict__ cnt,
+                                                 const uint32_t* __restrict__ off,
+                                                 const int64_t* __restrict__ base,
+                                                 uint16_t* __restrict__ ent) {
+  const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int t = threadIdx.x;  // row 4*lane + i of the K1 epilogue
+  const int64_t q = (int64_t)blockIdx.x * 32 + (t >> 2);
+  const int i = t & 3;
+  const int64_t w0 = (int64_t)blockIdx.y * tileW, w1 = min(W, w0 + tileW);
+  uint32_t c = 0;
+  int64_t pos = kFill ? base[b] + off[b * 129 + t] : 0;
+  if (q < P4)
+    for (int64_t w = w0; w < w1; ++w) {
+      const uint4 v = layA[q * W + w];
+      uint32_t m = missing_mask(i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w);
+      if (kFill) {
+        while (m) {
+          const int bit = __ffs(m) - 1;
+          ent[pos++] = (uint16_t)(16 * (w - w0) + (bit >> 1));
+          m &= m - 1;
+        }
+      } else {
+        c += __popc(m);
+      }
+    }
+  if (!kFill) cnt[b * 128 + t] = c;
 }
 
-// warp per SNP row: sorted sample ids of its missing entries
-__global__ void k_fill_missing_rows(const uint4* __restrict__ layA, int64_t P4, int64_t W,
-                                    int64_t p_loc, const int64_t* __restrict__ row_ptr,
-                                    int32_t* __restrict__ row_idx) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < p_loc; j += warps) {
-    const int64_t q = j >> 2;
-    const int i = (int)(j & 3);
-    if (row_ptr[j + 1] == row_ptr[j]) continue;
-    int64_t base = row_ptr[j];
-    for (int64_t w0 = 0; w0 < W; w0 += 32) {
-      const int64_t w = w0 + lane;
-      uint32_t m = 0;
-      if (w < W) {
-        const uint4 v = layA[q * W + w];
-        const uint32_t r = i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-        m = missing_mask(r);
-      }
-      const int c = __popc(m);
-      int incl = c;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      int64_t pos = base + incl - c;
-      while (m) {
-        const int b = __ffs(m) - 1;
-        row_idx[pos++] = (int32_t)(16 * w + (b >> 1));
-        m &= m - 1;
-      }
-      base += __shfl_sync(0xffffffffu, incl, 31);
-    }
+template <bool kFill>
+__global__ void __launch_bounds__(32) k_miss_k2(const uint4* __restrict__ layA, int64_t P4,
+                                                int64_t W, int qc, uint32_t* __restrict__ cnt,
+                                                const uint32_t* __restrict__ off,
+                                                const int64_t* __restrict__ base,
+                                                uint16_t* __restrict__ ent) {
+  const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int lane = threadIdx.x;
+  const int64_t w = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t q0 = (int64_t)blockIdx.y * qc, q1 = min(P4, q0 + qc);
+  uint32_t c[16];
+  int64_t pos[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    c[k] = 0;
+    pos[k] = kFill ? base[b] + off[b * 513 + 16 * lane + k] : 0;
   }
+  if (w < W)
+    for (int64_t q = q0; q < q1; ++q) {
+      const uint4 v = layA[q * W + w];
+      const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t m = missing_mask(ws[i]);
+        if (m == 0) continue;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if ((m >> (2 * k)) & 1u) {
+            if (kFill)
+              ent[pos[k]++] = (uint16_t)(4 * (q - q0) + i);
+            else
+              ++c[k];
+          }
+      }
+    }
+  if (!kFill)
+#pragma unroll
+    for (int k = 0; k < 16; ++k) cnt[b * 512 + 16 * lane + k] = c[k];
 }
 
-// thread per word position: sorted local SNP ids per sample (ascending j)
-__global__ void k_fill_missing_cols(const uint4* __restrict__ layA, int64_t P4, int64_t W,
-                                    int64_t p_loc, int64_t n, const int64_t* __restrict__ col_ptr,
-                                    int32_t* __restrict__ col_idx) {
-  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= W) return;
-  int64_t cur[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) cur[k] = (16 * w + k < n) ? col_ptr[16 * w + k] : 0;
-  for (int64_t q = 0; q < P4; ++q) {
-    const uint4 v = layA[q * W + w];
-    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
-    if ((missing_mask(v.x) | missing_mask(v.y) | missing_mask(v.z) | missing_mask(v.w)) == 0)
-      continue;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t m = missing_mask(ws[i]);
-#pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if ((m >> (2 * k)) & 1u) col_idx[cur[k]++] = (int32_t)(4 * q + i);
-    }
+// CTA per block: exclusive scan of the block's span counts -> off, block total -> tot.
+__global__ void __launch_bounds__(512) k_block_scan(const uint32_t* __restrict__ cnt, int span,
+                                                    uint32_t* __restrict__ off,
+                                                    int64_t* __restrict__ tot) {
+  __shared__ uint32_t s[512];
+  const int64_t b = blockIdx.x;
+  const int t = threadIdx.x;
+  s[t] = t < span ? cnt[b * span + t] : 0u;
+  __syncthreads();
+  for (int o = 1; o < 512; o <<= 1) {
+    const uint32_t v = t >= o ? s[t - o] : 0u;
+    __syncthreads();
+    s[t] += v;
+    __syncthreads();
   }
-  (void)p_loc;
+  if (t == 0) off[b * (span + 1)] = 0;
+  if (t < span) off[b * (span + 1) + t + 1] = s[t];
+  if (t == span - 1) tot[b] = s[t];
 }
 
 __global__ void k_layout_to_bed(const uint4* __restrict__ layA, int64_t P4, int64_t W, int64_t n,
@@ -310,8 +325,11 @@ __device__ __forceinline__ void k2_quad(const uint4 c, const double2 ca, const d
 __global__ void __launch_bounds__(kThreads) k1_main(const uint4* __restrict__ layB, int64_t P4,
                                                     int64_t W, const double* __restrict__ x,
                                                     int64_t n, int tileW,
-                                                    double* __restrict__ ypart,
-                                                    double* __restrict__ xsum) {
+                                                    const double* __restrict__ mu,
+                                                    const uint32_t* __restrict__ m_off,
+                                                    const int64_t* __restrict__ m_base,
+                                                    const uint16_t* __restrict__ m_ent,
+                                                    double* __restrict__ ypart) {
   extern __shared__ double2 xp2[];  // tileW * 8 double2: scaled coefficients
   __shared__ double red[33];
   __shared__ int redi[33];
@@ -335,7 +353,6 @@ __global__ void __launch_bounds__(kThreads) k1_main(const uint4* __restrict__ la
   const double tsum = block_sum(part, red);
   for (int t = threadIdx.x; t < ns; t += kThreads) xp[t] = scalbn(xp[t], kS - E - 2 * (t & 15));
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) xsum[tile] = tsum;
 
   // Lane = SNP quad (32 consecutive quads per CTA, 512-B coalesced rows of
   // layout B); warp w takes the w-th eighth of the tile's word positions, and
@@ -375,6 +392,11 @@ __global__ void __launch_bounds__(kThreads) k1_main(const uint4* __restrict__ la
   wsum[warp][2][lane] = a2;
   wsum[warp][3][lane] = a3;
   __syncthreads();
+  // Epilogue: thread (i, lane) owns SNP j = 4*(32*blockIdx.x + lane) + i and
+  // writes this tile's exact partial
+  //   sum_{observed s} r_js x_s - mu_j X_tile = sum_s r_js x_s - mu_j X_tile - (3 - mu_j) S_miss
+  // with S_miss summed over the block's own missing list (scaled domain:
+  // xp[s] * 2^(2(s&15)) = x_s * 2^(kS-E), exact).
   if (threadIdx.x < 128) {
     const int i = threadIdx.x >> 5;  // SNP within the quad
     const int64_t qq = (int64_t)blockIdx.x * 32 + lane;
@@ -382,59 +404,65 @@ __global__ void __launch_bounds__(kThreads) k1_main(const uint4* __restrict__ la
       double t = 0.0;
 #pragma unroll
       for (int w = 0; w < 8; ++w) t += wsum[w][i][lane];
-      ypart[(int64_t)tile * 4 * P4 + 4 * qq + i] = scalbn(t, 1074 - kS + E);
+      const double m = mu[4 * qq + i];
+      double v = scalbn(t, 1074 - kS + E) - m * tsum;
+      if (m_off) {
+        const int64_t b = (int64_t)tile * gridDim.x + blockIdx.x;
+        const uint32_t* o = m_off + b * 129 + 4 * lane + i;
+        const uint16_t* e = m_ent + m_base[b];
+        const uint32_t e0 = o[0], e1 = o[1];
+        double sm = 0.0;
+        uint32_t k = e0;
+        for (; k + 8 <= e1; k += 8) {  // 8 index loads in flight, summed in order
+          int s[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s[u] = e[k + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            sm += xp[s[u]] * __hiloint2double((1023 + 2 * (s[u] & 15)) << 20, 0);
+        }
+        for (; k < e1; ++k) {
+          const int s1 = e[k];
+          sm += xp[s1] * __hiloint2double((1023 + 2 * (s1 & 15)) << 20, 0);
+        }
+        if (e1 > e0) v -= (3.0 - m) * scalbn(sm, E - kS);
+      }
+      ypart[(int64_t)tile * 4 * P4 + 4 * qq + i] = v;
     }
   }
 }
 
-// y_j = inv_s_j * (sum_t ypart - mu_j X_tot - (3 - mu_j) S_miss_j)
-__global__ void k1_reduce(const double* __restrict__ ypart, const double* __restrict__ xsum,
-                          int ntiles, int64_t P4, int64_t p_loc, const double* __restrict__ x,
-                          const double* __restrict__ mu, const double* __restrict__ inv_s,
-                          const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ row_idx,
-                          double* __restrict__ y) {
-  // One warp per SNP: lanes stride over the sample tiles and over the SNP's
-  // sorted missing list; fixed shuffle tree -> deterministic.
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  double xt = 0.0;
-  for (int t = lane; t < ntiles; t += 32) xt += xsum[t];
-  for (int o = 16; o > 0; o >>= 1) xt += __shfl_xor_sync(0xffffffffu, xt, o);
-  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < p_loc; j += nwarps) {
-    double acc = 0.0, sm = 0.0;
-    for (int t = lane; t < ntiles; t += 32) acc += ypart[(int64_t)t * 4 * P4 + j];
-    if (row_ptr) {
-      const int64_t e0 = row_ptr[j], e1 = row_ptr[j + 1];
-#pragma unroll 8
-      for (int64_t e = e0 + lane; e < e1; e += 32) sm += x[row_idx[e]];
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      acc += __shfl_down_sync(0xffffffffu, acc, o);
-      sm += __shfl_down_sync(0xffffffffu, sm, o);
-    }
-    if (lane == 0) {
-      const double m = mu[j];
-      y[j] = inv_s[j] * (acc - m * xt - (3.0 - m) * sm);
-    }
-  }
+// y_j = inv_s_j * sum_t ypart[t][j]  (tiles in order -> deterministic)
+__global__ void k1_reduce(const double* __restrict__ ypart, int ntiles, int64_t P4, int64_t p_loc,
+                          const double* __restrict__ inv_s, double* __restrict__ y) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= p_loc) return;
+  double acc = 0.0;
+  for (int t = 0; t < ntiles; ++t) acc += ypart[(int64_t)t * 4 * P4 + j];
+  y[j] = inv_s[j] * acc;
 }
 
 // ---------------------------------------------------------------- K2 adjoint
 // grid (ceil(W/32), nchunks). Lane = word position w (16 samples, 16
 // accumulators); loops over the chunk's SNP quads; lanes read 32 consecutive
 // 16-byte chunks of one quad row (512 B).
-__global__ void __launch_bounds__(kThreads, 4) k2_main(const uint4* __restrict__ layA, int64_t P4,
+template <int kMinB>
+__global__ void __launch_bounds__(kThreads, kMinB) k2_main(const uint4* __restrict__ layA, int64_t P4,
                                                     int64_t W, const double* __restrict__ y,
                                                     const double* __restrict__ mu,
                                                     const double* __restrict__ inv_s,
                                                     int64_t p_loc, int qc,
-                                                    double* __restrict__ zpart,
-                                                    double* __restrict__ kpart,
-                                                    double* __restrict__ cmiss) {
-  extern __shared__ double2 cs2[];  // 2*qc double2 = 4*qc scaled coefficients
+                                                    const uint32_t* __restrict__ m_off,
+                                                    const int64_t* __restrict__ m_base,
+                                                    const uint16_t* __restrict__ m_ent,
+                                                    double* __restrict__ zpart) {
+  // dynamic smem: cs = max(4*qc, 2048) scaled coefficients (reused for the
+  // cross-warp combine), then cm = 4*qc missing-entry corrections c_j (3 - mu_j)
+  extern __shared__ double2 cs2[];
   __shared__ double red[33];
   __shared__ int redi[33];
   double* cs = reinterpret_cast<double*>(cs2);
+  double* cm = cs + max(4 * qc, 2048);
   const int chunk = blockIdx.y;
   const int64_t q0 = (int64_t)chunk * qc;
   const int64_t q1 = min(P4, q0 + qc);
@@ -446,17 +474,17 @@ __global__ void __launch_bounds__(kThreads, 4) k2_main(const uint4* __restrict__
     const int64_t j = 4 * q0 + t;
     const double c = j < p_loc ? inv_s[j] * y[j] : 0.0;
     emax = max(emax, exp_of(c));
-    if (j < p_loc) {
-      kp += c * mu[j];
-      if (cmiss && blockIdx.x == 0) cmiss[j] = c * (3.0 - mu[j]);  // missing-entry correction
-    }
+    const double m = j < p_loc ? mu[j] : 0.0;
+    kp += c * m;
+    if (m_off) cm[t] = c * (3.0 - m);
     cs[t] = c;
   }
-  const int E = block_max_int(emax, redi);
-  const double ksum = block_sum(kp, red);
-  for (int t = threadIdx.x; t < 4 * nq; t += kThreads) cs[t] = scalbn(cs[t], kS - E);
+  {
+    const int E = block_max_int(emax, redi);
+    block_sum(kp, red);  // chunk's sum_j c_j mu_j, left in red[32]
+    for (int t = threadIdx.x; t < 4 * nq; t += kThreads) cs[t] = scalbn(cs[t], kS - E);
+  }
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) kpart[chunk] = ksum;
 
   // Lane = word position (32 consecutive words, 512-B coalesced rows of
   // layout A); warp w takes the w-th eighth of the chunk's SNP quads; the 8
@@ -491,11 +519,19 @@ __global__ void __launch_bounds__(kThreads, 4) k2_main(const uint4* __restrict__
     if (qq + 2 < qe) k2_quad(c2, cs2[2 * qq + 4], cs2[2 * qq + 5], acc);
   }
   // cross-warp combine in two halves of 8 fields (16 KB of the coefficient
-  // region, which is sized >= 2048 doubles)
+  // region, which is sized >= 2048 doubles). Thread (k_out, lane) owns sample
+  // 16*w_out + field and writes the chunk's exact partial
+  //   sum_j c_j r_js - sum_j c_j mu_j - sum_{j in miss(s)} c_j (3 - mu_j)
+  // with the last sum over the block's own missing list.
+  // E and ksum are re-read from shared memory (volatile: not kept live in
+  // registers across the main loop, which runs at the 64-register cap)
+  const int E = *reinterpret_cast<volatile int*>(&redi[32]);
+  const double ksum = *reinterpret_cast<volatile double*>(&red[32]);
   double* part = cs;
   const int k_out = threadIdx.x >> 5;  // field within the half, 0..7
   const int64_t w_out = (int64_t)blockIdx.x * 32 + lane;
   double* out = zpart + (int64_t)chunk * 16 * W;
+  const int64_t b = (int64_t)chunk * gridDim.x + blockIdx.x;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     __syncthreads();
@@ -506,196 +542,47 @@ __global__ void __launch_bounds__(kThreads, 4) k2_main(const uint4* __restrict__
 #pragma unroll
     for (int ww = 0; ww < 8; ++ww) t += part[(ww * 8 + k_out) * 32 + lane];
     const int field = 8 * h + k_out;
-    if (w_out < W) out[16 * w_out + field] = scalbn(t, 1074 - kS + E - 2 * field);
+    if (w_out < W) {
+      double v = scalbn(t, 1074 - kS + E - 2 * field) - ksum;
+      if (m_off) {
+        const uint32_t* o = m_off + b * 513 + 16 * lane + field;
+        const uint16_t* e = m_ent + m_base[b];
+        const uint32_t e0 = o[0], e1 = o[1];
+        double corr = 0.0;
+        uint32_t k = e0;
+        for (; k + 8 <= e1; k += 8) {  // 8 index loads in flight, summed in order
+          int jj[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) jj[u] = e[k + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) corr += cm[jj[u]];
+        }
+        for (; k < e1; ++k) corr += cm[e[k]];
+        v -= corr;
+      }
+      out[16 * w_out + field] = v;
+    }
   }
 }
 
-// ---------------------------------------------------------------- K2 hybrid
-// Same contract as k2_main, but the work of every SNP quad is split across
-// two pipes: SNPs (4q, 4q+1) go through a 16-entry fp64 pair table in shared
-// memory -- T_q[r_a | r_b << 2] = v_a(r_a) + v_b(r_b), v_j(r) = c_j (r - mu_j)
-// for r <= 2 and 0 for a missing entry -- so each lookup (one PRMT address
-// op, one LDS.64, one DADD) covers two genotypes on the LSU pipe; SNPs
-// (4q+2, 4q+3) go through the denormal-injection DFMA path on the FP64 pipe.
-// Table-path SNPs need no missing correction (cmiss = 0) and no mu term.
-// Lane = half a word (8 samples): lanes 2i, 2i+1 share word w0 + i.
-__device__ __forceinline__ double lds_f64(uint32_t addr) {
-  double v;
-  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));  // tables are read-only after setup
-  return v;
-}
-
-__global__ void __launch_bounds__(kThreads) k2_main_h(const uint4* __restrict__ layA, int64_t P4,
-                                                      int64_t W, const double* __restrict__ y,
-                                                      const double* __restrict__ mu,
-                                                      const double* __restrict__ inv_s,
-                                                      int64_t p_loc, int qc,
-                                                      double* __restrict__ zpart,
-                                                      double* __restrict__ kpart,
-                                                      double* __restrict__ cmiss) {
-  extern __shared__ __align__(16) double sm_raw[];
-  // tables start on a 256-byte boundary: table qq is at byte (qq>>1)*256 + (qq&1)*128
-  const uint32_t raw_addr = (uint32_t)__cvta_generic_to_shared(sm_raw);
-  double* sm2 = sm_raw + (((raw_addr + 255u) & ~255u) - raw_addr) / 8;
-  double* tabs = sm2;                                            // kSubQ * 16 (128 B per quad)
-  double2* csd = reinterpret_cast<double2*>(sm2 + 16 * kSubQ);   // qc scaled (c_{4q+2}, c_{4q+3})
-  __shared__ double red[33];
-  __shared__ int redi[33];
-  const int chunk = blockIdx.y;
-  const int64_t q0 = (int64_t)chunk * qc;
-  const int64_t q1 = min(P4, q0 + qc);
-  const int nq = (int)(q1 - q0);
-
-  // DFMA-path coefficients (SNPs 4q+2, 4q+3) of the whole chunk: exponent,
-  // mu term and missing corrections
-  int emax = -1100;
-  double kp = 0.0;
-  for (int t = threadIdx.x; t < 2 * nq; t += kThreads) {
-    const int64_t j = 4 * (q0 + (t >> 1)) + 2 + (t & 1);
-    const double c = j < p_loc ? inv_s[j] * y[j] : 0.0;
-    emax = max(emax, exp_of(c));
-    if (j < p_loc) kp += c * mu[j];
-    reinterpret_cast<double*>(csd)[t] = c;
-  }
-  if (cmiss && blockIdx.x == 0)
-    for (int t = threadIdx.x; t < 4 * nq; t += kThreads) {
-      const int64_t j = 4 * q0 + t;
-      if (j < p_loc) cmiss[j] = (t & 2) ? inv_s[j] * y[j] * (3.0 - mu[j]) : 0.0;
-    }
-  const int E = block_max_int(emax, redi);
-  const double ksum = block_sum(kp, red);
-  for (int t = threadIdx.x; t < 2 * nq; t += kThreads)
-    reinterpret_cast<double*>(csd)[t] = scalbn(reinterpret_cast<double*>(csd)[t], kS - E);
-  if (blockIdx.x == 0 && threadIdx.x == 0) kpart[chunk] = ksum;
-
-  // Warps split the CTA's 128 word positions (16 per warp, two lanes per
-  // word); every warp walks all quads of the chunk, kSubQ at a time, against
-  // pair tables shared by the whole CTA.
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int half = lane & 1;
-  const int64_t w = (int64_t)blockIdx.x * 128 + warp * 16 + (lane >> 1);
-  const bool active = w < W;
-  const uint32_t tab_addr = (uint32_t)__cvta_generic_to_shared(tabs);
-  const uint32_t sel_h = half ? 0x00007632u : 0x00005410u;  // bytes (2h, 2h+1) of te | to
-  const int sh = 16 * half;
-  const uint4* src = layA + q0 * W + (active ? w : 0);
-  double at[8], ad[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    at[k] = 0.0;
-    ad[k] = 0.0;
-  }
-  for (int s0 = 0; s0 < nq; s0 += kSubQ) {
-    const int s1 = min(nq, s0 + kSubQ);
-    __syncthreads();  // previous sub-chunk's tables fully consumed (and csd visible)
-    // pair tables for SNPs (4q, 4q+1) of quads [s0, s1)
-    for (int e = threadIdx.x; e < 16 * (s1 - s0); e += kThreads) {
-      const int qq = e >> 4, n = e & 15, ra = n & 3, rb = n >> 2;
-      const int64_t ja = 4 * (q0 + s0 + qq), jb = ja + 1;
-      double va = 0.0, vb = 0.0;
-      if (ra != 3 && ja < p_loc) va = inv_s[ja] * y[ja] * ((double)ra - mu[ja]);
-      if (rb != 3 && jb < p_loc) vb = inv_s[jb] * y[jb] * ((double)rb - mu[jb]);
-      tabs[e] = va + vb;
-    }
-    __syncthreads();
-    if (!active) continue;
-    const uint4 Z = make_uint4(0, 0, 0, 0);
-    uint4 n0 = ld_stream(src + (int64_t)s0 * W);
-    uint4 n1 = s0 + 1 < s1 ? ld_stream(src + (int64_t)(s0 + 1) * W) : Z;
-    uint4 n2 = s0 + 2 < s1 ? ld_stream(src + (int64_t)(s0 + 2) * W) : Z;
-    for (int qq = s0; qq < s1; ++qq) {
-      const uint4 c = n0;
-      n0 = n1;
-      n1 = n2;
-      n2 = qq + 3 < s1 ? ld_stream(src + (int64_t)(qq + 3) * W) : Z;
-      // ---- table path: nibble (r_x | r_y << 2) per sample
-      const uint32_t te = (c.x & 0x33333333u) | ((c.y << 2) & 0xCCCCCCCCu);  // fields 0,2,..,14
-      const uint32_t to = ((c.x >> 2) & 0x33333333u) | (c.y & 0xCCCCCCCCu);  // fields 1,3,..,15
-      // this lane's 8 fields: nibbles n0..n3 = fields 8h+{0,2,4,6}, n4..n7 = 8h+{1,3,5,7}
-      const uint32_t tt = __byte_perm(te, to, sel_h);
-      const uint32_t par = (qq & 1) ? 0x80808080u : 0u;
-      const uint32_t u0 = ((tt << 3) & 0x78787878u) | par;  // n0,n2,n4,n6 -> fields 0,4,1,5
-      const uint32_t u1 = ((tt >> 1) & 0x78787878u) | par;  // n1,n3,n5,n7 -> fields 2,6,3,7
-      const uint32_t base = tab_addr + (uint32_t)((qq - s0) >> 1) * 256u;
-      // address = table base (bytes 1..3, byte 0 == 0) with byte 0 = nibble*8 | parity*128
-      at[0] += lds_f64(__byte_perm(u0, base, 0x7650u));
-      at[4] += lds_f64(__byte_perm(u0, base, 0x7651u));
-      at[1] += lds_f64(__byte_perm(u0, base, 0x7652u));
-      at[5] += lds_f64(__byte_perm(u0, base, 0x7653u));
-      at[2] += lds_f64(__byte_perm(u1, base, 0x7650u));
-      at[6] += lds_f64(__byte_perm(u1, base, 0x7651u));
-      at[3] += lds_f64(__byte_perm(u1, base, 0x7652u));
-      at[7] += lds_f64(__byte_perm(u1, base, 0x7653u));
-      // ---- DFMA path for SNPs 4q+2, 4q+3 on this lane's 8 fields
-      const double2 cc = csd[qq];
-      const uint32_t zz = c.z >> sh, ww = c.w >> sh;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) ad[k] = fma(fld(zz, k), cc.x, ad[k]);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) ad[k] = fma(fld(ww, k), cc.y, ad[k]);
-    }
-  }
-  // lane's field f (0..7) = sample 16w + 8h + f: at[f] plain, ad[f] scaled by
-  // 2^(2f + kS - E - 1074)
-  if (active) {
-    double2* out = reinterpret_cast<double2*>(zpart + (int64_t)chunk * 16 * W + 16 * w + 8 * half);
-#pragma unroll
-    for (int f = 0; f < 8; f += 2)
-      out[f / 2] = make_double2(at[f] + scalbn(ad[f], 1074 - kS + E - 2 * f),
-                                at[f + 1] + scalbn(ad[f + 1], 1074 - kS + E - 2 * (f + 1)));
-  }
-}
-
-// z_s = sum_c zpart - sum_c kpart - sum_{j in miss(s)} cmiss_j,
-// cmiss_j = inv_s_j y_j (3 - mu_j) written by k2_main.
-// Block = 8 warps x 32 consecutive samples: warp w sums chunks c = w (mod 8)
-// with lanes on consecutive samples (coalesced), then the 8 partials are
-// added in warp order; each warp walks 4 samples' missing lists with lanes
-// striding the entries. Fixed trees -> deterministic.
-__global__ void __launch_bounds__(1024) k2_reduce(const double* __restrict__ zpart,
-                                                  const double* __restrict__ kpart, int nchunks,
-                                                  int64_t W, int64_t n,
-                                                  const double* __restrict__ cmiss,
-                                                  const int64_t* __restrict__ col_ptr,
-                                                  const int32_t* __restrict__ col_idx,
-                                                  double* __restrict__ z) {
-  // Block = 32 warps x 32 consecutive samples. Warp w sums chunks c = w (mod
-  // 32) with lanes on consecutive samples (coalesced), and walks sample
-  // s0 + w's missing list with lanes striding the entries. Partials are added
-  // in warp order -> deterministic.
+// z_s = sum_c zpart[c][s] (chunks in a fixed order -> deterministic).
+// Block = 32 warps x 32 consecutive samples: warp w sums chunks c = w (mod 32)
+// with lanes on consecutive samples (coalesced); partials added in warp order.
+__global__ void __launch_bounds__(1024) k2_reduce(const double* __restrict__ zpart, int nchunks,
+                                                  int64_t W, int64_t n, double* __restrict__ z) {
   __shared__ double part[32][33];
-  __shared__ double corr[32];
-  __shared__ double kt_s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t s0 = (int64_t)blockIdx.x * 32;
-  const int64_t s = s0 + lane;
+  const int64_t s = (int64_t)blockIdx.x * 32 + lane;
   double acc = 0.0;
   if (s < n)
 #pragma unroll 4
     for (int c = warp; c < nchunks; c += 32) acc += zpart[(int64_t)c * 16 * W + s];
   part[warp][lane] = acc;
-  {
-    const int64_t ss = s0 + warp;
-    double cs = 0.0;
-    if (col_ptr && ss < n) {
-      const int64_t e0 = col_ptr[ss], e1 = col_ptr[ss + 1];
-#pragma unroll 8
-      for (int64_t e = e0 + lane; e < e1; e += 32) cs += cmiss[col_idx[e]];
-    }
-    for (int o = 16; o > 0; o >>= 1) cs += __shfl_down_sync(0xffffffffu, cs, o);
-    if (lane == 0) corr[warp] = cs;
-  }
-  if (warp == 1) {
-    double kt = 0.0;
-    for (int c = lane; c < nchunks; c += 32) kt += kpart[c];
-    for (int o = 16; o > 0; o >>= 1) kt += __shfl_down_sync(0xffffffffu, kt, o);
-    if (lane == 0) kt_s = kt;
-  }
   __syncthreads();
   if (warp == 0 && s < n) {
     double t = 0.0;
     for (int w = 0; w < 32; ++w) t += part[w][lane];
-    z[s] = t - kt_s - corr[lane];
+    z[s] = t;
   }
 }
 
@@ -722,25 +609,30 @@ void marker_counts(const uint4* layA, int64_t P4, int64_t W, int64_t p_loc, int6
   k_marker_counts<<<grid_for(P4 * 32, 256), 256, 0, s>>>(layA, P4, W, p_loc, n, counts);
 }
 
-void sample_missing_counts(const uint4* layA, int64_t P4, int64_t W, int64_t p_loc, int64_t n,
-                           int64_t* col_counts, cudaStream_t s) {
-  if (W == 0) return;
-  k_sample_missing_counts<<<(unsigned)((W + 127) / 128), 128, 0, s>>>(layA, P4, W, p_loc, n,
-                                                                      col_counts);
+void miss_lists_k1(const uint4* layA, int64_t P4, int64_t W, const K1Plan& pl, bool fill,
+                   uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent,
+                   cudaStream_t s) {
+  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.ntiles);
+  if (fill)
+    k_miss_k1<true><<<grid, 128, 0, s>>>(layA, P4, W, pl.tileW, cnt, off, base, ent);
+  else
+    k_miss_k1<false><<<grid, 128, 0, s>>>(layA, P4, W, pl.tileW, cnt, off, base, ent);
 }
 
-void fill_missing_rows(const uint4* layA, int64_t P4, int64_t W, int64_t p_loc,
-                       const int64_t* row_ptr, int32_t* row_idx, cudaStream_t s) {
-  if (p_loc == 0) return;
-  k_fill_missing_rows<<<grid_for(p_loc * 32, 256), 256, 0, s>>>(layA, P4, W, p_loc, row_ptr,
-                                                                 row_idx);
+void miss_lists_k2(const uint4* layA, int64_t P4, int64_t W, const K2Plan& pl, bool fill,
+                   uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent,
+                   cudaStream_t s) {
+  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nchunks);
+  if (fill)
+    k_miss_k2<true><<<grid, 32, 0, s>>>(layA, P4, W, pl.qc, cnt, off, base, ent);
+  else
+    k_miss_k2<false><<<grid, 32, 0, s>>>(layA, P4, W, pl.qc, cnt, off, base, ent);
 }
 
-void fill_missing_cols(const uint4* layA, int64_t P4, int64_t W, int64_t p_loc, int64_t n,
-                       const int64_t* col_ptr, int32_t* col_idx, cudaStream_t s) {
-  if (W == 0) return;
-  k_fill_missing_cols<<<(unsigned)((W + 127) / 128), 128, 0, s>>>(layA, P4, W, p_loc, n, col_ptr,
-                                                                  col_idx);
+void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int64_t* tot,
+                cudaStream_t s) {
+  if (nblk == 0) return;
+  k_block_scan<<<(unsigned)nblk, 512, 0, s>>>(cnt, span, off, tot);
 }
 
 void layout_to_bed(const uint4* layA, int64_t P4, int64_t W, int64_t n, int64_t row0,
@@ -766,29 +658,6 @@ K1Plan k1_plan(int64_t W, int64_t P4) {
 
 K2Plan k2_plan(int64_t W, int64_t P4) {
   K2Plan pl;
-  // GKB_K2=hybrid selects the pair-table + DFMA split (k2_main_h); measured
-  // slower than the DFMA-only kernel so far, so off by default.
-  const char* env = getenv("GKB_K2");
-  pl.hybrid = env && env[0] == 'h';
-  if (pl.hybrid) {
-    // CTA = 128 word positions (2048 samples; 8 warps x 16 words, two lanes
-    // per word) x a chunk of up to 512 SNP quads walked in sub-chunks of
-    // kSubQ quads (8 KB of pair tables). The chunk shrinks (down to kSubQ)
-    // until there are >= 4 CTAs per SM; partial traffic is 8 B per sample per
-    // chunk (1/64 of the packed bytes at 512 quads).
-    pl.grid_x = (W + 127) / 128;
-    if (pl.grid_x < 1) pl.grid_x = 1;
-    int64_t want = (148 * 4 + pl.grid_x - 1) / pl.grid_x;
-    int64_t qc = (P4 + want - 1) / (want > 0 ? want : 1);
-    qc = ((qc + kSubQ - 1) / kSubQ) * kSubQ;
-    if (qc > 512) qc = 512;
-    if (qc < kSubQ) qc = kSubQ;
-    pl.qc = (int)qc;
-    pl.nchunks = (int)((P4 + qc - 1) / qc);
-    if (pl.nchunks < 1) pl.nchunks = 1;
-    pl.smem = (size_t)(16 * kSubQ + 2 * qc) * sizeof(double) + 256;
-    return pl;
-  }
   // CTA = 32 word positions (512 samples) x a chunk of up to 512 SNP quads
   // (2048 SNPs), each warp 64 quads. Partial traffic: 8 B per sample per
   // chunk (1/64 of the 512 packed bytes per sample and chunk).
@@ -800,47 +669,49 @@ K2Plan k2_plan(int64_t W, int64_t P4) {
   pl.qc = (int)qc;
   pl.nchunks = (int)((P4 + qc - 1) / qc);
   if (pl.nchunks < 1) pl.nchunks = 1;
-  pl.smem = (size_t)(qc * 4 > 2048 ? qc * 4 : 2048) * sizeof(double);
+  // register bound: 4 CTAs/SM (64 registers) by default; GKB_K2_MINB=3 -> 80
+  const char* env = getenv("GKB_K2_MINB");
+  pl.minb = (env && env[0] == '3') ? 3 : 4;
+  // coefficients / combine region + missing-entry corrections
+  pl.smem = (size_t)((qc * 4 > 2048 ? qc * 4 : 2048) + qc * 4) * sizeof(double);
   return pl;
 }
 
-void k1_main_only(const GenoView& g, const K1Plan& pl, const double* x, double* ypart, double* xsum,
+void k1_main_only(const GenoView& g, const K1Plan& pl, const double* x, double* ypart,
                   cudaStream_t s) {
   dim3 grid((unsigned)pl.grid_x, (unsigned)pl.ntiles);
-  k1_main<<<grid, kThreads, pl.smem, s>>>(g.layB, g.P4, g.W, x, g.n, pl.tileW, ypart, xsum);
+  k1_main<<<grid, kThreads, pl.smem, s>>>(g.layB, g.P4, g.W, x, g.n, pl.tileW, g.mu, g.m1_off,
+                                          g.m1_base, g.m1_ent, ypart);
 }
 
-void k1_apply(const GenoView& g, const K1Plan& pl, const double* x, double* ypart, double* xsum,
-              double* y, cudaStream_t s) {
+void k1_apply(const GenoView& g, const K1Plan& pl, const double* x, double* ypart, double* y,
+              cudaStream_t s) {
   if (g.p_loc == 0) return;
-  k1_main_only(g, pl, x, ypart, xsum, s);
-  k1_reduce<<<grid_for(g.p_loc * 32, 256), 256, 0, s>>>(
-      ypart, xsum, pl.ntiles, g.P4, g.p_loc, x, g.mu, g.inv_s,
-      g.nmissing ? g.miss_row_ptr : nullptr, g.miss_row_idx, y);
+  k1_main_only(g, pl, x, ypart, s);
+  k1_reduce<<<(unsigned)((g.p_loc + 255) / 256), 256, 0, s>>>(ypart, pl.ntiles, g.P4, g.p_loc,
+                                                              g.inv_s, y);
 }
 
 void k2_main_only(const GenoView& g, const K2Plan& pl, const double* y, double* zpart,
-                  double* kpart, cudaStream_t s) {
+                  cudaStream_t s) {
   dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nchunks);
-  if (pl.hybrid)
-    k2_main_h<<<grid, kThreads, pl.smem, s>>>(g.layA, g.P4, g.W, y, g.mu, g.inv_s, g.p_loc, pl.qc,
-                                              zpart, kpart, g.nmissing ? g.cmiss : nullptr);
+  if (pl.minb == 3)
+    k2_main<3><<<grid, kThreads, pl.smem, s>>>(g.layA, g.P4, g.W, y, g.mu, g.inv_s, g.p_loc, pl.qc,
+                                               g.m2_off, g.m2_base, g.m2_ent, zpart);
   else
-    k2_main<<<grid, kThreads, pl.smem, s>>>(g.layA, g.P4, g.W, y, g.mu, g.inv_s, g.p_loc, pl.qc,
-                                            zpart, kpart, g.nmissing ? g.cmiss : nullptr);
+    k2_main<4><<<grid, kThreads, pl.smem, s>>>(g.layA, g.P4, g.W, y, g.mu, g.inv_s, g.p_loc, pl.qc,
+                                               g.m2_off, g.m2_base, g.m2_ent, zpart);
 }
 
-void k2_adjoint(const GenoView& g, const K2Plan& pl, const double* y, double* zpart, double* kpart,
-                double* z, cudaStream_t s) {
+void k2_adjoint(const GenoView& g, const K2Plan& pl, const double* y, double* zpart, double* z,
+                cudaStream_t s) {
   if (g.n == 0) return;
   if (g.p_loc == 0) {
     cudaMemsetAsync(z, 0, sizeof(double) * (size_t)g.n, s);
     return;
   }
-  k2_main_only(g, pl, y, zpart, kpart, s);
-  k2_reduce<<<(unsigned)((g.n + 31) / 32), 1024, 0, s>>>(
-      zpart, kpart, pl.nchunks, g.W, g.n, g.cmiss, g.nmissing ? g.miss_col_ptr : nullptr,
-      g.miss_col_idx, z);
+  k2_main_only(g, pl, y, zpart, s);
+  k2_reduce<<<(unsigned)((g.n + 31) / 32), 1024, 0, s>>>(zpart, pl.nchunks, g.W, g.n, z);
 }
 
 }  // namespace dev

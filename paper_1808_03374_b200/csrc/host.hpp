@@ -98,17 +98,18 @@ struct GenoShard {
   double* inv_s = nullptr;
   int64_t* counts = nullptr;  // device p_loc*4
   int64_t nmissing = 0;
-  int64_t* row_ptr = nullptr;
-  int32_t* row_idx = nullptr;
-  int64_t* col_ptr = nullptr;
-  int32_t* col_idx = nullptr;
   dev::K1Plan k1{};
   dev::K2Plan k2{};
+  // per-CTA missing lists of the two plans (kernels.hpp GenoView)
+  uint32_t* m1_off = nullptr;
+  int64_t* m1_base = nullptr;
+  uint16_t* m1_ent = nullptr;
+  uint32_t* m2_off = nullptr;
+  int64_t* m2_base = nullptr;
+  uint16_t* m2_ent = nullptr;
+  int64_t list_bytes = 0;
   double* ypart = nullptr;
-  double* xsum = nullptr;
   double* zpart = nullptr;
-  double* kpart = nullptr;
-  double* cmiss = nullptr;
   dev::GenoView view() const;
 };
 

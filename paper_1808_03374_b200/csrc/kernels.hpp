@@ -24,13 +24,17 @@ struct GenoView {
   int64_t p_loc, n, W, P4;
   const double* mu;     // p_loc
   const double* inv_s;  // p_loc
-  // missing lists (sorted): CSR by SNP (sample ids) and CSC by sample (local SNP ids)
-  const int64_t* miss_row_ptr;
-  const int32_t* miss_row_idx;
-  const int64_t* miss_col_ptr;
-  const int32_t* miss_col_idx;
+  // Per-CTA missing lists (null when the shard has no missing entries):
+  // block b, row r owns ent[base[b] + off[b*(span+1)+r] .. base[b] + off[b*(span+1)+r+1]).
+  // m1: K1 blocks b = tile*grid_x + qb, span 128 SNP rows, entries = sample offset in the tile
+  // m2: K2 blocks b = chunk*grid_x + wb, span 512 samples, entries = SNP offset in the chunk
+  const uint32_t* m1_off;
+  const int64_t* m1_base;
+  const uint16_t* m1_ent;
+  const uint32_t* m2_off;
+  const int64_t* m2_base;
+  const uint16_t* m2_ent;
   int64_t nmissing;
-  double* cmiss;  // scratch 4*P4: per-SNP missing-entry correction written by K2
 };
 
 // K8: .bed records [rows of one staging block] -> both layouts.
@@ -39,13 +43,6 @@ void build_layouts(const uint8_t* bed, int64_t stride_bytes, int64_t rows_in_blo
 // K7: per-SNP [n0, n1, n2, nmiss] from layout A.
 void marker_counts(const uint4* layA, int64_t P4, int64_t W, int64_t p_loc, int64_t n,
                    int64_t* counts, cudaStream_t s);
-// per-sample missing counts (int64 n), then the two list fills.
-void sample_missing_counts(const uint4* layA, int64_t P4, int64_t W, int64_t p_loc, int64_t n,
-                           int64_t* col_counts, cudaStream_t s);
-void fill_missing_rows(const uint4* layA, int64_t P4, int64_t W, int64_t p_loc,
-                       const int64_t* row_ptr, int32_t* row_idx, cudaStream_t s);
-void fill_missing_cols(const uint4* layA, int64_t P4, int64_t W, int64_t p_loc, int64_t n,
-                       const int64_t* col_ptr, int32_t* col_idx, cudaStream_t s);
 // layout A -> .bed records for rows [row0, row0+nrows) (read-back check).
 void layout_to_bed(const uint4* layA, int64_t P4, int64_t W, int64_t n, int64_t row0,
                    int64_t nrows, uint8_t* out, cudaStream_t s);
@@ -58,27 +55,39 @@ struct K1Plan {
 };
 K1Plan k1_plan(int64_t W, int64_t P4);
 // K1 apply (reference X*x, per-SNP dot): y (p_loc) = inv_s*(sum r x - mu X_tot - (3-mu) S_miss)
-// scratch: ypart ntiles*4*P4 doubles, xsum ntiles doubles.
-void k1_apply(const GenoView& g, const K1Plan& pl, const double* x, double* ypart, double* xsum,
-              double* y, cudaStream_t s);
+// scratch: ypart ntiles*4*P4 doubles.
+void k1_apply(const GenoView& g, const K1Plan& pl, const double* x, double* ypart, double* y,
+              cudaStream_t s);
 
 struct K2Plan {
   int qc;        // SNP quads per chunk
   int nchunks;
   int64_t grid_x;
   size_t smem;
-  int hybrid;    // 1: pair-table (LSU) + DFMA split (k2_main_h); 0: DFMA only (k2_main)
+  int minb;      // __launch_bounds__ min blocks of the k2_main instance (3 or 4)
 };
 K2Plan k2_plan(int64_t W, int64_t P4);
 // K2 apply_adjoint (reference X^T*y, per-sample sum) over the local SNPs.
-// scratch: zpart nchunks*16*W doubles, kpart nchunks doubles. z has n entries.
-void k2_adjoint(const GenoView& g, const K2Plan& pl, const double* y, double* zpart, double* kpart,
-                double* z, cudaStream_t s);
+// scratch: zpart nchunks*16*W doubles. z has n entries.
+void k2_adjoint(const GenoView& g, const K2Plan& pl, const double* y, double* zpart, double* z,
+                cudaStream_t s);
 // The two main packed kernels alone (for timing breakdowns).
-void k1_main_only(const GenoView& g, const K1Plan& pl, const double* x, double* ypart, double* xsum,
+void k1_main_only(const GenoView& g, const K1Plan& pl, const double* x, double* ypart,
                   cudaStream_t s);
 void k2_main_only(const GenoView& g, const K2Plan& pl, const double* y, double* zpart,
-                  double* kpart, cudaStream_t s);
+                  cudaStream_t s);
+
+// Per-CTA missing lists for the two plans: count pass (fill = false, writes
+// cnt[nblk*span]), block_scan (cnt -> off[nblk*(span+1)], tot[nblk]), then the
+// fill pass (fill = true, needs off and base = exclusive scan of tot).
+void miss_lists_k1(const uint4* layA, int64_t P4, int64_t W, const K1Plan& pl, bool fill,
+                   uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent,
+                   cudaStream_t s);
+void miss_lists_k2(const uint4* layA, int64_t P4, int64_t W, const K2Plan& pl, bool fill,
+                   uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent,
+                   cudaStream_t s);
+void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int64_t* tot,
+                cudaStream_t s);
 
 // ---- dense fp64 basis / operator kernels (K3-K6) -------------------------
 // Reduction scratch: partial[nblk * K] plus the result buffer.

@@ -126,6 +126,42 @@ void marker_scaling(const int64_t* counts, int64_t p, int64_t n, int scheme, dou
 }
 
 // ---------------------------------------------------------------- GenoOp
+// Per-CTA missing lists of one plan: count pass, per-block scan on device,
+// block bases scanned on the host (nblk values), fill pass. Returns the number
+// of entries (== the shard's missing count).
+template <class Launch>
+static int64_t build_block_lists(int64_t nblk, int span, cudaStream_t st, uint32_t** off,
+                                 int64_t** base, uint16_t** ent, int64_t* bytes, Launch launch) {
+  uint32_t* cnt = nullptr;
+  int64_t* tot = nullptr;
+  GKB_CUDA(cudaMalloc(&cnt, sizeof(uint32_t) * (size_t)(nblk * span)));
+  GKB_CUDA(cudaMalloc(&tot, sizeof(int64_t) * (size_t)nblk));
+  GKB_CUDA(cudaMalloc(off, sizeof(uint32_t) * (size_t)(nblk * (span + 1))));
+  launch(false, cnt, nullptr, nullptr, nullptr);
+  GKB_LAUNCH_CHECK();
+  dev::block_scan(cnt, nblk, span, *off, tot, st);
+  GKB_LAUNCH_CHECK();
+  std::vector<int64_t> h((size_t)nblk);
+  GKB_CUDA(cudaMemcpyAsync(h.data(), tot, sizeof(int64_t) * (size_t)nblk, cudaMemcpyDeviceToHost, st));
+  GKB_CUDA(cudaStreamSynchronize(st));
+  cudaFree(cnt);
+  cudaFree(tot);
+  int64_t total = 0;
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t c = h[b];
+    h[b] = total;
+    total += c;
+  }
+  GKB_CUDA(cudaMalloc(base, sizeof(int64_t) * (size_t)nblk));
+  GKB_CUDA(cudaMemcpy(*base, h.data(), sizeof(int64_t) * (size_t)nblk, cudaMemcpyHostToDevice));
+  GKB_CUDA(cudaMalloc(ent, sizeof(uint16_t) * (size_t)std::max<int64_t>(total, 1)));
+  launch(true, nullptr, *off, *base, *ent);
+  GKB_LAUNCH_CHECK();
+  *bytes += (int64_t)(sizeof(uint32_t) * nblk * (span + 1) + sizeof(int64_t) * nblk +
+                      sizeof(uint16_t) * total);
+  return total;
+}
+
 dev::GenoView GenoShard::view() const {
   dev::GenoView v;
   v.layA = layA;
@@ -136,12 +172,14 @@ dev::GenoView GenoShard::view() const {
   v.P4 = P4;
   v.mu = mu;
   v.inv_s = inv_s;
-  v.miss_row_ptr = row_ptr;
-  v.miss_row_idx = row_idx;
-  v.miss_col_ptr = col_ptr;
-  v.miss_col_idx = col_idx;
+  const bool lists = nmissing > 0;
+  v.m1_off = lists ? m1_off : nullptr;
+  v.m1_base = m1_base;
+  v.m1_ent = m1_ent;
+  v.m2_off = lists ? m2_off : nullptr;
+  v.m2_base = m2_base;
+  v.m2_ent = m2_ent;
   v.nmissing = nmissing;
-  v.cmiss = cmiss;
   return v;
 }
 
@@ -149,8 +187,8 @@ GenoOp::~GenoOp() {
   for (size_t i = 0; i < gs.size(); ++i) {
     cudaSetDevice(ctx->shards[i].dev);
     GenoShard& g = gs[i];
-    void* ptrs[] = {g.layA, g.layB, g.mu, g.inv_s, g.counts, g.row_ptr, g.row_idx,
-                    g.col_ptr, g.col_idx, g.ypart, g.xsum, g.zpart, g.kpart, g.cmiss};
+    void* ptrs[] = {g.layA,   g.layB,   g.mu,    g.inv_s,  g.counts, g.m1_off, g.m1_base,
+                    g.m1_ent, g.m2_off, g.m2_base, g.m2_ent, g.ypart, g.zpart};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -289,43 +327,32 @@ void GenoOp::finish_build() {
                                sizeof(int64_t) * (size_t)(4 * g.p_loc), cudaMemcpyDeviceToHost,
                                sh.stream));
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
-    // missing lists
-    std::vector<int64_t> rp((size_t)g.p_loc + 1, 0);
-    for (int64_t j = 0; j < g.p_loc; ++j) rp[j + 1] = rp[j] + counts_host[4 * (row0(i) + j) + 3];
-    g.nmissing = rp[g.p_loc];
-    if (g.nmissing > 0) {
-      if (g.nmissing > INT32_MAX) fail(GKB_EINVAL, "too many missing entries in one shard");
-      GKB_CUDA(cudaMalloc(&g.row_ptr, sizeof(int64_t) * rp.size()));
-      GKB_CUDA(cudaMemcpy(g.row_ptr, rp.data(), sizeof(int64_t) * rp.size(), cudaMemcpyHostToDevice));
-      GKB_CUDA(cudaMalloc(&g.row_idx, sizeof(int32_t) * (size_t)g.nmissing));
-      dev::fill_missing_rows(g.layA, g.P4, g.W, g.p_loc, g.row_ptr, g.row_idx, sh.stream);
-      GKB_LAUNCH_CHECK();
-      int64_t* ccount = nullptr;
-      GKB_CUDA(cudaMalloc(&ccount, sizeof(int64_t) * (size_t)g.n));
-      dev::sample_missing_counts(g.layA, g.P4, g.W, g.p_loc, g.n, ccount, sh.stream);
-      GKB_LAUNCH_CHECK();
-      std::vector<int64_t> cc((size_t)g.n), cp((size_t)g.n + 1, 0);
-      GKB_CUDA(cudaMemcpyAsync(cc.data(), ccount, sizeof(int64_t) * (size_t)g.n,
-                               cudaMemcpyDeviceToHost, sh.stream));
-      GKB_CUDA(cudaStreamSynchronize(sh.stream));
-      cudaFree(ccount);
-      for (int64_t s = 0; s < g.n; ++s) cp[s + 1] = cp[s] + cc[s];
-      if (cp[g.n] != g.nmissing) fail(GKB_ECUDA, "missing-list count mismatch");
-      GKB_CUDA(cudaMalloc(&g.col_ptr, sizeof(int64_t) * cp.size()));
-      GKB_CUDA(cudaMemcpy(g.col_ptr, cp.data(), sizeof(int64_t) * cp.size(), cudaMemcpyHostToDevice));
-      GKB_CUDA(cudaMalloc(&g.col_idx, sizeof(int32_t) * (size_t)g.nmissing));
-      dev::fill_missing_cols(g.layA, g.P4, g.W, g.p_loc, g.n, g.col_ptr, g.col_idx, sh.stream);
-      GKB_LAUNCH_CHECK();
-    }
+    g.nmissing = 0;
+    for (int64_t j = 0; j < g.p_loc; ++j) g.nmissing += counts_host[4 * (row0(i) + j) + 3];
     g.k1 = dev::k1_plan(g.W, g.P4);
     g.k2 = dev::k2_plan(g.W, g.P4);
+    g.list_bytes = 0;
+    if (g.nmissing > 0) {
+      const uint4* A = g.layA;
+      const int64_t P4 = g.P4, W = g.W;
+      const dev::K1Plan k1 = g.k1;
+      const dev::K2Plan k2 = g.k2;
+      const int64_t t1 = build_block_lists(
+          k1.grid_x * k1.ntiles, 128, sh.stream, &g.m1_off, &g.m1_base, &g.m1_ent, &g.list_bytes,
+          [&](bool fill, uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent) {
+            dev::miss_lists_k1(A, P4, W, k1, fill, cnt, off, base, ent, sh.stream);
+          });
+      const int64_t t2 = build_block_lists(
+          k2.grid_x * k2.nchunks, 512, sh.stream, &g.m2_off, &g.m2_base, &g.m2_ent, &g.list_bytes,
+          [&](bool fill, uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent) {
+            dev::miss_lists_k2(A, P4, W, k2, fill, cnt, off, base, ent, sh.stream);
+          });
+      if (t1 != g.nmissing || t2 != g.nmissing) fail(GKB_ECUDA, "missing-list count mismatch");
+    }
     GKB_CUDA(cudaMalloc(&g.ypart, sizeof(double) * (size_t)std::max<int64_t>(
                                       (int64_t)g.k1.ntiles * 4 * g.P4, 1)));
-    GKB_CUDA(cudaMalloc(&g.xsum, sizeof(double) * (size_t)g.k1.ntiles));
     GKB_CUDA(cudaMalloc(&g.zpart, sizeof(double) * (size_t)std::max<int64_t>(
                                       (int64_t)g.k2.nchunks * 16 * g.W, 1)));
-    GKB_CUDA(cudaMalloc(&g.kpart, sizeof(double) * (size_t)g.k2.nchunks));
-    GKB_CUDA(cudaMalloc(&g.cmiss, sizeof(double) * (size_t)std::max<int64_t>(4 * g.P4, 4)));
     if (g.k1.smem > 48 * 1024)
       fail(GKB_EINVAL, "K1 tile exceeds 48 KB of shared memory");
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
@@ -381,8 +408,7 @@ void GenoOp::apply_dev(const std::vector<const double*>& x, const std::vector<do
   if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
   for (size_t i = 0; i < gs.size(); ++i) {
     ctx->set_device((int)i);
-    dev::k1_apply(gs[i].view(), gs[i].k1, x[i], gs[i].ypart, gs[i].xsum, y[i],
-                  ctx->shards[i].stream);
+    dev::k1_apply(gs[i].view(), gs[i].k1, x[i], gs[i].ypart, y[i], ctx->shards[i].stream);
     GKB_LAUNCH_CHECK();
   }
 }
@@ -391,8 +417,7 @@ void GenoOp::adjoint_dev(const std::vector<const double*>& y, const std::vector<
   if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
   for (size_t i = 0; i < gs.size(); ++i) {
     ctx->set_device((int)i);
-    dev::k2_adjoint(gs[i].view(), gs[i].k2, y[i], gs[i].zpart, gs[i].kpart, z[i],
-                    ctx->shards[i].stream);
+    dev::k2_adjoint(gs[i].view(), gs[i].k2, y[i], gs[i].zpart, z[i], ctx->shards[i].stream);
     GKB_LAUNCH_CHECK();
   }
   ctx->allreduce(z, n);
@@ -409,7 +434,7 @@ int64_t GenoOp::device_bytes() const {
   int64_t b = 0;
   for (const auto& g : gs) {
     b += 2 * 16 * g.P4 * g.W;
-    b += 8 * g.nmissing + 8 * (g.p_loc + g.n);
+    b += g.list_bytes + 16 * 4 * g.P4;  // missing lists, mu + inv_s
   }
   return b;
 }
