@@ -345,12 +345,12 @@ int gkb_op_bench(gkb_op* op, int which, int iters, int flush_l2, double* ms_per_
       gkb::GenoShard& g = op->geno->gs[0];
       const double t = timed([&] {
         if (flush_l2) flush_all();
-        if (which == 0 || which == 2) gkb::dev::k1_main_only(g.view(), g.k1, xi[0], g.ypart, st);
-        if (which == 1 || which == 2) gkb::dev::k2_main_only(g.view(), g.k2, yc[0], g.zpart, st);
+        if (which == 0 || which == 2) gkb::dev::k1_main_only(g.view(), xi[0], st);
+        if (which == 1 || which == 2) gkb::dev::k2_main_only(g.view(), st);
       });
       GKB_LAUNCH_CHECK();
       main_ms = (t - flush_ms) / iters;
-      launches = (which == 2 ? 4 : 2) * L;
+      launches = (which == 2 ? 6 : 3) * L;  // digitize + main + reduce per product
     } else {
       launches = (which == 2 ? 2 : 1) * L;
     }

@@ -1,27 +1,36 @@
-// Packed-genotype kernels for sm_100a: layout build (K8), marker counts (K7),
-// missing-entry lists, K1 = reference apply (X x, per-SNP dot) and
-// K2 = reference apply_adjoint (X^T y, per-sample sum).
+// Packed-genotype kernels for sm_100a: tile-layout build (K8), marker counts
+// (K7), per-CTA missing lists, coefficient digitization, and the packed
+// matrix-vector products
+//   K1 = reference apply         (X x,   per-SNP dot:   rows = SNPs,    cols = samples)
+//   K2 = reference apply_adjoint (X^T y, per-sample sum: rows = samples, cols = SNPs)
+// which are one kernel (k_pm_main) over two tile layouts of the same matrix.
 //
 // Reference semantics (/root/reference/proj):
 //   .bed code table            genio.cpp:33   (00->2, 01->missing, 10->1, 11->0)
 //   standardized entry          genio.cpp:124-185: (d - mu_j)/s_j, missing -> 0
 //   DenseOperator apply/adjoint linop.hpp:50-58
 //
-// Decode ("denormal injection"): each 2-bit dosage code r
-// of a 32-bit word is masked in place with one LOP3 and used as the low word
-// of an fp64 operand whose high word is 0, i.e. the denormal r * 2^(2k-1074)
-// for field k. One DFMA per genotype accumulates it against a coefficient
-// pre-scaled by 2^(S - E - 2k) (K1) or 2^(S - E) (K2), where E is the block's
-// largest coefficient exponent; products are exact-normal fp64 numbers and
-// the accumulator is rescaled once with scalbn. No constant offset is added,
-// so no precision is lost to cancellation; every sum is a plain fp64 sum in a
-// fixed order.
+// Arithmetic: exact fixed-point digits on the tensor
+// cores. For one CTA's column range (2048 columns) the fp64 coefficients v_c
+// are rounded to 62-bit fixed point relative to the range's largest exponent
+// E, M_c = rn(v_c 2^(62-E)), and split into 8 balanced base-256 digits
+// d_i(c) in [-128, 127]. The 2-bit dosage codes a_rc in {0,1,2,3} (3 =
+// missing) are expanded to u8 fragment registers and
+//   D_i(r) = sum_c a_rc d_i(c)
+// is accumulated EXACTLY in int32 by mma.sync.m16n8k32 (u8 x s8 -> s32; the
+// MMA's N = 8 is the 8 digits). The row value is 2^(E-62) sum_i D_i 256^i,
+// formed in fp64 (one rounding per partial; the only other error is the
+// 2^-63-relative rounding of the coefficients), which is at least as accurate
+// as the reference's fp64 dot products. Integer sums are order-free, and the
+// few fp64 combinations are in a fixed order, so results are bitwise
+// reproducible run to run.
 //
-// Missing entries are stored as r = 3 in the layouts (so the layouts retain
-// the full .bed information); their 3*coef contribution is removed exactly in
-// the main kernels' epilogues, each CTA walking its own block's sorted
-// missing list (16-bit local indices into its shared-memory coefficients).
-// The reduce kernels are plain fixed-order sums of the per-CTA partials.
+// Missing entries stay r = 3 in the layouts (the layouts keep the full .bed
+// information); their contribution is removed exactly in the main kernel's
+// epilogue from the CTA's own sorted missing list (16-bit local column
+// indices), together with the mean term:
+//   K1: y_j = inv_s_j (sum_s a_js x_s - mu_j X - (3 - mu_j) sum_{s miss} x_s)
+//   K2: z_s = sum_j c_j a_js - sum_j c_j mu_j - sum_{j miss} c_j (3 - mu_j),  c_j = inv_s_j y_j
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -34,13 +43,10 @@ namespace dev {
 
 namespace {
 
-constexpr int kS = 1000;  // coefficient scale exponent (see header comment)
 constexpr int kThreads = 256;
-constexpr int kDepth = 4;  // 16-byte loads in flight per thread in the main loops
-
-__device__ __forceinline__ double fld(uint32_t w, int k) {
-  return __hiloint2double(0, (int)(w & (3u << (2 * k))));
-}
+constexpr int kStripsPerWarp = 2;   // row strips sharing each B fragment
+constexpr int kDepth = 2;           // tiles in flight per strip
+constexpr int kRowsPerCta = 8 * kStripsPerWarp * 16;  // 256
 
 // .bed 2-bit code -> dosage code r (r_hi = ~h, r_lo = l ^ h per field).
 __device__ __forceinline__ uint32_t bed_to_r(uint32_t c) {
@@ -58,6 +64,17 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
+}
+
+// 32-bit word (row, word-column wc) of a tile layout: strips of 16 rows,
+// K tiles of 8 words (128 columns); tile = 512 B in mma fragment order,
+// uint4 #(4g + t) = {(g, t), (g+8, t), (g, t+4), (g+8, t+4)} (row, word in tile).
+__device__ __forceinline__ int64_t word_index(int64_t KT, int64_t row, int64_t wc) {
+  const int64_t s = row >> 4;
+  const int gg = (int)(row & 15), g = gg & 7, half = gg >> 3;
+  const int64_t kt = wc >> 3;
+  const int q = (int)(wc & 7), t = q & 3, hi = q >> 2;
+  return ((s * KT + kt) * 32 + 4 * g + t) * 4 + half + 2 * hi;
 }
 
 // Deterministic block sum (fixed shuffle tree, then warps in order).
@@ -98,154 +115,147 @@ __device__ __forceinline__ int exp_of(double v) {
   return e;
 }
 
+__device__ __forceinline__ double pow2(int k) {  // exact 2^k, -1022 <= k <= 1023
+  return __hiloint2double((1023 + k) << 20, 0);
+}
+
 // ---------------------------------------------------------------- K8 / K7
-__global__ void k_build_layouts(const uint8_t* __restrict__ bed, int64_t stride, int64_t rows,
-                                int64_t q_base, int64_t n, int64_t W, int64_t P4,
-                                uint4* __restrict__ layA, uint4* __restrict__ layB) {
-  const int64_t nq = (rows + 3) / 4;
-  const int64_t total = nq * W;
+// .bed records of one staging block (rows [row0, row0+rows) of the shard)
+// -> layout 1 (rows = SNPs): thread per (SNP row, word of 16 samples).
+__global__ void k_build_lt1(const uint8_t* __restrict__ bed, int64_t stride, int64_t rows,
+                            int64_t row0, int64_t n, int64_t W, int64_t KT,
+                            uint32_t* __restrict__ lay) {
+  const int64_t total = rows * W;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t qq = idx / W, w = idx - qq * W;
+    const int64_t rr = idx / W, w = idx - rr * W;
     const int64_t valid = n - 16 * w;
     const uint32_t pad_mask = valid >= 16 ? 0xFFFFFFFFu : ((1u << (2 * valid)) - 1u);
-    uint32_t words[4];
+    const uint8_t* rec = bed + rr * stride;
+    uint32_t v = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t row = 4 * qq + i;
-      uint32_t v = 0;
-      if (row < rows) {
-        const uint8_t* rec = bed + row * stride;
-        const int64_t b0 = 4 * w;
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (b0 + t < stride) v |= (uint32_t)rec[b0 + t] << (8 * t);
-        v = bed_to_r(v) & pad_mask;
-      }
-      words[i] = v;
-    }
-    const uint4 c = make_uint4(words[0], words[1], words[2], words[3]);
-    const int64_t q = q_base + qq;
-    layA[q * W + w] = c;
-    layB[w * P4 + q] = c;
+    for (int t = 0; t < 4; ++t)
+      if (4 * w + t < stride) v |= (uint32_t)rec[4 * w + t] << (8 * t);
+    lay[word_index(KT, row0 + rr, w)] = bed_to_r(v) & pad_mask;
   }
 }
 
-// one warp per SNP quad
-__global__ void k_marker_counts(const uint4* __restrict__ layA, int64_t P4, int64_t W,
-                                int64_t p_loc, int64_t n, int64_t* __restrict__ counts) {
+// -> layout 2 (rows = samples, cols = SNPs): thread per (group of 16 SNP rows,
+// word of 16 samples); a 16 x 16 transpose of 2-bit fields. row0 % 16 == 0.
+__global__ void k_build_lt2(const uint8_t* __restrict__ bed, int64_t stride, int64_t rows,
+                            int64_t row0, int64_t n, int64_t W, int64_t KT,
+                            uint32_t* __restrict__ lay) {
+  const int64_t groups = (rows + 15) / 16;
+  const int64_t total = groups * W;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jg = idx / W, w = idx - jg * W;
+    const int64_t valid = n - 16 * w;
+    const uint32_t pad_mask = valid >= 16 ? 0xFFFFFFFFu : ((1u << (2 * valid)) - 1u);
+    uint32_t out[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) out[k] = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int64_t rr = 16 * jg + i;
+      uint32_t v = 0;
+      if (rr < rows) {
+        const uint8_t* rec = bed + rr * stride;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (4 * w + t < stride) v |= (uint32_t)rec[4 * w + t] << (8 * t);
+        v = bed_to_r(v) & pad_mask;
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) out[k] |= ((v >> (2 * k)) & 3u) << (2 * i);
+    }
+    const int64_t wc = (row0 >> 4) + jg;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int64_t s = 16 * w + k;
+      if (s < n) lay[word_index(KT, s, wc)] = out[k];
+    }
+  }
+}
+
+// one warp per SNP row of layout 1: [n0, n1, n2, nmiss]
+__global__ void k_marker_counts(const uint32_t* __restrict__ lay, int64_t KT, int64_t p_loc,
+                                int64_t W, int64_t n, int64_t* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < P4; q += warps) {
-    int c1[4] = {0, 0, 0, 0}, c2[4] = {0, 0, 0, 0}, c3[4] = {0, 0, 0, 0};
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < p_loc; j += warps) {
+    int c1 = 0, c2 = 0, c3 = 0;
     for (int64_t w = lane; w < W; w += 32) {
-      const uint4 v = layA[q * W + w];
-      const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t r = ws[i], hi = (r >> 1) & 0x55555555u, lo = r & 0x55555555u;
-        c3[i] += __popc(hi & lo);
-        c2[i] += __popc(hi & ~lo);
-        c1[i] += __popc(~hi & lo & 0x55555555u);
-      }
+      const uint32_t r = lay[word_index(KT, j, w)], hi = (r >> 1) & 0x55555555u,
+                     lo = r & 0x55555555u;
+      c3 += __popc(hi & lo);
+      c2 += __popc(hi & ~lo);
+      c1 += __popc(~hi & lo & 0x55555555u);
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      for (int o = 16; o > 0; o >>= 1) {
-        c1[i] += __shfl_down_sync(0xffffffffu, c1[i], o);
-        c2[i] += __shfl_down_sync(0xffffffffu, c2[i], o);
-        c3[i] += __shfl_down_sync(0xffffffffu, c3[i], o);
-      }
+    for (int o = 16; o > 0; o >>= 1) {
+      c1 += __shfl_down_sync(0xffffffffu, c1, o);
+      c2 += __shfl_down_sync(0xffffffffu, c2, o);
+      c3 += __shfl_down_sync(0xffffffffu, c3, o);
+    }
     if (lane == 0) {
-      for (int i = 0; i < 4; ++i) {
-        const int64_t j = 4 * q + i;
-        if (j >= p_loc) break;
-        counts[4 * j + 0] = n - c1[i] - c2[i] - c3[i];
-        counts[4 * j + 1] = c1[i];
-        counts[4 * j + 2] = c2[i];
-        counts[4 * j + 3] = c3[i];
-      }
+      counts[4 * j + 0] = n - c1 - c2 - c3;
+      counts[4 * j + 1] = c1;
+      counts[4 * j + 2] = c2;
+      counts[4 * j + 3] = c3;
     }
+  }
+}
+
+__global__ void k_layout_to_bed(const uint32_t* __restrict__ lay, int64_t KT, int64_t n,
+                                int64_t row0, int64_t nrows, uint8_t* __restrict__ out) {
+  const int64_t stride = (n + 3) / 4, W = (n + 15) / 16;
+  const int64_t total = nrows * W;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rr = idx / W, w = idx - rr * W;
+    uint32_t c = r_to_bed(lay[word_index(KT, row0 + rr, w)]);
+    const int64_t valid = n - 16 * w;
+    if (valid < 16) c &= (1u << (2 * valid)) - 1u;  // pads 00 (genio.cpp:100)
+    uint8_t* rec = out + rr * stride;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (4 * w + t < stride) rec[4 * w + t] = (uint8_t)(c >> (8 * t));
   }
 }
 
 // ---------------------------------------------------------------- missing lists
-// Per-CTA missing lists. The missing entries of one
-// main-kernel CTA's block are stored in that block's own segment, grouped by
-// the output the owning thread writes and sorted ascending, as 16-bit local
-// indices:
-//   K1 block (qb, tile): 128 SNP rows 4*lane+i, entries = sample offset in the tile (< 4096)
-//   K2 block (wb, chunk): 512 samples 16*lane+k, entries = SNP offset in the chunk (< 2048)
-// Block b's row r owns ent[base[b] + off[b*(span+1)+r] .. base[b] + off[b*(span+1)+r+1]).
-// Count pass (kFill = false) writes cnt[b*span + r]; fill pass writes ent.
+// Per-CTA missing lists: block b = kc * grid_x + bx
+// covers rows [256 bx, 256 bx + 256) x columns [2048 kc, 2048 kc + 2048) of a
+// tile layout -- exactly one k_pm_main CTA. Row r of the block owns
+//   ent[base[b] + off[b*257 + r] .. base[b] + off[b*257 + r + 1])
+// = the block-local column indices (< 2048, ascending) of its missing entries.
+// Count pass (kFill = false) writes cnt[b*256 + r]; fill pass writes ent.
 template <bool kFill>
-__global__ void __launch_bounds__(128) k_miss_k1(const uint4* __restrict__ layA, int64_t P4,
-                                                 int64_t W, int tileW, uint32_t* __restrict__ cnt,
-                                                 const uint32_t* __restrict__ off,
-                                                 const int64_t* __restrict__ base,
-                                                 uint16_t* __restrict__ ent) {
+__global__ void __launch_bounds__(256) k_miss_tiles(const uint32_t* __restrict__ lay, int64_t KT,
+                                                    int kt_cta, uint32_t* __restrict__ cnt,
+                                                    const uint32_t* __restrict__ off,
+                                                    const int64_t* __restrict__ base,
+                                                    uint16_t* __restrict__ ent) {
   const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-  const int t = threadIdx.x;  // row 4*lane + i of the K1 epilogue
-  const int64_t q = (int64_t)blockIdx.x * 32 + (t >> 2);
-  const int i = t & 3;
-  const int64_t w0 = (int64_t)blockIdx.y * tileW, w1 = min(W, w0 + tileW);
+  const int r = threadIdx.x;
+  const int64_t row = (int64_t)blockIdx.x * kRowsPerCta + r;
+  const int64_t wc0 = (int64_t)blockIdx.y * kt_cta * 8;
+  const int64_t wc1 = min(KT * 8, wc0 + (int64_t)kt_cta * 8);
   uint32_t c = 0;
-  int64_t pos = kFill ? base[b] + off[b * 129 + t] : 0;
-  if (q < P4)
-    for (int64_t w = w0; w < w1; ++w) {
-      const uint4 v = layA[q * W + w];
-      uint32_t m = missing_mask(i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w);
-      if (kFill) {
-        while (m) {
-          const int bit = __ffs(m) - 1;
-          ent[pos++] = (uint16_t)(16 * (w - w0) + (bit >> 1));
-          m &= m - 1;
-        }
-      } else {
-        c += __popc(m);
+  int64_t pos = kFill ? base[b] + off[b * (kRowsPerCta + 1) + r] : 0;
+  for (int64_t wc = wc0; wc < wc1; ++wc) {
+    uint32_t m = missing_mask(lay[word_index(KT, row, wc)]);
+    if (kFill) {
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        ent[pos++] = (uint16_t)(16 * (wc - wc0) + (bit >> 1));
+        m &= m - 1;
       }
+    } else {
+      c += __popc(m);
     }
-  if (!kFill) cnt[b * 128 + t] = c;
-}
-
-template <bool kFill>
-__global__ void __launch_bounds__(32) k_miss_k2(const uint4* __restrict__ layA, int64_t P4,
-                                                int64_t W, int qc, uint32_t* __restrict__ cnt,
-                                                const uint32_t* __restrict__ off,
-                                                const int64_t* __restrict__ base,
-                                                uint16_t* __restrict__ ent) {
-  const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-  const int lane = threadIdx.x;
-  const int64_t w = (int64_t)blockIdx.x * 32 + lane;
-  const int64_t q0 = (int64_t)blockIdx.y * qc, q1 = min(P4, q0 + qc);
-  uint32_t c[16];
-  int64_t pos[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    c[k] = 0;
-    pos[k] = kFill ? base[b] + off[b * 513 + 16 * lane + k] : 0;
   }
-  if (w < W)
-    for (int64_t q = q0; q < q1; ++q) {
-      const uint4 v = layA[q * W + w];
-      const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t m = missing_mask(ws[i]);
-        if (m == 0) continue;
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if ((m >> (2 * k)) & 1u) {
-            if (kFill)
-              ent[pos[k]++] = (uint16_t)(4 * (q - q0) + i);
-            else
-              ++c[k];
-          }
-      }
-    }
-  if (!kFill)
-#pragma unroll
-    for (int k = 0; k < 16; ++k) cnt[b * 512 + 16 * lane + k] = c[k];
+  if (!kFill) cnt[b * kRowsPerCta + r] = c;
 }
 
 // CTA per block: exclusive scan of the block's span counts -> off, block total -> tot.
@@ -268,320 +278,222 @@ __global__ void __launch_bounds__(512) k_block_scan(const uint32_t* __restrict__
   if (t == span - 1) tot[b] = s[t];
 }
 
-__global__ void k_layout_to_bed(const uint4* __restrict__ layA, int64_t P4, int64_t W, int64_t n,
-                                int64_t row0, int64_t nrows, uint8_t* __restrict__ out) {
-  const int64_t stride = (n + 3) / 4;
-  const int64_t total = nrows * W;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rr = idx / W, w = idx - rr * W;
-    const int64_t j = row0 + rr;
-    const uint4 v = layA[(j >> 2) * W + w];
-    const int i = (int)(j & 3);
-    const uint32_t r = i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-    uint32_t c = r_to_bed(r);
-    const int64_t valid = n - 16 * w;
-    if (valid < 16) c &= (1u << (2 * valid)) - 1u;  // pads 00 (genio.cpp:100)
-    uint8_t* rec = out + rr * stride;
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (4 * w + t < stride) rec[4 * w + t] = (uint8_t)(c >> (8 * t));
-  }
-}
-
-// ---------------------------------------------------------------- K1 apply
-// One 16-byte chunk: 4 SNP words x 16 samples against the 16 (scaled) sample
-// coefficients of that word position.
-__device__ __forceinline__ void k1_word(const uint4 c, const double2* __restrict__ cf, double& a0,
-                                        double& a1, double& a2, double& a3) {
-#pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
-    const double2 xx = cf[kk];
-    a0 = fma(fld(c.x, 2 * kk), xx.x, a0);
-    a1 = fma(fld(c.y, 2 * kk), xx.x, a1);
-    a2 = fma(fld(c.z, 2 * kk), xx.x, a2);
-    a3 = fma(fld(c.w, 2 * kk), xx.x, a3);
-    a0 = fma(fld(c.x, 2 * kk + 1), xx.y, a0);
-    a1 = fma(fld(c.y, 2 * kk + 1), xx.y, a1);
-    a2 = fma(fld(c.z, 2 * kk + 1), xx.y, a2);
-    a3 = fma(fld(c.w, 2 * kk + 1), xx.y, a3);
-  }
-}
-
-// One 16-byte chunk of layout A: 4 SNP words x the lane's 16 samples.
-__device__ __forceinline__ void k2_quad(const uint4 c, const double2 ca, const double2 cb,
-                                        double (&acc)[16]) {
-#pragma unroll
-  for (int k = 0; k < 16; ++k) acc[k] = fma(fld(c.x, k), ca.x, acc[k]);
-#pragma unroll
-  for (int k = 0; k < 16; ++k) acc[k] = fma(fld(c.y, k), ca.y, acc[k]);
-#pragma unroll
-  for (int k = 0; k < 16; ++k) acc[k] = fma(fld(c.z, k), cb.x, acc[k]);
-#pragma unroll
-  for (int k = 0; k < 16; ++k) acc[k] = fma(fld(c.w, k), cb.y, acc[k]);
-}
-// grid (ceil(P4/32), ntiles). Lane = SNP quad q (4 SNPs), loops over the
-// tile's word positions; lanes read 32 consecutive 16-byte chunks (512 B).
-__global__ void __launch_bounds__(kThreads) k1_main(const uint4* __restrict__ layB, int64_t P4,
-                                                    int64_t W, const double* __restrict__ x,
-                                                    int64_t n, int tileW,
-                                                    const double* __restrict__ mu,
-                                                    const uint32_t* __restrict__ m_off,
-                                                    const int64_t* __restrict__ m_base,
-                                                    const uint16_t* __restrict__ m_ent,
-                                                    double* __restrict__ ypart) {
-  extern __shared__ double2 xp2[];  // tileW * 8 double2: scaled coefficients
+// ---------------------------------------------------------------- digitize
+// One CTA per column range kc (kt_cta * 128 columns): coefficients v_c
+//   MODE 0 (K1): v_c = x_c,            sum = sum_c v_c           (X of the range)
+//   MODE 1 (K2): v_c = inv_s_c * y_c,  sum = sum_c v_c mu_c, cm_c = v_c (3 - mu_c)
+// -> E (largest exponent), 8 balanced base-256 digits of rn(v 2^(62-E)) in
+// mma B-fragment order: uint4 (word-column wc, digit i) holds, in 32-bit word
+// q, byte e = digit i of column 16 wc + 4 e + q.
+template <int MODE>
+__global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_in,
+                                                   const double* __restrict__ inv_s,
+                                                   const double* __restrict__ mu, int64_t C,
+                                                   int kt_cta, uint4* __restrict__ dig,
+                                                   int* __restrict__ dexp,
+                                                   double* __restrict__ dsum,
+                                                   double* __restrict__ cm) {
+  extern __shared__ uint4 dsm[];  // kt_cta * 64 uint4 (digits), then kt_cta * 128 doubles
   __shared__ double red[33];
   __shared__ int redi[33];
-  double* xp = reinterpret_cast<double*>(xp2);
-  const int tile = blockIdx.y;
-  const int64_t w0 = (int64_t)tile * tileW;
-  const int64_t w1 = min(W, w0 + tileW);
-  const int nw = (int)(w1 - w0);
-  const int ns = nw * 16;
-
+  double* vals = reinterpret_cast<double*>(dsm + kt_cta * 64);
+  uint8_t* db = reinterpret_cast<uint8_t*>(dsm);
+  const int kc = blockIdx.x;
+  const int ncol = kt_cta * 128;
+  const int64_t c0 = (int64_t)kc * ncol;
   int emax = -1100;
   double part = 0.0;
-  for (int t = threadIdx.x; t < ns; t += kThreads) {
-    const int64_t sidx = 16 * w0 + t;
-    const double xv = sidx < n ? x[sidx] : 0.0;
-    emax = max(emax, exp_of(xv));
-    part += xv;
-    xp[t] = xv;
+  for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
+    const int64_t c = c0 + t;
+    double v = 0.0;
+    if (c < C) {
+      if (MODE == 0) {
+        v = v_in[c];
+        part += v;
+      } else {
+        v = inv_s[c] * v_in[c];
+        const double m = mu[c];
+        part += v * m;
+        cm[c] = v * (3.0 - m);
+      }
+    }
+    emax = max(emax, exp_of(v));
+    vals[t] = v;
   }
   const int E = block_max_int(emax, redi);
-  const double tsum = block_sum(part, red);
-  for (int t = threadIdx.x; t < ns; t += kThreads) xp[t] = scalbn(xp[t], kS - E - 2 * (t & 15));
-  __syncthreads();
-
-  // Lane = SNP quad (32 consecutive quads per CTA, 512-B coalesced rows of
-  // layout B); warp w takes the w-th eighth of the tile's word positions, and
-  // the 8 warp partials are added in warp order through shared memory.
-  __shared__ double wsum[8][4][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t q = (int64_t)blockIdx.x * 32 + lane;
-  const int sub = (nw + 7) / 8;
-  const int wa = min(nw, warp * sub), we = min(nw, wa + sub);
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  if (q < P4 && wa < we) {
-    const uint4* src = layB + w0 * P4 + q;
-    const uint4 Z = make_uint4(0, 0, 0, 0);
-    // four 16-byte loads in flight per thread; each slot is refilled right
-    // after it is consumed (no dynamic indexing, no early exits)
-    uint4 c0 = ld_stream(src + (int64_t)wa * P4);
-    uint4 c1 = wa + 1 < we ? ld_stream(src + (int64_t)(wa + 1) * P4) : Z;
-    uint4 c2 = wa + 2 < we ? ld_stream(src + (int64_t)(wa + 2) * P4) : Z;
-    uint4 c3 = wa + 3 < we ? ld_stream(src + (int64_t)(wa + 3) * P4) : Z;
-    int w = wa;
-    for (; w + 4 <= we; w += 4) {
-      k1_word(c0, xp2 + 8 * w, a0, a1, a2, a3);
-      c0 = w + 4 < we ? ld_stream(src + (int64_t)(w + 4) * P4) : Z;
-      k1_word(c1, xp2 + 8 * (w + 1), a0, a1, a2, a3);
-      c1 = w + 5 < we ? ld_stream(src + (int64_t)(w + 5) * P4) : Z;
-      k1_word(c2, xp2 + 8 * (w + 2), a0, a1, a2, a3);
-      c2 = w + 6 < we ? ld_stream(src + (int64_t)(w + 6) * P4) : Z;
-      k1_word(c3, xp2 + 8 * (w + 3), a0, a1, a2, a3);
-      c3 = w + 7 < we ? ld_stream(src + (int64_t)(w + 7) * P4) : Z;
+  const double s = block_sum(part, red);
+  for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
+    long long M = __double2ll_rn(scalbn(vals[t], 62 - E));
+    const int wc = t >> 4, k = t & 15, q = k & 3, e = k >> 2;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int d = (int)(signed char)(M & 0xFF);
+      M = (M - d) >> 8;
+      db[(wc * 8 + i) * 16 + 4 * q + e] = (uint8_t)d;
     }
-    if (w < we) k1_word(c0, xp2 + 8 * w, a0, a1, a2, a3);
-    if (w + 1 < we) k1_word(c1, xp2 + 8 * (w + 1), a0, a1, a2, a3);
-    if (w + 2 < we) k1_word(c2, xp2 + 8 * (w + 2), a0, a1, a2, a3);
   }
-  wsum[warp][0][lane] = a0;
-  wsum[warp][1][lane] = a1;
-  wsum[warp][2][lane] = a2;
-  wsum[warp][3][lane] = a3;
   __syncthreads();
-  // Epilogue: thread (i, lane) owns SNP j = 4*(32*blockIdx.x + lane) + i and
-  // writes this tile's exact partial
-  //   sum_{observed s} r_js x_s - mu_j X_tile = sum_s r_js x_s - mu_j X_tile - (3 - mu_j) S_miss
-  // with S_miss summed over the block's own missing list (scaled domain:
-  // xp[s] * 2^(2(s&15)) = x_s * 2^(kS-E), exact).
-  if (threadIdx.x < 128) {
-    const int i = threadIdx.x >> 5;  // SNP within the quad
-    const int64_t qq = (int64_t)blockIdx.x * 32 + lane;
-    if (qq < P4) {
-      double t = 0.0;
+  uint4* out = dig + (int64_t)kc * kt_cta * 64;
+  for (int t = threadIdx.x; t < kt_cta * 64; t += blockDim.x) out[t] = dsm[t];
+  if (threadIdx.x == 0) {
+    dexp[kc] = E;
+    dsum[kc] = s;
+  }
+}
+
+// ---------------------------------------------------------------- main
+__device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// One 512-byte tile (16 rows x 128 columns) against the tile's B fragments:
+// each 32-bit word expands to four u8 registers (w >> 2q) & 0x03030303 =
+// columns 4e + q of the word, e = byte.
+__device__ __forceinline__ void mma_tile(int (&acc)[4], const uint4 w, const uint4 b01,
+                                         const uint4 b23) {
+  const uint32_t m = 0x03030303u;
+  mma_u8s8(acc, w.x & m, w.y & m, (w.x >> 2) & m, (w.y >> 2) & m, b01.x, b01.y);
+  mma_u8s8(acc, (w.x >> 4) & m, (w.y >> 4) & m, (w.x >> 6) & m, (w.y >> 6) & m, b01.z, b01.w);
+  mma_u8s8(acc, w.z & m, w.w & m, (w.z >> 2) & m, (w.w >> 2) & m, b23.x, b23.y);
+  mma_u8s8(acc, (w.z >> 4) & m, (w.w >> 4) & m, (w.z >> 6) & m, (w.w >> 6) & m, b23.z, b23.w);
+}
+
+// grid (S / 16, nkc). CTA = 8 warps x 2 strips (256 rows) x one column range
+// of kt_cta tiles; B fragments (digits) of the range in shared memory, shared
+// by the 8 warps and reused across each warp's 2 strips. Writes the range's
+// exact partial (MODE 0: K1, MODE 1: K2 -- see the header) to part[kc][row].
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 4) k_pm_main(
+    const uint4* __restrict__ lay, int64_t KT, int kt_cta, const uint4* __restrict__ dig,
+    const int* __restrict__ dexp, const double* __restrict__ dsum,
+    const double* __restrict__ cval, const double* __restrict__ mu,
+    const uint32_t* __restrict__ m_off, const int64_t* __restrict__ m_base,
+    const uint16_t* __restrict__ m_ent, int64_t rows_pad, double* __restrict__ part) {
+  extern __shared__ uint4 dg[];  // kt_cta * 64
+  const int kc = blockIdx.y;
+  const int64_t kt0 = (int64_t)kc * kt_cta;
+  const int ktiles = (int)min((int64_t)kt_cta, KT - kt0);
+  {
+    const uint4* gd = dig + kt0 * 64;
+    for (int i = threadIdx.x; i < ktiles * 64; i += kThreads) dg[i] = gd[i];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tid = lane & 3;
+  const int64_t strip0 = ((int64_t)blockIdx.x * 8 + warp) * kStripsPerWarp;
+  const uint4* src = lay + (strip0 * KT + kt0) * 32 + lane;
+  const uint4 Z = make_uint4(0, 0, 0, 0);
+  int acc[kStripsPerWarp][4];
+  uint4 buf[kDepth][kStripsPerWarp];
 #pragma unroll
-      for (int w = 0; w < 8; ++w) t += wsum[w][i][lane];
-      const double m = mu[4 * qq + i];
-      double v = scalbn(t, 1074 - kS + E) - m * tsum;
-      if (m_off) {
-        const int64_t b = (int64_t)tile * gridDim.x + blockIdx.x;
-        const uint32_t* o = m_off + b * 129 + 4 * lane + i;
-        const uint16_t* e = m_ent + m_base[b];
-        const uint32_t e0 = o[0], e1 = o[1];
-        double sm = 0.0;
-        uint32_t k = e0;
-        for (; k + 8 <= e1; k += 8) {  // 8 index loads in flight, summed in order
-          int s[8];
+  for (int r = 0; r < kStripsPerWarp; ++r) {
+    acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) s[u] = e[k + u];
+    for (int d = 0; d < kDepth; ++d)
+      buf[d][r] = d < ktiles ? ld_stream(src + r * KT * 32 + d * 32) : Z;
+  }
+  __syncthreads();
+  for (int kt = 0; kt < ktiles; kt += kDepth) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            sm += xp[s[u]] * __hiloint2double((1023 + 2 * (s[u] & 15)) << 20, 0);
+    for (int d = 0; d < kDepth; ++d) {
+      if (kt + d < ktiles) {
+        const uint4 b01 = dg[((kt + d) * 8 + tid) * 8 + g];
+        const uint4 b23 = dg[((kt + d) * 8 + tid + 4) * 8 + g];
+#pragma unroll
+        for (int r = 0; r < kStripsPerWarp; ++r) {
+          const uint4 w = buf[d][r];
+          if (kt + d + kDepth < ktiles)
+            buf[d][r] = ld_stream(src + r * KT * 32 + (kt + d + kDepth) * 32);
+          mma_tile(acc[r], w, b01, b23);
         }
-        for (; k < e1; ++k) {
-          const int s1 = e[k];
-          sm += xp[s1] * __hiloint2double((1023 + 2 * (s1 & 15)) << 20, 0);
-        }
-        if (e1 > e0) v -= (3.0 - m) * scalbn(sm, E - kS);
       }
-      ypart[(int64_t)tile * 4 * P4 + 4 * qq + i] = v;
+    }
+  }
+  // Epilogue. Thread (g, tid) holds digits (2 tid, 2 tid + 1) of rows g and
+  // g + 8; 2^(16 tid) (D_2tid + 256 D_2tid+1) is exact in fp64, and the four
+  // threads of the group add their parts by a butterfly (identical bits in
+  // all four). Rows: tid 0/2 -> row g, tid 1/3 -> row g + 8; the two threads
+  // of a row each walk half of its missing list.
+  const int E = dexp[kc];
+  const double rsum = dsum[kc];
+  const double p0 = pow2(16 * tid), p1 = pow2(16 * tid + 8);
+  const int64_t b = (int64_t)kc * gridDim.x + blockIdx.x;
+  const int64_t col0 = kt0 * 128;
+#pragma unroll
+  for (int r = 0; r < kStripsPerWarp; ++r) {
+    double v0 = (double)acc[r][0] * p0 + (double)acc[r][1] * p1;
+    double v1 = (double)acc[r][2] * p0 + (double)acc[r][3] * p1;
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+    const int hi = tid & 1;
+    const int64_t row = (strip0 + r) * 16 + g + 8 * hi;
+    const double val = scalbn(hi ? v1 : v0, E - 62);
+    double corr = 0.0;
+    if (m_off) {
+      const int rl = (int)(row - (int64_t)blockIdx.x * kRowsPerCta);
+      const uint32_t* o = m_off + b * (kRowsPerCta + 1) + rl;
+      const uint16_t* e = m_ent + m_base[b];
+      const uint32_t e0 = o[0], e1 = o[1], mid = e0 + (e1 - e0) / 2;
+      uint32_t k = (tid >> 1) ? mid : e0;
+      const uint32_t ke = (tid >> 1) ? e1 : mid;
+      for (; k + 4 <= ke; k += 4) {  // 4 index loads in flight, summed in order
+        const int c0 = e[k], c1 = e[k + 1], c2 = e[k + 2], c3 = e[k + 3];
+        corr += cval[col0 + c0];
+        corr += cval[col0 + c1];
+        corr += cval[col0 + c2];
+        corr += cval[col0 + c3];
+      }
+      for (; k < ke; ++k) corr += cval[col0 + e[k]];
+      corr += __shfl_xor_sync(0xffffffffu, corr, 2);  // both halves, commutative -> same bits
+    }
+    if ((tid >> 1) == 0) {
+      double out;
+      if (MODE == 0) {
+        const double m = mu[row];
+        out = val - m * rsum - (3.0 - m) * corr;
+      } else {
+        out = val - rsum - corr;
+      }
+      part[(int64_t)kc * rows_pad + row] = out;
     }
   }
 }
 
-// y_j = inv_s_j * sum_t ypart[t][j]  (tiles in order -> deterministic)
-__global__ void k1_reduce(const double* __restrict__ ypart, int ntiles, int64_t P4, int64_t p_loc,
-                          const double* __restrict__ inv_s, double* __restrict__ y) {
+// K1 finish: y_j = inv_s_j * sum_kc part[kc][j] (ranges in order)
+__global__ void k1_reduce(const double* __restrict__ part, int nkc, int64_t rows_pad,
+                          int64_t p_loc, const double* __restrict__ inv_s,
+                          double* __restrict__ y) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= p_loc) return;
   double acc = 0.0;
-  for (int t = 0; t < ntiles; ++t) acc += ypart[(int64_t)t * 4 * P4 + j];
+  for (int c = 0; c < nkc; ++c) acc += part[(int64_t)c * rows_pad + j];
   y[j] = inv_s[j] * acc;
 }
 
-// ---------------------------------------------------------------- K2 adjoint
-// grid (ceil(W/32), nchunks). Lane = word position w (16 samples, 16
-// accumulators); loops over the chunk's SNP quads; lanes read 32 consecutive
-// 16-byte chunks of one quad row (512 B).
-template <int kMinB>
-__global__ void __launch_bounds__(kThreads, kMinB) k2_main(const uint4* __restrict__ layA, int64_t P4,
-                                                    int64_t W, const double* __restrict__ y,
-                                                    const double* __restrict__ mu,
-                                                    const double* __restrict__ inv_s,
-                                                    int64_t p_loc, int qc,
-                                                    const uint32_t* __restrict__ m_off,
-                                                    const int64_t* __restrict__ m_base,
-                                                    const uint16_t* __restrict__ m_ent,
-                                                    double* __restrict__ zpart) {
-  // dynamic smem: cs = max(4*qc, 2048) scaled coefficients (reused for the
-  // cross-warp combine), then cm = 4*qc missing-entry corrections c_j (3 - mu_j)
-  extern __shared__ double2 cs2[];
-  __shared__ double red[33];
-  __shared__ int redi[33];
-  double* cs = reinterpret_cast<double*>(cs2);
-  double* cm = cs + max(4 * qc, 2048);
-  const int chunk = blockIdx.y;
-  const int64_t q0 = (int64_t)chunk * qc;
-  const int64_t q1 = min(P4, q0 + qc);
-  const int nq = (int)(q1 - q0);
-
-  int emax = -1100;
-  double kp = 0.0;
-  for (int t = threadIdx.x; t < 4 * nq; t += kThreads) {
-    const int64_t j = 4 * q0 + t;
-    const double c = j < p_loc ? inv_s[j] * y[j] : 0.0;
-    emax = max(emax, exp_of(c));
-    const double m = j < p_loc ? mu[j] : 0.0;
-    kp += c * m;
-    if (m_off) cm[t] = c * (3.0 - m);
-    cs[t] = c;
-  }
-  {
-    const int E = block_max_int(emax, redi);
-    block_sum(kp, red);  // chunk's sum_j c_j mu_j, left in red[32]
-    for (int t = threadIdx.x; t < 4 * nq; t += kThreads) cs[t] = scalbn(cs[t], kS - E);
-  }
-  __syncthreads();
-
-  // Lane = word position (32 consecutive words, 512-B coalesced rows of
-  // layout A); warp w takes the w-th eighth of the chunk's SNP quads; the 8
-  // warp partials are added in warp order through shared memory.
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t w = (int64_t)blockIdx.x * 32 + lane;
-  const int sub = (nq + 7) / 8;
-  const int qa = min(nq, warp * sub), qe = min(nq, qa + sub);
-  double acc[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) acc[k] = 0.0;
-  if (w < W && qa < qe) {
-    const uint4* src = layA + q0 * W + w;
-    const uint4 Z = make_uint4(0, 0, 0, 0);
-    uint4 c0 = ld_stream(src + (int64_t)qa * W);
-    uint4 c1 = qa + 1 < qe ? ld_stream(src + (int64_t)(qa + 1) * W) : Z;
-    uint4 c2 = qa + 2 < qe ? ld_stream(src + (int64_t)(qa + 2) * W) : Z;
-    uint4 c3 = qa + 3 < qe ? ld_stream(src + (int64_t)(qa + 3) * W) : Z;
-    int qq = qa;
-    for (; qq + 4 <= qe; qq += 4) {
-      k2_quad(c0, cs2[2 * qq], cs2[2 * qq + 1], acc);
-      c0 = qq + 4 < qe ? ld_stream(src + (int64_t)(qq + 4) * W) : Z;
-      k2_quad(c1, cs2[2 * qq + 2], cs2[2 * qq + 3], acc);
-      c1 = qq + 5 < qe ? ld_stream(src + (int64_t)(qq + 5) * W) : Z;
-      k2_quad(c2, cs2[2 * qq + 4], cs2[2 * qq + 5], acc);
-      c2 = qq + 6 < qe ? ld_stream(src + (int64_t)(qq + 6) * W) : Z;
-      k2_quad(c3, cs2[2 * qq + 6], cs2[2 * qq + 7], acc);
-      c3 = qq + 7 < qe ? ld_stream(src + (int64_t)(qq + 7) * W) : Z;
-    }
-    if (qq < qe) k2_quad(c0, cs2[2 * qq], cs2[2 * qq + 1], acc);
-    if (qq + 1 < qe) k2_quad(c1, cs2[2 * qq + 2], cs2[2 * qq + 3], acc);
-    if (qq + 2 < qe) k2_quad(c2, cs2[2 * qq + 4], cs2[2 * qq + 5], acc);
-  }
-  // cross-warp combine in two halves of 8 fields (16 KB of the coefficient
-  // region, which is sized >= 2048 doubles). Thread (k_out, lane) owns sample
-  // 16*w_out + field and writes the chunk's exact partial
-  //   sum_j c_j r_js - sum_j c_j mu_j - sum_{j in miss(s)} c_j (3 - mu_j)
-  // with the last sum over the block's own missing list.
-  // E and ksum are re-read from shared memory (volatile: not kept live in
-  // registers across the main loop, which runs at the 64-register cap)
-  const int E = *reinterpret_cast<volatile int*>(&redi[32]);
-  const double ksum = *reinterpret_cast<volatile double*>(&red[32]);
-  double* part = cs;
-  const int k_out = threadIdx.x >> 5;  // field within the half, 0..7
-  const int64_t w_out = (int64_t)blockIdx.x * 32 + lane;
-  double* out = zpart + (int64_t)chunk * 16 * W;
-  const int64_t b = (int64_t)chunk * gridDim.x + blockIdx.x;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 8; ++k) part[(warp * 8 + k) * 32 + lane] = acc[8 * h + k];
-    __syncthreads();
-    double t = 0.0;
-#pragma unroll
-    for (int ww = 0; ww < 8; ++ww) t += part[(ww * 8 + k_out) * 32 + lane];
-    const int field = 8 * h + k_out;
-    if (w_out < W) {
-      double v = scalbn(t, 1074 - kS + E - 2 * field) - ksum;
-      if (m_off) {
-        const uint32_t* o = m_off + b * 513 + 16 * lane + field;
-        const uint16_t* e = m_ent + m_base[b];
-        const uint32_t e0 = o[0], e1 = o[1];
-        double corr = 0.0;
-        uint32_t k = e0;
-        for (; k + 8 <= e1; k += 8) {  // 8 index loads in flight, summed in order
-          int jj[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) jj[u] = e[k + u];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) corr += cm[jj[u]];
-        }
-        for (; k < e1; ++k) corr += cm[e[k]];
-        v -= corr;
-      }
-      out[16 * w_out + field] = v;
-    }
-  }
-}
-
-// z_s = sum_c zpart[c][s] (chunks in a fixed order -> deterministic).
-// Block = 32 warps x 32 consecutive samples: warp w sums chunks c = w (mod 32)
-// with lanes on consecutive samples (coalesced); partials added in warp order.
-__global__ void __launch_bounds__(1024) k2_reduce(const double* __restrict__ zpart, int nchunks,
-                                                  int64_t W, int64_t n, double* __restrict__ z) {
-  __shared__ double part[32][33];
+// K2 finish: z_s = sum_kc part[kc][s]. Block = 32 warps x 32 consecutive
+// samples: warp w sums ranges kc = w (mod 32) with lanes on consecutive
+// samples (coalesced); partials added in warp order -> deterministic.
+__global__ void __launch_bounds__(1024) k2_reduce(const double* __restrict__ part, int nkc,
+                                                  int64_t rows_pad, int64_t n,
+                                                  double* __restrict__ z) {
+  __shared__ double ps[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t s = (int64_t)blockIdx.x * 32 + lane;
   double acc = 0.0;
   if (s < n)
 #pragma unroll 4
-    for (int c = warp; c < nchunks; c += 32) acc += zpart[(int64_t)c * 16 * W + s];
-  part[warp][lane] = acc;
+    for (int c = warp; c < nkc; c += 32) acc += part[(int64_t)c * rows_pad + s];
+  ps[warp][lane] = acc;
   __syncthreads();
   if (warp == 0 && s < n) {
     double t = 0.0;
-    for (int w = 0; w < 32; ++w) t += part[w][lane];
+    for (int w = 0; w < 32; ++w) t += ps[w][lane];
     z[s] = t;
   }
 }
@@ -595,38 +507,63 @@ int grid_for(int64_t work, int threads, int cap = 148 * 16) {
 
 }  // namespace
 
-void build_layouts(const uint8_t* bed, int64_t stride_bytes, int64_t rows_in_block, int64_t q_base,
-                   int64_t n, int64_t W, int64_t P4, uint4* layA, uint4* layB, cudaStream_t s) {
-  const int64_t work = ((rows_in_block + 3) / 4) * W;
+// ---------------------------------------------------------------- host side
+PMPlan pm_plan(int64_t R, int64_t C) {
+  PMPlan pl;
+  pl.R = R;
+  pl.C = C;
+  pl.S = ((R + 15) / 16 + 15) / 16 * 16;  // strips, padded to whole CTAs
+  if (pl.S < 16) pl.S = 16;
+  pl.KT = (C + 127) / 128;
+  if (pl.KT < 1) pl.KT = 1;
+  pl.kt_cta = 16;  // 2048 columns per CTA (16 KB of digits)
+  pl.nkc = (int)((pl.KT + pl.kt_cta - 1) / pl.kt_cta);
+  pl.grid_x = pl.S / 16;
+  pl.rows_pad = pl.S * 16;
+  pl.smem = (size_t)pl.kt_cta * 64 * sizeof(uint4);
+  pl.dig_smem = (size_t)pl.kt_cta * 64 * sizeof(uint4) + (size_t)pl.kt_cta * 128 * sizeof(double);
+  return pl;
+}
+
+int64_t pm_words(const PMPlan& pl) { return pl.S * pl.KT * 128; }
+
+void build_lt1(const uint8_t* bed, int64_t stride_bytes, int64_t rows, int64_t row0, int64_t n,
+               const PMPlan& pl, uint32_t* lay, cudaStream_t s) {
+  const int64_t W = (n + 15) / 16;
+  if (rows * W == 0) return;
+  k_build_lt1<<<grid_for(rows * W, 256), 256, 0, s>>>(bed, stride_bytes, rows, row0, n, W, pl.KT,
+                                                      lay);
+}
+
+void build_lt2(const uint8_t* bed, int64_t stride_bytes, int64_t rows, int64_t row0, int64_t n,
+               const PMPlan& pl, uint32_t* lay, cudaStream_t s) {
+  const int64_t W = (n + 15) / 16;
+  const int64_t work = ((rows + 15) / 16) * W;
   if (work == 0) return;
-  k_build_layouts<<<grid_for(work, 256), 256, 0, s>>>(bed, stride_bytes, rows_in_block, q_base, n,
-                                                       W, P4, layA, layB);
+  k_build_lt2<<<grid_for(work, 128), 128, 0, s>>>(bed, stride_bytes, rows, row0, n, W, pl.KT, lay);
 }
 
-void marker_counts(const uint4* layA, int64_t P4, int64_t W, int64_t p_loc, int64_t n,
+void marker_counts(const uint32_t* lay1, const PMPlan& pl1, int64_t p_loc, int64_t n,
                    int64_t* counts, cudaStream_t s) {
-  if (P4 == 0) return;
-  k_marker_counts<<<grid_for(P4 * 32, 256), 256, 0, s>>>(layA, P4, W, p_loc, n, counts);
+  if (p_loc == 0) return;
+  k_marker_counts<<<grid_for(p_loc * 32, 256), 256, 0, s>>>(lay1, pl1.KT, p_loc, (n + 15) / 16, n,
+                                                             counts);
 }
 
-void miss_lists_k1(const uint4* layA, int64_t P4, int64_t W, const K1Plan& pl, bool fill,
-                   uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent,
-                   cudaStream_t s) {
-  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.ntiles);
-  if (fill)
-    k_miss_k1<true><<<grid, 128, 0, s>>>(layA, P4, W, pl.tileW, cnt, off, base, ent);
-  else
-    k_miss_k1<false><<<grid, 128, 0, s>>>(layA, P4, W, pl.tileW, cnt, off, base, ent);
+void layout_to_bed(const uint32_t* lay1, const PMPlan& pl1, int64_t n, int64_t row0,
+                   int64_t nrows, uint8_t* out, cudaStream_t s) {
+  const int64_t work = nrows * ((n + 15) / 16);
+  if (work == 0) return;
+  k_layout_to_bed<<<grid_for(work, 256), 256, 0, s>>>(lay1, pl1.KT, n, row0, nrows, out);
 }
 
-void miss_lists_k2(const uint4* layA, int64_t P4, int64_t W, const K2Plan& pl, bool fill,
-                   uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent,
-                   cudaStream_t s) {
-  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nchunks);
+void miss_lists(const uint32_t* lay, const PMPlan& pl, bool fill, uint32_t* cnt,
+                const uint32_t* off, const int64_t* base, uint16_t* ent, cudaStream_t s) {
+  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nkc);
   if (fill)
-    k_miss_k2<true><<<grid, 32, 0, s>>>(layA, P4, W, pl.qc, cnt, off, base, ent);
+    k_miss_tiles<true><<<grid, kRowsPerCta, 0, s>>>(lay, pl.KT, pl.kt_cta, cnt, off, base, ent);
   else
-    k_miss_k2<false><<<grid, 32, 0, s>>>(layA, P4, W, pl.qc, cnt, off, base, ent);
+    k_miss_tiles<false><<<grid, kRowsPerCta, 0, s>>>(lay, pl.KT, pl.kt_cta, cnt, off, base, ent);
 }
 
 void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int64_t* tot,
@@ -635,83 +572,54 @@ void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int6
   k_block_scan<<<(unsigned)nblk, 512, 0, s>>>(cnt, span, off, tot);
 }
 
-void layout_to_bed(const uint4* layA, int64_t P4, int64_t W, int64_t n, int64_t row0,
-                   int64_t nrows, uint8_t* out, cudaStream_t s) {
-  const int64_t work = nrows * W;
-  if (work == 0) return;
-  k_layout_to_bed<<<grid_for(work, 256), 256, 0, s>>>(layA, P4, W, n, row0, nrows, out);
+void k1_digitize(const GenoView& g, const double* x, cudaStream_t s) {
+  const PMPlan& pl = g.pl1;
+  k_digitize<0><<<(unsigned)pl.nkc, 1024, pl.dig_smem, s>>>(x, nullptr, nullptr, g.n, pl.kt_cta,
+                                                            g.s1.dig, g.s1.dexp, g.s1.dsum,
+                                                            nullptr);
 }
 
-K1Plan k1_plan(int64_t W, int64_t P4) {
-  K1Plan pl;
-  // CTA = 32 SNP quads x a sample tile of 256 words (4096 samples; 32 KB of
-  // coefficients), each warp 32 words. Partial traffic: 8 B per SNP per tile
-  // (1/128 of the 1 KB of packed bytes per SNP and tile).
-  pl.tileW = (int)(W < 256 ? (W > 0 ? W : 1) : 256);
-  pl.ntiles = (int)((W + pl.tileW - 1) / pl.tileW);
-  if (pl.ntiles < 1) pl.ntiles = 1;
-  pl.grid_x = (P4 + 31) / 32;
-  if (pl.grid_x < 1) pl.grid_x = 1;
-  pl.smem = (size_t)pl.tileW * 16 * sizeof(double);
-  return pl;
+void k2_digitize(const GenoView& g, const double* y, cudaStream_t s) {
+  const PMPlan& pl = g.pl2;
+  k_digitize<1><<<(unsigned)pl.nkc, 1024, pl.dig_smem, s>>>(y, g.inv_s, g.mu, g.p_loc, pl.kt_cta,
+                                                            g.s2.dig, g.s2.dexp, g.s2.dsum,
+                                                            g.s2.cm);
 }
 
-K2Plan k2_plan(int64_t W, int64_t P4) {
-  K2Plan pl;
-  // CTA = 32 word positions (512 samples) x a chunk of up to 512 SNP quads
-  // (2048 SNPs), each warp 64 quads. Partial traffic: 8 B per sample per
-  // chunk (1/64 of the 512 packed bytes per sample and chunk).
-  pl.grid_x = (W + 31) / 32;
-  if (pl.grid_x < 1) pl.grid_x = 1;
-  int64_t qc = 512;
-  const int64_t p4r = ((P4 + 7) / 8) * 8;
-  if (qc > p4r) qc = p4r > 0 ? p4r : 8;
-  pl.qc = (int)qc;
-  pl.nchunks = (int)((P4 + qc - 1) / qc);
-  if (pl.nchunks < 1) pl.nchunks = 1;
-  // register bound: 4 CTAs/SM (64 registers) by default; GKB_K2_MINB=3 -> 80
-  const char* env = getenv("GKB_K2_MINB");
-  pl.minb = (env && env[0] == '3') ? 3 : 4;
-  // coefficients / combine region + missing-entry corrections
-  pl.smem = (size_t)((qc * 4 > 2048 ? qc * 4 : 2048) + qc * 4) * sizeof(double);
-  return pl;
+void k1_main_only(const GenoView& g, const double* x, cudaStream_t s) {
+  const PMPlan& pl = g.pl1;
+  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nkc);
+  k_pm_main<0><<<grid, kThreads, pl.smem, s>>>(g.lt1, pl.KT, pl.kt_cta, g.s1.dig, g.s1.dexp,
+                                               g.s1.dsum, x, g.mu, g.m1.off, g.m1.base, g.m1.ent,
+                                               pl.rows_pad, g.s1.part);
 }
 
-void k1_main_only(const GenoView& g, const K1Plan& pl, const double* x, double* ypart,
-                  cudaStream_t s) {
-  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.ntiles);
-  k1_main<<<grid, kThreads, pl.smem, s>>>(g.layB, g.P4, g.W, x, g.n, pl.tileW, g.mu, g.m1_off,
-                                          g.m1_base, g.m1_ent, ypart);
+void k2_main_only(const GenoView& g, cudaStream_t s) {
+  const PMPlan& pl = g.pl2;
+  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nkc);
+  k_pm_main<1><<<grid, kThreads, pl.smem, s>>>(g.lt2, pl.KT, pl.kt_cta, g.s2.dig, g.s2.dexp,
+                                               g.s2.dsum, g.s2.cm, nullptr, g.m2.off, g.m2.base,
+                                               g.m2.ent, pl.rows_pad, g.s2.part);
 }
 
-void k1_apply(const GenoView& g, const K1Plan& pl, const double* x, double* ypart, double* y,
-              cudaStream_t s) {
+void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s) {
   if (g.p_loc == 0) return;
-  k1_main_only(g, pl, x, ypart, s);
-  k1_reduce<<<(unsigned)((g.p_loc + 255) / 256), 256, 0, s>>>(ypart, pl.ntiles, g.P4, g.p_loc,
-                                                              g.inv_s, y);
+  k1_digitize(g, x, s);
+  k1_main_only(g, x, s);
+  k1_reduce<<<(unsigned)((g.p_loc + 255) / 256), 256, 0, s>>>(g.s1.part, g.pl1.nkc,
+                                                              g.pl1.rows_pad, g.p_loc, g.inv_s, y);
 }
 
-void k2_main_only(const GenoView& g, const K2Plan& pl, const double* y, double* zpart,
-                  cudaStream_t s) {
-  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nchunks);
-  if (pl.minb == 3)
-    k2_main<3><<<grid, kThreads, pl.smem, s>>>(g.layA, g.P4, g.W, y, g.mu, g.inv_s, g.p_loc, pl.qc,
-                                               g.m2_off, g.m2_base, g.m2_ent, zpart);
-  else
-    k2_main<4><<<grid, kThreads, pl.smem, s>>>(g.layA, g.P4, g.W, y, g.mu, g.inv_s, g.p_loc, pl.qc,
-                                               g.m2_off, g.m2_base, g.m2_ent, zpart);
-}
-
-void k2_adjoint(const GenoView& g, const K2Plan& pl, const double* y, double* zpart, double* z,
-                cudaStream_t s) {
+void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s) {
   if (g.n == 0) return;
   if (g.p_loc == 0) {
     cudaMemsetAsync(z, 0, sizeof(double) * (size_t)g.n, s);
     return;
   }
-  k2_main_only(g, pl, y, zpart, s);
-  k2_reduce<<<(unsigned)((g.n + 31) / 32), 1024, 0, s>>>(zpart, pl.nchunks, g.W, g.n, z);
+  k2_digitize(g, y, s);
+  k2_main_only(g, s);
+  k2_reduce<<<(unsigned)((g.n + 31) / 32), 1024, 0, s>>>(g.s2.part, g.pl2.nkc, g.pl2.rows_pad,
+                                                         g.n, z);
 }
 
 }  // namespace dev

@@ -91,16 +91,15 @@ struct DevOp {
 };
 
 struct GenoShard {
-  int64_t p_loc = 0, n = 0, W = 0, P4 = 0;
-  uint4* layA = nullptr;
-  uint4* layB = nullptr;
-  double* mu = nullptr;
+  int64_t p_loc = 0, n = 0;
+  dev::PMPlan pl1{}, pl2{};   // layout 1 (rows SNPs) / layout 2 (rows samples)
+  uint32_t* lt1 = nullptr;
+  uint32_t* lt2 = nullptr;
+  double* mu = nullptr;       // pl1.rows_pad entries, zero beyond p_loc
   double* inv_s = nullptr;
   int64_t* counts = nullptr;  // device p_loc*4
   int64_t nmissing = 0;
-  dev::K1Plan k1{};
-  dev::K2Plan k2{};
-  // per-CTA missing lists of the two plans (kernels.hpp GenoView)
+  // per-CTA missing lists of the two layouts (kernels.hpp MissLists)
   uint32_t* m1_off = nullptr;
   int64_t* m1_base = nullptr;
   uint16_t* m1_ent = nullptr;
@@ -108,8 +107,7 @@ struct GenoShard {
   int64_t* m2_base = nullptr;
   uint16_t* m2_ent = nullptr;
   int64_t list_bytes = 0;
-  double* ypart = nullptr;
-  double* zpart = nullptr;
+  dev::PMScratch s1{}, s2{};
   dev::GenoView view() const;
 };
 

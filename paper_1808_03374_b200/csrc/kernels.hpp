@@ -12,82 +12,83 @@ namespace gkb {
 namespace dev {
 
 // ---- packed genotype operator -------------------------------------------
-// Device layout: the p_loc x n matrix of 2-bit dosage
-// codes r (0,1,2 = dosage, 3 = missing, pads 0) is cut into 16-byte chunks
-// (4 consecutive SNPs x one 32-bit word of 16 samples). Two orderings:
-//   layout A ("row-quad", for the adjoint K2): chunk (q, w) at q*W + w
-//   layout B ("col-quad", for the apply K1):   chunk (q, w) at w*P4 + q
-// W = ceil(n/16) words per SNP, P4 = ceil(p_loc/4) SNP quads.
+// Device layout: the matrix of 2-bit dosage codes r
+// (0,1,2 = dosage, 3 = missing, pads 0) is stored twice, as tile layouts:
+//   layout 1 (K1 = apply):   rows = local SNPs (p_loc), cols = samples (n)
+//   layout 2 (K2 = adjoint): rows = samples (n),       cols = local SNPs
+// A tile is 16 rows x 128 cols (8 words of 16 two-bit fields) = 512 B in
+// mma.sync fragment order; tiles are stored strip-major (a warp streams one
+// 16-row strip along K contiguously).
+struct PMPlan {
+  int64_t R, C;      // valid rows / cols
+  int64_t S;         // 16-row strips, padded to whole CTAs (16 strips = 256 rows)
+  int64_t KT;        // 128-col K tiles
+  int kt_cta;        // K tiles per CTA column range (2048 cols)
+  int nkc;           // column ranges
+  int64_t grid_x;    // CTAs along rows (S / 16)
+  int64_t rows_pad;  // S * 16
+  size_t smem;       // main kernel dynamic shared memory (digits)
+  size_t dig_smem;   // digitize kernel dynamic shared memory
+};
+PMPlan pm_plan(int64_t R, int64_t C);
+int64_t pm_words(const PMPlan& pl);  // 32-bit words of one layout
+
+// Per-CTA missing lists of one layout (null off when the shard has none):
+// block b = kc * grid_x + bx, row r (0..255) owns
+//   ent[base[b] + off[b*257 + r] .. base[b] + off[b*257 + r + 1])  (column offsets in the range)
+struct MissLists {
+  const uint32_t* off;
+  const int64_t* base;
+  const uint16_t* ent;
+};
+// Per-product scratch of one layout.
+struct PMScratch {
+  uint4* dig;     // nkc * kt_cta * 64 B-fragment digits
+  int* dexp;      // nkc
+  double* dsum;   // nkc
+  double* cm;     // K2: c_j (3 - mu_j) per local SNP
+  double* part;   // nkc * rows_pad partials
+};
 struct GenoView {
-  const uint4* layA;
-  const uint4* layB;
-  int64_t p_loc, n, W, P4;
-  const double* mu;     // p_loc
-  const double* inv_s;  // p_loc
-  // Per-CTA missing lists (null when the shard has no missing entries):
-  // block b, row r owns ent[base[b] + off[b*(span+1)+r] .. base[b] + off[b*(span+1)+r+1]).
-  // m1: K1 blocks b = tile*grid_x + qb, span 128 SNP rows, entries = sample offset in the tile
-  // m2: K2 blocks b = chunk*grid_x + wb, span 512 samples, entries = SNP offset in the chunk
-  const uint32_t* m1_off;
-  const int64_t* m1_base;
-  const uint16_t* m1_ent;
-  const uint32_t* m2_off;
-  const int64_t* m2_base;
-  const uint16_t* m2_ent;
+  const uint4* lt1;
+  const uint4* lt2;
+  PMPlan pl1, pl2;
+  int64_t p_loc, n;
+  const double* mu;     // >= pl1.rows_pad (zero beyond p_loc)
+  const double* inv_s;  // >= pl1.rows_pad
+  MissLists m1, m2;
+  PMScratch s1, s2;
   int64_t nmissing;
 };
 
-// K8: .bed records [rows of one staging block] -> both layouts.
-void build_layouts(const uint8_t* bed, int64_t stride_bytes, int64_t rows_in_block, int64_t q_base,
-                   int64_t n, int64_t W, int64_t P4, uint4* layA, uint4* layB, cudaStream_t s);
-// K7: per-SNP [n0, n1, n2, nmiss] from layout A.
-void marker_counts(const uint4* layA, int64_t P4, int64_t W, int64_t p_loc, int64_t n,
+// K8: .bed records of a staging block (rows [row0, row0+rows) of the shard) -> layouts.
+void build_lt1(const uint8_t* bed, int64_t stride_bytes, int64_t rows, int64_t row0, int64_t n,
+               const PMPlan& pl1, uint32_t* lay1, cudaStream_t s);
+void build_lt2(const uint8_t* bed, int64_t stride_bytes, int64_t rows, int64_t row0, int64_t n,
+               const PMPlan& pl2, uint32_t* lay2, cudaStream_t s);  // row0 % 16 == 0
+// K7: per-SNP [n0, n1, n2, nmiss] from layout 1.
+void marker_counts(const uint32_t* lay1, const PMPlan& pl1, int64_t p_loc, int64_t n,
                    int64_t* counts, cudaStream_t s);
-// layout A -> .bed records for rows [row0, row0+nrows) (read-back check).
-void layout_to_bed(const uint4* layA, int64_t P4, int64_t W, int64_t n, int64_t row0,
+// layout 1 -> .bed records for rows [row0, row0+nrows) (read-back check).
+void layout_to_bed(const uint32_t* lay1, const PMPlan& pl1, int64_t n, int64_t row0,
                    int64_t nrows, uint8_t* out, cudaStream_t s);
-
-struct K1Plan {
-  int tileW;     // 32-bit words (16 samples) per sample tile
-  int ntiles;
-  int64_t grid_x;
-  size_t smem;
-};
-K1Plan k1_plan(int64_t W, int64_t P4);
-// K1 apply (reference X*x, per-SNP dot): y (p_loc) = inv_s*(sum r x - mu X_tot - (3-mu) S_miss)
-// scratch: ypart ntiles*4*P4 doubles.
-void k1_apply(const GenoView& g, const K1Plan& pl, const double* x, double* ypart, double* y,
-              cudaStream_t s);
-
-struct K2Plan {
-  int qc;        // SNP quads per chunk
-  int nchunks;
-  int64_t grid_x;
-  size_t smem;
-  int minb;      // __launch_bounds__ min blocks of the k2_main instance (3 or 4)
-};
-K2Plan k2_plan(int64_t W, int64_t P4);
-// K2 apply_adjoint (reference X^T*y, per-sample sum) over the local SNPs.
-// scratch: zpart nchunks*16*W doubles. z has n entries.
-void k2_adjoint(const GenoView& g, const K2Plan& pl, const double* y, double* zpart, double* z,
-                cudaStream_t s);
-// The two main packed kernels alone (for timing breakdowns).
-void k1_main_only(const GenoView& g, const K1Plan& pl, const double* x, double* ypart,
-                  cudaStream_t s);
-void k2_main_only(const GenoView& g, const K2Plan& pl, const double* y, double* zpart,
-                  cudaStream_t s);
-
-// Per-CTA missing lists for the two plans: count pass (fill = false, writes
-// cnt[nblk*span]), block_scan (cnt -> off[nblk*(span+1)], tot[nblk]), then the
-// fill pass (fill = true, needs off and base = exclusive scan of tot).
-void miss_lists_k1(const uint4* layA, int64_t P4, int64_t W, const K1Plan& pl, bool fill,
-                   uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent,
-                   cudaStream_t s);
-void miss_lists_k2(const uint4* layA, int64_t P4, int64_t W, const K2Plan& pl, bool fill,
-                   uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent,
-                   cudaStream_t s);
+// Missing lists: count pass (fill = false, cnt[nblk*256]), block_scan
+// (cnt -> off[nblk*257], tot[nblk]), then the fill pass (needs off and base =
+// exclusive scan of tot).
+void miss_lists(const uint32_t* lay, const PMPlan& pl, bool fill, uint32_t* cnt,
+                const uint32_t* off, const int64_t* base, uint16_t* ent, cudaStream_t s);
 void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int64_t* tot,
                 cudaStream_t s);
+
+// K1 apply (reference X*x, per-SNP dot): y (p_loc) = inv_s*(sum r x - mu X_tot - (3-mu) S_miss)
+void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s);
+// K2 apply_adjoint (reference X^T*y, per-sample sum) over the local SNPs; z has n entries.
+void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s);
+// Pieces (for timing breakdowns): digitize, then the main tensor-core kernel.
+void k1_digitize(const GenoView& g, const double* x, cudaStream_t s);
+void k2_digitize(const GenoView& g, const double* y, cudaStream_t s);
+void k1_main_only(const GenoView& g, const double* x, cudaStream_t s);
+void k2_main_only(const GenoView& g, cudaStream_t s);
 
 // ---- dense fp64 basis / operator kernels (K3-K6) -------------------------
 // Reduction scratch: partial[nblk * K] plus the result buffer.

@@ -126,18 +126,19 @@ void marker_scaling(const int64_t* counts, int64_t p, int64_t n, int scheme, dou
 }
 
 // ---------------------------------------------------------------- GenoOp
-// Per-CTA missing lists of one plan: count pass, per-block scan on device,
+// Per-CTA missing lists of one layout: count pass, per-block scan on device,
 // block bases scanned on the host (nblk values), fill pass. Returns the number
 // of entries (== the shard's missing count).
-template <class Launch>
-static int64_t build_block_lists(int64_t nblk, int span, cudaStream_t st, uint32_t** off,
-                                 int64_t** base, uint16_t** ent, int64_t* bytes, Launch launch) {
+static int64_t build_block_lists(const uint32_t* lay, const dev::PMPlan& pl, cudaStream_t st,
+                                 uint32_t** off, int64_t** base, uint16_t** ent, int64_t* bytes) {
+  const int span = 256;
+  const int64_t nblk = pl.grid_x * pl.nkc;
   uint32_t* cnt = nullptr;
   int64_t* tot = nullptr;
   GKB_CUDA(cudaMalloc(&cnt, sizeof(uint32_t) * (size_t)(nblk * span)));
   GKB_CUDA(cudaMalloc(&tot, sizeof(int64_t) * (size_t)nblk));
   GKB_CUDA(cudaMalloc(off, sizeof(uint32_t) * (size_t)(nblk * (span + 1))));
-  launch(false, cnt, nullptr, nullptr, nullptr);
+  dev::miss_lists(lay, pl, false, cnt, nullptr, nullptr, nullptr, st);
   GKB_LAUNCH_CHECK();
   dev::block_scan(cnt, nblk, span, *off, tot, st);
   GKB_LAUNCH_CHECK();
@@ -147,38 +148,51 @@ static int64_t build_block_lists(int64_t nblk, int span, cudaStream_t st, uint32
   cudaFree(cnt);
   cudaFree(tot);
   int64_t total = 0;
-  for (int64_t b = 0; b < nblk; ++b) {
-    const int64_t c = h[b];
-    h[b] = total;
+  for (int64_t bb = 0; bb < nblk; ++bb) {
+    const int64_t c = h[bb];
+    h[bb] = total;
     total += c;
   }
   GKB_CUDA(cudaMalloc(base, sizeof(int64_t) * (size_t)nblk));
   GKB_CUDA(cudaMemcpy(*base, h.data(), sizeof(int64_t) * (size_t)nblk, cudaMemcpyHostToDevice));
   GKB_CUDA(cudaMalloc(ent, sizeof(uint16_t) * (size_t)std::max<int64_t>(total, 1)));
-  launch(true, nullptr, *off, *base, *ent);
+  dev::miss_lists(lay, pl, true, nullptr, *off, *base, *ent, st);
   GKB_LAUNCH_CHECK();
   *bytes += (int64_t)(sizeof(uint32_t) * nblk * (span + 1) + sizeof(int64_t) * nblk +
                       sizeof(uint16_t) * total);
   return total;
 }
 
+static void alloc_scratch(const dev::PMPlan& pl, bool with_cm, dev::PMScratch& sc) {
+  GKB_CUDA(cudaMalloc(&sc.dig, sizeof(uint4) * (size_t)(pl.nkc * pl.kt_cta * 64)));
+  GKB_CUDA(cudaMalloc(&sc.dexp, sizeof(int) * (size_t)pl.nkc));
+  GKB_CUDA(cudaMalloc(&sc.dsum, sizeof(double) * (size_t)pl.nkc));
+  GKB_CUDA(cudaMalloc(&sc.part, sizeof(double) * (size_t)(pl.nkc * pl.rows_pad)));
+  if (with_cm) GKB_CUDA(cudaMalloc(&sc.cm, sizeof(double) * (size_t)std::max<int64_t>(pl.C, 1)));
+}
+
+static void free_scratch(dev::PMScratch& sc) {
+  void* ptrs[] = {sc.dig, sc.dexp, sc.dsum, sc.part, sc.cm};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  sc = dev::PMScratch{};
+}
+
 dev::GenoView GenoShard::view() const {
   dev::GenoView v;
-  v.layA = layA;
-  v.layB = layB;
+  v.lt1 = reinterpret_cast<const uint4*>(lt1);
+  v.lt2 = reinterpret_cast<const uint4*>(lt2);
+  v.pl1 = pl1;
+  v.pl2 = pl2;
   v.p_loc = p_loc;
   v.n = n;
-  v.W = W;
-  v.P4 = P4;
   v.mu = mu;
   v.inv_s = inv_s;
   const bool lists = nmissing > 0;
-  v.m1_off = lists ? m1_off : nullptr;
-  v.m1_base = m1_base;
-  v.m1_ent = m1_ent;
-  v.m2_off = lists ? m2_off : nullptr;
-  v.m2_base = m2_base;
-  v.m2_ent = m2_ent;
+  v.m1 = dev::MissLists{lists ? m1_off : nullptr, m1_base, m1_ent};
+  v.m2 = dev::MissLists{lists ? m2_off : nullptr, m2_base, m2_ent};
+  v.s1 = s1;
+  v.s2 = s2;
   v.nmissing = nmissing;
   return v;
 }
@@ -187,10 +201,12 @@ GenoOp::~GenoOp() {
   for (size_t i = 0; i < gs.size(); ++i) {
     cudaSetDevice(ctx->shards[i].dev);
     GenoShard& g = gs[i];
-    void* ptrs[] = {g.layA,   g.layB,   g.mu,    g.inv_s,  g.counts, g.m1_off, g.m1_base,
-                    g.m1_ent, g.m2_off, g.m2_base, g.m2_ent, g.ypart, g.zpart};
+    void* ptrs[] = {g.lt1,    g.lt2,     g.mu,     g.inv_s,  g.counts, g.m1_off,
+                    g.m1_base, g.m1_ent, g.m2_off, g.m2_base, g.m2_ent};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    free_scratch(g.s1);
+    free_scratch(g.s2);
   }
 }
 
@@ -198,20 +214,27 @@ void GenoOp::alloc_shard(int i, int64_t p_loc, int64_t nn) {
   GenoShard& g = gs[i];
   g.p_loc = p_loc;
   g.n = nn;
-  g.W = (nn + 15) / 16;
-  g.P4 = (p_loc + 3) / 4;
+  g.pl1 = dev::pm_plan(p_loc, nn);
+  g.pl2 = dev::pm_plan(nn, p_loc);
   ctx->set_device(i);
-  const size_t chunks = (size_t)std::max<int64_t>(g.P4 * g.W, 1);
-  GKB_CUDA(cudaMalloc(&g.layA, sizeof(uint4) * chunks));
-  GKB_CUDA(cudaMalloc(&g.layB, sizeof(uint4) * chunks));
-  GKB_CUDA(cudaMemsetAsync(g.layA, 0, sizeof(uint4) * chunks, ctx->shards[i].stream));
-  GKB_CUDA(cudaMemsetAsync(g.layB, 0, sizeof(uint4) * chunks, ctx->shards[i].stream));
-  const size_t pp = (size_t)std::max<int64_t>(4 * g.P4, 4);
+  cudaStream_t st = ctx->shards[i].stream;
+  const size_t w1 = (size_t)dev::pm_words(g.pl1), w2 = (size_t)dev::pm_words(g.pl2);
+  GKB_CUDA(cudaMalloc(&g.lt1, sizeof(uint32_t) * w1));
+  GKB_CUDA(cudaMalloc(&g.lt2, sizeof(uint32_t) * w2));
+  GKB_CUDA(cudaMemsetAsync(g.lt1, 0, sizeof(uint32_t) * w1, st));
+  GKB_CUDA(cudaMemsetAsync(g.lt2, 0, sizeof(uint32_t) * w2, st));
+  const size_t pp = (size_t)g.pl1.rows_pad;
   GKB_CUDA(cudaMalloc(&g.mu, sizeof(double) * pp));
   GKB_CUDA(cudaMalloc(&g.inv_s, sizeof(double) * pp));
-  GKB_CUDA(cudaMemsetAsync(g.mu, 0, sizeof(double) * pp, ctx->shards[i].stream));
-  GKB_CUDA(cudaMemsetAsync(g.inv_s, 0, sizeof(double) * pp, ctx->shards[i].stream));
-  GKB_CUDA(cudaMalloc(&g.counts, sizeof(int64_t) * 4 * pp));  // [n0,n1,n2,nmiss] per row
+  GKB_CUDA(cudaMemsetAsync(g.mu, 0, sizeof(double) * pp, st));
+  GKB_CUDA(cudaMemsetAsync(g.inv_s, 0, sizeof(double) * pp, st));
+  GKB_CUDA(cudaMalloc(&g.counts, sizeof(int64_t) * 4 * (size_t)std::max<int64_t>(p_loc, 1)));
+}
+
+// Staging blocks are whole groups of 16 SNP rows (layout 2 transposes 16 at a time).
+static int64_t staging_rows(int64_t stride, int64_t budget_bytes, int64_t pr) {
+  int64_t br = std::max<int64_t>(16, (budget_bytes / stride) & ~int64_t(15));
+  return std::min(br, std::max<int64_t>(16, ((pr + 15) / 16) * 16));
 }
 
 void GenoOp::build_from_payload(const uint8_t* payload, int64_t p, int64_t nn) {
@@ -222,14 +245,12 @@ void GenoOp::build_from_payload(const uint8_t* payload, int64_t p, int64_t nn) {
   const int L = (int)ctx->shards.size();
   gs.resize(L);
   const int64_t stride = (nn + 3) / 4;
-  const int64_t max_block_bytes = 64ll << 20;
-  int64_t block_rows = std::max<int64_t>(4, (max_block_bytes / stride) & ~int64_t(3));
   for (int i = 0; i < L; ++i) {
     const int64_t r0 = row0(i), pr = rows(i);
     alloc_shard(i, pr, nn);
     Shard& sh = ctx->shards[i];
     ctx->set_device(i);
-    const int64_t br = std::min(block_rows, std::max<int64_t>(4, ((pr + 3) / 4) * 4));
+    const int64_t br = staging_rows(stride, 64ll << 20, pr);
     uint8_t* dstage = nullptr;
     uint8_t* hstage = nullptr;
     GKB_CUDA(cudaMalloc(&dstage, (size_t)(br * stride)));
@@ -240,8 +261,9 @@ void GenoOp::build_from_payload(const uint8_t* payload, int64_t p, int64_t nn) {
       std::memcpy(hstage, payload + (r0 + b0) * stride, (size_t)(rb * stride));
       GKB_CUDA(cudaMemcpyAsync(dstage, hstage, (size_t)(rb * stride), cudaMemcpyHostToDevice,
                                sh.stream));
-      dev::build_layouts(dstage, stride, rb, b0 / 4, nn, gs[i].W, gs[i].P4, gs[i].layA, gs[i].layB,
-                         sh.stream);
+      dev::build_lt1(dstage, stride, rb, b0, nn, gs[i].pl1, gs[i].lt1, sh.stream);
+      GKB_LAUNCH_CHECK();
+      dev::build_lt2(dstage, stride, rb, b0, nn, gs[i].pl2, gs[i].lt2, sh.stream);
       GKB_LAUNCH_CHECK();
     }
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
@@ -262,7 +284,6 @@ void GenoOp::build_from_synth(const dev::SynthDev& sp_in, const gkb_synth_spec* 
   const int L = (int)ctx->shards.size();
   gs.resize(L);
   const int64_t stride = (nn + 3) / 4;
-  const int64_t block_rows = std::max<int64_t>(4, ((256ll << 20) / stride) & ~int64_t(3));
   (void)sp_in;
   for (int i = 0; i < L; ++i) {
     const int64_t r0 = row0(i), pr = rows(i);
@@ -292,15 +313,16 @@ void GenoOp::build_from_synth(const dev::SynthDev& sp_in, const gkb_synth_spec* 
     }
     dev::SynthDev sd{p, nn, spec->seed, spec->npop, dfreq, dpop, dadmix, spec->missing_rate, dcopy,
                      spec->copy_prob};
-    const int64_t br = std::min(block_rows, std::max<int64_t>(4, ((pr + 3) / 4) * 4));
+    const int64_t br = staging_rows(stride, 256ll << 20, pr);
     uint8_t* dstage = nullptr;
     GKB_CUDA(cudaMalloc(&dstage, (size_t)(br * stride)));
     for (int64_t b0 = 0; b0 < pr; b0 += br) {
       const int64_t rb = std::min(br, pr - b0);
       dev::synth_bed(sd, r0 + b0, rb, dstage, sh.stream);
       GKB_LAUNCH_CHECK();
-      dev::build_layouts(dstage, stride, rb, b0 / 4, nn, gs[i].W, gs[i].P4, gs[i].layA, gs[i].layB,
-                         sh.stream);
+      dev::build_lt1(dstage, stride, rb, b0, nn, gs[i].pl1, gs[i].lt1, sh.stream);
+      GKB_LAUNCH_CHECK();
+      dev::build_lt2(dstage, stride, rb, b0, nn, gs[i].pl2, gs[i].lt2, sh.stream);
       GKB_LAUNCH_CHECK();
     }
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
@@ -320,7 +342,7 @@ void GenoOp::finish_build() {
     GenoShard& g = gs[i];
     Shard& sh = ctx->shards[i];
     ctx->set_device(i);
-    dev::marker_counts(g.layA, g.P4, g.W, g.p_loc, g.n, g.counts, sh.stream);
+    dev::marker_counts(g.lt1, g.pl1, g.p_loc, g.n, g.counts, sh.stream);
     GKB_LAUNCH_CHECK();
     if (g.p_loc > 0)
       GKB_CUDA(cudaMemcpyAsync(counts_host.data() + 4 * row0(i), g.counts,
@@ -329,32 +351,16 @@ void GenoOp::finish_build() {
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
     g.nmissing = 0;
     for (int64_t j = 0; j < g.p_loc; ++j) g.nmissing += counts_host[4 * (row0(i) + j) + 3];
-    g.k1 = dev::k1_plan(g.W, g.P4);
-    g.k2 = dev::k2_plan(g.W, g.P4);
     g.list_bytes = 0;
     if (g.nmissing > 0) {
-      const uint4* A = g.layA;
-      const int64_t P4 = g.P4, W = g.W;
-      const dev::K1Plan k1 = g.k1;
-      const dev::K2Plan k2 = g.k2;
-      const int64_t t1 = build_block_lists(
-          k1.grid_x * k1.ntiles, 128, sh.stream, &g.m1_off, &g.m1_base, &g.m1_ent, &g.list_bytes,
-          [&](bool fill, uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent) {
-            dev::miss_lists_k1(A, P4, W, k1, fill, cnt, off, base, ent, sh.stream);
-          });
-      const int64_t t2 = build_block_lists(
-          k2.grid_x * k2.nchunks, 512, sh.stream, &g.m2_off, &g.m2_base, &g.m2_ent, &g.list_bytes,
-          [&](bool fill, uint32_t* cnt, const uint32_t* off, const int64_t* base, uint16_t* ent) {
-            dev::miss_lists_k2(A, P4, W, k2, fill, cnt, off, base, ent, sh.stream);
-          });
+      const int64_t t1 = build_block_lists(g.lt1, g.pl1, sh.stream, &g.m1_off, &g.m1_base,
+                                           &g.m1_ent, &g.list_bytes);
+      const int64_t t2 = build_block_lists(g.lt2, g.pl2, sh.stream, &g.m2_off, &g.m2_base,
+                                           &g.m2_ent, &g.list_bytes);
       if (t1 != g.nmissing || t2 != g.nmissing) fail(GKB_ECUDA, "missing-list count mismatch");
     }
-    GKB_CUDA(cudaMalloc(&g.ypart, sizeof(double) * (size_t)std::max<int64_t>(
-                                      (int64_t)g.k1.ntiles * 4 * g.P4, 1)));
-    GKB_CUDA(cudaMalloc(&g.zpart, sizeof(double) * (size_t)std::max<int64_t>(
-                                      (int64_t)g.k2.nchunks * 16 * g.W, 1)));
-    if (g.k1.smem > 48 * 1024)
-      fail(GKB_EINVAL, "K1 tile exceeds 48 KB of shared memory");
+    alloc_scratch(g.pl1, false, g.s1);
+    alloc_scratch(g.pl2, true, g.s2);
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
   }
   if (ctx->use_nccl && ctx->nshards_total > 1) {
@@ -408,7 +414,7 @@ void GenoOp::apply_dev(const std::vector<const double*>& x, const std::vector<do
   if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
   for (size_t i = 0; i < gs.size(); ++i) {
     ctx->set_device((int)i);
-    dev::k1_apply(gs[i].view(), gs[i].k1, x[i], gs[i].ypart, y[i], ctx->shards[i].stream);
+    dev::k1_apply(gs[i].view(), x[i], y[i], ctx->shards[i].stream);
     GKB_LAUNCH_CHECK();
   }
 }
@@ -417,7 +423,7 @@ void GenoOp::adjoint_dev(const std::vector<const double*>& y, const std::vector<
   if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
   for (size_t i = 0; i < gs.size(); ++i) {
     ctx->set_device((int)i);
-    dev::k2_adjoint(gs[i].view(), gs[i].k2, y[i], gs[i].zpart, z[i], ctx->shards[i].stream);
+    dev::k2_adjoint(gs[i].view(), y[i], z[i], ctx->shards[i].stream);
     GKB_LAUNCH_CHECK();
   }
   ctx->allreduce(z, n);
@@ -433,8 +439,8 @@ int64_t GenoOp::packed_bytes() const {
 int64_t GenoOp::device_bytes() const {
   int64_t b = 0;
   for (const auto& g : gs) {
-    b += 2 * 16 * g.P4 * g.W;
-    b += g.list_bytes + 16 * 4 * g.P4;  // missing lists, mu + inv_s
+    b += 4 * (dev::pm_words(g.pl1) + dev::pm_words(g.pl2));
+    b += g.list_bytes + 16 * g.pl1.rows_pad;  // missing lists, mu + inv_s
   }
   return b;
 }
@@ -449,8 +455,7 @@ void GenoOp::read_bed(int64_t r0, int64_t nrows, uint8_t* out) {
     ctx->set_device(i);
     uint8_t* d = nullptr;
     GKB_CUDA(cudaMalloc(&d, (size_t)((b - a) * stride)));
-    dev::layout_to_bed(gs[i].layA, gs[i].P4, gs[i].W, n, a - row0(i), b - a, d,
-                       ctx->shards[i].stream);
+    dev::layout_to_bed(gs[i].lt1, gs[i].pl1, n, a - row0(i), b - a, d, ctx->shards[i].stream);
     GKB_LAUNCH_CHECK();
     GKB_CUDA(cudaMemcpyAsync(out + (a - r0) * stride, d, (size_t)((b - a) * stride),
                              cudaMemcpyDeviceToHost, ctx->shards[i].stream));
