@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
     for (int i = 0; i < 8; ++i) {
       const int d = (int)(signed char)(M & 0xFF);
       M = (M - d) >> 8;
-      db[(wc * 8 + i) * 16 + 4 * q + e] = (uint8_t)d;
+      db[(wc * 8 + (i ^ (2 * (wc & 3)))) * 16 + 4 * q + e] = (uint8_t)d;  // swizzled slot
     }
   }
   __syncthreads();
@@ -363,29 +363,56 @@ __device__ __forceinline__ void mma_tile(int (&acc)[4], const uint4 w, const uin
   mma_u8s8(acc, (w.z >> 4) & m, (w.w >> 4) & m, (w.z >> 6) & m, (w.w >> 6) & m, b23.z, b23.w);
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// Missing-list staging in shared memory (after the digits): 257 offsets and
+// up to kEntCap entries of the CTA's list (longer lists are read from global).
+constexpr int kEntCap = 8192;
+constexpr int kOffBytes = 1040;
+size_t pm_smem_bytes(int kt_cta) {
+  return (size_t)kt_cta * 64 * 16 + kOffBytes + 2 * kEntCap + 16 + (size_t)kt_cta * 128 * 8;
+}
+
 // grid (S / 16, nkc). CTA = 8 warps x 2 strips (256 rows) x one column range
 // of kt_cta tiles; B fragments (digits) of the range in shared memory, shared
 // by the 8 warps and reused across each warp's 2 strips. Writes the range's
 // exact partial (MODE 0: K1, MODE 1: K2 -- see the header) to part[kc][row].
+// The CTA's missing list (offsets + entries) and the range's correction
+// coefficients cval (K1: x, K2: c_j (3 - mu_j)) are staged into shared memory
+// by cp.async in the prologue, so the epilogue walk never touches global
+// memory (random 8-byte gathers from L2 cost ~30% of the kernel otherwise).
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
     const uint4* __restrict__ lay, int64_t KT, int kt_cta, const uint4* __restrict__ dig,
     const int* __restrict__ dexp, const double* __restrict__ dsum,
     const double* __restrict__ cval, const double* __restrict__ mu,
     const uint32_t* __restrict__ m_off, const int64_t* __restrict__ m_base,
-    const uint16_t* __restrict__ m_ent, int64_t rows_pad, double* __restrict__ part) {
-  extern __shared__ uint4 dg[];  // kt_cta * 64
+    const uint16_t* __restrict__ m_ent, int64_t rows_pad, int64_t C, double* __restrict__ part) {
+  extern __shared__ __align__(16) uint4 dg[];  // kt_cta * 64 digits, then list staging
   const int kc = blockIdx.y;
   const int64_t kt0 = (int64_t)kc * kt_cta;
   const int ktiles = (int)min((int64_t)kt_cta, KT - kt0);
-  {
-    const uint4* gd = dig + kt0 * 64;
-    for (int i = threadIdx.x; i < ktiles * 64; i += kThreads) dg[i] = gd[i];
-  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tid = lane & 3;
   const int64_t strip0 = ((int64_t)blockIdx.x * 8 + warp) * kStripsPerWarp;
   const uint4* src = lay + (strip0 * KT + kt0) * 32 + lane;
+  const int64_t b = (int64_t)kc * gridDim.x + blockIdx.x;
+  const int64_t col0 = kt0 * 128;
   const uint4 Z = make_uint4(0, 0, 0, 0);
   int acc[kStripsPerWarp][4];
   uint4 buf[kDepth][kStripsPerWarp];
@@ -396,13 +423,42 @@ __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
     for (int d = 0; d < kDepth; ++d)
       buf[d][r] = d < ktiles ? ld_stream(src + r * KT * 32 + d * 32) : Z;
   }
+  uint8_t* stage = reinterpret_cast<uint8_t*>(dg + kt_cta * 64);
+  uint32_t* offs = reinterpret_cast<uint32_t*>(stage);
+  double* cvs = reinterpret_cast<double*>(stage + kOffBytes + 2 * kEntCap + 16);
+  const uint16_t* ents = nullptr;
+  if (m_off) {
+    for (int i = threadIdx.x; i <= kRowsPerCta; i += kThreads)
+      cp_async4(offs + i, m_off + b * (kRowsPerCta + 1) + i);
+    const int64_t eb = m_base[b];
+    const int64_t ne = m_off[b * (kRowsPerCta + 1) + kRowsPerCta];
+    const int64_t a0 = (eb * 2) & ~int64_t(15), a1 = (eb * 2 + ne * 2 + 15) & ~int64_t(15);
+    if (a1 - a0 <= 2 * kEntCap) {
+      const uint8_t* esrc = reinterpret_cast<const uint8_t*>(m_ent) + a0;
+      for (int64_t i = threadIdx.x; i < (a1 - a0) / 16; i += kThreads)
+        cp_async16(stage + kOffBytes + 16 * i, esrc + 16 * i);
+      ents = reinterpret_cast<const uint16_t*>(stage + kOffBytes) + (eb - a0 / 2);
+    } else {
+      ents = m_ent + eb;  // (dense-missing block) walk the list in global memory
+    }
+    // 8-byte copies: x may be a Krylov-basis column with an odd leading dimension
+    const int ncol = (int)min((int64_t)ktiles * 128, C - col0);
+    for (int i = threadIdx.x; i < ncol; i += kThreads) cp_async8(cvs + i, cval + col0 + i);
+    cp_async_commit();
+  }
+  {
+    const uint4* gd = dig + kt0 * 64;
+    for (int i = threadIdx.x; i < ktiles * 64; i += kThreads) dg[i] = gd[i];
+  }
   __syncthreads();
+  // swizzled digit slots: the 8 lanes of each quarter-warp hit 8 distinct 16-byte bank groups
+  const int sw = g ^ (2 * tid);
   for (int kt = 0; kt < ktiles; kt += kDepth) {
 #pragma unroll
     for (int d = 0; d < kDepth; ++d) {
       if (kt + d < ktiles) {
-        const uint4 b01 = dg[((kt + d) * 8 + tid) * 8 + g];
-        const uint4 b23 = dg[((kt + d) * 8 + tid + 4) * 8 + g];
+        const uint4 b01 = dg[((kt + d) * 8 + tid) * 8 + sw];
+        const uint4 b23 = dg[((kt + d) * 8 + tid + 4) * 8 + sw];
 #pragma unroll
         for (int r = 0; r < kStripsPerWarp; ++r) {
           const uint4 w = buf[d][r];
@@ -413,6 +469,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
       }
     }
   }
+  if (m_off) {
+    cp_async_wait_all();
+    __syncthreads();
+  }
   // Epilogue. Thread (g, tid) holds digits (2 tid, 2 tid + 1) of rows g and
   // g + 8; 2^(16 tid) (D_2tid + 256 D_2tid+1) is exact in fp64, and the four
   // threads of the group add their parts by a butterfly (identical bits in
@@ -421,8 +481,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
   const int E = dexp[kc];
   const double rsum = dsum[kc];
   const double p0 = pow2(16 * tid), p1 = pow2(16 * tid + 8);
-  const int64_t b = (int64_t)kc * gridDim.x + blockIdx.x;
-  const int64_t col0 = kt0 * 128;
 #pragma unroll
   for (int r = 0; r < kStripsPerWarp; ++r) {
     double v0 = (double)acc[r][0] * p0 + (double)acc[r][1] * p1;
@@ -433,23 +491,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
     v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
     const int hi = tid & 1;
     const int64_t row = (strip0 + r) * 16 + g + 8 * hi;
+    const int rl = (int)(row - (int64_t)blockIdx.x * kRowsPerCta);
     const double val = scalbn(hi ? v1 : v0, E - 62);
     double corr = 0.0;
     if (m_off) {
-      const int rl = (int)(row - (int64_t)blockIdx.x * kRowsPerCta);
-      const uint32_t* o = m_off + b * (kRowsPerCta + 1) + rl;
-      const uint16_t* e = m_ent + m_base[b];
-      const uint32_t e0 = o[0], e1 = o[1], mid = e0 + (e1 - e0) / 2;
+      const uint32_t e0 = offs[rl], e1 = offs[rl + 1], mid = e0 + (e1 - e0) / 2;
       uint32_t k = (tid >> 1) ? mid : e0;
       const uint32_t ke = (tid >> 1) ? e1 : mid;
-      for (; k + 4 <= ke; k += 4) {  // 4 index loads in flight, summed in order
-        const int c0 = e[k], c1 = e[k + 1], c2 = e[k + 2], c3 = e[k + 3];
-        corr += cval[col0 + c0];
-        corr += cval[col0 + c1];
-        corr += cval[col0 + c2];
-        corr += cval[col0 + c3];
+      for (; k + 4 <= ke; k += 4) {  // 4 independent loads in flight, summed in order
+        const int c0 = ents[k], c1 = ents[k + 1], c2 = ents[k + 2], c3 = ents[k + 3];
+        corr += cvs[c0];
+        corr += cvs[c1];
+        corr += cvs[c2];
+        corr += cvs[c3];
       }
-      for (; k < ke; ++k) corr += cval[col0 + e[k]];
+      for (; k < ke; ++k) corr += cvs[ents[k]];
       corr += __shfl_xor_sync(0xffffffffu, corr, 2);  // both halves, commutative -> same bits
     }
     if ((tid >> 1) == 0) {
@@ -520,7 +576,7 @@ PMPlan pm_plan(int64_t R, int64_t C) {
   pl.nkc = (int)((pl.KT + pl.kt_cta - 1) / pl.kt_cta);
   pl.grid_x = pl.S / 16;
   pl.rows_pad = pl.S * 16;
-  pl.smem = (size_t)pl.kt_cta * 64 * sizeof(uint4);
+  pl.smem = pm_smem_bytes(pl.kt_cta);
   pl.dig_smem = (size_t)pl.kt_cta * 64 * sizeof(uint4) + (size_t)pl.kt_cta * 128 * sizeof(double);
   return pl;
 }
@@ -572,8 +628,17 @@ void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int6
   k_block_scan<<<(unsigned)nblk, 512, 0, s>>>(cnt, span, off, tot);
 }
 
+namespace {
+template <class K>
+void allow_smem(K kern, size_t bytes) {  // opt in above 48 KB
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+}  // namespace
+
 void k1_digitize(const GenoView& g, const double* x, cudaStream_t s) {
   const PMPlan& pl = g.pl1;
+  allow_smem(k_digitize<0>, pl.dig_smem);
   k_digitize<0><<<(unsigned)pl.nkc, 1024, pl.dig_smem, s>>>(x, nullptr, nullptr, g.n, pl.kt_cta,
                                                             g.s1.dig, g.s1.dexp, g.s1.dsum,
                                                             nullptr);
@@ -581,25 +646,30 @@ void k1_digitize(const GenoView& g, const double* x, cudaStream_t s) {
 
 void k2_digitize(const GenoView& g, const double* y, cudaStream_t s) {
   const PMPlan& pl = g.pl2;
+  allow_smem(k_digitize<1>, pl.dig_smem);
   k_digitize<1><<<(unsigned)pl.nkc, 1024, pl.dig_smem, s>>>(y, g.inv_s, g.mu, g.p_loc, pl.kt_cta,
                                                             g.s2.dig, g.s2.dexp, g.s2.dsum,
                                                             g.s2.cm);
 }
 
-void k1_main_only(const GenoView& g, const double* x, cudaStream_t s) {
-  const PMPlan& pl = g.pl1;
+namespace {
+template <int MODE>
+void launch_main(const GenoView& g, const PMPlan& pl, const uint4* lay, const PMScratch& sc,
+                 const double* cval, const MissLists& ml, cudaStream_t s) {
+  allow_smem(k_pm_main<MODE>, pl.smem);
   dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nkc);
-  k_pm_main<0><<<grid, kThreads, pl.smem, s>>>(g.lt1, pl.KT, pl.kt_cta, g.s1.dig, g.s1.dexp,
-                                               g.s1.dsum, x, g.mu, g.m1.off, g.m1.base, g.m1.ent,
-                                               pl.rows_pad, g.s1.part);
+  k_pm_main<MODE><<<grid, kThreads, pl.smem, s>>>(lay, pl.KT, pl.kt_cta, sc.dig, sc.dexp,
+                                                  sc.dsum, cval, g.mu, ml.off, ml.base, ml.ent,
+                                                  pl.rows_pad, pl.C, sc.part);
+}
+}  // namespace
+
+void k1_main_only(const GenoView& g, const double* x, cudaStream_t s) {
+  launch_main<0>(g, g.pl1, g.lt1, g.s1, x, g.m1, s);
 }
 
 void k2_main_only(const GenoView& g, cudaStream_t s) {
-  const PMPlan& pl = g.pl2;
-  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nkc);
-  k_pm_main<1><<<grid, kThreads, pl.smem, s>>>(g.lt2, pl.KT, pl.kt_cta, g.s2.dig, g.s2.dexp,
-                                               g.s2.dsum, g.s2.cm, nullptr, g.m2.off, g.m2.base,
-                                               g.m2.ent, pl.rows_pad, g.s2.part);
+  launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s);
 }
 
 void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s) {

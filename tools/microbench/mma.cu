@@ -184,8 +184,12 @@ int main() {
   uint4* lay;
   uint4* dig;
   double* out;
+  uint4* lay2;
   CK(cudaMalloc(&lay, bytes));
   CK(cudaMemset(lay, 0x55, bytes));
+  CK(cudaMalloc(&lay2, bytes));
+  CK(cudaMemset(lay2, 0x66, bytes));
+  bool alternate = false;
   CK(cudaMalloc(&dig, KT * 64 * 16));
   CK(cudaMemset(dig, 0x11, KT * 64 * 16));
   auto run = [&](auto kern, const char* name, int kt_cta, int rr = 1) -> int {
@@ -201,7 +205,8 @@ int main() {
     CK(cudaDeviceSynchronize());
     const int reps = 20;
     cudaEventRecord(e0);
-    for (int r = 0; r < reps; ++r) kern<<<grid, 256, smem>>>(lay, KT, kt_cta, dig, out);
+    for (int r = 0; r < reps; ++r)
+      kern<<<grid, 256, smem>>>((alternate && (r & 1)) ? lay2 : lay, KT, kt_cta, dig, out);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -212,13 +217,13 @@ int main() {
     cudaFree(out);
     return 0;
   };
-  for (int kt_cta : {16, 40}) {
-    run(gemv_proto<4, 4, 0>, "d4 m4 full", kt_cta);
-    run(gemv_multi<2, 4, 2>, "R2 d4 m2", kt_cta, 2);
-    run(gemv_multi<2, 2, 4>, "R2 d2 m4", kt_cta, 2);
-    run(gemv_multi<4, 2, 2>, "R4 d2 m2", kt_cta, 4);
-    run(gemv_multi<4, 4, 1>, "R4 d4 m1", kt_cta, 4);
-    run(gemv_multi<4, 1, 4>, "R4 d1 m4", kt_cta, 4);
+  for (int alt = 0; alt < 2; ++alt) {
+    alternate = alt;
+    printf("alternate buffers: %d\n", alt);
+    run(gemv_proto<4, 4, 0>, "d4 m4 full", 16);
+    run(gemv_proto<4, 4, 1>, "d4 m4 noMMA", 16);
+    run(gemv_multi<2, 2, 4>, "R2 d2 m4", 16, 2);
+    run(gemv_multi<2, 4, 3>, "R2 d4 m3", 16, 2);
   }
   return 0;
 }

@@ -1,5 +1,8 @@
-"""Short driver for ncu captures of the packed kernels (K1 apply, K2 adjoint)
-on the bench workload (BASELINE config 2, device-generated)."""
+"""Short driver for timing / ncu captures of the packed products (K1 apply,
+K2 adjoint) on a BASELINE config (device-generated).
+
+usage: prof_kernels.py [config] [iters] [missing_rate]
+"""
 import os
 import sys
 
@@ -10,6 +13,9 @@ from paper_1808_03374_b200 import synth  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-op = gkb.GenotypeOperator.from_synth(synth.config_spec(cfg), scheme=gkb.ScalingScheme.kHwe)
+spec = synth.config_spec(cfg)
+if len(sys.argv) > 3:
+    spec.missing_rate = float(sys.argv[3])
+op = gkb.GenotypeOperator.from_synth(spec, scheme=gkb.ScalingScheme.kHwe)
 t = op.bench(2, iters, flush_l2=False)
-print(f"config {cfg}: step {t[0]:.4f} ms, main kernels {t[1]:.4f} ms")
+print(f"config {cfg} (missing {spec.missing_rate}): step {t[0]:.4f} ms, main kernels {t[1]:.4f} ms")
