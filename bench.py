@@ -8,7 +8,10 @@ individuals x p = 100,000 SNPs per GPU, Balding-Nichols, 5 subpopulations,
 the seeded counter-based generator (synthetic data, same model as the
 config). A step is one reference apply (A^T u, per-SNP dot, kernel K1) plus
 one apply_adjoint (A v, per-sample sum, kernel K2) on device-resident
-vectors; `value` = 2 * packed bytes / step time, summed over ranks.
+vectors; `value` = 2 * packed bytes / step time, summed over ranks. Each
+product is three launches: k_digitize (coefficients -> fixed-point digits),
+k_pm_main (tensor-core packed product + missing/mean corrections) and a
+fixed-order partial-sum reduce.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -273,8 +276,11 @@ def run_ours(args):
     b_mvp = packed_local
     k1_gbs = b_mvp / (k1_main * 1e-3) / 1e9
     k2_gbs = b_mvp / (k2_main * 1e-3) / 1e9
-    dom = ("K2 apply_adjoint (A·v)", k2_gbs, k2_main, "k2_main") if k2_main >= k1_main else \
-        ("K1 apply (Aᵀ·u)", k1_gbs, k1_main, "k1_main")
+    # dominant kernel = the slower of the two tensor-core main kernels
+    # (k_pm_main<1> = K2 apply_adjoint, k_pm_main<0> = K1 apply); main_ms is
+    # its average launch duration from CUDA events on the library's stream
+    dom = ("K2 apply_adjoint (A·v): k_pm_main<1>", k2_gbs, k2_main, "k_pm_main<1>") \
+        if k2_main >= k1_main else ("K1 apply (Aᵀ·u): k_pm_main<0>", k1_gbs, k1_main, "k_pm_main<0>")
     traffic = ncu_traffic(dom[3]) if ws == 1 else None
 
     cpu = None
