@@ -122,6 +122,12 @@ int gkb_op_shape(gkb_op* op, int64_t* rows, int64_t* cols);
 int gkb_op_apply(gkb_op* op, const double* x, double* y);
 int gkb_op_apply_adjoint(gkb_op* op, const double* x, double* y);
 int64_t gkb_op_mvps(gkb_op* op);
+/* Page-locked host memory for the vectors passed to gkb_op_apply /
+ * gkb_op_apply_adjoint (no reference counterpart: the reference's vectors are
+ * Eigen::VectorXd in pageable memory). Copies from/to these buffers run at
+ * full PCIe/C2C DMA rate; any host pointer remains valid input. */
+int gkb_host_alloc(size_t bytes, void** ptr);
+int gkb_host_free(void* ptr);
 int gkb_op_destroy(gkb_op* op);
 
 /* Device-resident timing loop used by bench.py: `iters` applications of

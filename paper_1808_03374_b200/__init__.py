@@ -9,12 +9,13 @@ from ._lib import FormatError, GkbError, LogicError, LIB_PATH
 from .gkl import (Context, DenseOperator, GenotypeOperator, GklOptions, LanczosFactorization,
                   LinearOperator, ReorthMode, RestartMode, RitzSet, ScalingScheme, StepInfo,
                   StepStatus, SvdlResult, SvdlStats, cgs2, default_context, error_metric_l1,
-                  marker_scaling, partition_rows, rng_uniform_symmetric, svd_small, svdl)
+                  marker_scaling, partition_rows, pinned_empty, rng_uniform_symmetric, svd_small,
+                  svdl)
 
 __all__ = [
     "FormatError", "GkbError", "LogicError", "LIB_PATH", "Context", "DenseOperator",
     "GenotypeOperator", "GklOptions", "LanczosFactorization", "LinearOperator", "ReorthMode",
     "RestartMode", "RitzSet", "ScalingScheme", "StepInfo", "StepStatus", "SvdlResult", "SvdlStats",
     "cgs2", "default_context", "error_metric_l1", "marker_scaling", "partition_rows",
-    "rng_uniform_symmetric", "svd_small", "svdl",
+    "pinned_empty", "rng_uniform_symmetric", "svd_small", "svdl",
 ]

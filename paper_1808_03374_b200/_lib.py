@@ -117,6 +117,8 @@ SIGNATURES = {
     "gkb_op_apply": (I, [P, PD, PD]),
     "gkb_op_apply_adjoint": (I, [P, PD, PD]),
     "gkb_op_mvps": (I64, [P]),
+    "gkb_host_alloc": (I, [C.c_size_t, C.POINTER(P)]),
+    "gkb_host_free": (I, [P]),
     "gkb_op_destroy": (I, [P]),
     "gkb_op_bench": (I, [P, I, I, I, PD, PD, C.POINTER(C.c_int)]),
     "gkb_gkl_options_default": (None, [C.POINTER(gkb_gkl_options)]),

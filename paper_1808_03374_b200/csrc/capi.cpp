@@ -249,6 +249,21 @@ int gkb_op_apply(gkb_op* op, const double* x, double* y) {
   });
 }
 
+int gkb_host_alloc(size_t bytes, void** ptr) {
+  return guarded([&] {
+    need(ptr, "ptr");
+    *ptr = nullptr;
+    if (bytes == 0) gkb::fail(GKB_EINVAL, "host_alloc: zero bytes");
+    GKB_CUDA(cudaMallocHost(ptr, bytes));
+  });
+}
+
+int gkb_host_free(void* ptr) {
+  return guarded([&] {
+    if (ptr) GKB_CUDA(cudaFreeHost(ptr));
+  });
+}
+
 int gkb_op_apply_adjoint(gkb_op* op, const double* x, double* y) {
   return guarded([&] {
     need(op, "op");

@@ -27,7 +27,7 @@ __all__ = [
     "ReorthMode", "RestartMode", "ScalingScheme", "GklOptions", "SvdlStats", "SvdlResult",
     "Context", "LinearOperator", "DenseOperator", "GenotypeOperator", "LanczosFactorization",
     "StepInfo", "StepStatus", "RitzSet", "svdl", "cgs2", "svd_small", "rng_uniform_symmetric",
-    "partition_rows", "marker_scaling", "error_metric_l1",
+    "partition_rows", "marker_scaling", "error_metric_l1", "pinned_empty",
 ]
 
 
@@ -40,6 +40,32 @@ def _f64(a, n: Optional[int] = None) -> np.ndarray:
     if n is not None and a.size != n:
         raise ValueError(f"length mismatch: expected {n}, got {a.size}")
     return a
+
+
+def _out(out, n: int) -> np.ndarray:
+    if out is None:
+        return np.empty(n)
+    if (not isinstance(out, np.ndarray) or out.dtype != np.float64 or out.size != n
+            or not out.flags.c_contiguous or not out.flags.writeable):
+        raise ValueError(f"out must be a writeable contiguous float64 array of length {n}")
+    return out
+
+
+def pinned_empty(n: int) -> np.ndarray:
+    """Uninitialized float64 array of length n in page-locked host memory
+    (gkb_host_alloc), freed when the array is garbage collected. Inputs and
+    `out` arrays in pinned memory make gkb_op_apply's copies DMA-rate."""
+    import weakref
+    n = int(n)
+    if n <= 0:
+        raise ValueError("pinned_empty: n must be positive")
+    ptr = C.c_void_p()
+    check(lib.gkb_host_alloc(C.c_size_t(8 * n), C.byref(ptr)))
+    buf = (C.c_double * n).from_address(ptr.value)
+    arr = np.ctypeslib.as_array(buf)
+    weakref.finalize(buf, lib.gkb_host_free, C.c_void_p(ptr.value))
+    arr.setflags(write=True)
+    return arr
 
 
 class ReorthMode(enum.IntEnum):  # gkl.hpp:12
@@ -198,17 +224,19 @@ class LinearOperator:
     def shape(self):
         return (self._m, self._n)
 
-    def apply(self, x) -> np.ndarray:
-        """y = X x (linop.hpp:20-22); raises ValueError on length mismatch."""
+    def apply(self, x, out=None) -> np.ndarray:
+        """y = X x (linop.hpp:20-22); raises ValueError on length mismatch.
+        `out` (float64, length rows) receives the result; pass arrays from
+        `pinned_empty` for DMA-rate host<->device copies."""
         x = _f64(x, self._n)
-        y = np.empty(self._m)
+        y = _out(out, self._m)
         check(lib.gkb_op_apply(self._h, _pd(x), _pd(y)))
         return y
 
-    def apply_adjoint(self, x) -> np.ndarray:
-        """y = X^T x (linop.hpp:24-26)."""
+    def apply_adjoint(self, x, out=None) -> np.ndarray:
+        """y = X^T x (linop.hpp:24-26); `out` as for apply (length cols)."""
         x = _f64(x, self._m)
-        y = np.empty(self._n)
+        y = _out(out, self._n)
         check(lib.gkb_op_apply_adjoint(self._h, _pd(x), _pd(y)))
         return y
 

@@ -136,3 +136,27 @@ def test_format_errors(gkb):
         gkb.GenotypeOperator.from_bed_payload(np.zeros(10, np.uint8), 3, 16)
     with pytest.raises(ValueError):
         gkb.GenotypeOperator.from_bed_payload(np.zeros(0, np.uint8), 0, 16)
+
+
+def test_pinned_buffers_and_out(gkb):
+    """gkb.pinned_empty + out= (page-locked host vectors) give the same bits as
+    pageable numpy vectors; out= validation follows the reference's
+    invalid_argument behaviour (ValueError)."""
+    p, n = 257, 1000
+    payload, _ = random_payload(p, n, seed=5)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
+    x = np.random.default_rng(1).standard_normal(n)
+    xp = gkb.pinned_empty(n)
+    xp[:] = x
+    yp = gkb.pinned_empty(p)
+    zp = gkb.pinned_empty(n)
+    y = op.apply(x)
+    assert op.apply(xp, out=yp) is yp
+    assert np.array_equal(y, yp)
+    z = op.apply_adjoint(y)
+    op.apply_adjoint(yp, out=zp)
+    assert np.array_equal(z, zp)
+    with pytest.raises(ValueError):
+        op.apply(x, out=np.empty(p + 1))
+    with pytest.raises(ValueError):
+        op.apply(x, out=np.empty(p, dtype=np.float32))
