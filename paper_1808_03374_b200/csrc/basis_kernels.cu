@@ -144,6 +144,34 @@ __global__ void k_axpy_norms(double alpha, const double* __restrict__ u, double*
   block_reduce_write<2>(acc, partial + (int64_t)blockIdx.x * 2);
 }
 
+// alpha = sqrt(*nrm2) read on the device (IEEE sqrt: bitwise equal to the
+// host's std::sqrt of the same value) -- used to launch the next half-step
+// before the host has read the norm.
+__global__ void k_axpy_norms_dsq(const double* __restrict__ nrm2, const double* __restrict__ u,
+                                 double* __restrict__ v, int64_t len, int64_t rows_per_block,
+                                 double* __restrict__ partial) {
+  const double alpha = sqrt(*nrm2);
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r1 = min(len, r0 + rows_per_block);
+  double acc[2] = {0.0, 0.0};
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += kT) {
+    const double old = v[r];
+    const double nv = old - alpha * u[r];
+    v[r] = nv;
+    acc[0] += old * old;
+    acc[1] += nv * nv;
+  }
+  block_reduce_write<2>(acc, partial + (int64_t)blockIdx.x * 2);
+}
+
+__global__ void k_div_copy_dsq(const double* __restrict__ src, const double* __restrict__ nrm2,
+                               double* __restrict__ dst, int64_t len) {
+  const double divisor = sqrt(*nrm2);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < len;
+       r += (int64_t)gridDim.x * blockDim.x)
+    dst[r] = src[r] / divisor;
+}
+
 __global__ void k_div_copy(const double* __restrict__ src, double divisor, double* __restrict__ dst,
                            int64_t len) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < len;
@@ -256,6 +284,21 @@ void axpy_norms(double alpha, const double* u, double* v, int64_t len, RedScratc
   const int64_t nblk = (len + rpb - 1) / rpb > 0 ? (len + rpb - 1) / rpb : 1;
   k_axpy_norms<<<(unsigned)nblk, kT, 0, s>>>(alpha, u, v, len, rpb, rs.partial);
   k_finalize<<<1, 32, 0, s>>>(rs.partial, (int)nblk, 2, out);
+}
+
+void axpy_norms_dsq(const double* nrm2, const double* u, double* v, int64_t len, RedScratch& rs,
+                    double* out, cudaStream_t s) {
+  const int64_t nb = red_blocks(len);
+  const int64_t rpb = rows_per_block(len, nb);
+  const int64_t nblk = (len + rpb - 1) / rpb > 0 ? (len + rpb - 1) / rpb : 1;
+  k_axpy_norms_dsq<<<(unsigned)nblk, kT, 0, s>>>(nrm2, u, v, len, rpb, rs.partial);
+  k_finalize<<<1, 32, 0, s>>>(rs.partial, (int)nblk, 2, out);
+}
+
+void div_copy_dsq(const double* src, const double* nrm2, double* dst, int64_t len,
+                  cudaStream_t s) {
+  if (len == 0) return;
+  k_div_copy_dsq<<<elem_grid(len), kT, 0, s>>>(src, nrm2, dst, len);
 }
 
 void div_copy(const double* src, double divisor, double* dst, int64_t len, cudaStream_t s) {

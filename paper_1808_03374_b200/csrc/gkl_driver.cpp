@@ -107,6 +107,13 @@ Lanczos::Lanczos(DevOp* op, int64_t capacity, const double* start, uint64_t rng_
   mu_next_.assign((size_t)(cap_ + 2), 0.0);
   nu_.assign((size_t)(cap_ + 1), 0.0);
   nu_next_.assign((size_t)(cap_ + 1), 0.0);
+  ctx_->set_device(0);
+  GKB_CUDA(cudaEventCreateWithFlags(&ev_left_, cudaEventDisableTiming));
+  GKB_CUDA(cudaEventCreateWithFlags(&ev_right_, cudaEventDisableTiming));
+  {
+    const char* e = getenv("GKB_NO_SPECULATE");  // sequential order (equivalence tests)
+    speculate_ = !(e && e[0] == '1');
+  }
   std::vector<double> v0(start, start + n_);
   for (auto& x : v0) x /= nrm;
   host_to_all(v0.data(), n_, V_);
@@ -122,27 +129,52 @@ Lanczos::~Lanczos() {
       if (p) cudaFree(p);
     if (i < tmp_small_.size() && tmp_small_[i]) cudaFree(tmp_small_[i]);
   }
-  if (pinned_) cudaFreeHost(pinned_);
+  for (double* p : ring_slot_)
+    if (p) cudaFreeHost(p);
+  for (cudaEvent_t e : ring_ev_)
+    if (e) cudaEventDestroy(e);
+  if (ev_left_) cudaEventDestroy(ev_left_);
+  if (ev_right_) cudaEventDestroy(ev_right_);
 }
 
+// Small host->device uploads (coupling coefficients, restart matrices, start
+// vectors) go through a ring of pinned staging slots; a slot is reused only
+// after its previous copies (recorded events) have completed, so uploads never
+// synchronize the streams.
 void Lanczos::host_to_all(const double* h, int64_t count, std::vector<double*>& dst) {
   if (count == 0) return;
-  if (pinned_cap_ < count) {
-    if (pinned_) {
-      ctx_->sync_all();
-      GKB_CUDA(cudaFreeHost(pinned_));
-    }
-    pinned_cap_ = std::max<int64_t>(count, 1 << 12);
-    GKB_CUDA(cudaMallocHost(&pinned_, sizeof(double) * (size_t)pinned_cap_));
-  } else {
-    ctx_->sync_all();  // previous uploads from the staging buffer have completed
+  const int L = (int)dst.size();
+  if (ring_cap_ < count || (int)ring_ev_.size() != kRing * L) {
+    ctx_->sync_all();
+    for (double* p : ring_slot_)
+      if (p) GKB_CUDA(cudaFreeHost(p));
+    for (cudaEvent_t e : ring_ev_)
+      if (e) cudaEventDestroy(e);
+    ring_cap_ = std::max<int64_t>(std::max(count, ring_cap_), 1 << 12);
+    ring_slot_.assign(kRing, nullptr);
+    ring_ev_.assign((size_t)(kRing * L), nullptr);
+    for (int k = 0; k < kRing; ++k)
+      GKB_CUDA(cudaMallocHost(&ring_slot_[k], sizeof(double) * (size_t)ring_cap_));
+    for (int k = 0; k < kRing; ++k)
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        GKB_CUDA(cudaEventCreateWithFlags(&ring_ev_[k * L + i], cudaEventDisableTiming));
+      }
+    ring_used_.assign(kRing, 0);
+    ring_next_ = 0;
   }
-  std::memcpy(pinned_, h, sizeof(double) * (size_t)count);
-  for (size_t i = 0; i < dst.size(); ++i) {
-    ctx_->set_device((int)i);
-    GKB_CUDA(cudaMemcpyAsync(dst[i], pinned_, sizeof(double) * (size_t)count,
+  const int k = ring_next_;
+  ring_next_ = (ring_next_ + 1) % kRing;
+  if (ring_used_[k])
+    for (int i = 0; i < L; ++i) GKB_CUDA(cudaEventSynchronize(ring_ev_[k * L + i]));
+  std::memcpy(ring_slot_[k], h, sizeof(double) * (size_t)count);
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    GKB_CUDA(cudaMemcpyAsync(dst[i], ring_slot_[k], sizeof(double) * (size_t)count,
                              cudaMemcpyHostToDevice, ctx_->shards[i].stream));
+    GKB_CUDA(cudaEventRecord(ring_ev_[k * L + i], ctx_->shards[i].stream));
   }
+  ring_used_[k] = 1;
 }
 
 void Lanczos::upload_small(const std::vector<double>& W, std::vector<double*>& dst) {
@@ -160,6 +192,19 @@ void Lanczos::upload_small(const std::vector<double>& W, std::vector<double*>& d
   }
   host_to_all(W.data(), need, tmp_small_);
   dst = tmp_small_;
+}
+
+void Lanczos::read_async(int64_t off, int64_t count, cudaEvent_t ev) {
+  Shard& s = ctx_->shards[0];
+  ctx_->set_device(0);
+  GKB_CUDA(cudaMemcpyAsync(s.hres + off, s.dres + off, sizeof(double) * (size_t)count,
+                           cudaMemcpyDeviceToHost, s.stream));
+  GKB_CUDA(cudaEventRecord(ev, s.stream));
+}
+
+void Lanczos::wait_event(cudaEvent_t ev) {
+  GKB_CUDA(cudaEventSynchronize(ev));
+  ++host_syncs;
 }
 
 void Lanczos::read(int64_t count) {
@@ -231,10 +276,30 @@ double Lanczos::cgs2(Side side, int64_t ncols, const std::vector<double*>& vec) 
   return norm_after;
 }
 
+// Host-side prediction used to decide whether to launch the right half-step
+// before alpha is known: the left omega estimate (the same recurrence as
+// partial_reorth_update) evaluated with a pessimistic alpha (half the previous
+// one). Only a hint -- a wrong guess costs one discarded K2, never a result.
+bool Lanczos::left_reorth_unlikely(const Options& o, double norm_scale) const {
+  const int64_t j = j_;
+  if (j == 0) return false;
+  if (!monitors_side(true, m_, n_, o, norm_scale)) return true;
+  const double lvl = eps_level(m_, n_);
+  const double tau = 2.0 * lvl * norm_scale + lvl;
+  const double guess = 0.5 * Bc(j - 1, j - 1);
+  const double denom = std::max(guess, tau + kEps);
+  for (int64_t i = 0; i < j; ++i) {
+    double acc = 0.0;
+    for (int64_t c = i; c < j; ++c) acc += std::abs(Bc(i, c)) * mu_[c];
+    if (std::min(1.0, (acc + tau) / denom) > o.omega) return false;
+  }
+  return true;
+}
+
 // partial_reorth_update (gkl.cpp:112-176): omega recurrences on the host,
 // device cgs2 when the estimate crosses omega.
 bool Lanczos::partial_reorth_update(Side side, const std::vector<double*>& cand, double cand_coeff,
-                                    const Options& o, double norm_scale) {
+                                    const Options& o, double norm_scale, double* new_norm) {
   const int64_t j = j_;
   const double lvl = eps_level(m_, n_);
   const double tau = 2.0 * lvl * norm_scale + lvl;
@@ -257,7 +322,8 @@ bool Lanczos::partial_reorth_update(Side side, const std::vector<double*>& cand,
     }
     nu_next_[j] = 1.0;
     if (worst > o.omega && monitors_side(true, m_, n_, o, norm_scale)) {
-      cgs2(kLeft, j, cand);
+      // ||w|| after the passes (gkl.cpp:244 recomputes w.norm(); cgs2 returns it)
+      *new_norm = cgs2(kLeft, j, cand);
       for (int64_t i = 0; i < j; ++i) nu_next_[i] = lvl;
       return true;
     }
@@ -278,7 +344,7 @@ bool Lanczos::partial_reorth_update(Side side, const std::vector<double*>& cand,
   }
   mu_next_[j] = 1.0;
   if (worst > o.omega && monitors_side(false, m_, n_, o, norm_scale)) {
-    cgs2(kRight, j, cand);
+    *new_norm = cgs2(kRight, j, cand);  // = z.norm() after the passes (gkl.cpp:290)
     for (int64_t i = 0; i < j; ++i) mu_next_[i] = lvl;
     return true;
   }
@@ -317,6 +383,37 @@ void Lanczos::deflate_right() {
   right_exhausted_ = true;
 }
 
+// Right half-step kernels after alpha is fixed: u_s = w / alpha (or
+// w / sqrt(dres[nidx]) on the device when `dev_alpha`), z = X^T u_s (cross-
+// shard sum inside adjoint_dev), then in partial mode z -= alpha v_s with
+// both norms into dres[kRightSlot..+1] and their D2H + ev_right_.
+void Lanczos::launch_right(int64_t s, const std::vector<double*>& dres, int64_t nidx,
+                           bool dev_alpha, double alpha, bool partial) {
+  const int L = (int)ctx_->shards.size();
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    const int64_t r = op_->rows(i);
+    if (dev_alpha)
+      dev::div_copy_dsq(w_[i], dres[i] + nidx, U_[i] + s * r, r, ctx_->shards[i].stream);
+    else
+      dev::div_copy(w_[i], alpha, U_[i] + s * r, r, ctx_->shards[i].stream);
+  }
+  std::vector<const double*> uin(L);
+  for (int i = 0; i < L; ++i) uin[i] = U_[i] + s * op_->rows(i);
+  op_->adjoint_dev(uin, z_);
+  if (!partial) return;
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    Shard& sh = ctx_->shards[i];
+    if (dev_alpha)
+      dev::axpy_norms_dsq(dres[i] + nidx, V_[i] + s * n_, z_[i], n_, sh.rs, dres[i] + kRightSlot,
+                          sh.stream);
+    else
+      dev::axpy_norms(alpha, V_[i] + s * n_, z_[i], n_, sh.rs, dres[i] + kRightSlot, sh.stream);
+  }
+  read_async(kRightSlot, 2, ev_right_);
+}
+
 // bidiag_step (gkl.cpp:206-312)
 StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter) {
   const int64_t s = j_;
@@ -335,6 +432,7 @@ StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter
     for (int i = 0; i < L; ++i) b[i] = dres[i] + off;
     ctx_->allreduce(b, cnt);
   };
+  bool spec = false;  // right half already launched with the device-side alpha
 
   // Left half-step: alpha u_{s+1} = X v_pending - U coupling.
   {
@@ -353,15 +451,14 @@ StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter
         if (lo < 0) lo = i;
         hi = i;
       }
-    double w_norm0, alpha_cand;
+    int64_t nidx;  // dres[nidx] = alpha_cand^2 on every shard
     if (lo < 0) {
       for (int i = 0; i < L; ++i) {
         ctx_->set_device(i);
         dev::nrm2sq(w_[i], op_->rows(i), ctx_->shards[i].rs, dres[i], ctx_->shards[i].stream);
       }
       reduce_left(0, 1);
-      read(1);
-      w_norm0 = alpha_cand = std::sqrt(ctx_->shards[0].hres[0]);
+      nidx = 0;
     } else {
       std::vector<double> cf(coupling_.begin() + lo, coupling_.begin() + hi + 1);
       host_to_all(cf.data(), hi - lo + 1, cbuf_);
@@ -373,11 +470,23 @@ StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter
                     dres[i], sh.stream);
       }
       reduce_left(0, 2);
-      read(2);
-      w_norm0 = std::sqrt(ctx_->shards[0].hres[0]);
-      alpha_cand = std::sqrt(ctx_->shards[0].hres[1]);
+      nidx = 1;
     }
+    // The norms go to the host asynchronously; meanwhile the right half-step
+    // is launched with alpha = sqrt(dres[nidx]) taken on the device -- the
+    // same IEEE sqrt the host applies below, so every result is bitwise what
+    // the sequential order produces. It is discarded (and redone below) when
+    // the host's decisions change w: second pass or reorthogonalization.
+    read_async(0, nidx + 1, ev_left_);
+    if (speculate_ && lo < 0 && left_reorth_unlikely(o, norm_scale)) {
+      launch_right(s, dres, nidx, true, 0.0, true);
+      spec = true;
+    }
+    wait_event(ev_left_);
+    const double w_norm0 = std::sqrt(ctx_->shards[0].hres[0]);
+    double alpha_cand = std::sqrt(ctx_->shards[0].hres[nidx]);
     if (alpha_cand < kCgs2Eta * w_norm0) {
+      spec = false;
       // Local (modified) second pass over the structural pattern.
       for (int64_t c = 0; c < s; ++c) {
         if (coupling_[c] == 0.0) continue;
@@ -402,28 +511,23 @@ StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter
       read(1);
       alpha_cand = std::sqrt(ctx_->shards[0].hres[0]);
     }
-    if (partial_reorth_update(kLeft, w_, alpha_cand, o, norm_scale)) {
+    double reorth_norm = 0.0;
+    if (partial_reorth_update(kLeft, w_, alpha_cand, o, norm_scale, &reorth_norm)) {
+      spec = false;
       info.reorth_left = true;
-      for (int i = 0; i < L; ++i) {
-        ctx_->set_device(i);
-        dev::nrm2sq(w_[i], op_->rows(i), ctx_->shards[i].rs, dres[i], ctx_->shards[i].stream);
-      }
-      reduce_left(0, 1);
-      read(1);
-      alpha_cand = std::sqrt(ctx_->shards[0].hres[0]);
+      alpha_cand = reorth_norm;
     }
     alpha = alpha_cand;
+    // (a speculation that turned out wrong is simply overwritten: stream order)
+    if (spec) ++spec_hits; else if (speculate_) ++spec_misses;
   }
   if (!(alpha > breakdown_tol)) {
     info.status = 1;
-    return info;  // nothing appended
+    return info;  // nothing appended (a speculative u_s / z is unused scratch)
   }
   info.alpha = alpha;
-  for (int i = 0; i < L; ++i) {
-    ctx_->set_device(i);
-    const int64_t r = op_->rows(i);
-    dev::div_copy(w_[i], alpha, U_[i] + s * r, r, ctx_->shards[i].stream);
-  }
+  if (!spec) launch_right(s, dres, 0, false, alpha, !full);
+  if (mvp_counter) ++*mvp_counter;
   for (int64_t i = 0; i < s; ++i) B(i, s) = coupling_[i];
   B(s, s) = alpha;
   if (full) {
@@ -434,25 +538,15 @@ StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter
   }
   j_ = s + 1;
 
-  // Right half-step: beta v_new = X^T u_{s+1} - alpha v_pending.
-  {
-    std::vector<const double*> uin(L);
-    for (int i = 0; i < L; ++i) uin[i] = U_[i] + s * op_->rows(i);
-    op_->adjoint_dev(uin, z_);
-    if (mvp_counter) ++*mvp_counter;
-  }
+  // Right half-step: beta v_new = X^T u_{s+1} - alpha v_pending (z = X^T u
+  // and z -= alpha v_s with its norms were launched by launch_right).
   double beta;
   if (full) {
     beta = cgs2(kRight, s + 1, z_);
   } else {
-    for (int i = 0; i < L; ++i) {
-      ctx_->set_device(i);
-      Shard& sh = ctx_->shards[i];
-      dev::axpy_norms(alpha, V_[i] + s * n_, z_[i], n_, sh.rs, dres[i], sh.stream);
-    }
-    read(2);
-    const double z_norm0 = std::sqrt(ctx_->shards[0].hres[0]);
-    double beta_cand = std::sqrt(ctx_->shards[0].hres[1]);
+    wait_event(ev_right_);
+    const double z_norm0 = std::sqrt(ctx_->shards[0].hres[kRightSlot]);
+    double beta_cand = std::sqrt(ctx_->shards[0].hres[kRightSlot + 1]);
     if (beta_cand < kCgs2Eta * z_norm0) {
       for (int i = 0; i < L; ++i) {
         ctx_->set_device(i);
@@ -464,14 +558,10 @@ StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter
       read(1);
       beta_cand = std::sqrt(ctx_->shards[0].hres[0]);
     }
-    if (partial_reorth_update(kRight, z_, beta_cand, o, norm_scale)) {
+    double reorth_norm = 0.0;
+    if (partial_reorth_update(kRight, z_, beta_cand, o, norm_scale, &reorth_norm)) {
       info.reorth_right = true;
-      for (int i = 0; i < L; ++i) {
-        ctx_->set_device(i);
-        dev::nrm2sq(z_[i], n_, ctx_->shards[i].rs, dres[i], ctx_->shards[i].stream);
-      }
-      read(1);
-      beta_cand = std::sqrt(ctx_->shards[0].hres[0]);
+      beta_cand = reorth_norm;
     }
     beta = beta_cand;
   }
@@ -791,6 +881,11 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
   cudaEventDestroy(e1);
   out.device_seconds = ms * 1e-3;
   out.host_syncs = f.host_syncs;
+  if (const char* e = getenv("GKB_VERBOSE"))
+    if (e[0] == '1')
+      fprintf(stderr, "[gkb] svdl: %lld steps, host syncs %lld, speculative right half-steps kept %lld / "
+              "not used %lld\n", (long long)out.steps, (long long)f.host_syncs,
+              (long long)f.spec_hits, (long long)f.spec_misses);
   op->mvps += mvps;
   out.wall_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();

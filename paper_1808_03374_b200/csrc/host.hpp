@@ -193,6 +193,7 @@ class Lanczos {
   void ritz_vectors(const Ritz& r, int64_t kc, double* outU, double* outV);
   double cgs2_right_host(int64_t ncols);  // test hook
   int64_t host_syncs = 0;
+  int64_t spec_hits = 0, spec_misses = 0;  // speculative right half-steps kept / not launched or redone
   Rng rng;
 
  private:
@@ -210,14 +211,28 @@ class Lanczos {
   const std::vector<double*>& basis(Side s) const { return s == kLeft ? U_ : V_; }
   int64_t ld(Side s, int i) const { return s == kLeft ? op_->rows(i) : n_; }
   void read(int64_t count);  // D2H shard-0 dres[0..count) -> hres, sync
+  // D2H shard-0 dres[off..off+count) -> hres (same offsets) + event; no sync
+  void read_async(int64_t off, int64_t count, cudaEvent_t ev);
+  void wait_event(cudaEvent_t ev);  // host waits for a read_async (counts a host sync)
+  // u_s = w / alpha, z = X^T u_s, (partial) z -= alpha v_s + norms -> hres[kRightSlot..]
+  void launch_right(int64_t s, const std::vector<double*>& dres, int64_t nidx, bool dev_alpha,
+                    double alpha, bool partial);
+  static constexpr int64_t kRightSlot = 16;  // dres/hres slot of the right half-step norms
+  cudaEvent_t ev_left_ = nullptr, ev_right_ = nullptr;
+  bool speculate_ = true;  // launch the right half-step before the host reads alpha
+  bool left_reorth_unlikely(const Options& o, double norm_scale) const;
   double cgs2(Side side, int64_t ncols, const std::vector<double*>& vec);
   bool partial_reorth_update(Side side, const std::vector<double*>& cand, double cand_coeff,
-                             const Options& o, double norm_scale);
+                             const Options& o, double norm_scale, double* new_norm);
   void upload_small(const std::vector<double>& W, std::vector<double*>& dst);
   std::vector<double*> tmp_small_;
   int64_t tmp_cap_ = 0;
-  double* pinned_ = nullptr;
-  int64_t pinned_cap_ = 0;
+  static constexpr int kRing = 4;  // pinned staging slots for host_to_all
+  std::vector<double*> ring_slot_;
+  std::vector<cudaEvent_t> ring_ev_;  // kRing x shards
+  std::vector<char> ring_used_;
+  int64_t ring_cap_ = 0;
+  int ring_next_ = 0;
   void host_to_all(const double* h, int64_t count, std::vector<double*>& dst);
 };
 

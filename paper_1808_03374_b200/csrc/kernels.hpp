@@ -116,6 +116,12 @@ void axpy_norms(double alpha, const double* u, double* v, int64_t len, RedScratc
                 cudaStream_t s);
 // dst = src / divisor (the reference divides: w /= alpha, gkl.cpp:253)
 void div_copy(const double* src, double divisor, double* dst, int64_t len, cudaStream_t s);
+// Same two operations with the scalar taken as sqrt(*nrm2) on the device
+// (bitwise equal to the host's sqrt of the same value): lets the driver launch
+// the next half-step before the host has read the norm.
+void div_copy_dsq(const double* src, const double* nrm2, double* dst, int64_t len, cudaStream_t s);
+void axpy_norms_dsq(const double* nrm2, const double* u, double* v, int64_t len, RedScratch& rs,
+                    double* out, cudaStream_t s);
 // dst[:, 0:kc] = Q[:, 0:j] * W (W is j x kc, ldw rows, on device); dst may not alias Q
 void gemm_small(const double* Q, int64_t ld, int64_t len, int64_t j, const double* W, int64_t ldw,
                 int64_t kc, double* dst, int64_t ldd, cudaStream_t s);

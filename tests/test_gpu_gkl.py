@@ -255,3 +255,24 @@ def test_svdl_sharded_matches(gkb, orc):
     assert rel_err(a.singvals, b.singvals) <= 1e-9
     assert principal_angles(a.V, b.V) < 1e-6
     assert principal_angles(a.U, b.U) < 1e-6
+
+
+@pytest.mark.parametrize("cfg,scale,nshards", [(2, 0.05, 1), (3, 0.01, 2), (1, 0.1, 1)])
+def test_speculative_right_half_is_bitwise_sequential(gkb, orc, monkeypatch, cfg, scale, nshards):
+    """The driver launches the right half-step with alpha taken on the device
+    before the host has read it (and redoes it when the host's decision
+    changes w). Results must be bitwise those of the sequential order
+    (GKB_NO_SPECULATE=1), including the operation counts."""
+    from paper_1808_03374_b200 import synth
+    spec = synth.config_spec(cfg, scale=scale)
+    opts = synth.config_options(cfg)
+    op, _ = _geno_pair(gkb, orc, spec, nshards=nshards)
+    monkeypatch.setenv("GKB_NO_SPECULATE", "1")
+    a = gkb.svdl(op, opts)
+    monkeypatch.delenv("GKB_NO_SPECULATE")
+    b = gkb.svdl(op, opts)
+    assert np.array_equal(a.singvals, b.singvals)
+    assert np.array_equal(a.U, b.U) and np.array_equal(a.V, b.V)
+    assert np.array_equal(a.err_estimates, b.err_estimates)
+    for f in ("mvps", "steps", "restarts", "reorth_count", "deflations"):
+        assert getattr(a.stats, f) == getattr(b.stats, f), f
