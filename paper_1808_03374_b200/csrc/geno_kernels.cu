@@ -380,6 +380,24 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// sum_{k in [k0, ke)} cv[ent[k]] in order, 4 independent loads in flight
+__device__ __forceinline__ double walk_list(const uint16_t* __restrict__ ent, uint32_t k0,
+                                            uint32_t ke, const double* __restrict__ cv) {
+  double corr = 0.0;
+  uint32_t k = k0;
+#pragma unroll 1
+  for (; k + 4 <= ke; k += 4) {
+    const int c0 = ent[k], c1 = ent[k + 1], c2 = ent[k + 2], c3 = ent[k + 3];
+    corr += cv[c0];
+    corr += cv[c1];
+    corr += cv[c2];
+    corr += cv[c3];
+  }
+#pragma unroll 1
+  for (; k < ke; ++k) corr += cv[ent[k]];
+  return corr;
+}
+
 // Missing-list staging in shared memory (after the digits): 257 offsets and
 // up to kEntCap entries of the CTA's list (longer lists are read from global).
 constexpr int kEntCap = 8192;
@@ -426,20 +444,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
   uint8_t* stage = reinterpret_cast<uint8_t*>(dg + kt_cta * 64);
   uint32_t* offs = reinterpret_cast<uint32_t*>(stage);
   double* cvs = reinterpret_cast<double*>(stage + kOffBytes + 2 * kEntCap + 16);
-  const uint16_t* ents = nullptr;
+  // list entries: staged into shared memory (ent_shift = offset of the run's
+  // first entry in the staged 16-byte-aligned copy), or -- a block denser in
+  // missing entries than kEntCap -- walked in global memory (ent_shift < 0)
+  int ent_shift = -1;
+  int64_t eb = 0;
   if (m_off) {
     for (int i = threadIdx.x; i <= kRowsPerCta; i += kThreads)
       cp_async4(offs + i, m_off + b * (kRowsPerCta + 1) + i);
-    const int64_t eb = m_base[b];
+    eb = m_base[b];
     const int64_t ne = m_off[b * (kRowsPerCta + 1) + kRowsPerCta];
     const int64_t a0 = (eb * 2) & ~int64_t(15), a1 = (eb * 2 + ne * 2 + 15) & ~int64_t(15);
     if (a1 - a0 <= 2 * kEntCap) {
       const uint8_t* esrc = reinterpret_cast<const uint8_t*>(m_ent) + a0;
       for (int64_t i = threadIdx.x; i < (a1 - a0) / 16; i += kThreads)
         cp_async16(stage + kOffBytes + 16 * i, esrc + 16 * i);
-      ents = reinterpret_cast<const uint16_t*>(stage + kOffBytes) + (eb - a0 / 2);
-    } else {
-      ents = m_ent + eb;  // (dense-missing block) walk the list in global memory
+      ent_shift = (int)(eb - a0 / 2);
     }
     // 8-byte copies: x may be a Krylov-basis column with an odd leading dimension
     const int ncol = (int)min((int64_t)ktiles * 128, C - col0);
@@ -496,16 +516,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
     double corr = 0.0;
     if (m_off) {
       const uint32_t e0 = offs[rl], e1 = offs[rl + 1], mid = e0 + (e1 - e0) / 2;
-      uint32_t k = (tid >> 1) ? mid : e0;
-      const uint32_t ke = (tid >> 1) ? e1 : mid;
-      for (; k + 4 <= ke; k += 4) {  // 4 independent loads in flight, summed in order
-        const int c0 = ents[k], c1 = ents[k + 1], c2 = ents[k + 2], c3 = ents[k + 3];
-        corr += cvs[c0];
-        corr += cvs[c1];
-        corr += cvs[c2];
-        corr += cvs[c3];
-      }
-      for (; k < ke; ++k) corr += cvs[ents[k]];
+      const uint32_t k0 = (tid >> 1) ? mid : e0, ke = (tid >> 1) ? e1 : mid;
+      if (ent_shift >= 0)  // shared-memory run (pointer derived from the smem array: LDS)
+        corr = walk_list(reinterpret_cast<const uint16_t*>(stage + kOffBytes) + ent_shift, k0, ke,
+                         cvs);
+      else
+        corr = walk_list(m_ent + eb, k0, ke, cvs);
       corr += __shfl_xor_sync(0xffffffffu, corr, 2);  // both halves, commutative -> same bits
     }
     if ((tid >> 1) == 0) {
