@@ -78,6 +78,21 @@ int gkb_partition_rows(int64_t m, int nparts, int64_t* starts);
  * (impute_mean + standardize, genio.cpp:124-185). */
 int gkb_geno_from_bed(gkb_ctx* ctx, const uint8_t* payload, int64_t p, int64_t n, gkb_op** op);
 
+/* read_bed's checks (genio.cpp:53-70) without reading the payload: p = non-
+ * empty lines of the .bim, n = of the .fam (count_lines, genio.cpp:21-30);
+ * magic 6C 1B, mode 01, size == p*ceil(n/4)+3. GKB_EFORMAT with the
+ * reference's messages ("cannot open ...", ": bad magic", ": only marker-major
+ * mode (0x01) is supported", ": payload size mismatch (expected E bytes,
+ * found F)"). Needs no GPU. */
+int gkb_bed_check(const char* bed, const char* bim, const char* fam, int64_t* p, int64_t* n);
+
+/* .bed file -> HBM (replaces read_bed + load_matrix, gkpca.cpp:89-108): the
+ * checks above, then each shard's records are streamed from the file with
+ * positional reads into double-buffered pinned staging, overlapped with the
+ * device-side layout builds (each rank / shard reads only its own rows). */
+int gkb_geno_from_bed_file(gkb_ctx* ctx, const char* bed, const char* bim, const char* fam,
+                           gkb_op** op);
+
 /* Synthetic Balding-Nichols genotypes generated directly on the device with
  * the counter-based draws of oracle/gkb_oracle.c:orc_synth_bed (bit-identical
  * .bed bytes). freq: npop x p (row k at freq[k*p]); pop: n subpopulation ids

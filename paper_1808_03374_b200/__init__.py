@@ -6,7 +6,7 @@ CGS2 / partial reorthogonalization and thick restart, behind the reference's
 Importing requires the in-tree libgkb.so (sm_100a); there is no CPU fallback.
 """
 from ._lib import FormatError, GkbError, LogicError, LIB_PATH
-from .gkl import (Context, DenseOperator, GenotypeOperator, GklOptions, LanczosFactorization,
+from .gkl import (bed_check, Context, DenseOperator, GenotypeOperator, GklOptions, LanczosFactorization,
                   LinearOperator, ReorthMode, RestartMode, RitzSet, ScalingScheme, StepInfo,
                   StepStatus, SvdlResult, SvdlStats, cgs2, default_context, error_metric_l1,
                   marker_scaling, partition_rows, pinned_empty, rng_uniform_symmetric, svd_small,
@@ -17,5 +17,5 @@ __all__ = [
     "GenotypeOperator", "GklOptions", "LanczosFactorization", "LinearOperator", "ReorthMode",
     "RestartMode", "RitzSet", "ScalingScheme", "StepInfo", "StepStatus", "SvdlResult", "SvdlStats",
     "cgs2", "default_context", "error_metric_l1", "marker_scaling", "partition_rows",
-    "pinned_empty", "rng_uniform_symmetric", "svd_small", "svdl",
+    "pinned_empty", "rng_uniform_symmetric", "svd_small", "svdl", "bed_check",
 ]

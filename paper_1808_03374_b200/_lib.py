@@ -106,6 +106,8 @@ SIGNATURES = {
     "gkb_partition_rows": (I, [I64, I, PI64]),
     "gkb_geno_from_bed": (I, [P, PU8, I64, I64, C.POINTER(P)]),
     "gkb_geno_from_synth": (I, [P, C.POINTER(gkb_synth_spec), C.POINTER(P)]),
+    "gkb_bed_check": (I, [C.c_char_p, C.c_char_p, C.c_char_p, PI64, PI64]),
+    "gkb_geno_from_bed_file": (I, [P, C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(P)]),
     "gkb_geno_counts": (I, [P, PI64]),
     "gkb_geno_standardize": (I, [P, I]),
     "gkb_geno_set_scaling": (I, [P, PD, PD]),

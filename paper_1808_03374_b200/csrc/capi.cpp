@@ -139,6 +139,38 @@ int gkb_geno_from_bed(gkb_ctx* ctx, const uint8_t* payload, int64_t p, int64_t n
   });
 }
 
+int gkb_bed_check(const char* bed, const char* bim, const char* fam, int64_t* p, int64_t* n) {
+  return guarded([&] {
+    need(bed, "bed");
+    need(bim, "bim");
+    need(fam, "fam");
+    need(p, "p");
+    need(n, "n");
+    gkb::bed_check(bed, bim, fam, p, n);
+  });
+}
+
+int gkb_geno_from_bed_file(gkb_ctx* ctx, const char* bed, const char* bim, const char* fam,
+                           gkb_op** op) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(bed, "bed");
+    need(bim, "bim");
+    need(fam, "fam");
+    need(op, "op");
+    int64_t p = 0, n = 0;
+    gkb::bed_check(bed, bim, fam, &p, &n);
+    auto h = std::make_unique<gkb_op>();
+    h->ctx = ctx;
+    auto g = std::make_unique<gkb::GenoOp>();
+    g->ctx = &ctx->c;
+    g->build_from_bed_file(bed, p, n);
+    h->geno = g.get();
+    h->op = std::move(g);
+    *op = h.release();
+  });
+}
+
 int gkb_geno_from_synth(gkb_ctx* ctx, const gkb_synth_spec* spec, gkb_op** op) {
   return guarded([&] {
     need(ctx, "ctx");

@@ -90,6 +90,9 @@ struct DevOp {
   void adjoint_host(const double* y, double* z);
 };
 
+// read_bed's checks (genio.cpp:53-70) on the three files; fills p, n.
+void bed_check(const char* bed, const char* bim, const char* fam, int64_t* p, int64_t* n);
+
 struct GenoShard {
   int64_t p_loc = 0, n = 0;
   dev::PMPlan pl1{}, pl2{};   // layout 1 (rows SNPs) / layout 2 (rows samples)
@@ -117,6 +120,7 @@ struct GenoOp : DevOp {
   bool scaled = false;
   ~GenoOp() override;
   void build_from_payload(const uint8_t* payload, int64_t p, int64_t n);
+  void build_from_bed_file(const char* bed, int64_t p, int64_t n);  // after bed_check
   void build_from_synth(const dev::SynthDev& spec_host_ptrs, const gkb_synth_spec* spec);
   void finish_build();  // counts, missing lists, plans, scratch
   void set_scaling(const double* mu, const double* inv_s);  // global p arrays

@@ -2,9 +2,15 @@
 // DenseOperator over the imputed, standardized matrix) and a device
 // DenseOperator (linop.hpp:43-64). Rows (reference markers) are sharded;
 // columns (samples) are replicated.
+#include <fcntl.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "host.hpp"
 
@@ -270,6 +276,114 @@ void GenoOp::build_from_payload(const uint8_t* payload, int64_t p, int64_t nn) {
     cudaFree(dstage);
     cudaFreeHost(hstage);
   }
+  finish_build();
+}
+
+// ---------------------------------------------------------------- .bed files
+static int64_t count_lines(const char* path) {  // genio.cpp:21-30 (non-empty lines)
+  FILE* f = std::fopen(path, "rb");
+  if (!f) fail(GKB_EFORMAT, std::string("cannot open ") + path);
+  int64_t lines = 0;
+  bool nonempty = false;
+  char buf[1 << 16];
+  size_t got;
+  while ((got = std::fread(buf, 1, sizeof buf, f)) > 0)
+    for (size_t i = 0; i < got; ++i) {
+      if (buf[i] == '\n') {
+        lines += nonempty;
+        nonempty = false;
+      } else {
+        nonempty = true;  // (getline keeps '\r'; a line of just "\r" counts, as there)
+      }
+    }
+  lines += nonempty;  // last line without a newline
+  std::fclose(f);
+  return lines;
+}
+
+void bed_check(const char* bed, const char* bim, const char* fam, int64_t* p, int64_t* n) {
+  const int64_t m = count_lines(bim), nn = count_lines(fam);
+  FILE* f = std::fopen(bed, "rb");
+  if (!f) fail(GKB_EFORMAT, std::string("cannot open ") + bed);
+  unsigned char hdr[3] = {0, 0, 0};
+  const size_t got = std::fread(hdr, 1, 3, f);
+  std::fseek(f, 0, SEEK_END);
+  const int64_t size = (int64_t)std::ftell(f);
+  std::fclose(f);
+  if (got < 3 || size < 3 || hdr[0] != 0x6c || hdr[1] != 0x1b)
+    fail(GKB_EFORMAT, std::string(bed) + ": bad magic");
+  if (hdr[2] != 0x01)
+    fail(GKB_EFORMAT, std::string(bed) + ": only marker-major mode (0x01) is supported");
+  const int64_t expected = m * ((nn + 3) / 4) + 3;
+  if (size != expected)
+    fail(GKB_EFORMAT, std::string(bed) + ": payload size mismatch (expected " +
+                          std::to_string(expected) + " bytes, found " + std::to_string(size) + ")");
+  *p = m;
+  *n = nn;
+}
+
+void GenoOp::build_from_bed_file(const char* bed, int64_t p, int64_t nn) {
+  if (p <= 0 || nn <= 0) fail(GKB_EINVAL, "genotype operator: empty dimension");
+  m = p;
+  n = nn;
+  starts = partition_rows(p, ctx->nshards_total);
+  const int L = (int)ctx->shards.size();
+  gs.resize(L);
+  const int64_t stride = (nn + 3) / 4;
+  const int fd = ::open(bed, O_RDONLY);
+  if (fd < 0) fail(GKB_EFORMAT, std::string("cannot open ") + bed);
+  try {
+    for (int i = 0; i < L; ++i) {
+      const int64_t r0 = row0(i), pr = rows(i);
+      alloc_shard(i, pr, nn);
+      Shard& sh = ctx->shards[i];
+      ctx->set_device(i);
+      // staging block: 64 MB (GKB_STAGE_MB overrides; tests use small blocks to
+      // exercise the double buffering)
+      int64_t budget = 64ll << 20;
+      if (const char* e = std::getenv("GKB_STAGE_MB")) budget = std::max<int64_t>(1, atoll(e)) << 20;
+      const int64_t br = staging_rows(stride, budget, pr);
+      uint8_t* dstage[2] = {nullptr, nullptr};
+      uint8_t* hstage[2] = {nullptr, nullptr};
+      cudaEvent_t ev[2] = {nullptr, nullptr};
+      for (int k = 0; k < 2; ++k) {
+        GKB_CUDA(cudaMalloc(&dstage[k], (size_t)(br * stride)));
+        GKB_CUDA(cudaMallocHost(&hstage[k], (size_t)(br * stride)));
+        GKB_CUDA(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+      }
+      int k = 0;
+      for (int64_t b0 = 0; b0 < pr; b0 += br, k ^= 1) {
+        const int64_t rb = std::min(br, pr - b0);
+        GKB_CUDA(cudaEventSynchronize(ev[k]));  // staging k consumed by its layout builds
+        // positional read of this block's records while the device works on the other buffer
+        const int64_t want = rb * stride;
+        int64_t done = 0;
+        while (done < want) {
+          const ssize_t r = ::pread(fd, hstage[k] + done, (size_t)(want - done),
+                                    (off_t)(3 + (r0 + b0) * stride + done));
+          if (r <= 0) fail(GKB_EFORMAT, std::string(bed) + ": short read");
+          done += r;
+        }
+        GKB_CUDA(cudaMemcpyAsync(dstage[k], hstage[k], (size_t)want, cudaMemcpyHostToDevice,
+                                 sh.stream));
+        dev::build_lt1(dstage[k], stride, rb, b0, nn, gs[i].pl1, gs[i].lt1, sh.stream);
+        GKB_LAUNCH_CHECK();
+        dev::build_lt2(dstage[k], stride, rb, b0, nn, gs[i].pl2, gs[i].lt2, sh.stream);
+        GKB_LAUNCH_CHECK();
+        GKB_CUDA(cudaEventRecord(ev[k], sh.stream));
+      }
+      GKB_CUDA(cudaStreamSynchronize(sh.stream));
+      for (int kk = 0; kk < 2; ++kk) {
+        cudaFree(dstage[kk]);
+        cudaFreeHost(hstage[kk]);
+        cudaEventDestroy(ev[kk]);
+      }
+    }
+  } catch (...) {
+    ::close(fd);
+    throw;
+  }
+  ::close(fd);
   finish_build();
 }
 

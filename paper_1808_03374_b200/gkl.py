@@ -27,7 +27,7 @@ __all__ = [
     "ReorthMode", "RestartMode", "ScalingScheme", "GklOptions", "SvdlStats", "SvdlResult",
     "Context", "LinearOperator", "DenseOperator", "GenotypeOperator", "LanczosFactorization",
     "StepInfo", "StepStatus", "RitzSet", "svdl", "cgs2", "svd_small", "rng_uniform_symmetric",
-    "partition_rows", "marker_scaling", "error_metric_l1", "pinned_empty",
+    "partition_rows", "marker_scaling", "error_metric_l1", "pinned_empty", "bed_check",
 ]
 
 
@@ -49,6 +49,14 @@ def _out(out, n: int) -> np.ndarray:
             or not out.flags.c_contiguous or not out.flags.writeable):
         raise ValueError(f"out must be a writeable contiguous float64 array of length {n}")
     return out
+
+
+def bed_check(bed: str, bim: str, fam: str):
+    """(p, n) of a PLINK fileset after read_bed's checks (genio.cpp:53-70);
+    raises FormatError with the reference's messages. Needs no GPU."""
+    p, n = C.c_int64(), C.c_int64()
+    check(lib.gkb_bed_check(bed.encode(), bim.encode(), fam.encode(), C.byref(p), C.byref(n)))
+    return p.value, n.value
 
 
 def pinned_empty(n: int) -> np.ndarray:
@@ -301,6 +309,26 @@ class GenotypeOperator(LinearOperator):
         h = C.c_void_p()
         check(lib.gkb_geno_from_bed(ctx._h, buf.ctypes.data_as(C.POINTER(C.c_uint8)), p, n,
                                     C.byref(h)))
+        op = cls(ctx, h, p, n)
+        if scheme is not None:
+            op.standardize(scheme)
+        return op
+
+    @classmethod
+    def from_bed_file(cls, bed: str, bim: Optional[str] = None, fam: Optional[str] = None,
+                      ctx: Optional[Context] = None,
+                      scheme: Optional[ScalingScheme] = ScalingScheme.kHwe):
+        """Streams a PLINK .bed file into HBM (gkb_geno_from_bed_file; read_bed's
+        checks, genio.cpp:53-70). `bed` may be the fileset prefix; .bim/.fam default
+        to the same prefix."""
+        from . import genio
+        b, bi, fa = genio.bed_paths(bed)
+        bim, fam = bim or bi, fam or fa
+        ctx = ctx or default_context()
+        p, n = bed_check(b, bim, fam)
+        h = C.c_void_p()
+        check(lib.gkb_geno_from_bed_file(ctx._h, b.encode(), bim.encode(), fam.encode(),
+                                         C.byref(h)))
         op = cls(ctx, h, p, n)
         if scheme is not None:
             op.standardize(scheme)
