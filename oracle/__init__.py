@@ -50,7 +50,7 @@ orc_op._fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("ctx", C.c_void_p)
 
 class orc_geno(C.Structure):
     _fields_ = [("payload", PU8), ("p", C.c_int64), ("n", C.c_int64), ("stride", C.c_int64),
-                ("mu", PD), ("inv_s", PD), ("nthreads", C.c_int)]
+                ("mu", PD), ("inv_s", PD), ("nthreads", C.c_int), ("mean", PD)]
 
 
 class orc_svdl_result(C.Structure):
@@ -108,6 +108,7 @@ _sig("orc_bed_decode", None, [PU8, C.c_int64, C.c_int64, PU8])
 _sig("orc_bed_encode", None, [PU8, C.c_int64, C.c_int64, PU8])
 _sig("orc_marker_counts", None, [PU8, C.c_int64, C.c_int64, PI64])
 _sig("orc_marker_scaling", None, [PI64, C.c_int64, C.c_int64, C.c_int, PD, PD])
+_sig("orc_marker_means", None, [PI64, C.c_int64, PD])
 _sig("orc_dense_op", None, [C.POINTER(orc_op), PD, C.c_int64, C.c_int64])
 _sig("orc_geno_op", None, [C.POINTER(orc_op), C.POINTER(orc_geno)])
 _sig("orc_geno_apply", None, [C.POINTER(orc_geno), PD, PD])
@@ -212,14 +213,24 @@ def marker_scaling(counts, n, scheme):
     return mu, inv_s
 
 
+def marker_means(counts):
+    """Observed mean per marker (0 when all missing, genio.cpp:139)."""
+    c = np.ascontiguousarray(counts, dtype=np.int64).reshape(-1, 4)
+    mean = np.empty(c.shape[0])
+    _o.orc_marker_means(c.ctypes.data_as(PI64), c.shape[0], _pd(mean))
+    return mean
+
+
 class GenoOracle:
     """Packed standardized operator on the CPU (keeps its buffers alive)."""
 
     def __init__(self, payload, p, n, mu, inv_s, nthreads: int = 1):
         self.payload = np.ascontiguousarray(payload, dtype=np.uint8)
         self.mu, self.inv_s = _f64(mu), _f64(inv_s)
+        # observed means: the value impute_mean gives a missing entry (genio.cpp:144)
+        self.mean = marker_means(marker_counts(self.payload, p, n))
         self.g = orc_geno(self.payload.ctypes.data_as(PU8), p, n, (n + 3) // 4, _pd(self.mu),
-                          _pd(self.inv_s), int(nthreads))
+                          _pd(self.inv_s), int(nthreads), _pd(self.mean))
         self.op = orc_op()
         _o.orc_geno_op(C.byref(self.op), C.byref(self.g))
         self.p, self.n = p, n

@@ -165,7 +165,9 @@ void orc_marker_counts(const uint8_t* payload, int64_t p, int64_t n, int64_t* co
  *   unit:     s = sqrt(var)                                 (genio.cpp:174-175)
  *   binomial: s = sqrt(q(1-q)), q = clamp(mu/2, 1/(2n+2))   (genio.cpp:176-180)
  *   hwe:      s = sqrt(2 f (1-f)), f = mu/2  (BASELINE.json config standardization)
- *   none:     inv_s = 1, mu = 0 (raw dosages, missing -> 0)
+ *   none:     inv_s = 1, mu = 0: the raw mean-imputed dosages of the
+ *             reference CLI's --standardize none (missing -> observed mean,
+ *             via orc_geno.mean)
  * The operator entry is (d - mu) * inv_s; the reference divides by s, which
  * differs by at most one rounding per entry. */
 void orc_marker_scaling(const int64_t* counts, int64_t p, int64_t n, int scheme, double* mu,
@@ -238,12 +240,25 @@ void orc_dense_op(orc_op* op, const double* X, int64_t m, int64_t n) {
   op->apply_adjoint = dense_apply_adjoint;
 }
 
-/* One marker's dot product: sum over observed samples of (d - mu) x_s. */
-static double geno_row_dot(const uint8_t* rec, int64_t n, double mu, const double* x) {
+void orc_marker_means(const int64_t* counts, int64_t p, double* mean) {
+  for (int64_t j = 0; j < p; ++j) {
+    const int64_t n1 = counts[4 * j + 1], n2 = counts[4 * j + 2];
+    const int64_t obs = counts[4 * j] + n1 + n2;
+    mean[j] = obs > 0 ? (double)(n1 + 2 * n2) / (double)obs : 0.0;
+  }
+}
+
+/* One marker's dot product: sum over samples of (d - mu) x_s, a missing
+ * entry taking the imputed value `imp` (its mean; genio.cpp:144). */
+static double geno_row_dot(const uint8_t* rec, int64_t n, double mu, double imp, const double* x) {
   double acc = 0.0;
+  const double vmiss = imp - mu; /* 0 for the standardizing schemes */
   for (int64_t s = 0; s < n; ++s) {
     const unsigned code = (rec[s >> 2] >> (2 * (s & 3))) & 3u;
-    if (code == 1u) continue; /* missing: mean-imputed, centers to 0 */
+    if (code == 1u) {
+      if (vmiss != 0.0) acc += vmiss * x[s];
+      continue;
+    }
     acc += ((double)kCodeToDosage[code] - mu) * x[s];
   }
   return acc;
@@ -254,7 +269,8 @@ void orc_geno_apply_rows(const orc_geno* g, int64_t j0, int64_t j1, const double
 #pragma omp parallel for schedule(static) num_threads(g->nthreads > 1 ? g->nthreads : 1)
 #endif
   for (int64_t j = j0; j < j1; ++j)
-    y[j - j0] = geno_row_dot(g->payload + j * g->stride, g->n, g->mu[j], x) * g->inv_s[j];
+    y[j - j0] = geno_row_dot(g->payload + j * g->stride, g->n, g->mu[j],
+                             g->mean ? g->mean[j] : g->mu[j], x) * g->inv_s[j];
 }
 
 void orc_geno_apply(const orc_geno* g, const double* x, double* y) {
@@ -282,14 +298,15 @@ void orc_geno_apply_adjoint_rows(const orc_geno* g, int64_t j0, int64_t j1, cons
     for (int64_t j = j0; j < j1; ++j) {
       const double w = g->inv_s[j] * y[j - j0];
       const double mu = g->mu[j];
-      const double v[4] = {(2.0 - mu) * w, 0.0, (1.0 - mu) * w, (0.0 - mu) * w};
+      const double imp = g->mean ? g->mean[j] : mu;
+      const double v[4] = {(2.0 - mu) * w, (imp - mu) * w, (1.0 - mu) * w, (0.0 - mu) * w};
       const uint8_t* rec = g->payload + j * g->stride;
       for (int64_t b = b0; b < b1; ++b) {
         const unsigned byte = rec[b];
         const int64_t s0 = 4 * b;
         for (int k = 0; k < 4 && s0 + k < n; ++k) {
           const unsigned code = (byte >> (2 * k)) & 3u;
-          if (code != 1u) z[s0 + k] += v[code];
+          if (code != 1u || v[1] != 0.0) z[s0 + k] += v[code];
         }
       }
     }

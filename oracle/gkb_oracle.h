@@ -85,15 +85,22 @@ typedef struct orc_op {
 void orc_dense_op(orc_op* op, const double* X, int64_t m, int64_t n);
 
 /* Packed standardized genotype operator: entry (j,s) = (d_js - mu_j)*inv_s_j
- * when observed, 0 when missing (mean imputation then centering,
- * genio.cpp:144,182). All buffers borrowed. nthreads<=1: one thread. */
+ * when observed, (mean_j - mu_j)*inv_s_j when missing (impute_mean, then the
+ * affine standardization: genio.cpp:144,182). mean_j is the observed mean
+ * (orc_marker_means); for the standardizing schemes mu_j = mean_j and missing
+ * entries are 0; mean == NULL means 0 for missing entries. All buffers
+ * borrowed. nthreads<=1: one thread. */
 typedef struct {
   const uint8_t* payload;
   int64_t p, n, stride;
   const double* mu;
   const double* inv_s;
   int nthreads;
+  const double* mean;
 } orc_geno;
+/* Observed mean per marker from counts [n0,n1,n2,nmiss] (0 when all missing,
+ * genio.cpp:139). */
+void orc_marker_means(const int64_t* counts, int64_t p, double* mean);
 void orc_geno_op(orc_op* op, orc_geno* g);
 void orc_geno_apply(const orc_geno* g, const double* x, double* y);
 void orc_geno_apply_adjoint(const orc_geno* g, const double* y, double* z);

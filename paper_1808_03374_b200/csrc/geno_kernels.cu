@@ -29,8 +29,11 @@
 // information); their contribution is removed exactly in the main kernel's
 // epilogue from the CTA's own sorted missing list (16-bit local column
 // indices), together with the mean term:
-//   K1: y_j = inv_s_j (sum_s a_js x_s - mu_j X - (3 - mu_j) sum_{s miss} x_s)
-//   K2: z_s = sum_j c_j a_js - sum_j c_j mu_j - sum_{j miss} c_j (3 - mu_j),  c_j = inv_s_j y_j
+//   K1: y_j = inv_s_j (sum_s a_js x_s - mu_j X - (3 - m_j) sum_{s miss} x_s)
+//   K2: z_s = sum_j c_j a_js - sum_j c_j mu_j - sum_{j miss} c_j (3 - m_j),  c_j = inv_s_j y_j
+// m_j = observed mean = the value impute_mean gives a missing entry
+// (genio.cpp:144); m_j = mu_j for the standardizing schemes, so missing
+// entries are 0 there, and the raw mean-imputed value for scheme none.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -281,14 +284,15 @@ __global__ void __launch_bounds__(512) k_block_scan(const uint32_t* __restrict__
 // ---------------------------------------------------------------- digitize
 // One CTA per column range kc (kt_cta * 128 columns): coefficients v_c
 //   MODE 0 (K1): v_c = x_c,            sum = sum_c v_c           (X of the range)
-//   MODE 1 (K2): v_c = inv_s_c * y_c,  sum = sum_c v_c mu_c, cm_c = v_c (3 - mu_c)
+//   MODE 1 (K2): v_c = inv_s_c * y_c,  sum = sum_c v_c mu_c, cm_c = v_c (3 - mean_c)
 // -> E (largest exponent), 8 balanced base-256 digits of rn(v 2^(62-E)) in
 // mma B-fragment order: uint4 (word-column wc, digit i) holds, in 32-bit word
 // q, byte e = digit i of column 16 wc + 4 e + q.
 template <int MODE>
 __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_in,
                                                    const double* __restrict__ inv_s,
-                                                   const double* __restrict__ mu, int64_t C,
+                                                   const double* __restrict__ mu,
+                                                   const double* __restrict__ mean, int64_t C,
                                                    int kt_cta, uint4* __restrict__ dig,
                                                    int* __restrict__ dexp,
                                                    double* __restrict__ dsum,
@@ -312,9 +316,8 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
         part += v;
       } else {
         v = inv_s[c] * v_in[c];
-        const double m = mu[c];
-        part += v * m;
-        cm[c] = v * (3.0 - m);
+        part += v * mu[c];
+        cm[c] = v * (3.0 - mean[c]);  // a missing entry holds the imputed mean (genio.cpp:144)
       }
     }
     emax = max(emax, exp_of(v));
@@ -419,8 +422,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
     const uint4* __restrict__ lay, int64_t KT, int kt_cta, const uint4* __restrict__ dig,
     const int* __restrict__ dexp, const double* __restrict__ dsum,
     const double* __restrict__ cval, const double* __restrict__ mu,
-    const uint32_t* __restrict__ m_off, const int64_t* __restrict__ m_base,
-    const uint16_t* __restrict__ m_ent, int64_t rows_pad, int64_t C, double* __restrict__ part) {
+    const double* __restrict__ mean, const uint32_t* __restrict__ m_off,
+    const int64_t* __restrict__ m_base, const uint16_t* __restrict__ m_ent, int64_t rows_pad,
+    int64_t C, double* __restrict__ part) {
   extern __shared__ __align__(16) uint4 dg[];  // kt_cta * 64 digits, then list staging
   const int kc = blockIdx.y;
   const int64_t kt0 = (int64_t)kc * kt_cta;
@@ -526,9 +530,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
     }
     if ((tid >> 1) == 0) {
       double out;
-      if (MODE == 0) {
-        const double m = mu[row];
-        out = val - m * rsum - (3.0 - m) * corr;
+      if (MODE == 0) {  // a missing entry holds the imputed mean (genio.cpp:144)
+        out = val - mu[row] * rsum - (3.0 - mean[row]) * corr;
       } else {
         out = val - rsum - corr;
       }
@@ -655,7 +658,8 @@ void allow_smem(K kern, size_t bytes) {  // opt in above 48 KB
 void k1_digitize(const GenoView& g, const double* x, cudaStream_t s) {
   const PMPlan& pl = g.pl1;
   allow_smem(k_digitize<0>, pl.dig_smem);
-  k_digitize<0><<<(unsigned)pl.nkc, 1024, pl.dig_smem, s>>>(x, nullptr, nullptr, g.n, pl.kt_cta,
+  k_digitize<0><<<(unsigned)pl.nkc, 1024, pl.dig_smem, s>>>(x, nullptr, nullptr, nullptr, g.n,
+                                                            pl.kt_cta,
                                                             g.s1.dig, g.s1.dexp, g.s1.dsum,
                                                             nullptr);
 }
@@ -663,7 +667,8 @@ void k1_digitize(const GenoView& g, const double* x, cudaStream_t s) {
 void k2_digitize(const GenoView& g, const double* y, cudaStream_t s) {
   const PMPlan& pl = g.pl2;
   allow_smem(k_digitize<1>, pl.dig_smem);
-  k_digitize<1><<<(unsigned)pl.nkc, 1024, pl.dig_smem, s>>>(y, g.inv_s, g.mu, g.p_loc, pl.kt_cta,
+  k_digitize<1><<<(unsigned)pl.nkc, 1024, pl.dig_smem, s>>>(y, g.inv_s, g.mu, g.mean, g.p_loc,
+                                                            pl.kt_cta,
                                                             g.s2.dig, g.s2.dexp, g.s2.dsum,
                                                             g.s2.cm);
 }
@@ -675,8 +680,8 @@ void launch_main(const GenoView& g, const PMPlan& pl, const uint4* lay, const PM
   allow_smem(k_pm_main<MODE>, pl.smem);
   dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nkc);
   k_pm_main<MODE><<<grid, kThreads, pl.smem, s>>>(lay, pl.KT, pl.kt_cta, sc.dig, sc.dexp,
-                                                  sc.dsum, cval, g.mu, ml.off, ml.base, ml.ent,
-                                                  pl.rows_pad, pl.C, sc.part);
+                                                  sc.dsum, cval, g.mu, g.mean, ml.off, ml.base,
+                                                  ml.ent, pl.rows_pad, pl.C, sc.part);
 }
 }  // namespace
 

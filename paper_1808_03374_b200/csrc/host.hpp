@@ -99,6 +99,7 @@ struct GenoShard {
   uint32_t* lt1 = nullptr;
   uint32_t* lt2 = nullptr;
   double* mu = nullptr;       // pl1.rows_pad entries, zero beyond p_loc
+  double* mean = nullptr;     // observed means (impute_mean's value), pl1.rows_pad entries
   double* inv_s = nullptr;
   int64_t* counts = nullptr;  // device p_loc*4
   int64_t nmissing = 0;

@@ -55,6 +55,7 @@ struct GenoView {
   PMPlan pl1, pl2;
   int64_t p_loc, n;
   const double* mu;     // >= pl1.rows_pad (zero beyond p_loc)
+  const double* mean;   // observed mean per SNP (imputed value of a missing entry), >= rows_pad
   const double* inv_s;  // >= pl1.rows_pad
   MissLists m1, m2;
   PMScratch s1, s2;

@@ -193,6 +193,7 @@ dev::GenoView GenoShard::view() const {
   v.p_loc = p_loc;
   v.n = n;
   v.mu = mu;
+  v.mean = mean;
   v.inv_s = inv_s;
   const bool lists = nmissing > 0;
   v.m1 = dev::MissLists{lists ? m1_off : nullptr, m1_base, m1_ent};
@@ -207,7 +208,7 @@ GenoOp::~GenoOp() {
   for (size_t i = 0; i < gs.size(); ++i) {
     cudaSetDevice(ctx->shards[i].dev);
     GenoShard& g = gs[i];
-    void* ptrs[] = {g.lt1,    g.lt2,     g.mu,     g.inv_s,  g.counts, g.m1_off,
+    void* ptrs[] = {g.lt1,    g.lt2,     g.mu,     g.mean,   g.inv_s,  g.counts, g.m1_off,
                     g.m1_base, g.m1_ent, g.m2_off, g.m2_base, g.m2_ent};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -231,6 +232,8 @@ void GenoOp::alloc_shard(int i, int64_t p_loc, int64_t nn) {
   GKB_CUDA(cudaMemsetAsync(g.lt2, 0, sizeof(uint32_t) * w2, st));
   const size_t pp = (size_t)g.pl1.rows_pad;
   GKB_CUDA(cudaMalloc(&g.mu, sizeof(double) * pp));
+  GKB_CUDA(cudaMalloc(&g.mean, sizeof(double) * pp));
+  GKB_CUDA(cudaMemsetAsync(g.mean, 0, sizeof(double) * pp, st));
   GKB_CUDA(cudaMalloc(&g.inv_s, sizeof(double) * pp));
   GKB_CUDA(cudaMemsetAsync(g.mu, 0, sizeof(double) * pp, st));
   GKB_CUDA(cudaMemsetAsync(g.inv_s, 0, sizeof(double) * pp, st));
@@ -465,6 +468,16 @@ void GenoOp::finish_build() {
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
     g.nmissing = 0;
     for (int64_t j = 0; j < g.p_loc; ++j) g.nmissing += counts_host[4 * (row0(i) + j) + 3];
+    if (g.p_loc > 0) {  // observed means (orc_marker_means' formula, bit-identical)
+      std::vector<double> mh((size_t)g.p_loc);
+      for (int64_t j = 0; j < g.p_loc; ++j) {
+        const int64_t* c = counts_host.data() + 4 * (row0(i) + j);
+        const int64_t obs = c[0] + c[1] + c[2];
+        mh[j] = obs > 0 ? (double)(c[1] + 2 * c[2]) / (double)obs : 0.0;
+      }
+      GKB_CUDA(cudaMemcpy(g.mean, mh.data(), sizeof(double) * (size_t)g.p_loc,
+                          cudaMemcpyHostToDevice));
+    }
     g.list_bytes = 0;
     if (g.nmissing > 0) {
       const int64_t t1 = build_block_lists(g.lt1, g.pl1, sh.stream, &g.m1_off, &g.m1_base,

@@ -160,3 +160,19 @@ def test_pinned_buffers_and_out(gkb):
         op.apply(x, out=np.empty(p + 1))
     with pytest.raises(ValueError):
         op.apply(x, out=np.empty(p, dtype=np.float32))
+
+
+@pytest.mark.parametrize("scheme", [0, 1, 3])
+def test_schemes_vs_oracle(gkb, orc, scheme):
+    """unit / binomial / none (the reference CLI's mean-imputed raw matrix:
+    missing -> observed row mean) against the oracle, with missing entries and
+    all-missing / zero-variance rows."""
+    p, n = 1031, 2049
+    payload, _ = random_payload(p, n, seed=17 + scheme, missing=0.05)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme(scheme))
+    mu, inv_s = op.scaling()
+    ref = orc.GenoOracle(payload, p, n, mu, inv_s)
+    x = np.random.default_rng(scheme).standard_normal(n)
+    assert rel_err(op.apply(x), ref.apply(x)) <= 1e-12
+    y = np.random.default_rng(scheme + 10).standard_normal(p)
+    assert rel_err(op.apply_adjoint(y), ref.apply_adjoint(y)) <= 1e-12

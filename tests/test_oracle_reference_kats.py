@@ -406,6 +406,29 @@ def test_packed_operator_matches_dense_standardized():
         assert np.abs(g.apply_adjoint(y) - Xs.T @ y).max() <= 1e-12 * np.abs(Xs).max() * np.sqrt(p)
 
 
+def test_packed_operator_matches_dense_none():
+    """Scheme none = the reference CLI's --standardize none: the operator is
+    impute_mean's matrix itself (missing -> observed row mean, all-missing
+    row -> 0; genio.cpp:124-148, gkpca.cpp:89-103), not centered."""
+    r = np.random.default_rng(6)
+    p, n = 40, 57
+    d = r.integers(0, 3, size=(p, n)).astype(np.uint8)
+    d[r.random((p, n)) < 0.15] = 3
+    d[2, :] = 3
+    pay = O.bed_encode(d)
+    mu, inv_s = O.marker_scaling(O.marker_counts(pay, p, n), n, 3)
+    assert np.all(mu == 0.0) and np.all(inv_s == 1.0)
+    obs = d != 3
+    dd = d.astype(float)
+    means = np.array([dd[i, obs[i]].mean() if obs[i].any() else 0.0 for i in range(p)])
+    imp = np.where(obs, dd, means[:, None])
+    g = O.GenoOracle(pay, p, n, mu, inv_s)
+    x = r.standard_normal(n)
+    assert np.abs(g.apply(x) - imp @ x).max() <= 1e-12 * np.sqrt(n) * 2
+    y = r.standard_normal(p)
+    assert np.abs(g.apply_adjoint(y) - imp.T @ y).max() <= 1e-12 * np.sqrt(p) * 2
+
+
 def test_oracle_threads_deterministic():
     r = np.random.default_rng(1)
     p, n = 300, 1001
