@@ -1,0 +1,192 @@
+"""Command-line front end of the hot path: the reference's ``gkpca pca``
+(/root/reference/proj/tools/gkpca.cpp:170-308, options :706-736), run on the
+B200 operator and driver.
+
+    python -m paper_1808_03374_b200.cli pca INPUT [--algo gkl] [-k K] [--tol T]
+        [--max-mvps N] [--seed S] [--standardize none|unit|binomial|hwe]
+        [--out DIR] [--reorth partial|full] [--omega W] [--restart none|thick]
+        [--max-subspace D] [--keep K] [--variant qr|normalize] [--max-iters N]
+
+Same inputs (.bed with companion .bim/.fam, or GMX1 .gmx), outputs
+(singvals.csv, U.gmx, V.gmx, stats.json, manifest.json; genio.cpp:203-275,
+gkpca.cpp:56-74,282-301) and exit codes (0 ok, 2 not converged with partial
+results written, 3 FormatError, 4 usage / invalid argument, 1 other;
+gkpca.cpp:43-46,803-832). A .bed input is streamed into HBM as the packed
+operator (no dense copy); `--standardize none` is the reference's mean-
+imputed raw matrix (`impute_mean`, genio.cpp:124-148). `hwe` adds BASELINE's
+sqrt(2f(1-f)) scaling. JSON files are written with sorted keys and 2-space
+indent like nlohmann::json::dump(2).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+from typing import List, Optional
+
+import numpy as np
+
+TOOL_VERSION = "0.1.0"
+EXIT_OK, EXIT_UNCONVERGED, EXIT_FORMAT, EXIT_USAGE = 0, 2, 3, 4
+
+
+class UsageError(Exception):
+    pass
+
+
+class _Parser(argparse.ArgumentParser):
+    def error(self, message):  # CLI11 ParseError -> kExitUsage (gkpca.cpp:809-811)
+        raise UsageError(message)
+
+
+def _write_json(path: str, obj) -> None:
+    from ._lib import FormatError
+    try:
+        f = open(path, "w")
+    except OSError as e:
+        raise FormatError(f"cannot open {path} for writing") from e
+    with f:
+        f.write(json.dumps(obj, indent=2, sort_keys=True, allow_nan=False) + "\n")
+
+
+def _versions():
+    from . import _lib
+    return {"gkpca": TOOL_VERSION, "libgkb": _lib.lib.gkb_version().decode()}
+
+
+def make_gkl_options(a, minmn: int):
+    """make_gkl_options (gkpca.cpp:192-212)."""
+    from .gkl import GklOptions, ReorthMode, RestartMode
+    o = GklOptions()
+    o.k = int(a.k)
+    o.tol = float(a.tol)
+    o.max_mvps = int(a.max_mvps)
+    o.seed = int(a.seed)
+    o.record_history = True
+    o.reorth = ReorthMode.kFull if a.reorth == "full" else ReorthMode.kPartial
+    o.omega = float(a.omega)
+    if a.restart == "thick":
+        o.restart = RestartMode.kThick
+        o.max_subspace = int(a.max_subspace) if a.max_subspace > 0 else max(2 * o.k, 20)
+        o.max_subspace = min(o.max_subspace, minmn)
+        o.keep = int(a.keep) if a.keep > 0 else max(o.k, o.max_subspace // 2)
+    return o
+
+
+def load_operator(path: str, standardize: str):
+    """load_matrix + apply_standardize (gkpca.cpp:89-108): a .bed input becomes
+    the packed device operator, a .gmx input a device DenseOperator."""
+    from . import genio
+    from ._lib import FormatError
+    from .gkl import DenseOperator, GenotypeOperator, ScalingScheme
+    ext = os.path.splitext(path)[1]
+    if ext == ".bed":
+        scheme = {"none": ScalingScheme.kNone, "unit": ScalingScheme.kUnitVariance,
+                  "binomial": ScalingScheme.kBinomial, "hwe": ScalingScheme.kHwe}[standardize]
+        base = path[:-4]
+        return GenotypeOperator.from_bed_file(path, base + ".bim", base + ".fam", scheme=scheme)
+    if ext == ".gmx":
+        X = genio.read_dense(path)
+        if standardize in ("unit", "binomial"):
+            X = genio.standardize_dense(X, standardize)
+        elif standardize == "hwe":
+            raise ValueError("--standardize hwe applies to .bed genotype inputs")
+        return DenseOperator(X)
+    raise FormatError(f"{path}: unsupported input format (expect .gmx or .bed)")
+
+
+def run_pca(a) -> int:
+    """run_pca (gkpca.cpp:214-308), GKL branch."""
+    from . import genio
+    from .gkl import svdl
+    if a.algo != "gkl":
+        raise ValueError("--algo subspace is not available in this build (SURVEY.md §8(f) row 3)")
+    op = load_operator(a.input, a.standardize)
+    os.makedirs(a.out, exist_ok=True)
+    opts = make_gkl_options(a, min(op.rows(), op.cols()))
+    r = svdl(op, opts)
+    converged = bool(r.stats.converged)
+
+    def trim(h):  # history rows are NaN-padded to k; the reference keeps head(min(k, j))
+        h = np.asarray(h, dtype=np.float64)
+        return [float(v) for v in h if not math.isnan(v)]
+
+    stats = {"algorithm": "gkl", "mvps": r.stats.mvps, "steps": r.stats.steps,
+             "restarts": r.stats.restarts, "reorth_count": r.stats.reorth_count,
+             "deflations": r.stats.deflations, "converged": converged,
+             "wall_seconds": r.stats.wall_seconds,
+             "err_estimates": [float(v) for v in r.err_estimates],
+             "ritz_history": [trim(h) for h in r.stats.ritz_history],
+             "err_history": [trim(h) for h in r.stats.err_history]}
+    genio.write_csv_matrix(os.path.join(a.out, "singvals.csv"), r.singvals)
+    genio.write_dense(os.path.join(a.out, "U.gmx"), r.U)
+    genio.write_dense(os.path.join(a.out, "V.gmx"), r.V)
+    stats["partial_results"] = not converged
+    _write_json(os.path.join(a.out, "stats.json"), stats)
+    config = {"input": a.input, "algo": a.algo, "k": a.k, "tol": a.tol, "max_mvps": a.max_mvps,
+              "standardize": a.standardize, "reorth": a.reorth, "omega": a.omega,
+              "restart": a.restart, "max_subspace": a.max_subspace, "keep": a.keep,
+              "variant": a.variant, "max_iters": a.max_iters}
+    # write_manifest (gkpca.cpp:61-71): no timestamps -> reruns are byte-identical
+    _write_json(os.path.join(a.out, "manifest.json"),
+                {"command": "pca", "config": config, "seed": a.seed, "versions": _versions()})
+    if not converged:
+        sys.stderr.write("gkpca pca: not converged within budget; partial results written "
+                         "(stats.json has partial_results=true)\n")
+        return EXIT_UNCONVERGED
+    return EXIT_OK
+
+
+def build_parser() -> argparse.ArgumentParser:
+    p = _Parser(prog="gkpca", description="Truncated SVD / PCA of genotype matrices on B200")
+    p.add_argument("--threads", type=int, default=0,
+                   help="accepted for compatibility (host threads are not used on this path)")
+    sub = p.add_subparsers(dest="command", parser_class=_Parser)
+    c = sub.add_parser("pca", help="Truncated SVD of a genotype/dense matrix")
+    c.add_argument("input", help="Input matrix (.gmx or .bed)")
+    c.add_argument("--algo", default="gkl", choices=["gkl", "subspace"])
+    c.add_argument("-k", "--k", type=int, default=10)
+    c.add_argument("--tol", type=float, default=1e-8)
+    c.add_argument("--max-mvps", dest="max_mvps", type=int, default=1000000)
+    c.add_argument("--seed", type=int, default=0)
+    c.add_argument("--standardize", default="none", choices=["none", "unit", "binomial", "hwe"])
+    c.add_argument("--out", default=".")
+    c.add_argument("--reorth", default="partial", choices=["partial", "full"])
+    c.add_argument("--omega", type=float, default=1e-8)
+    c.add_argument("--restart", default="none", choices=["none", "thick"])
+    c.add_argument("--max-subspace", dest="max_subspace", type=int, default=0)
+    c.add_argument("--keep", type=int, default=0)
+    c.add_argument("--variant", default="qr", choices=["qr", "normalize"])
+    c.add_argument("--max-iters", dest="max_iters", type=int, default=1000)
+    return p
+
+
+def main(argv: Optional[List[str]] = None) -> int:
+    from ._lib import FormatError
+    parser = build_parser()
+    try:
+        a = parser.parse_args(argv)
+        if a.command is None:
+            raise UsageError("a subcommand is required")
+    except UsageError as e:
+        sys.stderr.write(f"gkpca: {e}\n")
+        return EXIT_USAGE
+    try:
+        if a.command == "pca":
+            return run_pca(a)
+    except FormatError as e:
+        sys.stderr.write(f"gkpca: {e}\n")
+        return EXIT_FORMAT
+    except ValueError as e:  # std::invalid_argument
+        sys.stderr.write(f"gkpca: {e}\n")
+        return EXIT_USAGE
+    except Exception as e:  # noqa: BLE001 -- std::exception -> 1 (gkpca.cpp:828-831)
+        sys.stderr.write(f"gkpca: {e}\n")
+        return 1
+    return EXIT_USAGE
+
+
+if __name__ == "__main__":
+    sys.exit(main())

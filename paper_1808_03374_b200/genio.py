@@ -88,3 +88,80 @@ def encode(dosages: np.ndarray) -> np.ndarray:
 def bed_paths(prefix: str):
     base = os.path.splitext(prefix)[0] if prefix.endswith(".bed") else prefix
     return base + ".bed", base + ".bim", base + ".fam"
+
+
+# ---------------------------------------------------------------- GMX1 / CSV
+GMX_MAGIC = b"GMX1"
+
+
+def read_dense(path: str) -> np.ndarray:
+    """GMX1 dense matrix (genio.cpp:187-201): 'GMX1', u32 rows, u32 cols, u32
+    flags, column-major float64; FormatError on bad magic / size."""
+    try:
+        raw = open(path, "rb").read()
+    except OSError as e:
+        raise FormatError(f"cannot open {path}") from e
+    if len(raw) < 16 or raw[:4] != GMX_MAGIC:
+        raise FormatError(f"{path}: bad magic")
+    m, n = np.frombuffer(raw, dtype="<u4", count=2, offset=4)
+    expected = 16 + int(m) * int(n) * 8
+    if len(raw) != expected:
+        raise FormatError(f"{path}: payload size mismatch (expected {expected} bytes, "
+                          f"found {len(raw)})")
+    return np.frombuffer(raw, dtype="<f8", offset=16).reshape((int(n), int(m))).T.copy()
+
+
+def write_dense(path: str, M: np.ndarray, flags: int = 0) -> None:
+    """GMX1 writer (genio.cpp:203-217): column-major float64 payload."""
+    M = np.asarray(M, dtype=np.float64)
+    if M.ndim == 1:
+        M = M[:, None]
+    try:
+        f = open(path, "wb")
+    except OSError as e:
+        raise FormatError(f"cannot open {path} for writing") from e
+    with f:
+        f.write(GMX_MAGIC)
+        f.write(np.array([M.shape[0], M.shape[1], flags], dtype="<u4").tobytes())
+        f.write(np.asfortranarray(M).astype("<f8").tobytes(order="F"))
+
+
+def write_csv_matrix(path: str, M: np.ndarray) -> None:
+    """CSV writer (genio.cpp:261-275): header c1..cN, '%.17g' cells."""
+    M = np.asarray(M, dtype=np.float64)
+    if M.ndim == 1:
+        M = M[:, None]
+    try:
+        f = open(path, "w")
+    except OSError as e:
+        raise FormatError(f"cannot open {path} for writing") from e
+    with f:
+        f.write(",".join(f"c{j + 1}" for j in range(M.shape[1])) + "\n")
+        for i in range(M.shape[0]):
+            f.write(",".join("%.17g" % v for v in M[i]) + "\n")
+
+
+def standardize_dense(X: np.ndarray, scheme: str) -> np.ndarray:
+    """standardize (genio.cpp:150-185) on a dense matrix: row mean, population
+    variance over all n columns, zero-variance rows -> 0; unit: s = sqrt(var);
+    binomial: s = sqrt(q(1-q)), q = clamp(mean/2, 1/(2n+2))."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[1]
+    if n == 0:
+        raise ValueError("standardize: no samples")
+    out = np.zeros_like(X)
+    nd = float(n)
+    for i in range(X.shape[0]):
+        row = X[i]
+        mean = row.sum() / nd
+        var = ((row - mean) ** 2).sum() / nd
+        if var == 0.0:
+            continue
+        if scheme == "unit":
+            s = np.sqrt(var)
+        else:
+            cl = 1.0 / (2.0 * nd + 2.0)
+            q = min(max(mean / 2.0, cl), 1.0 - cl)
+            s = np.sqrt(q * (1.0 - q))
+        out[i] = (row - mean) / s
+    return out

@@ -324,8 +324,8 @@ class GenotypeOperator(LinearOperator):
         from . import genio
         b, bi, fa = genio.bed_paths(bed)
         bim, fam = bim or bi, fam or fa
+        p, n = bed_check(b, bim, fam)  # FormatError before touching the device
         ctx = ctx or default_context()
-        p, n = bed_check(b, bim, fam)
         h = C.c_void_p()
         check(lib.gkb_geno_from_bed_file(ctx._h, b.encode(), bim.encode(), fam.encode(),
                                          C.byref(h)))

@@ -1,0 +1,137 @@
+"""`gkpca pca` front end (gkpca.cpp:170-308): options, output artifacts
+(singvals.csv, U.gmx, V.gmx, stats.json, manifest.json) and exit codes."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import principal_angles, rel_err
+
+
+def _bed(tmp_path, p=120, n=90, seed=0, missing=0.03):
+    from paper_1808_03374_b200 import genio
+    rng = np.random.default_rng(seed)
+    # two populations so the spectrum has structure
+    f = rng.uniform(0.1, 0.9, size=p)
+    pop = np.arange(n) % 2
+    fp = np.clip(f[:, None] + np.where(pop[None, :] == 0, 0.15, -0.15), 0.02, 0.98)
+    d = rng.binomial(2, fp).astype(np.uint8)
+    d[rng.random((p, n)) < missing] = 3
+    pre = str(tmp_path / "geno")
+    genio.write_bed(genio.encode(d), p, n, pre + ".bed", pre + ".bim", pre + ".fam")
+    return pre, d
+
+
+def run(argv):
+    from paper_1808_03374_b200 import cli
+    return cli.main(argv)
+
+
+# ---------------------------------------------------------------- CPU
+def test_usage_errors_exit_4(capsys):
+    assert run([]) == 4
+    assert run(["pca"]) == 4                                    # missing input
+    assert run(["pca", "x.bed", "--standardize", "bogus"]) == 4
+    assert run(["pca", "x.bed", "--reorth", "sometimes"]) == 4
+    assert run(["nope"]) == 4
+
+
+def test_unsupported_input_exit_3(tmp_path, capsys):
+    p = tmp_path / "m.txt"
+    p.write_text("1,2\n")
+    assert run(["pca", str(p), "--out", str(tmp_path / "o")]) == 3
+    assert "unsupported input format (expect .gmx or .bed)" in capsys.readouterr().err
+
+
+def test_bad_bed_exit_3(tmp_path, capsys):
+    pre, _ = _bed(tmp_path, 8, 8)
+    with open(pre + ".bed", "r+b") as f:
+        f.write(b"\x00")
+    assert run(["pca", pre + ".bed", "--out", str(tmp_path / "o")]) == 3
+    assert "bad magic" in capsys.readouterr().err
+
+
+def test_gmx_and_csv_writers(tmp_path):
+    from paper_1808_03374_b200 import genio
+    M = np.arange(12, dtype=float).reshape(3, 4) / 7.0
+    genio.write_dense(str(tmp_path / "a.gmx"), M)
+    raw = (tmp_path / "a.gmx").read_bytes()
+    assert raw[:4] == b"GMX1" and len(raw) == 16 + 12 * 8
+    assert np.frombuffer(raw[4:16], dtype="<u4").tolist() == [3, 4, 0]
+    assert np.array_equal(np.frombuffer(raw[16:], dtype="<f8"), M.ravel(order="F"))
+    assert np.array_equal(genio.read_dense(str(tmp_path / "a.gmx")), M)
+    genio.write_csv_matrix(str(tmp_path / "s.csv"), np.array([1.0, 1 / 3, 1e-300]))
+    assert (tmp_path / "s.csv").read_text() == \
+        "c1\n1\n0.33333333333333331\n1e-300\n"
+    (tmp_path / "bad.gmx").write_bytes(b"GMX1" + bytes(12) + b"x")
+    with pytest.raises(Exception, match="payload size mismatch"):
+        genio.read_dense(str(tmp_path / "bad.gmx"))
+
+
+def test_make_gkl_options_defaults():
+    from paper_1808_03374_b200 import cli
+    a = cli.build_parser().parse_args(["pca", "x.bed", "-k", "7", "--restart", "thick"])
+    o = cli.make_gkl_options(a, 1000)
+    assert (o.max_subspace, o.keep, o.record_history) == (20, 10, True)   # max(2k,20), max(k, D/2)
+    o = cli.make_gkl_options(a, 15)
+    assert (o.max_subspace, o.keep) == (15, 7)                            # capped by min(m, n)
+
+
+# ---------------------------------------------------------------- GPU
+@pytest.mark.gpu
+@pytest.mark.parametrize("standardize,scheme", [("none", 3), ("unit", 0), ("binomial", 1),
+                                                ("hwe", 2)])
+def test_pca_bed_end_to_end(gkb, orc, tmp_path, standardize, scheme):
+    from paper_1808_03374_b200 import cli, genio
+    pre, _ = _bed(tmp_path)
+    out = tmp_path / f"out_{standardize}"
+    argv = ["pca", pre + ".bed", "-k", "5", "--tol", "1e-10", "--standardize", standardize,
+            "--restart", "thick", "--out", str(out), "--seed", "3"]
+    assert run(argv) == 0
+    names = sorted(os.listdir(out))
+    assert names == ["U.gmx", "V.gmx", "manifest.json", "singvals.csv", "stats.json"]
+    sv = np.loadtxt(out / "singvals.csv", delimiter=",", skiprows=1)
+    U, V = genio.read_dense(str(out / "U.gmx")), genio.read_dense(str(out / "V.gmx"))
+    assert U.shape == (120, 5) and V.shape == (90, 5)
+    stats = json.loads((out / "stats.json").read_text())
+    assert stats["algorithm"] == "gkl" and stats["converged"] and not stats["partial_results"]
+    assert len(stats["ritz_history"]) == len(stats["err_history"]) > 0
+    man = json.loads((out / "manifest.json").read_text())
+    assert man["command"] == "pca" and man["seed"] == 3 and man["config"]["k"] == 5
+    # oracle: same payload, same scaling, same options
+    payload, p, n = genio.read_bed(pre + ".bed", pre + ".bim", pre + ".fam")
+    mu, inv_s = orc.marker_scaling(orc.marker_counts(payload, p, n), n, scheme)
+    ref = orc.GenoOracle(payload, p, n, mu, inv_s)
+    a = cli.build_parser().parse_args(argv)
+    o = orc.svdl(ref, orc.Options.from_gkl(cli.make_gkl_options(a, min(p, n))))
+    assert rel_err(sv, o.singvals) <= 1e-9
+    assert principal_angles(U, o.U) < 1e-6 and principal_angles(V, o.V) < 1e-6
+    # a rerun writes byte-identical artifacts (no timestamps; wall time only in stats)
+    out2 = tmp_path / f"out2_{standardize}"
+    argv[argv.index("--out") + 1] = str(out2)
+    assert run(argv) == 0
+    for f in ("singvals.csv", "U.gmx", "V.gmx", "manifest.json"):
+        assert (out / f).read_bytes() == (out2 / f).read_bytes(), f
+
+
+@pytest.mark.gpu
+def test_pca_unconverged_exit_2(gkb, tmp_path, capsys):
+    pre, _ = _bed(tmp_path)
+    out = tmp_path / "o"
+    assert run(["pca", pre + ".bed", "-k", "5", "--max-mvps", "6", "--out", str(out)]) == 2
+    assert "not converged within budget" in capsys.readouterr().err
+    assert json.loads((out / "stats.json").read_text())["partial_results"] is True
+    assert (out / "singvals.csv").exists()
+
+
+@pytest.mark.gpu
+def test_pca_gmx_input(gkb, tmp_path):
+    from paper_1808_03374_b200 import genio
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((60, 4)) @ rng.standard_normal((4, 50)) + 0.01 * rng.standard_normal((60, 50))
+    genio.write_dense(str(tmp_path / "x.gmx"), X)
+    out = tmp_path / "o"
+    assert run(["pca", str(tmp_path / "x.gmx"), "-k", "3", "--tol", "1e-10", "--out", str(out)]) == 0
+    sv = np.loadtxt(out / "singvals.csv", delimiter=",", skiprows=1)
+    assert rel_err(sv, np.linalg.svd(X, compute_uv=False)[:3]) <= 1e-9
