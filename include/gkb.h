@@ -137,6 +137,12 @@ int gkb_op_shape(gkb_op* op, int64_t* rows, int64_t* cols);
 int gkb_op_apply(gkb_op* op, const double* x, double* y);
 int gkb_op_apply_adjoint(gkb_op* op, const double* x, double* y);
 int64_t gkb_op_mvps(gkb_op* op);
+/* k columns at once (column-major host blocks, X: cols x k -> Y: rows x k,
+ * and Y: rows x k -> Z: cols x k): one H2D, the k products back to back on
+ * the device, one D2H; k mvps. The column loops of subspace_iterate
+ * (subspace.cpp:70-77, :97-101) call these. */
+int gkb_op_apply_block(gkb_op* op, const double* X, int64_t k, double* Y);
+int gkb_op_apply_adjoint_block(gkb_op* op, const double* Y, int64_t k, double* Z);
 /* Page-locked host memory for the vectors passed to gkb_op_apply /
  * gkb_op_apply_adjoint (no reference counterpart: the reference's vectors are
  * Eigen::VectorXd in pageable memory). Copies from/to these buffers run at
@@ -232,6 +238,8 @@ int gkb_cgs2(gkb_ctx* ctx, const double* basis, int64_t len, int64_t ncols, doub
  * column-major; U r x k, s k, V c x k, k = min(r, c). */
 int gkb_svd_small(const double* M, int64_t r, int64_t c, double* U, double* s, double* V);
 /* Rng (rng.hpp:17-62): out[i] = uniform_symmetric() for i < n. */
+/* Rng(seed).normal() x n (Box-Muller, rng.hpp:46-60). */
+int gkb_rng_fill_normal(uint64_t seed, int64_t n, double* out);
 int gkb_rng_fill_symmetric(uint64_t seed, int64_t n, double* out);
 /* Marker scaling from counts with the reference formulas (see
  * gkb_geno_standardize); exposed for bit-exact checks against the oracle. */

@@ -119,6 +119,9 @@ SIGNATURES = {
     "gkb_op_apply": (I, [P, PD, PD]),
     "gkb_op_apply_adjoint": (I, [P, PD, PD]),
     "gkb_op_mvps": (I64, [P]),
+    "gkb_op_apply_block": (I, [P, PD, I64, PD]),
+    "gkb_op_apply_adjoint_block": (I, [P, PD, I64, PD]),
+    "gkb_rng_fill_normal": (I, [C.c_uint64, I64, PD]),
     "gkb_host_alloc": (I, [C.c_size_t, C.POINTER(P)]),
     "gkb_host_free": (I, [P]),
     "gkb_op_destroy": (I, [P]),

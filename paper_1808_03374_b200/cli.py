@@ -98,31 +98,50 @@ def load_operator(path: str, standardize: str):
 
 
 def run_pca(a) -> int:
-    """run_pca (gkpca.cpp:214-308), GKL branch."""
+    """run_pca (gkpca.cpp:214-308)."""
     from . import genio
     from .gkl import svdl
-    if a.algo != "gkl":
-        raise ValueError("--algo subspace is not available in this build (SURVEY.md §8(f) row 3)")
     op = load_operator(a.input, a.standardize)
     os.makedirs(a.out, exist_ok=True)
-    opts = make_gkl_options(a, min(op.rows(), op.cols()))
-    r = svdl(op, opts)
-    converged = bool(r.stats.converged)
+    if a.algo == "gkl":
+        opts = make_gkl_options(a, min(op.rows(), op.cols()))
+        r = svdl(op, opts)
+        converged = bool(r.stats.converged)
 
-    def trim(h):  # history rows are NaN-padded to k; the reference keeps head(min(k, j))
-        h = np.asarray(h, dtype=np.float64)
-        return [float(v) for v in h if not math.isnan(v)]
+        def trim(h):  # history rows are NaN-padded to k; the reference keeps head(min(k, j))
+            h = np.asarray(h, dtype=np.float64)
+            return [float(v) for v in h if not math.isnan(v)]
 
-    stats = {"algorithm": "gkl", "mvps": r.stats.mvps, "steps": r.stats.steps,
-             "restarts": r.stats.restarts, "reorth_count": r.stats.reorth_count,
-             "deflations": r.stats.deflations, "converged": converged,
-             "wall_seconds": r.stats.wall_seconds,
-             "err_estimates": [float(v) for v in r.err_estimates],
-             "ritz_history": [trim(h) for h in r.stats.ritz_history],
-             "err_history": [trim(h) for h in r.stats.err_history]}
-    genio.write_csv_matrix(os.path.join(a.out, "singvals.csv"), r.singvals)
-    genio.write_dense(os.path.join(a.out, "U.gmx"), r.U)
-    genio.write_dense(os.path.join(a.out, "V.gmx"), r.V)
+        singvals, U, V = r.singvals, r.U, r.V
+        stats = {"algorithm": "gkl", "mvps": r.stats.mvps, "steps": r.stats.steps,
+                 "restarts": r.stats.restarts, "reorth_count": r.stats.reorth_count,
+                 "deflations": r.stats.deflations, "converged": converged,
+                 "wall_seconds": r.stats.wall_seconds,
+                 "err_estimates": [float(v) for v in r.err_estimates],
+                 "ritz_history": [trim(h) for h in r.stats.ritz_history],
+                 "err_history": [trim(h) for h in r.stats.err_history]}
+    else:  # subspace (gkpca.cpp:251-279)
+        import time
+        from .subspace import SubspaceVariant, subspace_iterate
+        variant = SubspaceVariant.kNormalize if a.variant == "normalize" else SubspaceVariant.kQr
+        t0 = time.perf_counter()
+        r = subspace_iterate(op, int(a.k), variant, float(a.tol), int(a.max_iters), int(a.seed))
+        wall = time.perf_counter() - t0
+        singvals, U = r.singvals, r.basis
+        # right vectors from the left basis: v_i = X^T u_i / sigma_i (not counted as mvps)
+        V = op.apply_adjoint_block(U)
+        for i in range(U.shape[1]):
+            if i < singvals.size and singvals[i] > 0.0:
+                V[:, i] /= singvals[i]
+        converged = bool(r.converged)
+        stats = {"algorithm": "subspace", "variant": a.variant, "mvps": r.mvps,
+                 "iterations": r.state.iterations, "converged": converged,
+                 "rank_deficient": bool(r.rank_deficient), "wall_seconds": wall,
+                 "delta_history": [float(v) for v in r.state.delta_history],
+                 "invcond_history": [float(v) for v in r.state.invcond_history]}
+    genio.write_csv_matrix(os.path.join(a.out, "singvals.csv"), singvals)
+    genio.write_dense(os.path.join(a.out, "U.gmx"), U)
+    genio.write_dense(os.path.join(a.out, "V.gmx"), V)
     stats["partial_results"] = not converged
     _write_json(os.path.join(a.out, "stats.json"), stats)
     config = {"input": a.input, "algo": a.algo, "k": a.k, "tol": a.tol, "max_mvps": a.max_mvps,

@@ -624,6 +624,38 @@ int gkb_svd_small(const double* M, int64_t r, int64_t c, double* U, double* s, d
   });
 }
 
+int gkb_rng_fill_normal(uint64_t seed, int64_t n, double* out) {
+  return guarded([&] {
+    need(out, "out");
+    gkb::Rng r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.normal();
+  });
+}
+
+int gkb_op_apply_block(gkb_op* op, const double* X, int64_t k, double* Y) {
+  return guarded([&] {
+    need(op, "op");
+    need(X, "X");
+    need(Y, "Y");
+    if (k < 0) gkb::fail(GKB_EINVAL, "apply_block: k must be >= 0");
+    if (k == 0) return;
+    op->op->apply_block_host(X, k, Y);
+    op->op->mvps += k;
+  });
+}
+
+int gkb_op_apply_adjoint_block(gkb_op* op, const double* Y, int64_t k, double* Z) {
+  return guarded([&] {
+    need(op, "op");
+    need(Y, "Y");
+    need(Z, "Z");
+    if (k < 0) gkb::fail(GKB_EINVAL, "apply_adjoint_block: k must be >= 0");
+    if (k == 0) return;
+    op->op->adjoint_block_host(Y, k, Z);
+    op->op->mvps += k;
+  });
+}
+
 int gkb_rng_fill_symmetric(uint64_t seed, int64_t n, double* out) {
   return guarded([&] {
     need(out, "out");

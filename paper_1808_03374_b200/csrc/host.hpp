@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <cmath>
 #include <random>
 #include <string>
 #include <vector>
@@ -23,9 +24,27 @@ class Rng {
   uint64_t bits() { return engine_(); }
   double uniform() { return static_cast<double>(engine_() >> 11) * 0x1.0p-53; }
   double uniform_symmetric() { return 2.0 * uniform() - 1.0; }
+  // Box-Muller; one engine pair feeds two variates (rng.hpp:46-60, bit-exact:
+  // same draws, same libm calls)
+  double normal() {
+    if (have_spare_) {
+      have_spare_ = false;
+      return spare_;
+    }
+    double u1 = uniform();
+    while (u1 <= 0.0) u1 = uniform();
+    const double u2 = uniform();
+    const double radius = std::sqrt(-2.0 * std::log(u1));
+    constexpr double two_pi = 6.283185307179586476925286766559;
+    spare_ = radius * std::sin(two_pi * u2);
+    have_spare_ = true;
+    return radius * std::cos(two_pi * u2);
+  }
 
  private:
   std::mt19937_64 engine_;
+  double spare_ = 0.0;
+  bool have_spare_ = false;
 };
 
 // One SNP shard: a device, a stream, scratch for fixed-order reductions and
@@ -88,6 +107,13 @@ struct DevOp {
   void alloc_host_api_buffers();
   void apply_host(const double* x, double* y);
   void adjoint_host(const double* y, double* z);
+  // k columns per call (column-major host blocks): one H2D, k device products
+  // back to back, one D2H (the block form subspace iteration uses)
+  void apply_block_host(const double* X, int64_t k, double* Y);
+  void adjoint_block_host(const double* Y, int64_t k, double* Z);
+  std::vector<double*> bin_, bout_;  // per shard block buffers (grow-only)
+  int64_t bin_cap_ = 0, bout_cap_ = 0;
+  void ensure_block_buffers(int64_t in_doubles, int64_t out_doubles);
 };
 
 // read_bed's checks (genio.cpp:53-70) on the three files; fills p, n.

@@ -24,6 +24,8 @@ DevOp::~DevOp() {
     cudaFree(ybuf[i]);
     cudaFree(zbuf[i]);
     if (i < yfull.size()) cudaFree(yfull[i]);
+    if (i < bin_.size() && bin_[i]) cudaFree(bin_[i]);
+    if (i < bout_.size() && bout_[i]) cudaFree(bout_[i]);
   }
 }
 
@@ -84,6 +86,104 @@ void DevOp::adjoint_host(const double* y, double* z) {
   adjoint_dev(yi, zbuf);
   ctx->set_device(0);
   GKB_CUDA(cudaMemcpyAsync(z, zbuf[0], sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost,
+                           ctx->shards[0].stream));
+  ctx->sync_all();
+}
+
+void DevOp::ensure_block_buffers(int64_t in_doubles, int64_t out_doubles) {
+  const int L = (int)ctx->shards.size();
+  if ((int64_t)bin_.size() != L) {
+    bin_.assign(L, nullptr);
+    bout_.assign(L, nullptr);
+    bin_cap_ = bout_cap_ = 0;
+  }
+  if (in_doubles > bin_cap_ || out_doubles > bout_cap_) {
+    ctx->sync_all();
+    const int64_t ci = std::max(in_doubles, bin_cap_), co = std::max(out_doubles, bout_cap_);
+    for (int i = 0; i < L; ++i) {
+      ctx->set_device(i);
+      if (bin_[i]) cudaFree(bin_[i]);
+      if (bout_[i]) cudaFree(bout_[i]);
+      GKB_CUDA(cudaMalloc(&bin_[i], sizeof(double) * (size_t)std::max<int64_t>(ci, 1)));
+      GKB_CUDA(cudaMalloc(&bout_[i], sizeof(double) * (size_t)std::max<int64_t>(co, 1)));
+    }
+    bin_cap_ = ci;
+    bout_cap_ = co;
+  }
+}
+
+void DevOp::apply_block_host(const double* X, int64_t k, double* Y) {
+  const int L = (int)ctx->shards.size();
+  const bool spmd = ctx->use_nccl && ctx->nshards_total > 1;
+  int64_t rmax = 1;
+  for (int i = 0; i < L; ++i) rmax = std::max(rmax, rows(i));
+  // SPMD: every rank assembles the full m x k block for one allreduce;
+  // local shards: each holds its own rows x k
+  ensure_block_buffers(n * k, (spmd ? m : rmax) * k);
+  for (int i = 0; i < L; ++i) {
+    ctx->set_device(i);
+    GKB_CUDA(cudaMemcpyAsync(bin_[i], X, sizeof(double) * (size_t)(n * k), cudaMemcpyHostToDevice,
+                             ctx->shards[i].stream));
+  }
+  for (int64_t c = 0; c < k; ++c) {
+    std::vector<const double*> xi(L);
+    std::vector<double*> yi(L);
+    for (int i = 0; i < L; ++i) {
+      xi[i] = bin_[i] + c * n;
+      yi[i] = spmd ? bout_[i] + c * m + row0(i) : bout_[i] + c * rows(i);
+    }
+    apply_dev(xi, yi);
+  }
+  if (spmd) {
+    // zero the other ranks' rows of every column, then one allreduce of m*k
+    Shard& s = ctx->shards[0];
+    ctx->set_device(0);
+    const int64_t r0 = row0(0), r = rows(0);
+    for (int64_t c = 0; c < k; ++c) {
+      if (r0 > 0)
+        GKB_CUDA(cudaMemsetAsync(bout_[0] + c * m, 0, sizeof(double) * (size_t)r0, s.stream));
+      if (r0 + r < m)
+        GKB_CUDA(cudaMemsetAsync(bout_[0] + c * m + r0 + r, 0, sizeof(double) * (size_t)(m - r0 - r),
+                                 s.stream));
+    }
+    ctx->allreduce({bout_[0]}, m * k);
+    GKB_CUDA(cudaMemcpyAsync(Y, bout_[0], sizeof(double) * (size_t)(m * k), cudaMemcpyDeviceToHost,
+                             s.stream));
+  } else {
+    for (int i = 0; i < L; ++i) {
+      ctx->set_device(i);
+      if (rows(i) == 0) continue;
+      GKB_CUDA(cudaMemcpy2DAsync(Y + row0(i), sizeof(double) * (size_t)m, bout_[i],
+                                 sizeof(double) * (size_t)rows(i), sizeof(double) * (size_t)rows(i),
+                                 (size_t)k, cudaMemcpyDeviceToHost, ctx->shards[i].stream));
+    }
+  }
+  ctx->sync_all();
+}
+
+void DevOp::adjoint_block_host(const double* Yh, int64_t k, double* Z) {
+  const int L = (int)ctx->shards.size();
+  int64_t rmax = 1;
+  for (int i = 0; i < L; ++i) rmax = std::max(rmax, rows(i));
+  ensure_block_buffers(rmax * k, n * k);
+  for (int i = 0; i < L; ++i) {
+    ctx->set_device(i);
+    if (rows(i) == 0) continue;
+    GKB_CUDA(cudaMemcpy2DAsync(bin_[i], sizeof(double) * (size_t)rows(i), Yh + row0(i),
+                               sizeof(double) * (size_t)m, sizeof(double) * (size_t)rows(i),
+                               (size_t)k, cudaMemcpyHostToDevice, ctx->shards[i].stream));
+  }
+  for (int64_t c = 0; c < k; ++c) {
+    std::vector<const double*> yi(L);
+    std::vector<double*> zi(L);
+    for (int i = 0; i < L; ++i) {
+      yi[i] = bin_[i] + c * rows(i);
+      zi[i] = bout_[i] + c * n;
+    }
+    adjoint_dev(yi, zi);
+  }
+  ctx->set_device(0);
+  GKB_CUDA(cudaMemcpyAsync(Z, bout_[0], sizeof(double) * (size_t)(n * k), cudaMemcpyDeviceToHost,
                            ctx->shards[0].stream));
   ctx->sync_all();
 }

@@ -27,7 +27,7 @@ __all__ = [
     "ReorthMode", "RestartMode", "ScalingScheme", "GklOptions", "SvdlStats", "SvdlResult",
     "Context", "LinearOperator", "DenseOperator", "GenotypeOperator", "LanczosFactorization",
     "StepInfo", "StepStatus", "RitzSet", "svdl", "cgs2", "svd_small", "rng_uniform_symmetric",
-    "partition_rows", "marker_scaling", "error_metric_l1", "pinned_empty", "bed_check",
+    "partition_rows", "marker_scaling", "error_metric_l1", "pinned_empty", "bed_check", "rng_normal",
 ]
 
 
@@ -247,6 +247,26 @@ class LinearOperator:
         y = _out(out, self._n)
         check(lib.gkb_op_apply_adjoint(self._h, _pd(x), _pd(y)))
         return y
+
+    def apply_block(self, X) -> np.ndarray:
+        """Y = X_op X for a cols x k block (gkb_op_apply_block; k mvps)."""
+        X = np.asfortranarray(np.asarray(X, dtype=np.float64))
+        if X.ndim != 2 or X.shape[0] != self._n:
+            raise ValueError(f"apply_block: expected a {self._n} x k block")
+        k = X.shape[1]
+        Y = np.empty((self._m, k), order="F")
+        check(lib.gkb_op_apply_block(self._h, _pd(X), k, _pd(Y)))
+        return Y
+
+    def apply_adjoint_block(self, Y) -> np.ndarray:
+        """Z = X_op^T Y for a rows x k block (gkb_op_apply_adjoint_block; k mvps)."""
+        Y = np.asfortranarray(np.asarray(Y, dtype=np.float64))
+        if Y.ndim != 2 or Y.shape[0] != self._m:
+            raise ValueError(f"apply_adjoint_block: expected a {self._m} x k block")
+        k = Y.shape[1]
+        Z = np.empty((self._n, k), order="F")
+        check(lib.gkb_op_apply_adjoint_block(self._h, _pd(Y), k, _pd(Z)))
+        return Z
 
     def mvps(self) -> int:
         return int(lib.gkb_op_mvps(self._h))
@@ -576,6 +596,13 @@ def rng_uniform_symmetric(seed: int, n: int) -> np.ndarray:
     """Rng(seed).uniform_symmetric() x n (rng.hpp:27; gkl.cpp:428-429)."""
     out = np.empty(n)
     check(lib.gkb_rng_fill_symmetric(int(seed) & 0xFFFFFFFFFFFFFFFF, n, _pd(out)))
+    return out
+
+
+def rng_normal(seed: int, n: int) -> np.ndarray:
+    """Rng(seed).normal() x n (Box-Muller, rng.hpp:46-60)."""
+    out = np.empty(n)
+    check(lib.gkb_rng_fill_normal(int(seed) & 0xFFFFFFFFFFFFFFFF, n, _pd(out)))
     return out
 
 

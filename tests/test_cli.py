@@ -135,3 +135,31 @@ def test_pca_gmx_input(gkb, tmp_path):
     assert run(["pca", str(tmp_path / "x.gmx"), "-k", "3", "--tol", "1e-10", "--out", str(out)]) == 0
     sv = np.loadtxt(out / "singvals.csv", delimiter=",", skiprows=1)
     assert rel_err(sv, np.linalg.svd(X, compute_uv=False)[:3]) <= 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["qr", "normalize"])
+def test_pca_subspace(gkb, tmp_path, variant):
+    """--algo subspace (gkpca.cpp:251-279): singular values from the block
+    iteration, V = X^T U / sigma, subspace stats keys."""
+    from paper_1808_03374_b200 import genio
+    pre, d = _bed(tmp_path)
+    out = tmp_path / f"s_{variant}"
+    rc = run(["pca", pre + ".bed", "--algo", "subspace", "--variant", variant, "-k", "3",
+              "--tol", "1e-10", "--max-iters", "400", "--standardize", "unit", "--out", str(out)])
+    stats = json.loads((out / "stats.json").read_text())
+    assert stats["algorithm"] == "subspace" and stats["variant"] == variant
+    assert set(stats) >= {"mvps", "iterations", "converged", "rank_deficient", "wall_seconds",
+                          "delta_history", "invcond_history", "partial_results"}
+    assert rc == (0 if stats["converged"] else 2)
+    sv = np.loadtxt(out / "singvals.csv", delimiter=",", skiprows=1)
+    U, V = genio.read_dense(str(out / "U.gmx")), genio.read_dense(str(out / "V.gmx"))
+    # dense reference: the operator's own matrix (X = op applied to the identity)
+    op = gkb.GenotypeOperator.from_bed_file(pre, scheme=gkb.ScalingScheme.kUnitVariance)
+    M = op.apply_block(np.eye(op.cols()))
+    ref = np.linalg.svd(M, compute_uv=False)[:3]
+    if variant == "qr":
+        assert rel_err(sv, ref) <= 1e-9
+    else:  # the normalize variant's bar (test_subspace.cpp:139-142): top value to 1e-4 sigma_1
+        assert abs(sv[0] - ref[0]) <= 1e-4 * ref[0]
+    assert np.allclose(M.T @ U[:, 0] / sv[0], V[:, 0], atol=1e-10)
