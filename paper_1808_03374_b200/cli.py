@@ -2,6 +2,7 @@
 (/root/reference/proj/tools/gkpca.cpp:170-308, options :706-736), run on the
 B200 operator and driver.
 
+    python -m paper_1808_03374_b200.cli regress INPUT --pheno CSV [--design CSV] [-k K] ...
     python -m paper_1808_03374_b200.cli pca INPUT [--algo gkl] [-k K] [--tol T]
         [--max-mvps N] [--seed S] [--standardize none|unit|binomial|hwe]
         [--out DIR] [--reorth partial|full] [--omega W] [--restart none|thick]
@@ -158,6 +159,67 @@ def run_pca(a) -> int:
     return EXIT_OK
 
 
+def run_regress(a) -> int:
+    """run_regress (gkpca.cpp:554-680): PC-adjusted regression of a phenotype
+    on every marker (device scan) or on a joint design."""
+    from . import genio
+    from ._lib import FormatError
+    from . import regress as R
+    from .gkl import DenseOperator, GklOptions, svdl
+    op = load_operator(a.input, a.standardize)
+    n = op.cols()
+    ph = genio.read_csv_matrix(a.pheno)
+    if ph.shape[1] != 1:
+        raise FormatError(f"{a.pheno}: phenotype must be a single column")
+    if ph.shape[0] != n:
+        raise FormatError(f"{a.pheno}: phenotype rows ({ph.shape[0]}) do not match samples ({n})")
+    y = ph[:, 0]
+    Z = np.zeros((n, 0))
+    pca_converged, pca_mvps = True, 0
+    if a.k > 0:
+        r = svdl(op, GklOptions(k=int(a.k), tol=float(a.tol), max_mvps=int(a.max_mvps),
+                                seed=int(a.seed)))
+        Z = r.V
+        pca_converged, pca_mvps = bool(r.stats.converged), int(r.stats.mvps)
+    if a.design:
+        X = genio.read_csv_matrix(a.design)
+        if X.shape[0] != n:
+            raise FormatError(f"{a.design}: design rows do not match samples")
+        try:
+            if Z.shape[1] > 0:
+                fit = R.pc_adjusted_fit(X, Z, y, a.unbiased)
+                entry = {"beta": [float(v) for v in fit.beta_hat],
+                         "gamma": [float(v) for v in fit.gamma_hat],
+                         "sigma2": fit.joint.sigma2_hat}
+            else:
+                fit = R.ols_fit(X, y, a.unbiased)
+                entry = {"beta": [float(v) for v in fit.beta_hat], "sigma2": fit.sigma2_hat}
+            entry["se"] = [float(np.sqrt(fit.cov_beta[i, i])) for i in range(fit.beta_hat.size)]
+        except R.RankDeficiencyError as e:
+            entry = {"error": str(e), "column": e.column}
+        result = {"mode": "design", "k": a.k, "pca_converged": pca_converged,
+                  "pca_mvps": pca_mvps, "fit": entry}
+    else:
+        if isinstance(op, DenseOperator):  # .gmx: row statistics on the host matrix
+            M = op.apply_block(np.eye(n))
+            scan = R.marker_scan(op, y, Z, a.unbiased, sumsq=(M * M).sum(axis=1),
+                                 constant=M.max(axis=1) == M.min(axis=1))
+        else:
+            scan = R.marker_scan(op, y, Z, a.unbiased)
+        result = {"mode": "per-marker", "k": a.k, "pca_converged": pca_converged,
+                  "pca_mvps": pca_mvps, "markers": R.scan_entries(scan)}
+    os.makedirs(a.out, exist_ok=True)
+    _write_json(os.path.join(a.out, "regression.json"), result)
+    config = {"input": a.input, "pheno": a.pheno, "design": a.design, "k": a.k, "tol": a.tol,
+              "max_mvps": a.max_mvps, "standardize": a.standardize, "unbiased": a.unbiased}
+    _write_json(os.path.join(a.out, "manifest.json"),
+                {"command": "regress", "config": config, "seed": a.seed, "versions": _versions()})
+    if not pca_converged:
+        sys.stderr.write("gkpca regress: PCA step not converged; results use the partial basis\n")
+        return EXIT_UNCONVERGED
+    return EXIT_OK
+
+
 def build_parser() -> argparse.ArgumentParser:
     p = _Parser(prog="gkpca", description="Truncated SVD / PCA of genotype matrices on B200")
     p.add_argument("--threads", type=int, default=0,
@@ -179,6 +241,17 @@ def build_parser() -> argparse.ArgumentParser:
     c.add_argument("--keep", type=int, default=0)
     c.add_argument("--variant", default="qr", choices=["qr", "normalize"])
     c.add_argument("--max-iters", dest="max_iters", type=int, default=1000)
+    r = sub.add_parser("regress", help="Per-marker regression with PC adjustment")
+    r.add_argument("input", help="Genotype matrix (.gmx or .bed)")
+    r.add_argument("--pheno", required=True, help="Phenotype CSV (one column, one row per sample)")
+    r.add_argument("--design", default="", help="Joint design CSV instead of the per-marker scan")
+    r.add_argument("-k", "--k", type=int, default=0)
+    r.add_argument("--tol", type=float, default=1e-8)
+    r.add_argument("--max-mvps", dest="max_mvps", type=int, default=1000000)
+    r.add_argument("--seed", type=int, default=0)
+    r.add_argument("--standardize", default="none", choices=["none", "unit", "binomial", "hwe"])
+    r.add_argument("--unbiased", action="store_true")
+    r.add_argument("--out", default=".")
     return p
 
 
@@ -195,6 +268,8 @@ def main(argv: Optional[List[str]] = None) -> int:
     try:
         if a.command == "pca":
             return run_pca(a)
+        if a.command == "regress":
+            return run_regress(a)
     except FormatError as e:
         sys.stderr.write(f"gkpca: {e}\n")
         return EXIT_FORMAT

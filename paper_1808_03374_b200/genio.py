@@ -165,3 +165,39 @@ def standardize_dense(X: np.ndarray, scheme: str) -> np.ndarray:
             s = np.sqrt(q * (1.0 - q))
         out[i] = (row - mean) / s
     return out
+
+
+def read_csv_matrix(path: str) -> np.ndarray:
+    """read_csv_matrix (genio.cpp:219-259): comma-separated numbers, an optional
+    non-numeric header row; FormatError on a non-numeric cell elsewhere, ragged
+    rows or no data rows."""
+    try:
+        f = open(path)
+    except OSError as e:
+        raise FormatError(f"cannot open {path}") from e
+    rows, first = [], True
+    with f:
+        for line in f:
+            line = line.rstrip("\n")
+            if not line:
+                continue
+            row, numeric = [], True
+            for cell in line.split(","):
+                c = cell.rstrip("\r").rstrip(" ")
+                try:
+                    row.append(float(c))
+                except ValueError:
+                    numeric = False
+                    break
+            if not numeric:
+                if first:
+                    first = False
+                    continue
+                raise FormatError(f"{path}: non-numeric cell outside header")
+            first = False
+            if rows and len(row) != len(rows[0]):
+                raise FormatError(f"{path}: ragged rows")
+            rows.append(row)
+    if not rows:
+        raise FormatError(f"{path}: no data rows")
+    return np.array(rows, dtype=np.float64)

@@ -163,3 +163,70 @@ def test_pca_subspace(gkb, tmp_path, variant):
     else:  # the normalize variant's bar (test_subspace.cpp:139-142): top value to 1e-4 sigma_1
         assert abs(sv[0] - ref[0]) <= 1e-4 * ref[0]
     assert np.allclose(M.T @ U[:, 0] / sv[0], V[:, 0], atol=1e-10)
+
+
+def test_read_csv_matrix(tmp_path):
+    from paper_1808_03374_b200 import genio
+    p = tmp_path / "a.csv"
+    p.write_text("y\n1.5\n2\n\n-3e-2\r\n")
+    assert genio.read_csv_matrix(str(p)).ravel().tolist() == [1.5, 2.0, -0.03]
+    p.write_text("1,2\n3\n")
+    with pytest.raises(Exception, match="ragged rows"):
+        genio.read_csv_matrix(str(p))
+    p.write_text("a\nb\n")
+    with pytest.raises(Exception, match="non-numeric cell outside header"):
+        genio.read_csv_matrix(str(p))
+    p.write_text("h\n")
+    with pytest.raises(Exception, match="no data rows"):
+        genio.read_csv_matrix(str(p))
+
+
+def test_regress_bad_pheno_exit_3(tmp_path, capsys):
+    pre, _ = _bed(tmp_path, 8, 8)
+    ph = tmp_path / "ph.csv"
+    ph.write_text("a,b\n1,2\n")
+    assert run(["regress", pre + ".bed", "--pheno", str(ph), "--out", str(tmp_path / "o")]) in (3, 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [0, 2])
+def test_regress_end_to_end(gkb, tmp_path, k):
+    """gkpca regress: per-marker scan entries vs the reference loop on the
+    operator's dense matrix; design mode; manifest."""
+    from paper_1808_03374_b200 import regress as R
+    pre, d = _bed(tmp_path)
+    n = d.shape[1]
+    rng = np.random.default_rng(4)
+    y = rng.standard_normal(n)
+    ph = tmp_path / "ph.csv"
+    ph.write_text("y\n" + "\n".join("%.17g" % v for v in y) + "\n")
+    out = tmp_path / f"r{k}"
+    rc = run(["regress", pre + ".bed", "--pheno", str(ph), "-k", str(k), "--tol", "1e-10",
+              "--standardize", "unit", "--out", str(out)])
+    assert rc == 0
+    res = json.loads((out / "regression.json").read_text())
+    assert res["mode"] == "per-marker" and res["k"] == k and res["pca_converged"]
+    op = gkb.GenotypeOperator.from_bed_file(pre, scheme=gkb.ScalingScheme.kUnitVariance)
+    M = op.apply_block(np.eye(n))
+    Z = np.zeros((n, 0))
+    if k:
+        Z = gkb.svdl(op, gkb.GklOptions(k=k, tol=1e-10)).V
+    for i in (0, 7, 33, 101):
+        X = np.column_stack([np.ones(n), M[i]])
+        f = R.pc_adjusted_fit(X, Z, y) if k else R.ols_fit(X, y)
+        e = res["markers"][i]
+        assert e["marker"] == i
+        assert abs(e["beta"] - f.beta_hat[1]) <= 1e-8 * max(1, abs(f.beta_hat[1]))
+        assert abs(e["se"] - np.sqrt(f.cov_beta[1, 1])) <= 1e-8 * np.sqrt(f.cov_beta[1, 1])
+    man = json.loads((out / "manifest.json").read_text())
+    assert man["command"] == "regress" and man["config"]["k"] == k
+    # design mode
+    dz = tmp_path / "design.csv"
+    Xd = np.column_stack([np.ones(n), rng.standard_normal(n)])
+    dz.write_text("\n".join(",".join("%.17g" % v for v in row) for row in Xd) + "\n")
+    out2 = tmp_path / f"d{k}"
+    assert run(["regress", pre + ".bed", "--pheno", str(ph), "--design", str(dz), "-k", str(k),
+                "--tol", "1e-10", "--standardize", "unit", "--out", str(out2)]) == 0
+    fit = json.loads((out2 / "regression.json").read_text())["fit"]
+    ref = R.pc_adjusted_fit(Xd, Z, y) if k else R.ols_fit(Xd, y)
+    assert np.allclose(fit["beta"], ref.beta_hat, rtol=1e-8, atol=1e-12)
