@@ -22,11 +22,31 @@ void Shard::ensure_partial(int64_t doubles) {
   rs.cap = cap;
 }
 
+uint8_t* Shard::pinned_stage(int k, size_t bytes) {
+  if (bytes > hstage_bytes) {
+    for (int q = 0; q < 2; ++q) {
+      if (hstage[q]) cudaFreeHost(hstage[q]);
+      hstage[q] = nullptr;
+    }
+    for (int q = 0; q < 2; ++q) GKB_CUDA(cudaMallocHost(&hstage[q], bytes));
+    hstage_bytes = bytes;
+  }
+  return hstage[k];
+}
+
 static void init_shard(Shard& s, int index, int dev) {
   s.index = index;
   s.dev = dev;
   GKB_CUDA(cudaSetDevice(dev));
   GKB_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+  // stream-ordered allocations (layouts, staging) come from the device's
+  // default pool; keep freed memory in the pool so rebuilding an operator of
+  // the same size does not go back to the driver
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   GKB_CUDA(cudaMalloc(&s.dres, sizeof(double) * kResCap));
   GKB_CUDA(cudaMallocHost(&s.hres, sizeof(double) * kResCap));
   GKB_CUDA(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
@@ -65,6 +85,8 @@ Context::~Context() {
     if (s.rs.partial) cudaFree(s.rs.partial);
     if (s.dres) cudaFree(s.dres);
     if (s.hres) cudaFreeHost(s.hres);
+    for (int q = 0; q < 2; ++q)
+      if (s.hstage[q]) cudaFreeHost(s.hstage[q]);
     if (s.flush_buf) cudaFree(s.flush_buf);
     if (s.ev) cudaEventDestroy(s.ev);
     if (s.stream) cudaStreamDestroy(s.stream);

@@ -60,6 +60,10 @@ struct Shard {
   size_t flush_bytes = 0;
   cudaEvent_t ev = nullptr;
   void ensure_partial(int64_t doubles);
+  // pinned host staging for file ingest (two buffers, grow-only, kept)
+  uint8_t* hstage[2] = {nullptr, nullptr};
+  size_t hstage_bytes = 0;
+  uint8_t* pinned_stage(int k, size_t bytes);
 };
 
 constexpr int64_t kResCap = 1 << 16;

@@ -6,11 +6,13 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "host.hpp"
 
@@ -308,8 +310,11 @@ GenoOp::~GenoOp() {
   for (size_t i = 0; i < gs.size(); ++i) {
     cudaSetDevice(ctx->shards[i].dev);
     GenoShard& g = gs[i];
-    void* ptrs[] = {g.lt1,    g.lt2,     g.mu,     g.mean,   g.inv_s,  g.counts, g.m1_off,
-                    g.m1_base, g.m1_ent, g.m2_off, g.m2_base, g.m2_ent};
+    cudaStream_t st = ctx->shards[i].stream;
+    if (g.lt1) cudaFreeAsync(g.lt1, st);  // back to the pool (cudaMallocAsync)
+    if (g.lt2) cudaFreeAsync(g.lt2, st);
+    void* ptrs[] = {g.mu, g.mean, g.inv_s, g.counts, g.m1_off, g.m1_base, g.m1_ent, g.m2_off,
+                    g.m2_base, g.m2_ent};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     free_scratch(g.s1);
@@ -326,8 +331,9 @@ void GenoOp::alloc_shard(int i, int64_t p_loc, int64_t nn) {
   ctx->set_device(i);
   cudaStream_t st = ctx->shards[i].stream;
   const size_t w1 = (size_t)dev::pm_words(g.pl1), w2 = (size_t)dev::pm_words(g.pl2);
-  GKB_CUDA(cudaMalloc(&g.lt1, sizeof(uint32_t) * w1));
-  GKB_CUDA(cudaMalloc(&g.lt2, sizeof(uint32_t) * w2));
+  // the two layouts are the large allocations: stream-ordered from the pool
+  GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g.lt1), sizeof(uint32_t) * w1, st));
+  GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g.lt2), sizeof(uint32_t) * w2, st));
   GKB_CUDA(cudaMemsetAsync(g.lt1, 0, sizeof(uint32_t) * w1, st));
   GKB_CUDA(cudaMemsetAsync(g.lt2, 0, sizeof(uint32_t) * w2, st));
   const size_t pp = (size_t)g.pl1.rows_pad;
@@ -425,8 +431,18 @@ void bed_check(const char* bed, const char* bim, const char* fam, int64_t* p, in
   *n = nn;
 }
 
+static bool verbose() {
+  const char* e = std::getenv("GKB_VERBOSE");
+  return e && e[0] == '1';
+}
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void GenoOp::build_from_bed_file(const char* bed, int64_t p, int64_t nn) {
   if (p <= 0 || nn <= 0) fail(GKB_EINVAL, "genotype operator: empty dimension");
+  const double t0 = now_s();
+  double t_alloc = 0.0, t_read = 0.0;
   m = p;
   n = nn;
   starts = partition_rows(p, ctx->nshards_total);
@@ -438,35 +454,60 @@ void GenoOp::build_from_bed_file(const char* bed, int64_t p, int64_t nn) {
   try {
     for (int i = 0; i < L; ++i) {
       const int64_t r0 = row0(i), pr = rows(i);
+      const double ta = now_s();
       alloc_shard(i, pr, nn);
       Shard& sh = ctx->shards[i];
       ctx->set_device(i);
-      // staging block: 64 MB (GKB_STAGE_MB overrides; tests use small blocks to
-      // exercise the double buffering)
-      int64_t budget = 64ll << 20;
+      // staging block: 16 MB (GKB_STAGE_MB overrides; tests use small blocks to
+      // exercise the double buffering); each block is read by several threads
+      int64_t budget = 16ll << 20;
       if (const char* e = std::getenv("GKB_STAGE_MB")) budget = std::max<int64_t>(1, atoll(e)) << 20;
       const int64_t br = staging_rows(stride, budget, pr);
+      const int nthr = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
       uint8_t* dstage[2] = {nullptr, nullptr};
       uint8_t* hstage[2] = {nullptr, nullptr};
       cudaEvent_t ev[2] = {nullptr, nullptr};
       for (int k = 0; k < 2; ++k) {
-        GKB_CUDA(cudaMalloc(&dstage[k], (size_t)(br * stride)));
-        GKB_CUDA(cudaMallocHost(&hstage[k], (size_t)(br * stride)));
+        GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dstage[k]), (size_t)(br * stride),
+                                 sh.stream));
+        hstage[k] = sh.pinned_stage(k, (size_t)(br * stride));  // cached across loads
         GKB_CUDA(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
       }
+      t_alloc += now_s() - ta;
       int k = 0;
       for (int64_t b0 = 0; b0 < pr; b0 += br, k ^= 1) {
         const int64_t rb = std::min(br, pr - b0);
         GKB_CUDA(cudaEventSynchronize(ev[k]));  // staging k consumed by its layout builds
-        // positional read of this block's records while the device works on the other buffer
+        const double tr = now_s();
+        // positional reads of this block's records (nthr slices in parallel)
+        // while the device works on the other buffer
         const int64_t want = rb * stride;
-        int64_t done = 0;
-        while (done < want) {
-          const ssize_t r = ::pread(fd, hstage[k] + done, (size_t)(want - done),
-                                    (off_t)(3 + (r0 + b0) * stride + done));
-          if (r <= 0) fail(GKB_EFORMAT, std::string(bed) + ": short read");
-          done += r;
+        const off_t base = (off_t)(3 + (r0 + b0) * stride);
+        std::vector<int> bad(nthr, 0);
+        auto read_slice = [&](int t) {
+          int64_t done = want * t / nthr;
+          const int64_t end = want * (t + 1) / nthr;
+          while (done < end) {
+            const ssize_t r = ::pread(fd, hstage[k] + done, (size_t)(end - done), base + done);
+            if (r <= 0) {
+              bad[t] = 1;
+              return;
+            }
+            done += r;
+          }
+        };
+        if (nthr == 1 || want < (1 << 20)) {
+          read_slice(0);
+          for (int t = 1; t < nthr; ++t) read_slice(t);
+        } else {
+          std::vector<std::thread> pool;
+          for (int t = 1; t < nthr; ++t) pool.emplace_back(read_slice, t);
+          read_slice(0);
+          for (auto& th : pool) th.join();
         }
+        for (int t = 0; t < nthr; ++t)
+          if (bad[t]) fail(GKB_EFORMAT, std::string(bed) + ": short read");
+        t_read += now_s() - tr;
         GKB_CUDA(cudaMemcpyAsync(dstage[k], hstage[k], (size_t)want, cudaMemcpyHostToDevice,
                                  sh.stream));
         dev::build_lt1(dstage[k], stride, rb, b0, nn, gs[i].pl1, gs[i].lt1, sh.stream);
@@ -475,19 +516,21 @@ void GenoOp::build_from_bed_file(const char* bed, int64_t p, int64_t nn) {
         GKB_LAUNCH_CHECK();
         GKB_CUDA(cudaEventRecord(ev[k], sh.stream));
       }
+      for (int kk = 0; kk < 2; ++kk) cudaFreeAsync(dstage[kk], sh.stream);
       GKB_CUDA(cudaStreamSynchronize(sh.stream));
-      for (int kk = 0; kk < 2; ++kk) {
-        cudaFree(dstage[kk]);
-        cudaFreeHost(hstage[kk]);
-        cudaEventDestroy(ev[kk]);
-      }
+      for (int kk = 0; kk < 2; ++kk) cudaEventDestroy(ev[kk]);
     }
   } catch (...) {
     ::close(fd);
     throw;
   }
   ::close(fd);
+  const double t1 = now_s();
   finish_build();
+  if (verbose())
+    std::fprintf(stderr, "[gkb] bed ingest: alloc %.4f s, reads %.4f s, stream+build %.4f s, "
+                 "finish (counts, lists, scratch) %.4f s\n", t_alloc, t_read,
+                 t1 - t0 - t_alloc - t_read, now_s() - t1);
 }
 
 void GenoOp::build_from_synth(const dev::SynthDev& sp_in, const gkb_synth_spec* spec) {
