@@ -91,13 +91,19 @@ Lanczos::Lanczos(DevOp* op, int64_t capacity, const double* start, uint64_t rng_
   for (int i = 0; i < L; ++i) {
     ctx_->set_device(i);
     const size_t r = (size_t)std::max<int64_t>(op_->rows(i), 1);
-    GKB_CUDA(cudaMalloc(&U_[i], sizeof(double) * r * (size_t)cap_));
-    GKB_CUDA(cudaMalloc(&U2_[i], sizeof(double) * r * (size_t)cap_));
-    GKB_CUDA(cudaMalloc(&V_[i], sizeof(double) * (size_t)n_ * (size_t)(cap_ + 1)));
-    GKB_CUDA(cudaMalloc(&V2_[i], sizeof(double) * (size_t)n_ * (size_t)(cap_ + 1)));
-    GKB_CUDA(cudaMalloc(&w_[i], sizeof(double) * r));
-    GKB_CUDA(cudaMalloc(&z_[i], sizeof(double) * (size_t)n_));
-    GKB_CUDA(cudaMalloc(&cbuf_[i], sizeof(double) * (size_t)(cap_ + 2)));
+    // bases and work vectors: stream-ordered from the device pool (an svdl
+    // call allocates them; repeated solves reuse the pooled memory)
+    cudaStream_t st = ctx_->shards[i].stream;
+    auto pool_alloc = [&](double** p, size_t doubles) {
+      GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(double) * doubles, st));
+    };
+    pool_alloc(&U_[i], r * (size_t)cap_);
+    pool_alloc(&U2_[i], r * (size_t)cap_);
+    pool_alloc(&V_[i], (size_t)n_ * (size_t)(cap_ + 1));
+    pool_alloc(&V2_[i], (size_t)n_ * (size_t)(cap_ + 1));
+    pool_alloc(&w_[i], r);
+    pool_alloc(&z_[i], (size_t)n_);
+    pool_alloc(&cbuf_[i], (size_t)(cap_ + 2));
     const int64_t need = dev::red_blocks(std::max<int64_t>(op_->rows(i), n_)) * (cap_ + 4) + 64;
     ctx_->shards[i].ensure_partial(need);
   }
@@ -124,9 +130,10 @@ Lanczos::Lanczos(DevOp* op, int64_t capacity, const double* start, uint64_t rng_
 Lanczos::~Lanczos() {
   for (size_t i = 0; i < U_.size(); ++i) {
     cudaSetDevice(ctx_->shards[i].dev);
-    cudaStreamSynchronize(ctx_->shards[i].stream);
+    cudaStream_t st = ctx_->shards[i].stream;
     for (double* p : {U_[i], U2_[i], V_[i], V2_[i], w_[i], z_[i], cbuf_[i]})
-      if (p) cudaFree(p);
+      if (p) cudaFreeAsync(p, st);  // back to the pool, stream-ordered
+    cudaStreamSynchronize(st);
     if (i < tmp_small_.size() && tmp_small_[i]) cudaFree(tmp_small_[i]);
   }
   for (double* p : ring_slot_)
