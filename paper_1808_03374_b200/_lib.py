@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgkb.so")
+LIB_PATH = os.environ.get("GKB_LIB", os.path.join(_HERE, "libgkb.so"))  # GKB_LIB: A/B builds
 
 GKB_OK, GKB_EINVAL, GKB_ELOGIC, GKB_ECUDA, GKB_ENCCL, GKB_EOOM, GKB_EFORMAT = range(7)
 

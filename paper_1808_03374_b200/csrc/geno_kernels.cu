@@ -36,6 +36,7 @@
 // entries are 0 there, and the raw mean-imputed value for scheme none.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -47,9 +48,14 @@ namespace dev {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kStripsPerWarp = 2;   // row strips sharing each B fragment
-constexpr int kDepth = 2;           // tiles in flight per strip
+#ifndef GKB_SPW
+#define GKB_SPW 2
+#endif
+constexpr int kStripsPerWarp = GKB_SPW;  // row strips sharing each B fragment
+constexpr int kDepth = 2;                // tiles in flight per strip
 constexpr int kRowsPerCta = 8 * kStripsPerWarp * 16;  // 256
+constexpr int kStripsPerCta = 8 * kStripsPerWarp;
+constexpr int kMinCtas = kStripsPerWarp <= 2 ? 4 : 3;  // per SM (register budget)
 
 // .bed 2-bit code -> dosage code r (r_hi = ~h, r_lo = l ^ h per field).
 __device__ __forceinline__ uint32_t bed_to_r(uint32_t c) {
@@ -60,6 +66,19 @@ __device__ __forceinline__ uint32_t r_to_bed(uint32_t r) {
   return ((~r) & 0xAAAAAAAAu) | ((r ^ ((~r) >> 1)) & 0x55555555u);
 }
 __device__ __forceinline__ uint32_t missing_mask(uint32_t r) { return r & (r >> 1) & 0x55555555u; }
+
+// Programmatic dependent launch (PDL). The product kernels (digitize -> main
+// -> reduce) are launched with programmatic stream serialization: a kernel may
+// be scheduled while its predecessor drains, runs only work on data that is
+// immutable for the whole solve (tile layouts, missing lists) before
+// pdl_wait(), and nothing that writes global memory or reads a predecessor's
+// output. pdl_wait() returns once the predecessor grid has completed and its
+// writes are visible, so completion stays ordered along the stream. Without
+// the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 v;
@@ -234,7 +253,7 @@ __global__ void k_layout_to_bed(const uint32_t* __restrict__ lay, int64_t KT, in
 // = the block-local column indices (< 2048, ascending) of its missing entries.
 // Count pass (kFill = false) writes cnt[b*256 + r]; fill pass writes ent.
 template <bool kFill>
-__global__ void __launch_bounds__(256) k_miss_tiles(const uint32_t* __restrict__ lay, int64_t KT,
+__global__ void __launch_bounds__(kRowsPerCta) k_miss_tiles(const uint32_t* __restrict__ lay, int64_t KT,
                                                     int kt_cta, uint32_t* __restrict__ cnt,
                                                     const uint32_t* __restrict__ off,
                                                     const int64_t* __restrict__ base,
@@ -302,6 +321,10 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
   __shared__ int redi[33];
   double* vals = reinterpret_cast<double*>(dsm + kt_cta * 64);
   uint8_t* db = reinterpret_cast<uint8_t*>(dsm);
+  // trigger only after the wait: the main kernel's early reads of the lists and
+  // layout then follow the completion of every kernel before this one
+  pdl_wait();
+  pdl_trigger();
   const int kc = blockIdx.x;
   const int ncol = kt_cta * 128;
   const int64_t c0 = (int64_t)kc * ncol;
@@ -403,8 +426,8 @@ __device__ __forceinline__ double walk_list(const uint16_t* __restrict__ ent, ui
 
 // Missing-list staging in shared memory (after the digits): 257 offsets and
 // up to kEntCap entries of the CTA's list (longer lists are read from global).
-constexpr int kEntCap = 8192;
-constexpr int kOffBytes = 1040;
+constexpr int kEntCap = 4096 * kStripsPerWarp;
+constexpr int kOffBytes = ((kRowsPerCta + 1) * 4 + 15) / 16 * 16;
 size_t pm_smem_bytes(int kt_cta) {
   return (size_t)kt_cta * 64 * 16 + kOffBytes + 2 * kEntCap + 16 + (size_t)kt_cta * 128 * 8;
 }
@@ -418,7 +441,7 @@ size_t pm_smem_bytes(int kt_cta) {
 // by cp.async in the prologue, so the epilogue walk never touches global
 // memory (random 8-byte gathers from L2 cost ~30% of the kernel otherwise).
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 4) k_pm_main(
+__global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     const uint4* __restrict__ lay, int64_t KT, int kt_cta, const uint4* __restrict__ dig,
     const int* __restrict__ dexp, const double* __restrict__ dsum,
     const double* __restrict__ cval, const double* __restrict__ mu,
@@ -438,6 +461,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
   const uint4 Z = make_uint4(0, 0, 0, 0);
   int acc[kStripsPerWarp][4];
   uint4 buf[kDepth][kStripsPerWarp];
+  pdl_trigger();  // the reduce kernel may be scheduled once every CTA has started
 #pragma unroll
   for (int r = 0; r < kStripsPerWarp; ++r) {
     acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0;
@@ -465,6 +489,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_pm_main(
         cp_async16(stage + kOffBytes + 16 * i, esrc + 16 * i);
       ent_shift = (int)(eb - a0 / 2);
     }
+  }
+  // everything above reads only the layout and the missing lists; from here
+  // on the predecessor's outputs (digits, x / cm) are used
+  pdl_wait();
+  if (m_off) {
     // 8-byte copies: x may be a Krylov-basis column with an odd leading dimension
     const int ncol = (int)min((int64_t)ktiles * 128, C - col0);
     for (int i = threadIdx.x; i < ncol; i += kThreads) cp_async8(cvs + i, cval + col0 + i);
@@ -545,6 +574,7 @@ __global__ void k1_reduce(const double* __restrict__ part, int nkc, int64_t rows
                           int64_t p_loc, const double* __restrict__ inv_s,
                           double* __restrict__ y) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
   if (j >= p_loc) return;
   double acc = 0.0;
   for (int c = 0; c < nkc; ++c) acc += part[(int64_t)c * rows_pad + j];
@@ -560,6 +590,7 @@ __global__ void __launch_bounds__(1024) k2_reduce(const double* __restrict__ par
   __shared__ double ps[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t s = (int64_t)blockIdx.x * 32 + lane;
+  pdl_wait();
   double acc = 0.0;
   if (s < n)
 #pragma unroll 4
@@ -587,13 +618,15 @@ PMPlan pm_plan(int64_t R, int64_t C) {
   PMPlan pl;
   pl.R = R;
   pl.C = C;
-  pl.S = ((R + 15) / 16 + 15) / 16 * 16;  // strips, padded to whole CTAs
-  if (pl.S < 16) pl.S = 16;
+  pl.S = ((R + 15) / 16 + kStripsPerCta - 1) / kStripsPerCta * kStripsPerCta;  // whole CTAs
+  if (pl.S < kStripsPerCta) pl.S = kStripsPerCta;
   pl.KT = (C + 127) / 128;
   if (pl.KT < 1) pl.KT = 1;
   pl.kt_cta = 16;  // 2048 columns per CTA (16 KB of digits)
+  if (const char* e = std::getenv("GKB_KT_CTA")) pl.kt_cta = std::max(1, std::atoi(e));  // sweeps
   pl.nkc = (int)((pl.KT + pl.kt_cta - 1) / pl.kt_cta);
-  pl.grid_x = pl.S / 16;
+  pl.grid_x = pl.S / kStripsPerCta;
+  pl.rows_cta = kRowsPerCta;
   pl.rows_pad = pl.S * 16;
   pl.smem = pm_smem_bytes(pl.kt_cta);
   pl.dig_smem = (size_t)pl.kt_cta * 64 * sizeof(uint4) + (size_t)pl.kt_cta * 128 * sizeof(double);
@@ -648,6 +681,28 @@ void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int6
 }
 
 namespace {
+// Launch with programmatic stream serialization (see pdl_wait); GKB_NO_PDL=1
+// launches every product kernel fully serialized instead.
+bool pdl_enabled() {
+  static const bool on = std::getenv("GKB_NO_PDL") == nullptr;
+  return on;
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 template <class K>
 void allow_smem(K kern, size_t bytes) {  // opt in above 48 KB
   if (bytes > 48 * 1024)
@@ -658,47 +713,48 @@ void allow_smem(K kern, size_t bytes) {  // opt in above 48 KB
 void k1_digitize(const GenoView& g, const double* x, cudaStream_t s) {
   const PMPlan& pl = g.pl1;
   allow_smem(k_digitize<0>, pl.dig_smem);
-  k_digitize<0><<<(unsigned)pl.nkc, 1024, pl.dig_smem, s>>>(x, nullptr, nullptr, nullptr, g.n,
-                                                            pl.kt_cta,
-                                                            g.s1.dig, g.s1.dexp, g.s1.dsum,
-                                                            nullptr);
+  launch_pdl(k_digitize<0>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, true, x,
+             (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, g.n, pl.kt_cta,
+             g.s1.dig, g.s1.dexp, g.s1.dsum, (double*)nullptr);
 }
 
 void k2_digitize(const GenoView& g, const double* y, cudaStream_t s) {
   const PMPlan& pl = g.pl2;
   allow_smem(k_digitize<1>, pl.dig_smem);
-  k_digitize<1><<<(unsigned)pl.nkc, 1024, pl.dig_smem, s>>>(y, g.inv_s, g.mu, g.mean, g.p_loc,
-                                                            pl.kt_cta,
-                                                            g.s2.dig, g.s2.dexp, g.s2.dsum,
-                                                            g.s2.cm);
+  launch_pdl(k_digitize<1>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, true, y,
+             (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc,
+             pl.kt_cta, g.s2.dig, g.s2.dexp, g.s2.dsum, g.s2.cm);
 }
 
 namespace {
 template <int MODE>
 void launch_main(const GenoView& g, const PMPlan& pl, const uint4* lay, const PMScratch& sc,
-                 const double* cval, const MissLists& ml, cudaStream_t s) {
+                 const double* cval, const MissLists& ml, cudaStream_t s, bool pdl) {
   allow_smem(k_pm_main<MODE>, pl.smem);
   dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nkc);
-  k_pm_main<MODE><<<grid, kThreads, pl.smem, s>>>(lay, pl.KT, pl.kt_cta, sc.dig, sc.dexp,
-                                                  sc.dsum, cval, g.mu, g.mean, ml.off, ml.base,
-                                                  ml.ent, pl.rows_pad, pl.C, sc.part);
+  launch_pdl(k_pm_main<MODE>, grid, dim3(kThreads), pl.smem, s, pdl, lay, pl.KT, pl.kt_cta,
+             (const uint4*)sc.dig, (const int*)sc.dexp, (const double*)sc.dsum, cval,
+             (const double*)g.mu, (const double*)g.mean, ml.off, ml.base, ml.ent, pl.rows_pad,
+             pl.C, sc.part);
 }
 }  // namespace
 
+// main kernel alone, fully serialized (the roofline timing in gkb_op_bench)
 void k1_main_only(const GenoView& g, const double* x, cudaStream_t s) {
-  launch_main<0>(g, g.pl1, g.lt1, g.s1, x, g.m1, s);
+  launch_main<0>(g, g.pl1, g.lt1, g.s1, x, g.m1, s, false);
 }
 
 void k2_main_only(const GenoView& g, cudaStream_t s) {
-  launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s);
+  launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, false);
 }
 
 void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s) {
   if (g.p_loc == 0) return;
   k1_digitize(g, x, s);
-  k1_main_only(g, x, s);
-  k1_reduce<<<(unsigned)((g.p_loc + 255) / 256), 256, 0, s>>>(g.s1.part, g.pl1.nkc,
-                                                              g.pl1.rows_pad, g.p_loc, g.inv_s, y);
+  launch_main<0>(g, g.pl1, g.lt1, g.s1, x, g.m1, s, true);
+  launch_pdl(k1_reduce, dim3((unsigned)((g.p_loc + 255) / 256)), dim3(256), 0, s, true,
+             (const double*)g.s1.part, g.pl1.nkc, g.pl1.rows_pad, g.p_loc, (const double*)g.inv_s,
+             y);
 }
 
 void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s) {
@@ -708,9 +764,9 @@ void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s) {
     return;
   }
   k2_digitize(g, y, s);
-  k2_main_only(g, s);
-  k2_reduce<<<(unsigned)((g.n + 31) / 32), 1024, 0, s>>>(g.s2.part, g.pl2.nkc, g.pl2.rows_pad,
-                                                         g.n, z);
+  launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, true);
+  launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
+             (const double*)g.s2.part, g.pl2.nkc, g.pl2.rows_pad, g.n, z);
 }
 
 }  // namespace dev

@@ -25,7 +25,8 @@ struct PMPlan {
   int64_t KT;        // 128-col K tiles
   int kt_cta;        // K tiles per CTA column range (2048 cols)
   int nkc;           // column ranges
-  int64_t grid_x;    // CTAs along rows (S / 16)
+  int64_t grid_x;    // CTAs along rows (S / strips per CTA)
+  int rows_cta;      // rows per CTA (= rows per missing-list block)
   int64_t rows_pad;  // S * 16
   size_t smem;       // main kernel dynamic shared memory (digits)
   size_t dig_smem;   // digitize kernel dynamic shared memory

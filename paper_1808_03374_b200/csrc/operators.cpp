@@ -239,7 +239,7 @@ void marker_scaling(const int64_t* counts, int64_t p, int64_t n, int scheme, dou
 // of entries (== the shard's missing count).
 static int64_t build_block_lists(const uint32_t* lay, const dev::PMPlan& pl, cudaStream_t st,
                                  uint32_t** off, int64_t** base, uint16_t** ent, int64_t* bytes) {
-  const int span = 256;
+  const int span = pl.rows_cta;
   const int64_t nblk = pl.grid_x * pl.nkc;
   uint32_t* cnt = nullptr;
   int64_t* tot = nullptr;
