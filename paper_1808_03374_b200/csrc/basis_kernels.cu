@@ -4,14 +4,20 @@
 // (gkl.cpp:233-242, :277-284), thick-restart / compress recombination
 // (gkl.cpp:355-359, :396-400) and the final Ritz vectors (:503-507).
 //
-// Every reduction writes per-block partials and a one-block finalize sums
-// them in block order, so results are bitwise reproducible for a given
-// length (the block count is a function of the length only).
+// All of them stream a few vectors of 10^4..10^6 doubles: HBM/L2 bound and,
+// at these lengths, latency bound. Each kernel therefore works on row chunks
+// of kT * U rows per CTA (U rows per thread, loads of a batch issued together)
+// with the CTA count near 2 per SM, and every reduction finishes inside the
+// same launch: each CTA writes its partials, and the last CTA to arrive (an
+// atomic ticket) sums them -- in a fixed segment order, so results are bitwise
+// reproducible for a given length (the chunking is a function of the length
+// only), without a second finalize launch.
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "kernels.hpp"
+#include "pdl.hpp"
 
 namespace gkb {
 namespace dev {
@@ -19,17 +25,76 @@ namespace dev {
 namespace {
 
 constexpr int kT = 256;
-constexpr int kCB = 8;  // columns per CTA in gemv_t
+constexpr int kWarps = kT / 32;
+constexpr int kCB = 8;      // columns per pass in gemv_t
+constexpr int kBatch = 4;   // rows per thread with loads in flight together
+constexpr int kSeg = 8;     // final-sum segments (one per warp)
 
 __device__ __forceinline__ double warp_sum(double v) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-// Reduces vals[0..K) across the block; thread 0 writes out[k].
+// Device-side gating (the Lanczos step control, ctl_kernels.cu): a kernel
+// launched with a gate does nothing when *gate == 0 -- uniformly for all CTAs,
+// so a gated-off reduction never touches its ticket.
+__device__ __forceinline__ bool gated_off(const int* gate) { return gate && *gate == 0; }
+
+// L2 load (partials written by other CTAs of this grid: skip L1)
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// After every CTA has written partial[b * K + k] (b = CTA index, k < K): the
+// last CTA to arrive sums them into out[k]. Order: segment s of the nblk
+// partials (fixed boundaries) summed sequentially, then the kSeg segment sums
+// in order -- a function of (nblk, K) only.
+__device__ void grid_finalize(const double* partial, int nblk, int K, double* out,
+                              unsigned* ticket, unsigned nctas) {
+  __shared__ bool last;
+  __shared__ double seg[kSeg][33];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == nctas - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b0 = (int)((int64_t)nblk * warp / kSeg), b1 = (int)((int64_t)nblk * (warp + 1) / kSeg);
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    const int k = k0 + lane;
+    double t = 0.0;
+    if (k < K) {
+      int b = b0;
+      for (; b + 4 <= b1; b += 4) {
+        const double p0 = ld_cg(partial + (int64_t)b * K + k);
+        const double p1 = ld_cg(partial + (int64_t)(b + 1) * K + k);
+        const double p2 = ld_cg(partial + (int64_t)(b + 2) * K + k);
+        const double p3 = ld_cg(partial + (int64_t)(b + 3) * K + k);
+        t += p0;
+        t += p1;
+        t += p2;
+        t += p3;
+      }
+      for (; b < b1; ++b) t += ld_cg(partial + (int64_t)b * K + k);
+    }
+    seg[warp][lane] = t;
+    __syncthreads();
+    if (warp == 0 && k < K) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kSeg; ++w) s += seg[w][lane];
+      out[k] = s;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *ticket = 0u;  // ready for the next launch on this stream
+}
+
+// Reduces vals[0..K) across the CTA into partial[blockIdx.x * K + k] (warp
+// sums, then the kWarps warp sums in order), then the grid-level finalize.
 template <int K>
-__device__ void block_reduce_write(double (&vals)[K], double* out) {
-  __shared__ double sred[K][kT / 32];
+__device__ void block_partial_finalize(double (&vals)[K], double* partial, double* out,
+                                       unsigned* ticket) {
+  __shared__ double sred[K][kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -39,134 +104,223 @@ __device__ void block_reduce_write(double (&vals)[K], double* out) {
   __syncthreads();
   if (threadIdx.x < K) {
     double t = 0.0;
-    for (int i = 0; i < kT / 32; ++i) t += sred[threadIdx.x][i];
-    out[threadIdx.x] = t;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) t += sred[threadIdx.x][i];
+    partial[(int64_t)blockIdx.x * K + threadIdx.x] = t;
   }
+  grid_finalize(partial, gridDim.x, K, out, ticket, gridDim.x);
 }
 
-__global__ void k_gemv_t(const double* __restrict__ Q, int64_t ld, int64_t len, int64_t ncols,
-                         const double* __restrict__ v, int with_norm, int64_t rows_per_block,
-                         int K, double* __restrict__ partial) {
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r1 = min(len, r0 + rows_per_block);
+// Row chunk of CTA b: [b * rpb, min(len, (b + 1) * rpb)), rpb = kT * U.
+struct Chunk {
+  int64_t r0, r1;
+};
+__device__ __forceinline__ Chunk chunk(int64_t len, int64_t rpb) {
+  Chunk c;
+  c.r0 = (int64_t)blockIdx.x * rpb;
+  c.r1 = min(len, c.r0 + rpb);
+  return c;
+}
+
+// c[k] = Q[:, k]^T v (k < ncols), c[ncols] = ||v||^2 (with_norm). CTA (bx, by)
+// covers row chunk bx and partial columns [kCB by, kCB by + kCB): kCB x kBatch
+// independent loads per thread in flight, warp sums per column, then the
+// kWarps warp sums in order into partial[bx * K + k].
+__global__ void __launch_bounds__(kT) k_gemv_t(const double* __restrict__ Q, int64_t ld,
+                                               int64_t len, int64_t ncols,
+                                               const double* __restrict__ v, int with_norm,
+                                               int64_t rpb, int K, double* __restrict__ partial,
+                                               double* __restrict__ out,
+                                               unsigned* __restrict__ ticket, const int* gate) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
+  __shared__ double ws[kCB][kWarps];
+  if (gated_off(gate)) return;
+  const Chunk ch = chunk(len, rpb);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t c0 = (int64_t)blockIdx.y * kCB;
-  double acc[kCB + 1];
+  double acc[kCB];
 #pragma unroll
-  for (int k = 0; k <= kCB; ++k) acc[k] = 0.0;
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += kT) {
-    const double vr = v[r];
+  for (int k = 0; k < kCB; ++k) acc[k] = 0.0;
+  for (int64_t rb = ch.r0 + threadIdx.x; rb < ch.r1; rb += (int64_t)kT * kBatch) {
+    double vr[kBatch];
 #pragma unroll
-    for (int k = 0; k < kCB; ++k)
-      if (c0 + k < ncols) acc[k] += Q[(c0 + k) * ld + r] * vr;
-    acc[kCB] += vr * vr;
+    for (int i = 0; i < kBatch; ++i) {
+      const int64_t r = rb + (int64_t)i * kT;
+      vr[i] = r < ch.r1 ? v[r] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kCB; ++k) {
+      const int64_t c = c0 + k;
+      if (c < ncols) {
+        const double* q = Q + c * ld;
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+          const int64_t r = rb + (int64_t)i * kT;
+          if (r < ch.r1) acc[k] += q[r] * vr[i];
+        }
+      } else if (c == ncols && with_norm) {
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) acc[k] += vr[i] * vr[i];
+      }
+    }
   }
-  __shared__ double outv[kCB + 1];
-  block_reduce_write<kCB + 1>(acc, outv);
+#pragma unroll
+  for (int k = 0; k < kCB; ++k) {
+    const double t = warp_sum(acc[k]);
+    if (lane == 0) ws[k][warp] = t;
+  }
   __syncthreads();
-  if (threadIdx.x < kCB + 1) {
-    const int k = threadIdx.x;
-    if (k < kCB && c0 + k < ncols) partial[(int64_t)blockIdx.x * K + c0 + k] = outv[k];
-    if (k == kCB && with_norm && blockIdx.y == 0) partial[(int64_t)blockIdx.x * K + ncols] = outv[k];
-  }
-}
-
-// out[k] = sum_b partial[b*K + k]
-__global__ void k_finalize(const double* __restrict__ partial, int nblk, int K,
-                           double* __restrict__ out) {
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+  if (threadIdx.x < kCB && c0 + threadIdx.x < K) {
     double t = 0.0;
-    for (int b = 0; b < nblk; ++b) t += partial[(int64_t)b * K + k];
-    out[k] = t;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) t += ws[threadIdx.x][w];
+    partial[(int64_t)blockIdx.x * K + c0 + threadIdx.x] = t;
   }
+  grid_finalize(partial, gridDim.x, K, out, ticket, gridDim.x * gridDim.y);
 }
 
-// v = beta*v + sign*(Q c); optional norms before/after into block partials
-__global__ void k_gemv_n(const double* __restrict__ Q, int64_t ld, int64_t len, int64_t ncols,
-                         const double* __restrict__ c, double* __restrict__ v, double beta,
-                         double sign, int norms, int64_t rows_per_block,
-                         double* __restrict__ partial) {
+// v = beta*v + sign*(Q c); optional norms before/after (out[0], out[1]).
+__global__ void __launch_bounds__(kT) k_gemv_n(const double* __restrict__ Q, int64_t ld,
+                                               int64_t len, int64_t ncols,
+                                               const double* __restrict__ c,
+                                               double* __restrict__ v, double beta, double sign,
+                                               int norms, int64_t rpb,
+                                               double* __restrict__ partial,
+                                               double* __restrict__ out,
+                                               unsigned* __restrict__ ticket, const int* gate) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
   __shared__ double cs[1024];
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r1 = min(len, r0 + rows_per_block);
-  double acc2[2] = {0.0, 0.0};
-  // rows handled by this thread: r0 + threadIdx.x + i*kT
-  for (int64_t rb = r0; rb < r1; rb += kT) {
-    const int64_t r = rb + threadIdx.x;
-    double s = 0.0;
+  if (gated_off(gate)) return;
+  const Chunk ch = chunk(len, rpb);
+  double nrm[2] = {0.0, 0.0};
+  for (int64_t rb = ch.r0 + threadIdx.x; rb - threadIdx.x < ch.r1; rb += (int64_t)kT * kBatch) {
+    double s[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) s[i] = 0.0;
     for (int64_t cb = 0; cb < ncols; cb += 1024) {
       const int64_t cn = min((int64_t)1024, ncols - cb);
       __syncthreads();
       for (int t = threadIdx.x; t < cn; t += kT) cs[t] = c[cb + t];
       __syncthreads();
-      if (r < r1)
-        for (int64_t l = 0; l < cn; ++l) s += Q[(cb + l) * ld + r] * cs[l];
+      int64_t l = 0;
+      for (; l + kCB <= cn; l += kCB) {  // kCB columns x kBatch rows of loads in flight
+        double q[kCB][kBatch];
+#pragma unroll
+        for (int k = 0; k < kCB; ++k)
+#pragma unroll
+          for (int i = 0; i < kBatch; ++i) {
+            const int64_t r = rb + (int64_t)i * kT;
+            q[k][i] = r < ch.r1 ? Q[(cb + l + k) * ld + r] : 0.0;
+          }
+#pragma unroll
+        for (int k = 0; k < kCB; ++k)
+#pragma unroll
+          for (int i = 0; i < kBatch; ++i) s[i] += q[k][i] * cs[l + k];
+      }
+      for (; l < cn; ++l) {
+        const double* q0 = Q + (cb + l) * ld;
+        const double w0 = cs[l];
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+          const int64_t r = rb + (int64_t)i * kT;
+          if (r < ch.r1) s[i] += q0[r] * w0;
+        }
+      }
     }
-    if (r < r1) {
-      const double old = v[r];
-      const double nv = beta == 0.0 ? sign * s : beta * old + sign * s;
-      v[r] = nv;
-      acc2[0] += old * old;
-      acc2[1] += nv * nv;
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int64_t r = rb + (int64_t)i * kT;
+      if (r < ch.r1) {
+        const double old = v[r];
+        const double nv = beta == 0.0 ? sign * s[i] : beta * old + sign * s[i];
+        v[r] = nv;
+        nrm[0] += old * old;
+        nrm[1] += nv * nv;
+      }
     }
   }
-  if (norms) block_reduce_write<2>(acc2, partial + (int64_t)blockIdx.x * 2);
+  if (norms) block_partial_finalize<2>(nrm, partial, out, ticket);
 }
 
-__global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t len,
-                      int64_t rows_per_block, double* __restrict__ partial) {
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r1 = min(len, r0 + rows_per_block);
+__global__ void __launch_bounds__(kT) k_dot(const double* __restrict__ a,
+                                            const double* __restrict__ b, int64_t len,
+                                            int64_t rpb, double* __restrict__ partial,
+                                            double* __restrict__ out,
+                                            unsigned* __restrict__ ticket, const int* gate) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
+  if (gated_off(gate)) return;
+  const Chunk ch = chunk(len, rpb);
   double acc[1] = {0.0};
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += kT) acc[0] += a[r] * b[r];
-  block_reduce_write<1>(acc, partial + blockIdx.x);
+  for (int64_t rb = ch.r0 + threadIdx.x; rb < ch.r1; rb += (int64_t)kT * kBatch) {
+    double x[kBatch], y[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int64_t r = rb + (int64_t)i * kT;
+      x[i] = r < ch.r1 ? a[r] : 0.0;
+      y[i] = r < ch.r1 ? b[r] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) acc[0] += x[i] * y[i];
+  }
+  block_partial_finalize<1>(acc, partial, out, ticket);
 }
 
 __global__ void k_axpy_dev(const double* __restrict__ d, const double* __restrict__ u,
-                           double* __restrict__ v, int64_t len) {
+                           double* __restrict__ v, int64_t len, const int* gate) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
+  if (gated_off(gate)) return;
   const double a = *d;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < len;
        r += (int64_t)gridDim.x * blockDim.x)
     v[r] -= a * u[r];
 }
 
-__global__ void k_axpy_norms(double alpha, const double* __restrict__ u, double* __restrict__ v,
-                             int64_t len, int64_t rows_per_block, double* __restrict__ partial) {
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r1 = min(len, r0 + rows_per_block);
+// v = v - alpha*u with ||v_before||^2, ||v_after||^2. alpha is the host value,
+// or read on the device from `dval`: sqrt(*dval) (take_sqrt; IEEE sqrt, bitwise
+// equal to the host's std::sqrt of the same value) or *dval itself.
+__global__ void __launch_bounds__(kT) k_axpy_norms(double alpha, const double* __restrict__ dval,
+                                                   int take_sqrt, const double* __restrict__ u,
+                                                   double* __restrict__ v, int64_t len,
+                                                   int64_t rpb, double* __restrict__ partial,
+                                                   double* __restrict__ out,
+                                                   unsigned* __restrict__ ticket, const int* gate) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
+  if (gated_off(gate)) return;
+  if (dval) alpha = take_sqrt ? sqrt(*dval) : *dval;
+  const Chunk ch = chunk(len, rpb);
   double acc[2] = {0.0, 0.0};
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += kT) {
-    const double old = v[r];
-    const double nv = old - alpha * u[r];
-    v[r] = nv;
-    acc[0] += old * old;
-    acc[1] += nv * nv;
+  for (int64_t rb = ch.r0 + threadIdx.x; rb < ch.r1; rb += (int64_t)kT * kBatch) {
+    double x[kBatch], y[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int64_t r = rb + (int64_t)i * kT;
+      x[i] = r < ch.r1 ? v[r] : 0.0;
+      y[i] = r < ch.r1 ? u[r] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int64_t r = rb + (int64_t)i * kT;
+      const double nv = x[i] - alpha * y[i];
+      if (r < ch.r1) v[r] = nv;
+      acc[0] += x[i] * x[i];
+      acc[1] += nv * nv;
+    }
   }
-  block_reduce_write<2>(acc, partial + (int64_t)blockIdx.x * 2);
+  block_partial_finalize<2>(acc, partial, out, ticket);
 }
 
-// alpha = sqrt(*nrm2) read on the device (IEEE sqrt: bitwise equal to the
-// host's std::sqrt of the same value) -- used to launch the next half-step
-// before the host has read the norm.
-__global__ void k_axpy_norms_dsq(const double* __restrict__ nrm2, const double* __restrict__ u,
-                                 double* __restrict__ v, int64_t len, int64_t rows_per_block,
-                                 double* __restrict__ partial) {
-  const double alpha = sqrt(*nrm2);
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r1 = min(len, r0 + rows_per_block);
-  double acc[2] = {0.0, 0.0};
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += kT) {
-    const double old = v[r];
-    const double nv = old - alpha * u[r];
-    v[r] = nv;
-    acc[0] += old * old;
-    acc[1] += nv * nv;
-  }
-  block_reduce_write<2>(acc, partial + (int64_t)blockIdx.x * 2);
-}
-
-__global__ void k_div_copy_dsq(const double* __restrict__ src, const double* __restrict__ nrm2,
-                               double* __restrict__ dst, int64_t len) {
-  const double divisor = sqrt(*nrm2);
+__global__ void k_div_copy_dev(const double* __restrict__ src, const double* __restrict__ dval,
+                               int take_sqrt, double* __restrict__ dst, int64_t len,
+                               const int* gate) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
+  if (gated_off(gate)) return;
+  const double divisor = take_sqrt ? sqrt(*dval) : *dval;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < len;
        r += (int64_t)gridDim.x * blockDim.x)
     dst[r] = src[r] / divisor;
@@ -174,31 +328,52 @@ __global__ void k_div_copy_dsq(const double* __restrict__ src, const double* __r
 
 __global__ void k_div_copy(const double* __restrict__ src, double divisor, double* __restrict__ dst,
                            int64_t len) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < len;
        r += (int64_t)gridDim.x * blockDim.x)
     dst[r] = src[r] / divisor;
 }
 
-// dst[:, c] = sum_l Q[:, l] * W[l, c], 8 output columns per pass
-__global__ void k_gemm_small(const double* __restrict__ Q, int64_t ld, int64_t len, int64_t j,
-                             const double* __restrict__ W, int64_t ldw, int64_t kc,
-                             double* __restrict__ dst, int64_t ldd) {
+// dst[:, c] = sum_l Q[:, l] * W[l, c] for c in [c0, c0 + NC): one row per
+// thread, Q read once per pass of NC output columns, W staged in smem.
+template <int NC>
+__global__ void __launch_bounds__(128) k_gemm_small(const double* __restrict__ Q, int64_t ld,
+                                                    int64_t len, int64_t j,
+                                                    const double* __restrict__ W, int64_t ldw,
+                                                    int64_t kc, int64_t c0,
+                                                    double* __restrict__ dst, int64_t ldd) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
+  extern __shared__ double wsm[];  // j x NC
+  for (int64_t t = threadIdx.x; t < j * NC; t += blockDim.x) {
+    const int64_t l = t / NC, c = c0 + t % NC;
+    wsm[t] = c < kc ? W[c * ldw + l] : 0.0;
+  }
+  __syncthreads();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= len) return;
-  for (int64_t c0 = 0; c0 < kc; c0 += 8) {
-    double acc[8];
+  double acc[NC];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0.0;
-    for (int64_t l = 0; l < j; ++l) {
-      const double q = Q[l * ld + r];
+  for (int k = 0; k < NC; ++k) acc[k] = 0.0;
+  int64_t l = 0;
+  for (; l + 4 <= j; l += 4) {
+    double q[4];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (c0 + k < kc) acc[k] += q * __ldg(W + (c0 + k) * ldw + l);
-    }
+    for (int i = 0; i < 4; ++i) q[i] = Q[(l + i) * ld + r];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (c0 + k < kc) dst[(c0 + k) * ldd + r] = acc[k];
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) acc[k] += q[i] * wsm[(l + i) * NC + k];
   }
+  for (; l < j; ++l) {
+    const double q = Q[l * ld + r];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) acc[k] += q * wsm[l * NC + k];
+  }
+#pragma unroll
+  for (int k = 0; k < NC; ++k)
+    if (c0 + k < kc) dst[(c0 + k) * ldd + r] = acc[k];
 }
 
 struct SrcList {
@@ -206,6 +381,8 @@ struct SrcList {
 };
 
 __global__ void k_sum_buffers(SrcList l, int nsrc, double* __restrict__ dst, int64_t len) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < len;
        r += (int64_t)gridDim.x * blockDim.x) {
     double t = 0.0;
@@ -221,102 +398,131 @@ int elem_grid(int64_t len) {
   return (int)g;
 }
 
-int64_t rows_per_block(int64_t len, int64_t nblk) {
-  int64_t rpb = (len + nblk - 1) / nblk;
-  rpb = ((rpb + kT - 1) / kT) * kT;
-  return rpb > 0 ? rpb : kT;
+// rows per thread: enough CTAs for ~2 per SM, at most 64 rows per thread
+int64_t rows_per_thread(int64_t len) {
+  int64_t u = (len + (int64_t)kT * 296 - 1) / ((int64_t)kT * 296);
+  if (u < 1) u = 1;
+  if (u > 64) u = 64;
+  return u;
 }
+
+int64_t rpb_of(int64_t len) { return (int64_t)kT * rows_per_thread(len); }
 
 }  // namespace
 
 int64_t red_blocks(int64_t len) {
-  // function of len only (determinism); ~4 rows per thread, at most 296 blocks
-  int64_t b = (len + kT * 4 - 1) / (kT * 4);
-  if (b > 296) b = 296;
-  if (b < 1) b = 1;
-  return b;
+  // a function of len only (determinism)
+  const int64_t rpb = rpb_of(len);
+  const int64_t b = (len + rpb - 1) / rpb;
+  return b > 0 ? b : 1;
+}
+
+void init_red_scratch(RedScratch& rs) {
+  if (!rs.ticket) {
+    cudaMalloc(&rs.ticket, sizeof(unsigned));
+    cudaMemset(rs.ticket, 0, sizeof(unsigned));
+  }
 }
 
 void gemv_t(const double* Q, int64_t ld, int64_t len, int64_t ncols, const double* v, bool with_norm,
-            RedScratch& rs, double* out, cudaStream_t s) {
+            RedScratch& rs, double* out, cudaStream_t s, const int* gate) {
   const int K = (int)(ncols + (with_norm ? 1 : 0));
   if (K == 0) return;
-  const int64_t nb = red_blocks(len);
-  const int64_t rpb = rows_per_block(len, nb);
-  const int64_t nblk = (len + rpb - 1) / rpb > 0 ? (len + rpb - 1) / rpb : 1;
-  const int64_t cb = ncols > 0 ? (ncols + kCB - 1) / kCB : 1;
-  k_gemv_t<<<dim3((unsigned)nblk, (unsigned)cb), kT, 0, s>>>(Q, ld, len, ncols, v, with_norm ? 1 : 0,
-                                                            rpb, K, rs.partial);
-  k_finalize<<<1, 256, 0, s>>>(rs.partial, (int)nblk, K, out);
+  const dim3 grid((unsigned)red_blocks(len), (unsigned)((K + kCB - 1) / kCB));
+  launch_pdl(k_gemv_t, grid, dim3(kT), 0, s, true, Q, ld, len, ncols, v, with_norm ? 1 : 0,
+                                                     rpb_of(len), K, rs.partial, out, rs.ticket,
+                                                     gate);
 }
 
 void gemv_n(const double* Q, int64_t ld, int64_t len, int64_t ncols, const double* c, double* v,
-            double beta, double sign, bool norms, RedScratch& rs, double* out, cudaStream_t s) {
-  const int64_t nb = red_blocks(len);
-  const int64_t rpb = rows_per_block(len, nb);
-  const int64_t nblk = (len + rpb - 1) / rpb > 0 ? (len + rpb - 1) / rpb : 1;
-  k_gemv_n<<<(unsigned)nblk, kT, 0, s>>>(Q, ld, len, ncols, c, v, beta, sign, norms ? 1 : 0, rpb,
-                                         rs.partial);
-  if (norms) k_finalize<<<1, 32, 0, s>>>(rs.partial, (int)nblk, 2, out);
+            double beta, double sign, bool norms, RedScratch& rs, double* out, cudaStream_t s,
+            const int* gate) {
+  if (len == 0 && !norms) return;
+  launch_pdl(k_gemv_n, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, Q, ld, len, ncols, c, v, beta, sign,
+                                                     norms ? 1 : 0, rpb_of(len), rs.partial, out,
+                                                     rs.ticket, gate);
 }
 
-void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* out, cudaStream_t s) {
-  const int64_t nb = red_blocks(len);
-  const int64_t rpb = rows_per_block(len, nb);
-  const int64_t nblk = (len + rpb - 1) / rpb > 0 ? (len + rpb - 1) / rpb : 1;
-  k_dot<<<(unsigned)nblk, kT, 0, s>>>(a, b, len, rpb, rs.partial);
-  k_finalize<<<1, 32, 0, s>>>(rs.partial, (int)nblk, 1, out);
+void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
+         const int* gate) {
+  launch_pdl(k_dot, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, a, b, len, rpb_of(len), rs.partial, out,
+                                                  rs.ticket, gate);
 }
 
-void nrm2sq(const double* a, int64_t len, RedScratch& rs, double* out, cudaStream_t s) {
-  dot(a, a, len, rs, out, s);
+void nrm2sq(const double* a, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
+            const int* gate) {
+  dot(a, a, len, rs, out, s, gate);
 }
 
-void axpy_dev(const double* dptr, const double* u, double* v, int64_t len, cudaStream_t s) {
+void axpy_dev(const double* dptr, const double* u, double* v, int64_t len, cudaStream_t s,
+              const int* gate) {
   if (len == 0) return;
-  k_axpy_dev<<<elem_grid(len), kT, 0, s>>>(dptr, u, v, len);
+  launch_pdl(k_axpy_dev, dim3(elem_grid(len)), dim3(kT), 0, s, true, dptr, u, v, len, gate);
 }
 
 void axpy_norms(double alpha, const double* u, double* v, int64_t len, RedScratch& rs, double* out,
                 cudaStream_t s) {
-  const int64_t nb = red_blocks(len);
-  const int64_t rpb = rows_per_block(len, nb);
-  const int64_t nblk = (len + rpb - 1) / rpb > 0 ? (len + rpb - 1) / rpb : 1;
-  k_axpy_norms<<<(unsigned)nblk, kT, 0, s>>>(alpha, u, v, len, rpb, rs.partial);
-  k_finalize<<<1, 32, 0, s>>>(rs.partial, (int)nblk, 2, out);
+  launch_pdl(k_axpy_norms, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, alpha, nullptr, 0, u, v, len,
+                                                         rpb_of(len), rs.partial, out, rs.ticket,
+                                                         nullptr);
 }
 
 void axpy_norms_dsq(const double* nrm2, const double* u, double* v, int64_t len, RedScratch& rs,
                     double* out, cudaStream_t s) {
-  const int64_t nb = red_blocks(len);
-  const int64_t rpb = rows_per_block(len, nb);
-  const int64_t nblk = (len + rpb - 1) / rpb > 0 ? (len + rpb - 1) / rpb : 1;
-  k_axpy_norms_dsq<<<(unsigned)nblk, kT, 0, s>>>(nrm2, u, v, len, rpb, rs.partial);
-  k_finalize<<<1, 32, 0, s>>>(rs.partial, (int)nblk, 2, out);
+  launch_pdl(k_axpy_norms, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, 0.0, nrm2, 1, u, v, len, rpb_of(len),
+                                                         rs.partial, out, rs.ticket, nullptr);
+}
+
+void axpy_norms_dv(const double* alpha, const double* u, double* v, int64_t len, RedScratch& rs,
+                   double* out, cudaStream_t s, const int* gate) {
+  launch_pdl(k_axpy_norms, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, 0.0, alpha, 0, u, v, len, rpb_of(len),
+                                                         rs.partial, out, rs.ticket, gate);
 }
 
 void div_copy_dsq(const double* src, const double* nrm2, double* dst, int64_t len,
                   cudaStream_t s) {
   if (len == 0) return;
-  k_div_copy_dsq<<<elem_grid(len), kT, 0, s>>>(src, nrm2, dst, len);
+  launch_pdl(k_div_copy_dev, dim3(elem_grid(len)), dim3(kT), 0, s, true, src, nrm2, 1, dst, len, nullptr);
+}
+
+void div_copy_dv(const double* src, const double* divisor, double* dst, int64_t len,
+                 cudaStream_t s, const int* gate) {
+  if (len == 0) return;
+  launch_pdl(k_div_copy_dev, dim3(elem_grid(len)), dim3(kT), 0, s, true, src, divisor, 0, dst, len, gate);
 }
 
 void div_copy(const double* src, double divisor, double* dst, int64_t len, cudaStream_t s) {
   if (len == 0) return;
-  k_div_copy<<<elem_grid(len), kT, 0, s>>>(src, divisor, dst, len);
+  launch_pdl(k_div_copy, dim3(elem_grid(len)), dim3(kT), 0, s, true, src, divisor, dst, len);
 }
 
 void gemm_small(const double* Q, int64_t ld, int64_t len, int64_t j, const double* W, int64_t ldw,
                 int64_t kc, double* dst, int64_t ldd, cudaStream_t s) {
   if (len == 0 || kc == 0) return;
-  k_gemm_small<<<(unsigned)((len + 127) / 128), 128, 0, s>>>(Q, ld, len, j, W, ldw, kc, dst, ldd);
+  const unsigned grid = (unsigned)((len + 127) / 128);
+  for (int64_t c0 = 0; c0 < kc; c0 += 32) {
+    const int64_t rem = kc - c0;
+    if (rem > 16) {
+      const size_t sm = sizeof(double) * (size_t)(j * 32);
+      if (sm > 48 * 1024)
+        cudaFuncSetAttribute(k_gemm_small<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+      launch_pdl(k_gemm_small<32>, grid, dim3(128), sm, s, true, Q, ld, len, j, W, ldw, kc, c0, dst, ldd);
+    } else if (rem > 8) {
+      launch_pdl(k_gemm_small<16>, grid, dim3(128), sizeof(double) * (size_t)(j * 16), s, true, Q, ld, len, j, W, ldw,
+                                                                            kc, c0, dst, ldd);
+    } else {
+      launch_pdl(k_gemm_small<8>, grid, dim3(128), sizeof(double) * (size_t)(j * 8), s, true, Q, ld, len, j, W, ldw,
+                                                                          kc, c0, dst, ldd);
+    }
+  }
 }
 
 void sum_buffers(const double* const* srcs, int nsrc, double* dst, int64_t len, cudaStream_t s) {
   SrcList l;
   for (int k = 0; k < 16; ++k) l.p[k] = k < nsrc ? srcs[k] : nullptr;
   if (len == 0) return;
-  k_sum_buffers<<<elem_grid(len), kT, 0, s>>>(l, nsrc, dst, len);
+  launch_pdl(k_sum_buffers, dim3(elem_grid(len)), dim3(kT), 0, s, true, l, nsrc, dst, len);
 }
 
 void flush_l2(void* buf, size_t bytes, cudaStream_t s) { cudaMemsetAsync(buf, 0, bytes, s); }

@@ -51,6 +51,7 @@ static void init_shard(Shard& s, int index, int dev) {
   GKB_CUDA(cudaMallocHost(&s.hres, sizeof(double) * kResCap));
   GKB_CUDA(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
   s.ensure_partial(1 << 16);
+  dev::init_red_scratch(s.rs);
 }
 
 void Context::init_local(const std::vector<int>& devices) {
@@ -83,6 +84,7 @@ Context::~Context() {
     cudaSetDevice(s.dev);
     if (s.stream) cudaStreamSynchronize(s.stream);
     if (s.rs.partial) cudaFree(s.rs.partial);
+    if (s.rs.ticket) cudaFree(s.rs.ticket);
     if (s.dres) cudaFree(s.dres);
     if (s.hres) cudaFreeHost(s.hres);
     for (int q = 0; q < 2; ++q)

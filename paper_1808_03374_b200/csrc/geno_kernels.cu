@@ -41,6 +41,7 @@
 #include <cstdlib>
 
 #include "kernels.hpp"
+#include "pdl.hpp"
 
 namespace gkb {
 namespace dev {
@@ -67,18 +68,9 @@ __device__ __forceinline__ uint32_t r_to_bed(uint32_t r) {
 }
 __device__ __forceinline__ uint32_t missing_mask(uint32_t r) { return r & (r >> 1) & 0x55555555u; }
 
-// Programmatic dependent launch (PDL). The product kernels (digitize -> main
-// -> reduce) are launched with programmatic stream serialization: a kernel may
-// be scheduled while its predecessor drains, runs only work on data that is
-// immutable for the whole solve (tile layouts, missing lists) before
-// pdl_wait(), and nothing that writes global memory or reads a predecessor's
-// output. pdl_wait() returns once the predecessor grid has completed and its
-// writes are visible, so completion stays ordered along the stream. Without
-// the launch attribute both instructions are no-ops.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
+// Programmatic dependent launch (pdl.hpp). The product kernels (digitize ->
+// main -> reduce) run only work on data that is immutable for the whole solve
+// (tile layouts, missing lists) before pdl_wait().
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 v;
@@ -681,28 +673,6 @@ void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int6
 }
 
 namespace {
-// Launch with programmatic stream serialization (see pdl_wait); GKB_NO_PDL=1
-// launches every product kernel fully serialized instead.
-bool pdl_enabled() {
-  static const bool on = std::getenv("GKB_NO_PDL") == nullptr;
-  return on;
-}
-template <class... KArgs, class... Args>
-void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                bool pdl, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
-
 template <class K>
 void allow_smem(K kern, size_t bytes) {  // opt in above 48 KB
   if (bytes > 48 * 1024)

@@ -136,6 +136,13 @@ Lanczos::~Lanczos() {
     cudaStreamSynchronize(st);
     if (i < tmp_small_.size() && tmp_small_[i]) cudaFree(tmp_small_[i]);
   }
+  for (size_t i = 0; i < ctl_d_.size(); ++i)
+    if (ctl_d_[i]) {
+      cudaSetDevice(ctx_->shards[i].dev);
+      cudaFree(ctl_d_[i]);
+    }
+  if (ctl_up_) cudaFreeHost(ctl_up_);
+  if (ctl_down_) cudaFreeHost(ctl_down_);
   for (double* p : ring_slot_)
     if (p) cudaFreeHost(p);
   for (cudaEvent_t e : ring_ev_)
@@ -593,6 +600,259 @@ StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter
   return info;
 }
 
+// ---------------------------------------------------------------- device-controlled steps
+// The same step as Lanczos::step (gkl.cpp:206-312), enqueued without reading
+// anything back: each decision is a ctl kernel (ctl_kernels.cu) writing gates,
+// and the kernels of both branches are enqueued with the gate that enables
+// them. Kernels and result slots are the host path's, so the values are too.
+dev::ctl::Params Lanczos::ctl_params(const Options& o, int op, int64_t s) const {
+  dev::ctl::Params p{};
+  p.op = op;
+  p.full = o.full ? 1 : 0;
+  p.omega_rec = o.omega_recurrence;
+  p.one_sided = o.one_sided ? 1 : 0;
+  p.s = s;
+  p.m = m_;
+  p.n = n_;
+  p.cap = cap_;
+  p.omega = o.omega;
+  p.lvl = eps_level(m_, n_);
+  p.bfac = kBreakdownFactor;
+  p.guard = kOneSidedGuard;
+  p.eta = kCgs2Eta;
+  p.eps = kEps;
+  p.lo = p.hi = -1;
+  return p;
+}
+
+// cgs2 (orth.hpp:19-44) with its second-pass test on the device; pass 1 runs
+// when the int at gate_slot is set (full mode: alive; partial: reorthogonalize).
+void Lanczos::cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec, int gate_slot,
+                       const Options& o, int64_t s) {
+  using namespace dev::ctl;
+  const int L = (int)ctx_->shards.size();
+  const auto& Q = basis(side);
+  auto res = [&](int i, int64_t off) { return cd(i) + ctl_L_.res + off; };
+  auto reduce = [&](int64_t off, int64_t cnt) {
+    if (side != kLeft) return;
+    std::vector<double*> b(L);
+    for (int i = 0; i < L; ++i) b[i] = res(i, off);
+    ctx_->allreduce(b, cnt);
+  };
+  auto ctl = [&](const Params& p) {
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      launch(cd(i), ci(i), p, ctx_->shards[i].stream);
+    }
+  };
+  const int64_t o2 = R_CG + ncols + 3;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int64_t oc = pass == 0 ? R_CG : o2;  // coefficients (+ ||v||^2 in pass 1)
+    const int64_t on = pass == 0 ? R_CG + ncols + 1 : o2 + ncols;  // norms of gemv_n
+    const int slot = pass == 0 ? gate_slot : (int)I_GRE2;
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      Shard& sh = ctx_->shards[i];
+      dev::gemv_t(Q[i], ld(side, i), len(side, i), ncols, vec[i], pass == 0, sh.rs, res(i, oc),
+                  sh.stream, ci(i) + slot);
+    }
+    reduce(oc, ncols + (pass == 0 ? 1 : 0));
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      Shard& sh = ctx_->shards[i];
+      dev::gemv_n(Q[i], ld(side, i), len(side, i), ncols, res(i, oc), vec[i], 1.0, -1.0, true,
+                  sh.rs, res(i, on), sh.stream, ci(i) + slot);
+    }
+    reduce(on, 2);
+    Params p = ctl_params(o, pass == 0 ? OP_CG_MID : OP_CG_END, s);
+    p.ncols = ncols;
+    p.side = side == kLeft ? 0 : 1;
+    ctl(p);
+  }
+}
+
+void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t hi) {
+  using namespace dev::ctl;
+  const int L = (int)ctx_->shards.size();
+  auto res = [&](int i, int64_t off) { return cd(i) + ctl_L_.res + off; };
+  auto reduce_left = [&](int64_t off, int64_t cnt) {
+    std::vector<double*> b(L);
+    for (int i = 0; i < L; ++i) b[i] = res(i, off);
+    ctx_->allreduce(b, cnt);
+  };
+  auto ctl = [&](const Params& p) {
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      launch(cd(i), ci(i), p, ctx_->shards[i].stream);
+    }
+  };
+  // Left half-step: alpha u_{s+1} = X v_s - U coupling.
+  {
+    std::vector<const double*> vin(L);
+    for (int i = 0; i < L; ++i) vin[i] = V_[i] + s * n_;
+    op_->apply_dev(vin, w_);
+  }
+  if (o.full) {
+    if (s == 0) {
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        Shard& sh = ctx_->shards[i];
+        dev::nrm2sq(w_[i], op_->rows(i), sh.rs, res(i, R_N), sh.stream, ci(i) + I_ALIVE);
+      }
+      reduce_left(R_N, 1);
+      ctl(ctl_params(o, OP_SQRT_L, s));
+    } else {
+      cgs2_dev(kLeft, s, w_, I_ALIVE, o, s);
+    }
+  } else {
+    const bool pat = lo >= 0;
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      Shard& sh = ctx_->shards[i];
+      const int64_t r = op_->rows(i);
+      if (pat)
+        dev::gemv_n(U_[i] + lo * r, r, r, hi - lo + 1, cd(i) + ctl_L_.coup + lo, w_[i], 1.0, -1.0,
+                    true, sh.rs, res(i, R_N), sh.stream, ci(i) + I_ALIVE);
+      else
+        dev::nrm2sq(w_[i], r, sh.rs, res(i, R_N), sh.stream, ci(i) + I_ALIVE);
+    }
+    reduce_left(R_N, pat ? 2 : 1);
+    Params pa = ctl_params(o, OP_L_A, s);
+    pa.nidx = pat ? 1 : 0;
+    pa.has_pattern = pat ? 1 : 0;
+    pa.lo = lo;
+    pa.hi = hi;
+    ctl(pa);
+    if (pat) {  // local second pass over the structural pattern (gkl.cpp:233-242)
+      for (int64_t c = lo; c <= hi; ++c) {
+        for (int i = 0; i < L; ++i) {
+          ctx_->set_device(i);
+          Shard& sh = ctx_->shards[i];
+          const int64_t r = op_->rows(i);
+          dev::dot(U_[i] + c * r, w_[i], r, sh.rs, res(i, R_DOT), sh.stream, ci(i) + I_G2PC + c);
+        }
+        reduce_left(R_DOT, 1);
+        for (int i = 0; i < L; ++i) {
+          ctx_->set_device(i);
+          const int64_t r = op_->rows(i);
+          dev::axpy_dev(res(i, R_DOT), U_[i] + c * r, w_[i], r, ctx_->shards[i].stream,
+                        ci(i) + I_G2PC + c);
+        }
+      }
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        Shard& sh = ctx_->shards[i];
+        dev::nrm2sq(w_[i], op_->rows(i), sh.rs, res(i, R_N), sh.stream, ci(i) + I_G2P);
+      }
+      reduce_left(R_N, 1);
+    }
+    ctl(ctl_params(o, OP_L_B, s));
+    if (s > 0) cgs2_dev(kLeft, s, w_, I_GRE, o, s);
+  }
+  ctl(ctl_params(o, OP_L_END, s));
+
+  // Right half-step: beta v_{s+1} = X^T u_{s+1} - alpha v_s.
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    const int64_t r = op_->rows(i);
+    dev::div_copy_dv(w_[i], cd(i) + ctl_L_.sc + S_ALPHA, U_[i] + s * r, r, ctx_->shards[i].stream,
+                     ci(i) + I_ALIVE);
+  }
+  {
+    std::vector<const double*> uin(L);
+    for (int i = 0; i < L; ++i) uin[i] = U_[i] + s * op_->rows(i);
+    op_->adjoint_dev(uin, z_);
+  }
+  if (!o.full) {
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      Shard& sh = ctx_->shards[i];
+      dev::axpy_norms_dv(cd(i) + ctl_L_.sc + S_ALPHA, V_[i] + s * n_, z_[i], n_, sh.rs,
+                         res(i, R_N), sh.stream, ci(i) + I_ALIVE);
+    }
+    ctl(ctl_params(o, OP_R_A, s));
+    for (int i = 0; i < L; ++i) {  // local second pass against v_s (gkl.cpp:277-284)
+      ctx_->set_device(i);
+      Shard& sh = ctx_->shards[i];
+      const int* g = ci(i) + I_G2P;
+      dev::dot(V_[i] + s * n_, z_[i], n_, sh.rs, res(i, R_DOT), sh.stream, g);
+      dev::axpy_dev(res(i, R_DOT), V_[i] + s * n_, z_[i], n_, sh.stream, g);
+      dev::nrm2sq(z_[i], n_, sh.rs, res(i, R_N), sh.stream, g);
+    }
+    ctl(ctl_params(o, OP_R_B, s));
+    cgs2_dev(kRight, s + 1, z_, I_GRE, o, s);
+  } else {
+    cgs2_dev(kRight, s + 1, z_, I_ALIVE, o, s);
+  }
+  ctl(ctl_params(o, OP_R_END, s));
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    dev::div_copy_dv(z_[i], cd(i) + ctl_L_.sc + S_BETA, V_[i] + (s + 1) * n_, n_,
+                     ctx_->shards[i].stream, ci(i) + I_ALIVE);
+  }
+}
+
+Lanczos::DevRun Lanczos::run_dev(const Options& o, int64_t nsteps, double* norm_scale) {
+  using namespace dev::ctl;
+  const int L = (int)ctx_->shards.size();
+  if (ctl_d_.empty()) {
+    ctl_L_ = layout(cap_);
+    ctl_d_.assign(L, nullptr);
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      GKB_CUDA(cudaMalloc(&ctl_d_[i], ctl_L_.bytes));
+    }
+    GKB_CUDA(cudaMallocHost(&ctl_up_, ctl_L_.bytes));
+    GKB_CUDA(cudaMallocHost(&ctl_down_, ctl_L_.bytes));
+  }
+  // host state -> every replica
+  double* hd = reinterpret_cast<double*>(ctl_up_);
+  int* hi = reinterpret_cast<int*>(hd + ctl_L_.nd);
+  std::memset(ctl_up_, 0, ctl_L_.bytes);
+  std::copy(B_.begin(), B_.end(), hd + ctl_L_.B);
+  std::copy(coupling_.begin(), coupling_.end(), hd + ctl_L_.coup);
+  std::copy(mu_.begin(), mu_.end(), hd + ctl_L_.mu);
+  std::copy(nu_.begin(), nu_.end(), hd + ctl_L_.nu);
+  hd[ctl_L_.sc + S_NS] = *norm_scale;
+  hi[I_ALIVE] = 1;
+  hi[I_J] = (int)j_;
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    GKB_CUDA(cudaMemcpyAsync(ctl_d_[i], ctl_up_, ctl_L_.bytes, cudaMemcpyHostToDevice,
+                             ctx_->shards[i].stream));
+  }
+  // first step: the coupling pattern of the host state; later steps: {s - 1}
+  int64_t lo = -1, hi_c = -1;
+  for (int64_t i = 0; i < j_; ++i)
+    if (coupling_[i] != 0.0) {
+      if (lo < 0) lo = i;
+      hi_c = i;
+    }
+  for (int64_t t = 0; t < nsteps; ++t) {
+    const int64_t s = j_ + t;
+    if (t > 0) lo = hi_c = s - 1;
+    enqueue_step_dev(o, s, lo, hi_c);
+  }
+  ctx_->set_device(0);
+  Shard& s0 = ctx_->shards[0];
+  GKB_CUDA(cudaMemcpyAsync(ctl_down_, ctl_d_[0], ctl_L_.bytes, cudaMemcpyDeviceToHost, s0.stream));
+  ctx_->sync_all();
+  ++host_syncs;
+  const double* dd = reinterpret_cast<const double*>(ctl_down_);
+  const int* di = reinterpret_cast<const int*>(dd + ctl_L_.nd);
+  std::copy(dd + ctl_L_.B, dd + ctl_L_.B + cap_ * cap_, B_.begin());
+  std::copy(dd + ctl_L_.coup, dd + ctl_L_.coup + cap_, coupling_.begin());
+  std::copy(dd + ctl_L_.mu, dd + ctl_L_.mu + cap_ + 2, mu_.begin());
+  std::copy(dd + ctl_L_.nu, dd + ctl_L_.nu + cap_ + 1, nu_.begin());
+  *norm_scale = dd[ctl_L_.sc + S_NS];
+  j_ = di[I_J];
+  DevRun r;
+  r.completed = di[I_STEPS];
+  r.status = di[I_STATUS];
+  r.reorth = di[I_REORTH];
+  return r;
+}
+
 // ritz_extract (gkl.cpp:314-339)
 Ritz Lanczos::ritz_extract(double tol) const {
   Ritz out;
@@ -629,11 +889,15 @@ Ritz Lanczos::ritz_extract(double tol) const {
 }
 
 // thick_restart (gkl.cpp:341-378)
-void Lanczos::thick_restart(int64_t keep) {
+void Lanczos::thick_restart(int64_t keep, const Ritz* current) {
   const int64_t j = j_;
   if (keep < 1 || keep >= j) fail(GKB_EINVAL, "thick_restart: need 1 <= keep < steps");
   const int L = (int)ctx_->shards.size();
-  const Ritz ritz = ritz_extract(0.0);
+  // (the convergence tolerance only sets Ritz::converged: any extract of this
+  // factorization has the values and vectors used here)
+  Ritz own;
+  if (!current || current->j != j) own = ritz_extract(0.0);
+  const Ritz& ritz = (current && current->j == j) ? *current : own;
   std::vector<double> rho((size_t)keep);
   for (int64_t i = 0; i < keep; ++i) {
     double acc = 0.0;
@@ -830,10 +1094,54 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
     return true;
   };
 
+  // Device-controlled steps (one read-back per restart cycle) unless
+  // GKB_HOST_STEP=1; without restarts the convergence test reads B after every
+  // step, so that mode uses them only while the factorization is small.
+  bool dev_steps = o.thick || cap <= 128;
+  if (const char* e = getenv("GKB_HOST_STEP"))
+    if (e[0] == '1') dev_steps = false;
   while (true) {
     if (f.steps() >= minmn) break;  // factorization complete
     if (mvps + 2 > o.max_mvps) break;
     if (f.right_exhausted()) break;
+    if (dev_steps) {
+      // steps until the next host decision: the restart point (thick) or the
+      // per-step convergence test; never past the mvp budget
+      int64_t nmax = o.thick ? o.max_subspace - f.steps() : 1;
+      nmax = std::min(nmax, minmn - f.steps());
+      nmax = std::min(nmax, (o.max_mvps - mvps) / 2);
+      nmax = std::max<int64_t>(nmax, 1);
+      const Lanczos::DevRun r = f.run_dev(o, nmax, &norm_scale);
+      mvps += 2 * r.completed + (r.status == 1 ? 1 : 0);
+      out.steps += r.completed;
+      out.reorth_count += (int)r.reorth;
+      if (r.completed > (r.status == 2 ? 1 : 0)) consecutive_breakdowns = 0;
+      if (r.status == 1) {  // as below: alpha breakdown
+        ++out.deflations;
+        ++consecutive_breakdowns;
+        f.compress_exhausted();
+        extract();
+        if (top_k_converged() || consecutive_breakdowns > 3) break;
+        f.deflate_right();
+        continue;
+      }
+      if (r.status == 2) {  // beta breakdown: step() deflates before returning
+        ++out.deflations;
+        ++consecutive_breakdowns;
+        f.deflate_right();
+      }
+      if (!o.thick) {
+        extract();
+        if (top_k_converged()) break;
+      } else if (f.steps() == o.max_subspace) {
+        extract();
+        if (top_k_converged()) break;
+        if (mvps + 2 > o.max_mvps) break;
+        f.thick_restart(o.keep, &ritz);
+        ++out.restarts;
+      }
+      continue;
+    }
     const StepInfo step = f.step(o, norm_scale, &mvps);
     if (step.status == 1) {
       ++out.deflations;
@@ -861,7 +1169,7 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
       extract();
       if (top_k_converged()) break;
       if (mvps + 2 > o.max_mvps) break;
-      f.thick_restart(o.keep);
+      f.thick_restart(o.keep, &ritz);
       ++out.restarts;
     }
   }

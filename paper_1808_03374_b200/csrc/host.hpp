@@ -219,7 +219,8 @@ class Lanczos {
   bool right_exhausted() const { return right_exhausted_; }
   StepInfo step(const Options& o, double norm_scale, int64_t* mvp_counter);
   Ritz ritz_extract(double tol) const;
-  void thick_restart(int64_t keep);
+  // `current`: ritz_extract of the present factorization if the caller has it
+  void thick_restart(int64_t keep, const Ritz* current = nullptr);
   void compress_exhausted();
   void deflate_right();
   // downloads (host arrays sized by the caller)
@@ -227,6 +228,16 @@ class Lanczos {
   // out_U (m x kc) = U[:, :j] W_L[:, :kc], out_V (n x kc) = V[:, :j] W_R[:, :kc]
   void ritz_vectors(const Ritz& r, int64_t kc, double* outU, double* outV);
   double cgs2_right_host(int64_t ncols);  // test hook
+  // Device-controlled steps (ctl_kernels.cu): enqueues up to `nsteps` steps
+  // with every decision taken on the device, then one read-back. Stops at the
+  // first breakdown (status 1 / 2 as in StepInfo); the host then handles it
+  // as after step(). norm_scale is read and updated (svdl's running value).
+  struct DevRun {
+    int64_t completed = 0;  // steps with status 0 or 2
+    int status = 0;
+    int64_t reorth = 0;
+  };
+  DevRun run_dev(const Options& o, int64_t nsteps, double* norm_scale);
   int64_t host_syncs = 0;
   int64_t spec_hits = 0, spec_misses = 0;  // speculative right half-steps kept / not launched or redone
   Rng rng;
@@ -269,6 +280,17 @@ class Lanczos {
   int64_t ring_cap_ = 0;
   int ring_next_ = 0;
   void host_to_all(const double* h, int64_t count, std::vector<double*>& dst);
+  // device step control state (one replica per shard) and pinned staging
+  dev::ctl::Layout ctl_L_{};
+  std::vector<void*> ctl_d_;
+  void* ctl_up_ = nullptr;
+  void* ctl_down_ = nullptr;
+  double* cd(int i) const { return reinterpret_cast<double*>(ctl_d_[i]); }
+  int* ci(int i) const { return reinterpret_cast<int*>(cd(i) + ctl_L_.nd); }
+  void enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t hi);
+  void cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec, int gate_slot,
+                const Options& o, int64_t s);
+  dev::ctl::Params ctl_params(const Options& o, int op, int64_t s) const;
 };
 
 struct SvdlOutput {

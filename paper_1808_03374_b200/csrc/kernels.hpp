@@ -93,26 +93,33 @@ void k1_main_only(const GenoView& g, const double* x, cudaStream_t s);
 void k2_main_only(const GenoView& g, cudaStream_t s);
 
 // ---- dense fp64 basis / operator kernels (K3-K6) -------------------------
-// Reduction scratch: partial[nblk * K] plus the result buffer.
+// Reduction scratch: per-CTA partials and the last-CTA ticket of the
+// single-launch reductions (one reduction in flight per stream).
 struct RedScratch {
   double* partial;
   int64_t cap;  // doubles
+  unsigned* ticket = nullptr;
 };
-int64_t red_blocks(int64_t len);
+int64_t red_blocks(int64_t len);  // CTAs of a reduction over len rows (partials per column)
+void init_red_scratch(RedScratch& rs);  // allocates the zeroed ticket
 
 // out[0..ncols) = Q[:, c0:c0+ncols]^T v ; out[ncols] = ||v||^2 (if with_norm)
 void gemv_t(const double* Q, int64_t ld, int64_t len, int64_t ncols, const double* v, bool with_norm,
-            RedScratch& rs, double* out, cudaStream_t s);
+            RedScratch& rs, double* out, cudaStream_t s, const int* gate = nullptr);
 // v = beta*v - Q c (c on device, ncols) ; if norms: out[0] = ||v_before||^2, out[1] = ||v_after||^2
 // (beta applies to v before the subtraction; used for dense apply with beta = 0 -> y = -Qc).
 void gemv_n(const double* Q, int64_t ld, int64_t len, int64_t ncols, const double* c, double* v,
-            double beta, double sign, bool norms, RedScratch& rs, double* out, cudaStream_t s);
+            double beta, double sign, bool norms, RedScratch& rs, double* out, cudaStream_t s,
+            const int* gate = nullptr);
 // out[0] = sum a*b ; (dot into device scalar)
-void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* out, cudaStream_t s);
+void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
+         const int* gate = nullptr);
 // out[0] = ||a||^2
-void nrm2sq(const double* a, int64_t len, RedScratch& rs, double* out, cudaStream_t s);
+void nrm2sq(const double* a, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
+            const int* gate = nullptr);
 // v -= (*dptr) * u   (device scalar)
-void axpy_dev(const double* dptr, const double* u, double* v, int64_t len, cudaStream_t s);
+void axpy_dev(const double* dptr, const double* u, double* v, int64_t len, cudaStream_t s,
+              const int* gate = nullptr);
 // v = v - alpha*u, with out[0] = ||v_before||^2, out[1] = ||v_after||^2
 void axpy_norms(double alpha, const double* u, double* v, int64_t len, RedScratch& rs, double* out,
                 cudaStream_t s);
@@ -124,6 +131,13 @@ void div_copy(const double* src, double divisor, double* dst, int64_t len, cudaS
 void div_copy_dsq(const double* src, const double* nrm2, double* dst, int64_t len, cudaStream_t s);
 void axpy_norms_dsq(const double* nrm2, const double* u, double* v, int64_t len, RedScratch& rs,
                     double* out, cudaStream_t s);
+// Device-scalar variants for the device-controlled step (scalar = *alpha /
+// *divisor, no sqrt), gated: nothing happens when *gate == 0. Every kernel
+// above that takes a `gate` behaves the same way.
+void axpy_norms_dv(const double* alpha, const double* u, double* v, int64_t len, RedScratch& rs,
+                   double* out, cudaStream_t s, const int* gate);
+void div_copy_dv(const double* src, const double* divisor, double* dst, int64_t len,
+                 cudaStream_t s, const int* gate);
 // dst[:, 0:kc] = Q[:, 0:j] * W (W is j x kc, ldw rows, on device); dst may not alias Q
 void gemm_small(const double* Q, int64_t ld, int64_t len, int64_t j, const double* W, int64_t ldw,
                 int64_t kc, double* dst, int64_t ldd, cudaStream_t s);
@@ -131,6 +145,54 @@ void gemm_small(const double* Q, int64_t ld, int64_t len, int64_t j, const doubl
 void sum_buffers(const double* const* srcs, int nsrc, double* dst, int64_t len, cudaStream_t s);
 // L2 flush: write `bytes` of scratch
 void flush_l2(void* buf, size_t bytes, cudaStream_t s);
+
+// ---- device-side step control (ctl_kernels.cu) ----------------------------
+// Per shard: one double area (B, couplings, omega rows, scalars, reduction
+// results) and one int area (gates, status, counters), identical replicas on
+// every shard. Gates are read by the gated kernels above.
+namespace ctl {
+enum : int {  // int slots
+  I_ALIVE = 0,   // 0 after a breakdown: every later gated kernel does nothing
+  I_STATUS,      // 0, or the StepInfo status of the step that halted the run
+  I_J,           // factorization size
+  I_STEPS,       // completed steps (status 0 or 2)
+  I_REORTH,      // partial-mode reorthogonalizations (both sides)
+  I_G2P,         // local second pass on
+  I_GRE,         // reorthogonalize (cgs2 pass 1) on
+  I_GRE2,        // cgs2 second pass on
+  I_RPEND,       // reorthogonalizations of the current step (committed with the step)
+  I_G2PC         // + c: second-pass term c on (cap entries)
+};
+enum : int { S_NS = 0, S_ALPHA, S_BETA, S_ACAND, S_BCAND, S_NAFTER, S_COUNT = 16 };  // scalars
+enum : int { R_N = 0, R_DOT = 8, R_CG = 16 };  // result slots: norm pair, dot, cgs2 coefficients
+struct Layout {  // offsets in doubles
+  int64_t cap, B, coup, mu, nu, mun, nun, sc, res, nd, ni;
+  size_t bytes;
+};
+__host__ __device__ inline Layout layout(int64_t cap) {
+  Layout L;
+  L.cap = cap;
+  L.B = 0;
+  L.coup = L.B + cap * cap;
+  L.mu = L.coup + cap;
+  L.nu = L.mu + cap + 2;
+  L.mun = L.nu + cap + 1;
+  L.nun = L.mun + cap + 2;
+  L.sc = L.nun + cap + 1;
+  L.res = L.sc + S_COUNT;
+  L.nd = L.res + 3 * cap + 32;
+  L.ni = I_G2PC + cap;
+  L.bytes = sizeof(double) * (size_t)L.nd + sizeof(int) * (size_t)L.ni;
+  return L;
+}
+enum Op { OP_L_A, OP_L_B, OP_CG_MID, OP_CG_END, OP_L_END, OP_R_A, OP_R_B, OP_R_END, OP_SQRT_L };
+struct Params {
+  int op, side, full, nidx, has_pattern, omega_rec, one_sided;
+  int64_t s, ncols, lo, hi, m, n, cap;
+  double omega, lvl, bfac, guard, eta, eps;
+};
+void launch(double* d, int* iv, const Params& p, cudaStream_t st);
+}  // namespace ctl
 
 // ---- synthetic generator ------------------------------------------------
 struct SynthDev {

@@ -16,22 +16,39 @@ namespace gkb {
 
 namespace {
 
+// x.y with four interleaved partial sums (short dependency chains; fixed order)
+inline double dot4(const double* x, const double* y, int64_t r) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t i = 0;
+  for (; i + 4 <= r; i += 4) {
+    s0 += x[i] * y[i];
+    s1 += x[i + 1] * y[i + 1];
+    s2 += x[i + 2] * y[i + 2];
+    s3 += x[i + 3] * y[i + 3];
+  }
+  for (; i < r; ++i) s0 += x[i] * y[i];
+  return (s0 + s1) + (s2 + s3);
+}
+
 // A (r x c, r >= c) -> U (r x c), s (c), V (c x c)
 void jacobi_tall(const double* M, int64_t r, int64_t c, double* U, double* s, double* V) {
   std::vector<double> A(M, M + r * c), R((size_t)(c * c), 0.0);
   for (int64_t i = 0; i < c; ++i) R[i + i * c] = 1.0;
+  // column norms: recomputed at the start of every sweep, updated exactly as
+  // the rotation changes them in between (a_p.a_p - t g, a_q.a_q + t g)
+  std::vector<double> nrm((size_t)c);
   for (int sweep = 0; sweep < 80; ++sweep) {
+    for (int64_t p = 0; p < c; ++p) {
+      const double* ap = A.data() + p * r;
+      nrm[p] = dot4(ap, ap, r);
+    }
     bool rotated = false;
     for (int64_t p = 0; p + 1 < c; ++p) {
+      double* ap = A.data() + p * r;
       for (int64_t q = p + 1; q < c; ++q) {
-        double* ap = A.data() + p * r;
         double* aq = A.data() + q * r;
-        double alpha = 0.0, beta = 0.0, gamma = 0.0;
-        for (int64_t i = 0; i < r; ++i) {
-          alpha += ap[i] * ap[i];
-          beta += aq[i] * aq[i];
-          gamma += ap[i] * aq[i];
-        }
+        const double gamma = dot4(ap, aq, r);
+        const double alpha = nrm[p], beta = nrm[q];
         if (gamma == 0.0 || std::fabs(gamma) <= DBL_EPSILON * std::sqrt(alpha) * std::sqrt(beta))
           continue;
         rotated = true;
@@ -44,6 +61,8 @@ void jacobi_tall(const double* M, int64_t r, int64_t c, double* U, double* s, do
           ap[i] = cs * x - sn * y;
           aq[i] = sn * x + cs * y;
         }
+        nrm[p] = alpha - t * gamma;
+        nrm[q] = beta + t * gamma;
         double* rp = R.data() + p * c;
         double* rq = R.data() + q * c;
         for (int64_t i = 0; i < c; ++i) {

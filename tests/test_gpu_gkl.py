@@ -267,6 +267,7 @@ def test_speculative_right_half_is_bitwise_sequential(gkb, orc, monkeypatch, cfg
     spec = synth.config_spec(cfg, scale=scale)
     opts = synth.config_options(cfg)
     op, _ = _geno_pair(gkb, orc, spec, nshards=nshards)
+    monkeypatch.setenv("GKB_HOST_STEP", "1")  # speculation lives in the host-driven step
     monkeypatch.setenv("GKB_NO_SPECULATE", "1")
     a = gkb.svdl(op, opts)
     monkeypatch.delenv("GKB_NO_SPECULATE")
@@ -276,3 +277,67 @@ def test_speculative_right_half_is_bitwise_sequential(gkb, orc, monkeypatch, cfg
     assert np.array_equal(a.err_estimates, b.err_estimates)
     for f in ("mvps", "steps", "restarts", "reorth_count", "deflations"):
         assert getattr(a.stats, f) == getattr(b.stats, f), f
+
+
+def _same_solve(a, b):
+    # equal_nan: the literal left recurrence (omega_recurrence=0, a documented
+    # defect of the reference) can lose orthogonality completely -- both paths
+    # must then fail identically
+    eq = lambda x, y: np.array_equal(x, y, equal_nan=True)  # noqa: E731
+    assert eq(a.singvals, b.singvals)
+    assert eq(a.U, b.U) and eq(a.V, b.V)
+    assert eq(a.err_estimates, b.err_estimates)
+    for f in ("mvps", "steps", "restarts", "reorth_count", "deflations"):
+        assert getattr(a.stats, f) == getattr(b.stats, f), f
+
+
+def _opts_variants(gkb, base):
+    """Reorth / restart / one-sided / omega-recurrence variants of `base`."""
+    import dataclasses
+    R, T = gkb.ReorthMode, gkb.RestartMode
+    return [
+        base,
+        dataclasses.replace(base, reorth=R.kFull),
+        dataclasses.replace(base, one_sided=True),
+        dataclasses.replace(base, omega_recurrence=0),
+        dataclasses.replace(base, omega=1e-4),
+        dataclasses.replace(base, restart=T.kNone, max_mvps=120),
+    ]
+
+
+@pytest.mark.parametrize("cfg,scale,nshards", [(2, 0.05, 1), (3, 0.01, 2), (1, 0.1, 1)])
+def test_device_step_control_is_bitwise_host_step(gkb, orc, monkeypatch, cfg, scale, nshards):
+    """The device-controlled steps (decisions taken by ctl kernels, one
+    read-back per restart cycle) must reproduce the host-driven step
+    (GKB_HOST_STEP=1) bit for bit: same decisions, same kernels, same counts."""
+    from paper_1808_03374_b200 import synth
+    spec = synth.config_spec(cfg, scale=scale)
+    op, _ = _geno_pair(gkb, orc, spec, nshards=nshards)
+    for opts in _opts_variants(gkb, synth.config_options(cfg)):
+        monkeypatch.setenv("GKB_HOST_STEP", "1")
+        a = gkb.svdl(op, opts)
+        monkeypatch.delenv("GKB_HOST_STEP")
+        b = gkb.svdl(op, opts)
+        _same_solve(a, b)
+        if opts.restart == gkb.RestartMode.kThick:
+            assert b.stats.host_syncs < a.stats.host_syncs
+
+
+def test_device_step_control_breakdowns(gkb, monkeypatch):
+    """Low-rank dense operators force alpha / beta breakdowns (deflation,
+    compress_exhausted) inside device runs: the host must take over exactly
+    where the host-driven step would."""
+    import dataclasses
+    rng = np.random.default_rng(11)
+    for (m, n, r) in [(60, 40, 3), (40, 60, 5), (50, 50, 1)]:
+        X = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+        op = gkb.DenseOperator(X)
+        base = gkb.GklOptions(k=min(r + 2, 8), restart=gkb.RestartMode.kThick,
+                              max_subspace=20, keep=min(r + 2, 8) + 2, tol=1e-10)
+        for opts in _opts_variants(gkb, base):
+            opts = dataclasses.replace(opts, max_mvps=400)
+            monkeypatch.setenv("GKB_HOST_STEP", "1")
+            a = gkb.svdl(op, opts)
+            monkeypatch.delenv("GKB_HOST_STEP")
+            b = gkb.svdl(op, opts)
+            _same_solve(a, b)

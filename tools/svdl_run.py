@@ -21,5 +21,5 @@ t0 = time.perf_counter()
 res = gkb.svdl(op, opts)
 wall = time.perf_counter() - t0
 s = res.stats
-print(f"config {cfg}: wall {wall:.4f} s, device {s.device_seconds:.4f} s, mvps {s.mvps}, steps "
+print(f"config {cfg}: wall {wall:.4f} s (C {s.wall_seconds:.4f}), device {s.device_seconds:.4f} s, mvps {s.mvps}, steps "
       f"{s.steps}, restarts {s.restarts}, reorth {s.reorth_count}, host_syncs {s.host_syncs}")
