@@ -448,8 +448,8 @@ int gkb_svdl(gkb_op* op, const gkb_gkl_options* o, gkb_svdl_result** res) {
       return p;
     };
     r->singvals = dup(out.singvals);
-    r->U = dup(out.U);
-    r->V = dup(out.V);
+    r->U = out.U.release();  // new[] -> delete[] in gkb_svdl_result_free
+    r->V = out.V.release();
     r->err_estimates = dup(out.err);
     r->converged = new int32_t[out.converged.size() > 0 ? out.converged.size() : 1];
     std::copy(out.converged.begin(), out.converged.end(), r->converged);

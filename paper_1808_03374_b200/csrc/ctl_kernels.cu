@@ -30,6 +30,8 @@ namespace ctl {
 namespace {
 
 constexpr int kCtlThreads = 128;
+constexpr int64_t kStageJ = 64;  // factorizations up to this size staged in shared memory
+constexpr size_t kStageBytes = sizeof(double) * (size_t)(kStageJ * kStageJ + 3 * (kStageJ + 2));
 
 // std::min(1.0, x) / std::max(a, b) exactly as <algorithm> defines them
 __device__ __forceinline__ double min_1(double x) { return (x < 1.0) ? x : 1.0; }
@@ -105,31 +107,56 @@ __global__ void __launch_bounds__(kCtlThreads) k_ctl(double* __restrict__ d, int
         if (left) sc[S_ACAND] = c; else sc[S_BCAND] = c;
         cand = c;
       }
-      __syncthreads();
       const int64_t j = left ? p.s : p.s + 1;  // factorization size at this half-step
+      // The recurrences read the leading j x j block of B and the level rows:
+      // staged in shared memory (one coalesced pass) when they fit, so the
+      // per-i sequential sums below run at shared-memory latency.
+      extern __shared__ double stg[];
+      const bool staged = j <= kStageJ;
+      const double* Bs = B;
+      int64_t lds = cap;
+      const double *mus = mu, *nus = nu, *cps = coup;
+      if (staged) {
+        double* sB = stg;
+        double* smu = sB + kStageJ * kStageJ;
+        double* snu = smu + kStageJ + 2;
+        double* scp = snu + kStageJ + 2;
+        for (int64_t e = t; e < j * j; e += blockDim.x) sB[e] = B[(e % j) + (e / j) * cap];
+        for (int64_t e = t; e <= j; e += blockDim.x) {
+          smu[e] = mu[e];
+          snu[e] = nu[e];
+          scp[e] = e < cap ? coup[e] : 0.0;
+        }
+        Bs = sB;
+        lds = j;
+        mus = smu;
+        nus = snu;
+        cps = scp;
+      }
+      __syncthreads();
       const double denom = max_ab(cand, tau + p.eps);
       double worst = 0.0;
       if (left) {
         for (int64_t i = t; i < j; i += blockDim.x) {
           double acc = 0.0;
-          for (int64_t c = i; c < j; ++c) acc += fabs(B[i + c * cap]) * mu[c];
+          for (int64_t c = i; c < j; ++c) acc += fabs(Bs[i + c * lds]) * mus[c];
           if (p.omega_rec == 1)
             for (int64_t c = 0; c < j; ++c)
-              if (c != i && coup[c] != 0.0) acc += fabs(coup[c]) * nu[c < i ? c : i];
+              if (c != i && cps[c] != 0.0) acc += fabs(cps[c]) * nus[c < i ? c : i];
           const double est = min_1((acc + tau) / denom);
           nun[i] = est;
           worst = max_ab(worst, est);
         }
         if (t == 0) nun[j] = 1.0;
       } else {
-        const double alpha_last = B[(j - 1) + (j - 1) * cap];
+        const double alpha_last = Bs[(j - 1) + (j - 1) * lds];
         for (int64_t i = t; i < j; i += blockDim.x) {
           double acc = 0.0;
           if (i == j - 1) {
-            for (int64_t r = 0; r + 1 < j; ++r) acc += fabs(B[r + i * cap]) * nu[r];
+            for (int64_t r = 0; r + 1 < j; ++r) acc += fabs(Bs[r + i * lds]) * nus[r];
           } else {
-            for (int64_t r = 0; r <= i; ++r) acc += fabs(B[r + i * cap]) * nu[r];
-            acc += alpha_last * mu[i];
+            for (int64_t r = 0; r <= i; ++r) acc += fabs(Bs[r + i * lds]) * nus[r];
+            acc += alpha_last * mus[i];
           }
           const double est = min_1((acc + tau) / denom);
           mun[i] = est;
@@ -250,7 +277,7 @@ __global__ void __launch_bounds__(kCtlThreads) k_ctl(double* __restrict__ d, int
 }  // namespace
 
 void launch(double* d, int* iv, const Params& p, cudaStream_t st) {
-  launch_pdl(k_ctl, dim3(1), dim3(kCtlThreads), 0, st, true, d, iv, p);
+  launch_pdl(k_ctl, dim3(1), dim3(kCtlThreads), kStageBytes, st, true, d, iv, p);
 }
 
 }  // namespace ctl

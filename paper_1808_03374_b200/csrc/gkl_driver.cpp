@@ -1181,10 +1181,10 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
   out.singvals.assign(ritz.values.begin(), ritz.values.begin() + count);
   out.err.assign(ritz.err.begin(), ritz.err.begin() + count);
   out.converged.assign(ritz.converged.begin(), ritz.converged.begin() + count);
-  out.U.assign((size_t)(m * count), 0.0);
-  out.V.assign((size_t)(n * count), 0.0);
+  out.U.reset(new double[(size_t)std::max<int64_t>(m * count, 1)]);
+  out.V.reset(new double[(size_t)std::max<int64_t>(n * count, 1)]);
   // Ritz vectors U W_L, V W_R, returned as-is (gkl.cpp:500-507).
-  f.ritz_vectors(ritz, count, out.U.data(), out.V.data());
+  f.ritz_vectors(ritz, count, out.U.get(), out.V.get());
   out.all_converged = count == o.k && top_k_converged();
   out.mvps = mvps;
   ctx->set_device(0);

@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <memory>
 #include <cmath>
 #include <random>
 #include <string>
@@ -294,7 +295,10 @@ class Lanczos {
 };
 
 struct SvdlOutput {
-  std::vector<double> singvals, U, V, err;
+  std::vector<double> singvals, err;
+  // Ritz vectors, column-major m x count / n x count (new[]: handed to the C
+  // ABI result as they are, no copy or zero fill)
+  std::unique_ptr<double[]> U, V;
   std::vector<int32_t> converged;
   int64_t count = 0, mvps = 0, steps = 0;
   int restarts = 0, reorth_count = 0, deflations = 0;

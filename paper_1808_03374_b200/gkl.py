@@ -411,8 +411,13 @@ def svdl(op: LinearOperator, opts: GklOptions) -> SvdlResult:
             return np.ctypeslib.as_array(p, shape=(k,)).copy() if k > 0 else np.zeros(0)
 
         singvals = arr(r.singvals, cnt)
-        U = arr(r.U, m * cnt).reshape((cnt, m)).T.copy() if cnt else np.zeros((m, 0))
-        V = arr(r.V, n * cnt).reshape((cnt, n)).T.copy() if cnt else np.zeros((n, 0))
+        def cols(p, rows):  # column-major rows x cnt: one copy, Fortran order
+            if not cnt:
+                return np.zeros((rows, 0))
+            return np.ctypeslib.as_array(p, shape=(cnt, rows)).T.copy(order="F")
+
+        U = cols(r.U, m)
+        V = cols(r.V, n)
         err = arr(r.err_estimates, cnt)
         conv = (np.ctypeslib.as_array(r.converged, shape=(cnt,)).astype(bool).copy()
                 if cnt else np.zeros(0, dtype=bool))
