@@ -1,7 +1,10 @@
 """Command-line front end of the hot path: the reference's ``gkpca pca``
-(/root/reference/proj/tools/gkpca.cpp:170-308, options :706-736), run on the
-B200 operator and driver.
+(/root/reference/proj/tools/gkpca.cpp:170-308, options :706-736), ``bench``
+(:384-536, options :757-780) and ``regress`` (:554-682), run on the B200
+operator and driver.
 
+    python -m paper_1808_03374_b200.cli bench INPUT --seed S [--algos LIST] [-k K] [--tol T]
+        [--max-mvps N] [--max-iters N] [--oracle-cap C] [--standardize ...] [--out DIR]
     python -m paper_1808_03374_b200.cli regress INPUT --pheno CSV [--design CSV] [-k K] ...
     python -m paper_1808_03374_b200.cli pca INPUT [--algo gkl] [-k K] [--tol T]
         [--max-mvps N] [--seed S] [--standardize none|unit|binomial|hwe]
@@ -159,6 +162,87 @@ def run_pca(a) -> int:
     return EXIT_OK
 
 
+BENCH_ALGOS = ("gkl-pro-nr", "gkl-fro-nr", "gkl-pro-tr", "gkl-fro-tr", "subspace-qr",
+               "subspace-normalize")
+
+
+def _g17(x: float) -> str:  # std::snprintf("%.17g")
+    return "%.17g" % x
+
+
+def run_bench(a) -> int:
+    """run_bench (gkpca.cpp:424-536): every listed solver on the same operator,
+    mvps checked against the operator's own product counter, errors against a
+    dense SVD when min(m, n) <= --oracle-cap; bench.csv + manifest.json."""
+    import time
+    from .gkl import GklOptions, ReorthMode, RestartMode, svdl
+    from .subspace import SubspaceVariant, subspace_iterate
+    algos = [t for t in a.algos.split(",") if t]  # split_csv_list (:400-413)
+    op = load_operator(a.input, a.standardize)
+    k = int(a.k)
+    if not algos:
+        raise ValueError("bench: --algos list is empty")
+    for name in algos:
+        if name not in BENCH_ALGOS:
+            raise ValueError(f"bench: unknown algorithm '{name}'")
+    m, n = op.rows(), op.cols()
+    minmn = min(m, n)
+    oracle = None
+    if minmn <= int(a.oracle_cap):
+        # the dense matrix the operator applies, through the operator itself
+        M = op.apply_block(np.eye(n))
+        oracle = np.linalg.svd(M, compute_uv=False)[:min(k, minmn)]
+    else:
+        sys.stderr.write(f"gkpca bench: dense oracle skipped (min dimension {minmn} > cap "
+                         f"{a.oracle_cap}); error columns left as nan\n")
+    rows = []
+    for name in algos:
+        before = op.mvps()
+        if name.startswith("gkl"):
+            o = GklOptions(k=k, tol=float(a.tol), max_mvps=int(a.max_mvps), seed=int(a.seed))
+            o.reorth = ReorthMode.kFull if "fro" in name else ReorthMode.kPartial
+            if "-tr" in name:
+                o.restart = RestartMode.kThick
+                o.max_subspace = min(max(2 * k, 20), minmn)
+                o.keep = max(k, o.max_subspace // 2)
+            r = svdl(op, o)
+            vals, reported, seconds = r.singvals, r.stats.mvps, r.stats.wall_seconds
+        else:
+            variant = (SubspaceVariant.kNormalize if name == "subspace-normalize"
+                       else SubspaceVariant.kQr)
+            t0 = time.perf_counter()
+            r = subspace_iterate(op, k, variant, float(a.tol), int(a.max_iters), int(a.seed))
+            seconds = time.perf_counter() - t0
+            vals, reported = r.singvals, r.mvps
+        counted = op.mvps() - before
+        if reported != counted:
+            raise RuntimeError("bench: solver mvp count disagrees with the operator counter")
+        l1 = rel = float("nan")
+        if oracle is not None:
+            c = min(vals.size, oracle.size)
+            l1 = float(np.sum(np.abs(vals[:c] - oracle[:c])))
+            if vals.size >= k and oracle.size >= k and oracle[k - 1] > 0.0:
+                rel = float(abs(vals[k - 1] - oracle[k - 1]) / oracle[k - 1])
+        rows.append((name, counted, seconds, l1, rel))
+    os.makedirs(a.out, exist_ok=True)
+    path = os.path.join(a.out, "bench.csv")
+    from ._lib import FormatError
+    try:
+        f = open(path, "w")
+    except OSError as e:
+        raise FormatError(f"cannot open {path} for writing") from e
+    with f:
+        f.write("algorithm,mvps,seconds,l1_err,rel_err_k\n")
+        for name, mv, sec, l1, rel in rows:
+            f.write(f"{name},{mv},{_g17(sec)},{_g17(l1)},{_g17(rel)}\n")
+    config = {"input": a.input, "algos": a.algos, "k": a.k, "tol": a.tol,
+              "max_mvps": a.max_mvps, "max_iters": a.max_iters, "oracle_cap": a.oracle_cap,
+              "standardize": a.standardize}
+    _write_json(os.path.join(a.out, "manifest.json"),
+                {"command": "bench", "config": config, "seed": a.seed, "versions": _versions()})
+    return EXIT_OK
+
+
 def run_regress(a) -> int:
     """run_regress (gkpca.cpp:554-680): PC-adjusted regression of a phenotype
     on every marker (device scan) or on a joint design."""
@@ -241,6 +325,17 @@ def build_parser() -> argparse.ArgumentParser:
     c.add_argument("--keep", type=int, default=0)
     c.add_argument("--variant", default="qr", choices=["qr", "normalize"])
     c.add_argument("--max-iters", dest="max_iters", type=int, default=1000)
+    b = sub.add_parser("bench", help="Compare solvers on one operator with shared mvp counting")
+    b.add_argument("input", help="Input matrix (.gmx or .bed)")
+    b.add_argument("--algos", default="gkl-pro-nr,gkl-fro-nr,gkl-fro-tr,subspace-qr")
+    b.add_argument("-k", "--k", type=int, default=10)
+    b.add_argument("--tol", type=float, default=1e-8)
+    b.add_argument("--max-mvps", dest="max_mvps", type=int, default=1000000)
+    b.add_argument("--max-iters", dest="max_iters", type=int, default=1000)
+    b.add_argument("--oracle-cap", dest="oracle_cap", type=int, default=2000)
+    b.add_argument("--seed", type=int, required=True)
+    b.add_argument("--standardize", default="none", choices=["none", "unit", "binomial", "hwe"])
+    b.add_argument("--out", default=".")
     r = sub.add_parser("regress", help="Per-marker regression with PC adjustment")
     r.add_argument("input", help="Genotype matrix (.gmx or .bed)")
     r.add_argument("--pheno", required=True, help="Phenotype CSV (one column, one row per sample)")
@@ -268,6 +363,8 @@ def main(argv: Optional[List[str]] = None) -> int:
     try:
         if a.command == "pca":
             return run_pca(a)
+        if a.command == "bench":
+            return run_bench(a)
         if a.command == "regress":
             return run_regress(a)
     except FormatError as e:

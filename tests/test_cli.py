@@ -230,3 +230,42 @@ def test_regress_end_to_end(gkb, tmp_path, k):
     fit = json.loads((out2 / "regression.json").read_text())["fit"]
     ref = R.pc_adjusted_fit(Xd, Z, y) if k else R.ols_fit(Xd, y)
     assert np.allclose(fit["beta"], ref.beta_hat, rtol=1e-8, atol=1e-12)
+
+
+# ---------------------------------------------------------------- bench
+def test_bench_usage_exit_4(tmp_path, capsys):
+    assert run(["bench", "x.bed"]) == 4                         # --seed is required
+    assert run(["bench", "x.bed", "--seed", "1", "--standardize", "bogus"]) == 4
+
+
+@pytest.mark.gpu
+def test_bench_end_to_end(gkb, tmp_path, capsys):
+    """gkpca bench (gkpca.cpp:424-536): every solver on one operator, mvps
+    equal to the operator's own counter, errors against the dense SVD."""
+    pre, _ = _bed(tmp_path, 150, 100, seed=3)
+    out = tmp_path / "b"
+    algos = ",".join(["gkl-pro-nr", "gkl-fro-nr", "gkl-pro-tr", "gkl-fro-tr", "subspace-qr",
+                      "subspace-normalize"])
+    assert run(["bench", pre + ".bed", "--seed", "5", "-k", "4", "--tol", "1e-10",
+                "--algos", algos, "--standardize", "unit", "--out", str(out)]) == 0
+    lines = (out / "bench.csv").read_text().splitlines()
+    assert lines[0] == "algorithm,mvps,seconds,l1_err,rel_err_k"
+    rows = [ln.split(",") for ln in lines[1:]]
+    assert [r[0] for r in rows] == algos.split(",")
+    for name, mv, sec, l1, rel in rows:
+        assert int(mv) > 0 and float(sec) > 0.0
+        assert np.isfinite(float(l1)) and np.isfinite(float(rel))
+        if name == "subspace-normalize":  # the paper's naive variant: no re-orthogonalization,
+            continue                      # trailing values collapse onto the leading one
+        tol = 1e-8 if name.startswith("gkl") else 1e-4
+        assert float(l1) < tol and float(rel) < tol, (name, l1, rel)
+    man = json.loads((out / "manifest.json").read_text())
+    assert man["command"] == "bench" and man["seed"] == 5 and man["config"]["k"] == 4
+    # above the oracle cap the error columns are nan and a note goes to stderr
+    assert run(["bench", pre + ".bed", "--seed", "5", "-k", "3", "--algos", "gkl-pro-nr",
+                "--oracle-cap", "10", "--out", str(out)]) == 0
+    assert "dense oracle skipped" in capsys.readouterr().err
+    row = (out / "bench.csv").read_text().splitlines()[1].split(",")
+    assert row[3] == "nan" and row[4] == "nan"
+    assert run(["bench", pre + ".bed", "--seed", "5", "--algos", "gkl-xx", "--out",
+                str(out)]) == 4
