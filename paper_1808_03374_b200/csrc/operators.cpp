@@ -243,9 +243,12 @@ static int64_t build_block_lists(const uint32_t* lay, const dev::PMPlan& pl, cud
   const int64_t nblk = pl.grid_x * pl.nkc;
   uint32_t* cnt = nullptr;
   int64_t* tot = nullptr;
-  GKB_CUDA(cudaMalloc(&cnt, sizeof(uint32_t) * (size_t)(nblk * span)));
-  GKB_CUDA(cudaMalloc(&tot, sizeof(int64_t) * (size_t)nblk));
-  GKB_CUDA(cudaMalloc(off, sizeof(uint32_t) * (size_t)(nblk * (span + 1))));
+  auto pool = [&](auto** ptr, size_t bytes) {  // stream-ordered (no device sync)
+    GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, st));
+  };
+  pool(&cnt, sizeof(uint32_t) * (size_t)(nblk * span));
+  pool(&tot, sizeof(int64_t) * (size_t)nblk);
+  pool(off, sizeof(uint32_t) * (size_t)(nblk * (span + 1)));
   dev::miss_lists(lay, pl, false, cnt, nullptr, nullptr, nullptr, st);
   GKB_LAUNCH_CHECK();
   dev::block_scan(cnt, nblk, span, *off, tot, st);
@@ -253,17 +256,18 @@ static int64_t build_block_lists(const uint32_t* lay, const dev::PMPlan& pl, cud
   std::vector<int64_t> h((size_t)nblk);
   GKB_CUDA(cudaMemcpyAsync(h.data(), tot, sizeof(int64_t) * (size_t)nblk, cudaMemcpyDeviceToHost, st));
   GKB_CUDA(cudaStreamSynchronize(st));
-  cudaFree(cnt);
-  cudaFree(tot);
+  cudaFreeAsync(cnt, st);
+  cudaFreeAsync(tot, st);
   int64_t total = 0;
   for (int64_t bb = 0; bb < nblk; ++bb) {
     const int64_t c = h[bb];
     h[bb] = total;
     total += c;
   }
-  GKB_CUDA(cudaMalloc(base, sizeof(int64_t) * (size_t)nblk));
-  GKB_CUDA(cudaMemcpy(*base, h.data(), sizeof(int64_t) * (size_t)nblk, cudaMemcpyHostToDevice));
-  GKB_CUDA(cudaMalloc(ent, sizeof(uint16_t) * (size_t)std::max<int64_t>(total, 1)));
+  pool(base, sizeof(int64_t) * (size_t)nblk);
+  GKB_CUDA(cudaMemcpyAsync(*base, h.data(), sizeof(int64_t) * (size_t)nblk, cudaMemcpyHostToDevice,
+                           st));
+  pool(ent, sizeof(uint16_t) * (size_t)std::max<int64_t>(total, 1));
   dev::miss_lists(lay, pl, true, nullptr, *off, *base, *ent, st);
   GKB_LAUNCH_CHECK();
   *bytes += (int64_t)(sizeof(uint32_t) * nblk * (span + 1) + sizeof(int64_t) * nblk +
@@ -271,18 +275,22 @@ static int64_t build_block_lists(const uint32_t* lay, const dev::PMPlan& pl, cud
   return total;
 }
 
-static void alloc_scratch(const dev::PMPlan& pl, bool with_cm, dev::PMScratch& sc) {
-  GKB_CUDA(cudaMalloc(&sc.dig, sizeof(uint4) * (size_t)(pl.nkc * pl.kt_cta * 64)));
-  GKB_CUDA(cudaMalloc(&sc.dexp, sizeof(int) * (size_t)pl.nkc));
-  GKB_CUDA(cudaMalloc(&sc.dsum, sizeof(double) * (size_t)pl.nkc));
-  GKB_CUDA(cudaMalloc(&sc.part, sizeof(double) * (size_t)(pl.nkc * pl.rows_pad)));
-  if (with_cm) GKB_CUDA(cudaMalloc(&sc.cm, sizeof(double) * (size_t)std::max<int64_t>(pl.C, 1)));
+static void alloc_scratch(const dev::PMPlan& pl, bool with_cm, dev::PMScratch& sc,
+                          cudaStream_t st) {
+  auto pool = [&](auto** ptr, size_t bytes) {
+    GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, st));
+  };
+  pool(&sc.dig, sizeof(uint4) * (size_t)(pl.nkc * pl.kt_cta * 64));
+  pool(&sc.dexp, sizeof(int) * (size_t)pl.nkc);
+  pool(&sc.dsum, sizeof(double) * (size_t)pl.nkc);
+  pool(&sc.part, sizeof(double) * (size_t)(pl.nkc * pl.rows_pad));
+  if (with_cm) pool(&sc.cm, sizeof(double) * (size_t)std::max<int64_t>(pl.C, 1));
 }
 
-static void free_scratch(dev::PMScratch& sc) {
+static void free_scratch(dev::PMScratch& sc, cudaStream_t st) {
   void* ptrs[] = {sc.dig, sc.dexp, sc.dsum, sc.part, sc.cm};
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
   sc = dev::PMScratch{};
 }
 
@@ -316,9 +324,10 @@ GenoOp::~GenoOp() {
     void* ptrs[] = {g.mu, g.mean, g.inv_s, g.counts, g.m1_off, g.m1_base, g.m1_ent, g.m2_off,
                     g.m2_base, g.m2_ent};
     for (void* p : ptrs)
-      if (p) cudaFree(p);
-    free_scratch(g.s1);
-    free_scratch(g.s2);
+      if (p) cudaFreeAsync(p, st);
+    free_scratch(g.s1, st);
+    free_scratch(g.s2, st);
+    cudaStreamSynchronize(st);
   }
 }
 
@@ -337,13 +346,17 @@ void GenoOp::alloc_shard(int i, int64_t p_loc, int64_t nn) {
   GKB_CUDA(cudaMemsetAsync(g.lt1, 0, sizeof(uint32_t) * w1, st));
   GKB_CUDA(cudaMemsetAsync(g.lt2, 0, sizeof(uint32_t) * w2, st));
   const size_t pp = (size_t)g.pl1.rows_pad;
-  GKB_CUDA(cudaMalloc(&g.mu, sizeof(double) * pp));
-  GKB_CUDA(cudaMalloc(&g.mean, sizeof(double) * pp));
+  // everything else too: no implicit device synchronization during ingest
+  auto pool = [&](auto** ptr, size_t bytes) {
+    GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, st));
+  };
+  pool(&g.mu, sizeof(double) * pp);
+  pool(&g.mean, sizeof(double) * pp);
+  pool(&g.inv_s, sizeof(double) * pp);
   GKB_CUDA(cudaMemsetAsync(g.mean, 0, sizeof(double) * pp, st));
-  GKB_CUDA(cudaMalloc(&g.inv_s, sizeof(double) * pp));
   GKB_CUDA(cudaMemsetAsync(g.mu, 0, sizeof(double) * pp, st));
   GKB_CUDA(cudaMemsetAsync(g.inv_s, 0, sizeof(double) * pp, st));
-  GKB_CUDA(cudaMalloc(&g.counts, sizeof(int64_t) * 4 * (size_t)std::max<int64_t>(p_loc, 1)));
+  pool(&g.counts, sizeof(int64_t) * 4 * (size_t)std::max<int64_t>(p_loc, 1));
 }
 
 // Staging blocks are whole groups of 16 SNP rows (layout 2 transposes 16 at a time).
@@ -618,8 +631,9 @@ void GenoOp::finish_build() {
         const int64_t obs = c[0] + c[1] + c[2];
         mh[j] = obs > 0 ? (double)(c[1] + 2 * c[2]) / (double)obs : 0.0;
       }
-      GKB_CUDA(cudaMemcpy(g.mean, mh.data(), sizeof(double) * (size_t)g.p_loc,
-                          cudaMemcpyHostToDevice));
+      // (pageable source: staged by the call, the vector may go out of scope)
+      GKB_CUDA(cudaMemcpyAsync(g.mean, mh.data(), sizeof(double) * (size_t)g.p_loc,
+                               cudaMemcpyHostToDevice, sh.stream));
     }
     g.list_bytes = 0;
     if (g.nmissing > 0) {
@@ -629,8 +643,8 @@ void GenoOp::finish_build() {
                                            &g.m2_ent, &g.list_bytes);
       if (t1 != g.nmissing || t2 != g.nmissing) fail(GKB_ECUDA, "missing-list count mismatch");
     }
-    alloc_scratch(g.pl1, false, g.s1);
-    alloc_scratch(g.pl2, true, g.s2);
+    alloc_scratch(g.pl1, false, g.s1, sh.stream);
+    alloc_scratch(g.pl2, true, g.s2, sh.stream);
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
   }
   if (ctx->use_nccl && ctx->nshards_total > 1) {
