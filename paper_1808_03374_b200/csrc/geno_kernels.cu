@@ -341,8 +341,9 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
   const int E = block_max_int(emax, redi);
   const double s = block_sum(part, red);
   for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
-    long long M = __double2ll_rn(scalbn(vals[t], 62 - E));
     const int wc = t >> 4, k = t & 15, q = k & 3, e = k >> 2;
+    // group-q columns meet codes pre-multiplied by 4^q in the MMA (mma_tile)
+    long long M = __double2ll_rn(scalbn(vals[t], 62 - E - 2 * q));
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int d = (int)(signed char)(M & 0xFF);
@@ -370,15 +371,17 @@ __device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, 
 }
 
 // One 512-byte tile (16 rows x 128 columns) against the tile's B fragments:
-// each 32-bit word expands to four u8 registers (w >> 2q) & 0x03030303 =
-// columns 4e + q of the word, e = byte.
+// each 32-bit word gives four u8 registers w & (0x03030303 << 2q) = 4^q x the
+// codes of columns 4e + q of the word (e = byte) -- one LOP3 each, no shifts.
+// The 4^q is undone in the digits: k_digitize encodes a group-q column as
+// rn(v 2^(62-E-2q)), so every product is code x v x 2^(62-E), exactly.
 __device__ __forceinline__ void mma_tile(int (&acc)[4], const uint4 w, const uint4 b01,
                                          const uint4 b23) {
-  const uint32_t m = 0x03030303u;
-  mma_u8s8(acc, w.x & m, w.y & m, (w.x >> 2) & m, (w.y >> 2) & m, b01.x, b01.y);
-  mma_u8s8(acc, (w.x >> 4) & m, (w.y >> 4) & m, (w.x >> 6) & m, (w.y >> 6) & m, b01.z, b01.w);
-  mma_u8s8(acc, w.z & m, w.w & m, (w.z >> 2) & m, (w.w >> 2) & m, b23.x, b23.y);
-  mma_u8s8(acc, (w.z >> 4) & m, (w.w >> 4) & m, (w.z >> 6) & m, (w.w >> 6) & m, b23.z, b23.w);
+  const uint32_t m0 = 0x03030303u, m1 = m0 << 2, m2 = m0 << 4, m3 = m0 << 6;
+  mma_u8s8(acc, w.x & m0, w.y & m0, w.x & m1, w.y & m1, b01.x, b01.y);
+  mma_u8s8(acc, w.x & m2, w.y & m2, w.x & m3, w.y & m3, b01.z, b01.w);
+  mma_u8s8(acc, w.z & m0, w.w & m0, w.z & m1, w.w & m1, b23.x, b23.y);
+  mma_u8s8(acc, w.z & m2, w.w & m2, w.z & m3, w.w & m3, b23.z, b23.w);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -452,14 +455,19 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
   const int64_t col0 = kt0 * 128;
   const uint4 Z = make_uint4(0, 0, 0, 0);
   int acc[kStripsPerWarp][4];
-  uint4 buf[kDepth][kStripsPerWarp];
+  // Three register buffers per strip, rotated by the 3x unrolled main loop:
+  // tiles t and t + 1 in flight while tile t is consumed (kDepth = 2).
+  uint4 bA[kStripsPerWarp], bB[kStripsPerWarp], bC[kStripsPerWarp];
+  const uint4* nxt[kStripsPerWarp];  // next tile to prefetch, per strip
   pdl_trigger();  // the reduce kernel may be scheduled once every CTA has started
 #pragma unroll
   for (int r = 0; r < kStripsPerWarp; ++r) {
     acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0;
-#pragma unroll
-    for (int d = 0; d < kDepth; ++d)
-      buf[d][r] = d < ktiles ? ld_stream(src + r * KT * 32 + d * 32) : Z;
+    const uint4* p = src + r * KT * 32;
+    bA[r] = ktiles > 0 ? ld_stream(p) : Z;
+    bB[r] = ktiles > 1 ? ld_stream(p + 32) : Z;
+    bC[r] = Z;
+    nxt[r] = p + 32 * min(2, max(ktiles - 1, 0));
   }
   uint8_t* stage = reinterpret_cast<uint8_t*>(dg + kt_cta * 64);
   uint32_t* offs = reinterpret_cast<uint32_t*>(stage);
@@ -498,22 +506,28 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
   __syncthreads();
   // swizzled digit slots: the 8 lanes of each quarter-warp hit 8 distinct 16-byte bank groups
   const int sw = g ^ (2 * tid);
-  for (int kt = 0; kt < ktiles; kt += kDepth) {
-#pragma unroll
-    for (int d = 0; d < kDepth; ++d) {
-      if (kt + d < ktiles) {
-        const uint4 b01 = dg[((kt + d) * 8 + tid) * 8 + sw];
-        const uint4 b23 = dg[((kt + d) * 8 + tid + 4) * 8 + sw];
-#pragma unroll
-        for (int r = 0; r < kStripsPerWarp; ++r) {
-          const uint4 w = buf[d][r];
-          if (kt + d + kDepth < ktiles)
-            buf[d][r] = ld_stream(src + r * KT * 32 + (kt + d + kDepth) * 32);
-          mma_tile(acc[r], w, b01, b23);
-        }
-      }
-    }
+  const uint4* bp = dg + tid * 8 + sw;  // this thread's B fragments of tile t (64 uint4 per tile)
+  // One tile: B fragments from shared memory, prefetch tile t + 2 into the
+  // buffer freed by tile t - 1 (unconditional: past the last tile the pointer
+  // stays on it, an L2 hit), MMAs on tile t.
+#define GKB_PM_STEP(CUR, DST)                                              \
+  if (t < ktiles) {                                                        \
+    const uint4 b01 = bp[0], b23 = bp[32];                                 \
+    const bool adv = t + 2 < ktiles - 1;                                   \
+    _Pragma("unroll") for (int r = 0; r < kStripsPerWarp; ++r) {           \
+      DST[r] = ld_stream(nxt[r]);                                          \
+      nxt[r] += adv ? 32 : 0;                                              \
+      mma_tile(acc[r], CUR[r], b01, b23);                                  \
+    }                                                                      \
+    bp += 64;                                                              \
+    ++t;                                                                   \
   }
+  for (int t = 0; t < ktiles;) {
+    GKB_PM_STEP(bA, bC)
+    GKB_PM_STEP(bB, bA)
+    GKB_PM_STEP(bC, bB)
+  }
+#undef GKB_PM_STEP
   if (m_off) {
     cp_async_wait_all();
     __syncthreads();
