@@ -587,164 +587,6 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
 }
 
 
-// Variant with a shared-memory pipeline (GKB_RING): each warp streams its two
-// strips through a kRing-tile cp.async ring (16 bytes per lane per tile, no
-// registers), so 2 x kRing tiles per warp are in flight instead of 2 x 2 in
-// registers. The ring shares its space with the missing-list / cval staging,
-// which therefore happens after the main loop.
-constexpr int kRing = 4;
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N));
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_ring(
-    const uint4* __restrict__ lay, int64_t KT, int kt_cta, const uint4* __restrict__ dig,
-    const int* __restrict__ dexp, const double* __restrict__ dsum,
-    const double* __restrict__ cval, const double* __restrict__ mu,
-    const double* __restrict__ mean, const uint32_t* __restrict__ m_off,
-    const int64_t* __restrict__ m_base, const uint16_t* __restrict__ m_ent, int64_t rows_pad,
-    int64_t C, double* __restrict__ part) {
-  extern __shared__ __align__(16) uint4 dg[];  // kt_cta * 64 digits, then ring / list staging
-  const int kc = blockIdx.y;
-  const int64_t kt0 = (int64_t)kc * kt_cta;
-  const int ktiles = (int)min((int64_t)kt_cta, KT - kt0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, tid = lane & 3;
-  const int64_t strip0 = ((int64_t)blockIdx.x * 8 + warp) * kStripsPerWarp;
-  const uint4* src = lay + (strip0 * KT + kt0) * 32 + lane;
-  const int64_t b = (int64_t)kc * gridDim.x + blockIdx.x;
-  const int64_t col0 = kt0 * 128;
-  uint8_t* stage = reinterpret_cast<uint8_t*>(dg + kt_cta * 64);
-  uint32_t* offs = reinterpret_cast<uint32_t*>(stage);
-  double* cvs = reinterpret_cast<double*>(stage + kOffBytes + 2 * kEntCap + 16);
-  // ring slot (r, s) of this lane: ring + (r * kRing + s) * 32
-  uint4* ring = reinterpret_cast<uint4*>(stage) + warp * (kStripsPerWarp * kRing * 32) + lane;
-  pdl_trigger();
-#pragma unroll
-  for (int s = 0; s < kRing; ++s) {  // tiles 0 .. kRing - 1, one commit group per tile
-    if (s < ktiles) {
-#pragma unroll
-      for (int r = 0; r < kStripsPerWarp; ++r)
-        cp_async16(ring + (r * kRing + s) * 32, src + r * KT * 32 + s * 32);
-    }
-    cp_async_commit();
-  }
-  pdl_wait();
-  {
-    const uint4* gd = dig + kt0 * 64;
-    for (int i = threadIdx.x; i < ktiles * 64; i += kThreads) dg[i] = gd[i];
-  }
-  __syncthreads();
-  int acc[kStripsPerWarp][4];
-  uint4 cA[kStripsPerWarp], cB[kStripsPerWarp];
-  const uint4* gnx[kStripsPerWarp];
-  cp_async_wait_group<kRing - 1>();  // tile 0 (this lane's copies)
-#pragma unroll
-  for (int r = 0; r < kStripsPerWarp; ++r) {
-    acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0;
-    cA[r] = ring[(r * kRing) * 32];
-    gnx[r] = src + r * KT * 32 + kRing * 32;
-  }
-  const int sw = g ^ (2 * tid);
-  const uint4* bp = dg + tid * 8 + sw;
-  // tile i is commit group i; before the wait of step t, kRing + t groups exist
-#define GKB_RING_STEP(CUR, NXT)                                                   \
-  if (t < ktiles) {                                                               \
-    cp_async_wait_group<kRing - 2>(); /* tile t + 1 landed */                     \
-    const int s1 = (t + 1) & (kRing - 1);                                         \
-    if (t + 1 < ktiles) {                                                         \
-      _Pragma("unroll") for (int r = 0; r < kStripsPerWarp; ++r)                  \
-        NXT[r] = ring[(r * kRing + s1) * 32];                                     \
-    }                                                                             \
-    const uint4 b01 = bp[0], b23 = bp[32];                                        \
-    _Pragma("unroll") for (int r = 0; r < kStripsPerWarp; ++r)                    \
-      mma_tile(acc[r], CUR[r], b01, b23);                                         \
-    if (t + kRing < ktiles) { /* refill tile t's slot (consumed above) */        \
-      const int s0 = t & (kRing - 1);                                             \
-      _Pragma("unroll") for (int r = 0; r < kStripsPerWarp; ++r) {                \
-        cp_async16(ring + (r * kRing + s0) * 32, gnx[r]);                         \
-        gnx[r] += 32;                                                             \
-      }                                                                           \
-    }                                                                             \
-    cp_async_commit();                                                            \
-    bp += 64;                                                                     \
-    ++t;                                                                          \
-  }
-  for (int t = 0; t < ktiles;) {
-    GKB_RING_STEP(cA, cB)
-    GKB_RING_STEP(cB, cA)
-  }
-#undef GKB_RING_STEP
-  cp_async_wait_all();
-  __syncthreads();  // every warp is done with its ring: the space becomes list staging
-  int ent_shift = -1;
-  int64_t eb = 0;
-  if (m_off) {
-    for (int i = threadIdx.x; i <= kRowsPerCta; i += kThreads)
-      cp_async4(offs + i, m_off + b * (kRowsPerCta + 1) + i);
-    eb = m_base[b];
-    const int64_t ne = m_off[b * (kRowsPerCta + 1) + kRowsPerCta];
-    const int64_t a0 = (eb * 2) & ~int64_t(15), a1 = (eb * 2 + ne * 2 + 15) & ~int64_t(15);
-    if (a1 - a0 <= 2 * kEntCap) {
-      const uint8_t* esrc = reinterpret_cast<const uint8_t*>(m_ent) + a0;
-      for (int64_t i = threadIdx.x; i < (a1 - a0) / 16; i += kThreads)
-        cp_async16(stage + kOffBytes + 16 * i, esrc + 16 * i);
-      ent_shift = (int)(eb - a0 / 2);
-    }
-  }
-  if (m_off) {
-    const int ncol = (int)min((int64_t)ktiles * 128, C - col0);
-    for (int i = threadIdx.x; i < ncol; i += kThreads) cp_async8(cvs + i, cval + col0 + i);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-  }
-  // Epilogue. Thread (g, tid) holds digits (2 tid, 2 tid + 1) of rows g and
-  // g + 8; 2^(16 tid) (D_2tid + 256 D_2tid+1) is exact in fp64, and the four
-  // threads of the group add their parts by a butterfly (identical bits in
-  // all four). Rows: tid 0/2 -> row g, tid 1/3 -> row g + 8; the two threads
-  // of a row each walk half of its missing list.
-  const int E = dexp[kc];
-  const double rsum = dsum[kc];
-  const double p0 = pow2(16 * tid), p1 = pow2(16 * tid + 8);
-#pragma unroll
-  for (int r = 0; r < kStripsPerWarp; ++r) {
-    double v0 = (double)acc[r][0] * p0 + (double)acc[r][1] * p1;
-    double v1 = (double)acc[r][2] * p0 + (double)acc[r][3] * p1;
-    v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
-    v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
-    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
-    v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
-    const int hi = tid & 1;
-    const int64_t row = (strip0 + r) * 16 + g + 8 * hi;
-    const int rl = (int)(row - (int64_t)blockIdx.x * kRowsPerCta);
-    const double val = scalbn(hi ? v1 : v0, E - 62);
-    double corr = 0.0;
-    if (m_off) {
-      const uint32_t e0 = offs[rl], e1 = offs[rl + 1], mid = e0 + (e1 - e0) / 2;
-      const uint32_t k0 = (tid >> 1) ? mid : e0, ke = (tid >> 1) ? e1 : mid;
-      if (ent_shift >= 0)  // shared-memory run (pointer derived from the smem array: LDS)
-        corr = walk_list(reinterpret_cast<const uint16_t*>(stage + kOffBytes) + ent_shift, k0, ke,
-                         cvs);
-      else
-        corr = walk_list(m_ent + eb, k0, ke, cvs);
-      corr += __shfl_xor_sync(0xffffffffu, corr, 2);  // both halves, commutative -> same bits
-    }
-    if ((tid >> 1) == 0) {
-      double out;
-      if (MODE == 0) {  // a missing entry holds the imputed mean (genio.cpp:144)
-        out = val - mu[row] * rsum - (3.0 - mean[row]) * corr;
-      } else {
-        out = val - rsum - corr;
-      }
-      part[(int64_t)kc * rows_pad + row] = out;
-    }
-  }
-}
-
-
 // K1 finish: y_j = inv_s_j * sum_kc part[kc][j] (ranges in order)
 __global__ void k1_reduce(const double* __restrict__ part, int nkc, int64_t rows_pad,
                           int64_t p_loc, const double* __restrict__ inv_s,
@@ -884,11 +726,7 @@ namespace {
 template <int MODE>
 void launch_main(const GenoView& g, const PMPlan& pl, const uint4* lay, const PMScratch& sc,
                  const double* cval, const MissLists& ml, cudaStream_t s, bool pdl) {
-#ifdef GKB_RING
-  auto kern = k_pm_ring<MODE>;
-#else
   auto kern = k_pm_main<MODE>;
-#endif
   allow_smem(kern, pl.smem);
   dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nkc);
   launch_pdl(kern, grid, dim3(kThreads), pl.smem, s, pdl, lay, pl.KT, pl.kt_cta,
