@@ -101,12 +101,19 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+NCU_CAPTURE = "r1e_ncu_full_config2.json"  # ncu --set full of the current main kernels
+
+
 def ncu_traffic(kernel: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
     the committed `ncu --set full` capture of this workload (profiles/)."""
     import glob
     best = None
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_config2.json"))):
+    # the current capture last (the glob order is only a fallback for older ones)
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_config2.json")))
+    cur = os.path.join(ROOT, "profiles", NCU_CAPTURE)
+    paths = [q for q in paths if q != cur] + ([cur] if os.path.exists(cur) else [])
+    for p in paths:
         try:
             with open(p) as f:
                 d = json.load(f)
