@@ -451,16 +451,22 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     const double* __restrict__ cval, const double* __restrict__ mu,
     const double* __restrict__ mean, const uint32_t* __restrict__ m_off,
     const int64_t* __restrict__ m_base, const uint16_t* __restrict__ m_ent, int64_t rows_pad,
-    int64_t C, double* __restrict__ part) {
+    int64_t C, double* __restrict__ part, unsigned* __restrict__ tick,
+    const double* __restrict__ inv_s, double* __restrict__ yout, int64_t R) {
   extern __shared__ __align__(16) uint4 dg[];  // kt_cta * 64 digits, then list staging
-  const int kc = blockIdx.y;
+  // grid: (nkc, row blocks) when the reduce is fused (tick != null: the ranges
+  // of one row block are adjacent in launch order), else (row blocks, nkc)
+  const int kc = tick ? blockIdx.x : blockIdx.y;
+  const int bx = tick ? blockIdx.y : blockIdx.x;
+  const int nbx = tick ? gridDim.y : gridDim.x;
+  const int nkc = tick ? gridDim.x : gridDim.y;
   const int64_t kt0 = (int64_t)kc * kt_cta;
   const int ktiles = (int)min((int64_t)kt_cta, KT - kt0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tid = lane & 3;
-  const int64_t strip0 = ((int64_t)blockIdx.x * 8 + warp) * kStripsPerWarp;
+  const int64_t strip0 = ((int64_t)bx * 8 + warp) * kStripsPerWarp;
   const uint4* src = lay + (strip0 * KT + kt0) * 32 + lane;
-  const int64_t b = (int64_t)kc * gridDim.x + blockIdx.x;
+  const int64_t b = (int64_t)kc * nbx + bx;
   const int64_t col0 = kt0 * 128;
   const uint4 Z = make_uint4(0, 0, 0, 0);
   int acc[kStripsPerWarp][4];
@@ -561,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
     const int hi = tid & 1;
     const int64_t row = (strip0 + r) * 16 + g + 8 * hi;
-    const int rl = (int)(row - (int64_t)blockIdx.x * kRowsPerCta);
+    const int rl = (int)(row - (int64_t)bx * kRowsPerCta);
     const double val = scalbn(hi ? v1 : v0, E - 62);
     double corr = 0.0;
     if (m_off) {
@@ -582,6 +588,25 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
         out = val - rsum - corr;
       }
       part[(int64_t)kc * rows_pad + row] = out;
+    }
+  }
+  if (tick) {  // K1 finish fused: the last range CTA of this row block sums the ranges in order
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(tick + bx, 1u) == (unsigned)(nkc - 1);
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      for (int jr = threadIdx.x; jr < kRowsPerCta; jr += kThreads) {
+        const int64_t j = (int64_t)bx * kRowsPerCta + jr;
+        if (j < R) {
+          double a = 0.0;
+          for (int c = 0; c < nkc; ++c) a += __ldcg(part + (int64_t)c * rows_pad + j);
+          yout[j] = inv_s[j] * a;  // (may be a page-locked host buffer: one write per row)
+        }
+      }
+      if (threadIdx.x == 0) tick[bx] = 0u;
     }
   }
 }
@@ -725,14 +750,19 @@ void k2_digitize(const GenoView& g, const double* y, cudaStream_t s) {
 namespace {
 template <int MODE>
 void launch_main(const GenoView& g, const PMPlan& pl, const uint4* lay, const PMScratch& sc,
-                 const double* cval, const MissLists& ml, cudaStream_t s, bool pdl) {
+                 const double* cval, const MissLists& ml, cudaStream_t s, bool pdl,
+                 double* fused_out = nullptr) {
   auto kern = k_pm_main<MODE>;
   allow_smem(kern, pl.smem);
-  dim3 grid((unsigned)pl.grid_x, (unsigned)pl.nkc);
+  // fused K1 finish: grid (nkc, row blocks), ranges of a row block adjacent
+  const bool fused = fused_out != nullptr;
+  const dim3 grid = fused ? dim3((unsigned)pl.nkc, (unsigned)pl.grid_x)
+                          : dim3((unsigned)pl.grid_x, (unsigned)pl.nkc);
   launch_pdl(kern, grid, dim3(kThreads), pl.smem, s, pdl, lay, pl.KT, pl.kt_cta,
              (const uint4*)sc.dig, (const int*)sc.dexp, (const double*)sc.dsum, cval,
              (const double*)g.mu, (const double*)g.mean, ml.off, ml.base, ml.ent, pl.rows_pad,
-             pl.C, sc.part);
+             pl.C, sc.part, fused ? sc.tick : (unsigned*)nullptr,
+             (const double*)(fused ? g.inv_s : nullptr), fused_out, pl.R);
 }
 }  // namespace
 
@@ -745,9 +775,13 @@ void k2_main_only(const GenoView& g, cudaStream_t s) {
   launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, false);
 }
 
-void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s) {
+void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s, bool stream_out) {
   if (g.p_loc == 0) return;
   k1_digitize(g, x, s);
+  if (stream_out) {  // finish fused into the last CTA of each row block: y rows leave progressively
+    launch_main<0>(g, g.pl1, g.lt1, g.s1, x, g.m1, s, true, y);
+    return;
+  }
   launch_main<0>(g, g.pl1, g.lt1, g.s1, x, g.m1, s, true);
   launch_pdl(k1_reduce, dim3((unsigned)((g.p_loc + 255) / 256)), dim3(256), 0, s, true,
              (const double*)g.s1.part, g.pl1.nkc, g.pl1.rows_pad, g.p_loc, (const double*)g.inv_s,

@@ -101,6 +101,10 @@ struct DevOp {
   int64_t mvps = 0;
   // host-API staging buffers per local shard
   std::vector<double*> xbuf, ybuf, zbuf, yfull;
+  // the operator's kernels may read the adjoint input and write the results
+  // straight from/to page-locked host buffers (each element touched once)
+  bool direct_host_io = false;
+  bool host_out_ = false;  // set by apply_host while its result buffer is page-locked host memory
 
   virtual ~DevOp();
   int64_t row0(int i) const { return starts[ctx->shards[i].index]; }
@@ -112,6 +116,7 @@ struct DevOp {
   void alloc_host_api_buffers();
   void apply_host(const double* x, double* y);
   void adjoint_host(const double* y, double* z);
+  bool direct_io(const void* a, const void* b) const;
   // k columns per call (column-major host blocks): one H2D, k device products
   // back to back, one D2H (the block form subspace iteration uses)
   void apply_block_host(const double* X, int64_t k, double* Y);
@@ -147,6 +152,7 @@ struct GenoShard {
 };
 
 struct GenoOp : DevOp {
+  GenoOp() { direct_host_io = true; }  // k1_reduce writes y, k_digitize<1> reads y, k2_reduce writes z
   std::vector<GenoShard> gs;
   std::vector<int64_t> counts_host;  // p*4 (local rows only in SPMD mode, zero elsewhere)
   bool scaled = false;

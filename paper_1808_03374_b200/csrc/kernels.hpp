@@ -49,6 +49,7 @@ struct PMScratch {
   double* dsum;   // nkc
   double* cm;     // K2: c_j (3 - mu_j) per local SNP
   double* part;   // nkc * rows_pad partials
+  unsigned* tick; // grid_x arrival counters of the fused K1 finish (zero between launches)
 };
 struct GenoView {
   const uint4* lt1;
@@ -83,7 +84,11 @@ void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int6
                 cudaStream_t s);
 
 // K1 apply (reference X*x, per-SNP dot): y (p_loc) = inv_s*(sum r x - mu X_tot - (3-mu) S_miss)
-void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s);
+// stream_out: y is written by the main kernel's last CTA of each row block (for
+// a page-locked host y: the rows cross PCIe while other blocks still stream);
+// otherwise by a separate fixed-order reduce (faster when y stays on the device).
+void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s,
+              bool stream_out = false);
 // K2 apply_adjoint (reference X^T*y, per-sample sum) over the local SNPs; z has n entries.
 void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s);
 // Pieces (for timing breakdowns): digitize, then the main tensor-core kernel.

@@ -47,8 +47,42 @@ void DevOp::alloc_host_api_buffers() {
   }
 }
 
+// Page-locked host memory (cudaMallocHost, gkb_host_alloc / pinned_empty) is
+// mapped into the device address space at the same address (UVA).
+static bool device_accessible(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer == p;
+}
+
+// One local shard (no cross-shard sum) and an operator whose result kernels
+// write each element once: page-locked host buffers are used in place.
+bool DevOp::direct_io(const void* a, const void* b) const {
+  if (!direct_host_io || ctx->shards.size() != 1 || (ctx->use_nccl && ctx->nshards_total > 1))
+    return false;
+  return device_accessible(a) && (!b || device_accessible(b));
+}
+
 void DevOp::apply_host(const double* x, double* y) {
   const int L = (int)ctx->shards.size();
+  if (direct_io(y, nullptr)) {  // y written by the reduce kernel over PCIe, no D2H copy
+    ctx->set_device(0);
+    GKB_CUDA(cudaMemcpyAsync(xbuf[0], x, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice,
+                             ctx->shards[0].stream));
+    host_out_ = true;
+    try {
+      apply_dev({xbuf[0]}, {y});
+    } catch (...) {
+      host_out_ = false;
+      throw;
+    }
+    host_out_ = false;
+    ctx->sync_all();
+    return;
+  }
   std::vector<const double*> xi(L);
   for (int i = 0; i < L; ++i) {
     ctx->set_device(i);
@@ -78,6 +112,12 @@ void DevOp::apply_host(const double* x, double* y) {
 
 void DevOp::adjoint_host(const double* y, double* z) {
   const int L = (int)ctx->shards.size();
+  if (direct_io(y, z)) {  // y read once by digitize, z written by the reduce kernel
+    ctx->set_device(0);
+    adjoint_dev({y}, {z});
+    ctx->sync_all();
+    return;
+  }
   std::vector<const double*> yi(L);
   for (int i = 0; i < L; ++i) {
     ctx->set_device(i);
@@ -285,10 +325,12 @@ static void alloc_scratch(const dev::PMPlan& pl, bool with_cm, dev::PMScratch& s
   pool(&sc.dsum, sizeof(double) * (size_t)pl.nkc);
   pool(&sc.part, sizeof(double) * (size_t)(pl.nkc * pl.rows_pad));
   if (with_cm) pool(&sc.cm, sizeof(double) * (size_t)std::max<int64_t>(pl.C, 1));
+  pool(&sc.tick, sizeof(unsigned) * (size_t)std::max<int64_t>(pl.grid_x, 1));
+  GKB_CUDA(cudaMemsetAsync(sc.tick, 0, sizeof(unsigned) * (size_t)std::max<int64_t>(pl.grid_x, 1), st));
 }
 
 static void free_scratch(dev::PMScratch& sc, cudaStream_t st) {
-  void* ptrs[] = {sc.dig, sc.dexp, sc.dsum, sc.part, sc.cm};
+  void* ptrs[] = {sc.dig, sc.dexp, sc.dsum, sc.part, sc.cm, sc.tick};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, st);
   sc = dev::PMScratch{};
@@ -698,7 +740,7 @@ void GenoOp::apply_dev(const std::vector<const double*>& x, const std::vector<do
   if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
   for (size_t i = 0; i < gs.size(); ++i) {
     ctx->set_device((int)i);
-    dev::k1_apply(gs[i].view(), x[i], y[i], ctx->shards[i].stream);
+    dev::k1_apply(gs[i].view(), x[i], y[i], ctx->shards[i].stream, host_out_);
     GKB_LAUNCH_CHECK();
   }
 }
