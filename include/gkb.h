@@ -204,9 +204,31 @@ void gkb_gkl_options_default(gkb_gkl_options* o);
 /* GklOptions::validate (gkl.cpp:53-73): GKB_EINVAL with the reference message. */
 int gkb_gkl_options_validate(const gkb_gkl_options* o, int64_t m, int64_t n);
 /* svdl (gkl.hpp:196, gkl.cpp:416-514) with U (SNP side) sharded and V
- * replicated in HBM; the small SVD and omega recurrences run on the host. */
+ * replicated in HBM; the small SVD runs on the host, the per-step decisions
+ * (omega recurrences, second passes, breakdown tests) on the device. */
 int gkb_svdl(gkb_op* op, const gkb_gkl_options* o, gkb_svdl_result** res);
 int gkb_svdl_result_free(gkb_svdl_result* res);
+
+/* SubspaceResult + SubspaceState (subspace.hpp:21-35). Arrays owned by the result. */
+typedef struct {
+  int64_t m, k;
+  double* basis;            /* m x k, column-major */
+  double* eigvals;          /* k */
+  double* singvals;         /* k */
+  int64_t iterations;
+  double* delta_history;    /* iterations */
+  double* invcond_history;  /* iterations + 1 */
+  int32_t converged, rank_deficient;
+  int64_t mvps;
+} gkb_subspace_result;
+/* subspace_iterate (subspace.hpp:50-70, subspace.cpp:49-115), variant kQr,
+ * with the k-column blocks resident on the device: gram passes as k + k
+ * device products, CholeskyQR2 renormalization (device Gram, k x k host
+ * Cholesky), device convergence test. GKB_ELOGIC if the block loses rank
+ * (the caller then uses the host-side QR). */
+int gkb_subspace_qr(gkb_op* op, int64_t k, double tol, int64_t max_iter, uint64_t seed,
+                    int scaled_delta, gkb_subspace_result** res);
+int gkb_subspace_result_free(gkb_subspace_result* res);
 
 /* ---- step-level access (LanczosFactorization, gkl.hpp:59-125) ------------
  * For the reference's unit tests of bidiag_step / ritz_extract /

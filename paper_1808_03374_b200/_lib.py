@@ -69,6 +69,22 @@ class gkb_svdl_result(C.Structure):
     ]
 
 
+class gkb_subspace_result(C.Structure):
+    _fields_ = [
+        ("m", C.c_int64),
+        ("k", C.c_int64),
+        ("basis", C.POINTER(C.c_double)),
+        ("eigvals", C.POINTER(C.c_double)),
+        ("singvals", C.POINTER(C.c_double)),
+        ("iterations", C.c_int64),
+        ("delta_history", C.POINTER(C.c_double)),
+        ("invcond_history", C.POINTER(C.c_double)),
+        ("converged", C.c_int32),
+        ("rank_deficient", C.c_int32),
+        ("mvps", C.c_int64),
+    ]
+
+
 class gkb_synth_spec(C.Structure):
     _fields_ = [
         ("p", C.c_int64),
@@ -130,6 +146,9 @@ SIGNATURES = {
     "gkb_gkl_options_validate": (I, [C.POINTER(gkb_gkl_options), I64, I64]),
     "gkb_svdl": (I, [P, C.POINTER(gkb_gkl_options), C.POINTER(C.POINTER(gkb_svdl_result))]),
     "gkb_svdl_result_free": (I, [C.POINTER(gkb_svdl_result)]),
+    "gkb_subspace_qr": (I, [P, I64, C.c_double, I64, C.c_uint64, I,
+                            C.POINTER(C.POINTER(gkb_subspace_result))]),
+    "gkb_subspace_result_free": (I, [C.POINTER(gkb_subspace_result)]),
     "gkb_lanczos_create": (I, [P, I64, PD, C.c_uint64, C.POINTER(P)]),
     "gkb_lanczos_destroy": (I, [P]),
     "gkb_bidiag_step": (I, [P, C.POINTER(gkb_gkl_options), D, C.POINTER(C.c_int),

@@ -268,6 +268,29 @@ __global__ void __launch_bounds__(kT) k_dot(const double* __restrict__ a,
   block_partial_finalize<1>(acc, partial, out, ticket);
 }
 
+// sum (a - b)^2 (subspace delta criterion)
+__global__ void __launch_bounds__(kT) k_diff_nrm2(const double* __restrict__ a,
+                                                  const double* __restrict__ b, int64_t len,
+                                                  int64_t rpb, double* __restrict__ partial,
+                                                  double* __restrict__ out,
+                                                  unsigned* __restrict__ ticket) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
+  const Chunk ch = chunk(len, rpb);
+  double acc[1] = {0.0};
+  for (int64_t rb = ch.r0 + threadIdx.x; rb < ch.r1; rb += (int64_t)kT * kBatch) {
+    double d[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int64_t r = rb + (int64_t)i * kT;
+      d[i] = r < ch.r1 ? a[r] - b[r] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) acc[0] += d[i] * d[i];
+  }
+  block_partial_finalize<1>(acc, partial, out, ticket);
+}
+
 __global__ void k_axpy_dev(const double* __restrict__ d, const double* __restrict__ u,
                            double* __restrict__ v, int64_t len, const int* gate) {
   pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
@@ -452,6 +475,12 @@ void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* 
 void nrm2sq(const double* a, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
             const int* gate) {
   dot(a, a, len, rs, out, s, gate);
+}
+
+void diff_nrm2sq(const double* a, const double* b, int64_t len, RedScratch& rs, double* out,
+                 cudaStream_t s) {
+  launch_pdl(k_diff_nrm2, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, a, b, len,
+             rpb_of(len), rs.partial, out, rs.ticket);
 }
 
 void axpy_dev(const double* dptr, const double* u, double* v, int64_t len, cudaStream_t s,

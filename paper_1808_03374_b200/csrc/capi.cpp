@@ -469,6 +469,44 @@ int gkb_svdl(gkb_op* op, const gkb_gkl_options* o, gkb_svdl_result** res) {
   });
 }
 
+int gkb_subspace_qr(gkb_op* op, int64_t k, double tol, int64_t max_iter, uint64_t seed,
+                    int scaled_delta, gkb_subspace_result** res) {
+  return guarded([&] {
+    need(op, "op");
+    need(res, "res");
+    gkb::SubspaceOutput o =
+        gkb::subspace_qr_device(op->op.get(), k, tol, max_iter, seed, scaled_delta != 0);
+    auto* r = new gkb_subspace_result();
+    std::memset(r, 0, sizeof(*r));
+    auto dup = [](const std::vector<double>& v) {
+      double* p = new double[v.size() > 0 ? v.size() : 1];
+      std::copy(v.begin(), v.end(), p);
+      return p;
+    };
+    r->m = op->op->m;
+    r->k = k;
+    r->basis = dup(o.basis);
+    r->eigvals = dup(o.eigvals);
+    r->singvals = dup(o.singvals);
+    r->iterations = o.iterations;
+    r->delta_history = dup(o.delta_history);
+    r->invcond_history = dup(o.invcond_history);
+    r->converged = o.converged ? 1 : 0;
+    r->rank_deficient = o.rank_deficient ? 1 : 0;
+    r->mvps = o.mvps;
+    *res = r;
+  });
+}
+
+int gkb_subspace_result_free(gkb_subspace_result* r) {
+  return guarded([&] {
+    if (!r) return;
+    for (double* p : {r->basis, r->eigvals, r->singvals, r->delta_history, r->invcond_history})
+      delete[] p;
+    delete r;
+  });
+}
+
 int gkb_svdl_result_free(gkb_svdl_result* r) {
   return guarded([&] {
     if (!r) return;

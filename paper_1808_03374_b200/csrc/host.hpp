@@ -316,4 +316,13 @@ struct SvdlOutput {
 };
 SvdlOutput svdl(DevOp* op, const Options& o);
 
+// subspace_iterate, QR variant, device-resident blocks (subspace_driver.cpp)
+struct SubspaceOutput {
+  std::vector<double> basis, eigvals, singvals, delta_history, invcond_history;
+  int64_t iterations = 0, mvps = 0;
+  bool converged = false, rank_deficient = false;
+};
+SubspaceOutput subspace_qr_device(DevOp* op, int64_t k, double tol, int64_t max_iter,
+                                  uint64_t seed, bool scaled_delta);
+
 }  // namespace gkb

@@ -122,6 +122,9 @@ void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* 
 // out[0] = ||a||^2
 void nrm2sq(const double* a, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
             const int* gate = nullptr);
+// out[0] = sum (a - b)^2
+void diff_nrm2sq(const double* a, const double* b, int64_t len, RedScratch& rs, double* out,
+                 cudaStream_t s);
 // v -= (*dptr) * u   (device scalar)
 void axpy_dev(const double* dptr, const double* u, double* v, int64_t len, cudaStream_t s,
               const int* gate = nullptr);

@@ -96,6 +96,10 @@ def subspace_iterate(op, k: int, variant: SubspaceVariant = SubspaceVariant.kQr,
         raise ValueError("subspace_iterate: k out of range")
     if max_iter < 0:
         raise ValueError("subspace_iterate: max_iter must be >= 0")
+    if variant == SubspaceVariant.kQr and getattr(op, "_h", None):
+        res = _subspace_qr_device(op, k, tol, max_iter, seed, scaled_delta)
+        if res is not None:
+            return res
     from .gkl import rng_normal
     mv0 = op.mvps()
     # Y(i, j) = rng.normal(), j outer, i inner (subspace.cpp:64-66)
@@ -127,3 +131,36 @@ def subspace_iterate(op, k: int, variant: SubspaceVariant = SubspaceVariant.kQr,
     return SubspaceResult(basis=Y, eigvals=sv ** 2, singvals=sv, state=state,
                           converged=converged, rank_deficient=rank_deficient,
                           mvps=op.mvps() - mv0)
+
+
+def _subspace_qr_device(op, k, tol, max_iter, seed, scaled_delta):
+    """The QR variant with the blocks resident on the device
+    (gkb_subspace_qr: CholeskyQR2 renormalization, device convergence test,
+    one small read-back per pass). None if the block lost rank on the way --
+    the host path's Householder QR then reruns the solve."""
+    import ctypes as C
+    from . import _lib
+    res = C.POINTER(_lib.gkb_subspace_result)()
+    st = _lib.lib.gkb_subspace_qr(op._h, int(k), float(tol), int(max_iter),
+                                  int(seed) & 0xFFFFFFFFFFFFFFFF, int(bool(scaled_delta)),
+                                  C.byref(res))
+    if st != 0:
+        if st == _lib.GKB_ELOGIC and "lost rank" in _lib.lib.gkb_last_error().decode():
+            return None
+        _lib.check(st)
+    try:
+        r = res.contents
+        m, it = int(r.m), int(r.iterations)
+
+        def arr(p, cnt):
+            return np.ctypeslib.as_array(p, shape=(cnt,)).copy() if cnt > 0 else np.zeros(0)
+
+        basis = np.ctypeslib.as_array(r.basis, shape=(k, m)).T.copy(order="F")
+        state = SubspaceState(iterations=it,
+                              delta_history=[float(v) for v in arr(r.delta_history, it)],
+                              invcond_history=[float(v) for v in arr(r.invcond_history, it + 1)])
+        return SubspaceResult(basis=basis, eigvals=arr(r.eigvals, k), singvals=arr(r.singvals, k),
+                              state=state, converged=bool(r.converged),
+                              rank_deficient=bool(r.rank_deficient), mvps=int(r.mvps))
+    finally:
+        _lib.lib.gkb_subspace_result_free(res)
