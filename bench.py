@@ -305,6 +305,33 @@ def run_ours(args):
     res = gkb.svdl(op, opts)
     tts = time.perf_counter() - t0
 
+    # widened rows on the same operator: subspace iteration
+    # (QR variant, device-resident blocks; a bounded 40-iteration sample) and
+    # the per-marker PC-adjusted regression scan with the solve's first 10 PCs
+    widened = None
+    if rank == 0 and ws == 1 and not args.no_widen:
+        from paper_1808_03374_b200 import regress as Rg
+        from paper_1808_03374_b200 import subspace as Sb
+        t0 = time.perf_counter()
+        sres = Sb.subspace_iterate(op, 10, Sb.SubspaceVariant.kQr, 1e-8, 40, 0)
+        t_sub = time.perf_counter() - t0
+        pheno = np.random.default_rng(11).standard_normal(spec.n)
+        Zpc = res.V[:, :10]
+        Rg.marker_scan(op, pheno, Zpc)  # warm-up (block buffers)
+        t0 = time.perf_counter()
+        scan = Rg.marker_scan(op, pheno, Zpc)
+        t_reg = time.perf_counter() - t0
+        widened = {
+            "subspace": {"seconds": round(t_sub, 4), "k": 10, "iterations": sres.state.iterations,
+                         "mvps": sres.mvps, "converged": bool(sres.converged),
+                         "matvec_gbs": round(sres.mvps * packed_local / t_sub / 1e9, 1),
+                         "sample": "subspace_iterate kQr, k=10, tol 1e-8, max 40 iterations"},
+            "regress": {"seconds": round(t_reg, 4), "markers": int(scan.beta.size),
+                        "markers_per_s": round(scan.beta.size / t_reg, 1), "pcs": 10,
+                        "sample": "marker_scan: y ~ [1, m_i, Z] for every SNP (one 12-column "
+                                  "block product + host algebra)"},
+        }
+
     peak, peak_src = load_peaks()
     b_mvp = packed_local
     k1_gbs = b_mvp / (k1_main * 1e-3) / 1e9
@@ -357,6 +384,8 @@ def run_ours(args):
         }
         if ingest:
             line["ingest"] = ingest
+        if widened:
+            line["widened"] = widened
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -373,6 +402,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-ingest", action="store_true", help="skip the .bed ingest timing")
+    ap.add_argument("--no-widen", action="store_true",
+                    help="skip the subspace / regression timings")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
