@@ -665,7 +665,7 @@ PMPlan pm_plan(int64_t R, int64_t C) {
   if (pl.S < kStripsPerCta) pl.S = kStripsPerCta;
   pl.KT = (C + 127) / 128;
   if (pl.KT < 1) pl.KT = 1;
-  pl.kt_cta = 16;  // 2048 columns per CTA (16 KB of digits)
+  pl.kt_cta = 14;  // 1792 columns per CTA (14 KB of digits); 12-20 swept, 14 best (config 2 and 3)
   if (const char* e = std::getenv("GKB_KT_CTA")) pl.kt_cta = std::max(1, std::atoi(e));  // sweeps
   pl.nkc = (int)((pl.KT + pl.kt_cta - 1) / pl.kt_cta);
   pl.grid_x = pl.S / kStripsPerCta;
