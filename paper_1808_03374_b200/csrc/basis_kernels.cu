@@ -14,7 +14,9 @@
 // only), without a second finalize launch.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.hpp"
 #include "pdl.hpp"
@@ -29,6 +31,7 @@ constexpr int kWarps = kT / 32;
 constexpr int kCB = 8;      // columns per pass in gemv_t
 constexpr int kBatch = 4;   // rows per thread with loads in flight together
 constexpr int kSeg = 8;     // final-sum segments (one per warp)
+constexpr int kTickets = 4096;  // last-CTA tickets per RedScratch
 
 __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -47,8 +50,17 @@ __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 // last CTA to arrive sums them into out[k]. Order: segment s of the nblk
 // partials (fixed boundaries) summed sequentially, then the kSeg segment sums
 // in order -- a function of (nblk, K) only.
+__device__ void grid_finalize_cols(const double* partial, int nblk, int K, int kb, int ke,
+                                   double* out, unsigned* ticket, unsigned nctas);
+
 __device__ void grid_finalize(const double* partial, int nblk, int K, double* out,
                               unsigned* ticket, unsigned nctas) {
+  grid_finalize_cols(partial, nblk, K, 0, K, out, ticket, nctas);
+}
+
+// Columns [kb, ke) only; `ticket` counts the nctas CTAs that write them.
+__device__ void grid_finalize_cols(const double* partial, int nblk, int K, int kb, int ke,
+                                   double* out, unsigned* ticket, unsigned nctas) {
   __shared__ bool last;
   __shared__ double seg[kSeg][33];
   __threadfence();
@@ -59,10 +71,10 @@ __device__ void grid_finalize(const double* partial, int nblk, int K, double* ou
   __threadfence();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b0 = (int)((int64_t)nblk * warp / kSeg), b1 = (int)((int64_t)nblk * (warp + 1) / kSeg);
-  for (int k0 = 0; k0 < K; k0 += 32) {
+  for (int k0 = kb; k0 < ke; k0 += 32) {
     const int k = k0 + lane;
     double t = 0.0;
-    if (k < K) {
+    if (k < ke) {
       int b = b0;
       for (; b + 4 <= b1; b += 4) {
         const double p0 = ld_cg(partial + (int64_t)b * K + k);
@@ -78,7 +90,7 @@ __device__ void grid_finalize(const double* partial, int nblk, int K, double* ou
     }
     seg[warp][lane] = t;
     __syncthreads();
-    if (warp == 0 && k < K) {
+    if (warp == 0 && k < ke) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < kSeg; ++w) s += seg[w][lane];
@@ -177,7 +189,10 @@ __global__ void __launch_bounds__(kT) k_gemv_t(const double* __restrict__ Q, int
     for (int w = 0; w < kWarps; ++w) t += ws[threadIdx.x][w];
     partial[(int64_t)blockIdx.x * K + c0 + threadIdx.x] = t;
   }
-  grid_finalize(partial, gridDim.x, K, out, ticket, gridDim.x * gridDim.y);
+  // the last row chunk of this column group sums its kCB columns (one ticket
+  // per group: the groups finish in parallel, same per-column order)
+  grid_finalize_cols(partial, gridDim.x, K, (int)c0, (int)min((int64_t)K, c0 + kCB), out,
+                     ticket + blockIdx.y, gridDim.x);
 }
 
 // v = beta*v + sign*(Q c); optional norms before/after (out[0], out[1]).
@@ -431,6 +446,18 @@ int64_t rows_per_thread(int64_t len) {
 
 int64_t rpb_of(int64_t len) { return (int64_t)kT * rows_per_thread(len); }
 
+// gemv_t / gemv_n row chunking (their partials are their own, so it may differ
+// from the other reductions'): about `blocks` row chunks (GKB_GT_BLOCKS,
+// GKB_GN_BLOCKS for sweeps)
+int64_t rpb_target(int64_t len, const char* env, int64_t dflt) {
+  int64_t blocks = dflt;
+  if (const char* e = getenv(env)) blocks = std::max<int64_t>(1, atoll(e));
+  int64_t u = (len + (int64_t)kT * blocks - 1) / ((int64_t)kT * blocks);
+  if (u < 1) u = 1;
+  if (u > 256) u = 256;
+  return (int64_t)kT * u;
+}
+
 }  // namespace
 
 int64_t red_blocks(int64_t len) {
@@ -441,9 +468,9 @@ int64_t red_blocks(int64_t len) {
 }
 
 void init_red_scratch(RedScratch& rs) {
-  if (!rs.ticket) {
-    cudaMalloc(&rs.ticket, sizeof(unsigned));
-    cudaMemset(rs.ticket, 0, sizeof(unsigned));
+  if (!rs.ticket) {  // one per gemv_t column group (K <= 8 * kTickets), [0] for the rest
+    cudaMalloc(&rs.ticket, sizeof(unsigned) * kTickets);
+    cudaMemset(rs.ticket, 0, sizeof(unsigned) * kTickets);
   }
 }
 
@@ -451,19 +478,29 @@ void gemv_t(const double* Q, int64_t ld, int64_t len, int64_t ncols, const doubl
             RedScratch& rs, double* out, cudaStream_t s, const int* gate) {
   const int K = (int)(ncols + (with_norm ? 1 : 0));
   if (K == 0) return;
-  const dim3 grid((unsigned)red_blocks(len), (unsigned)((K + kCB - 1) / kCB));
-  launch_pdl(k_gemv_t, grid, dim3(kT), 0, s, true, Q, ld, len, ncols, v, with_norm ? 1 : 0,
-                                                     rpb_of(len), K, rs.partial, out, rs.ticket,
-                                                     gate);
+  if ((K + kCB - 1) / kCB > kTickets) {  // (beyond 32K columns: column blocks of 32K)
+    for (int64_t c0 = 0; c0 < ncols; c0 += 8 * (int64_t)kTickets) {
+      const int64_t cn = std::min<int64_t>(8 * (int64_t)kTickets, ncols - c0);
+      const bool nrm = with_norm && c0 + cn == ncols;
+      gemv_t(Q + c0 * ld, ld, len, cn, v, nrm, rs, out + c0, s, gate);
+    }
+    return;
+  }
+  const int64_t rpb = rpb_target(len, "GKB_GT_BLOCKS", 296);
+  const int64_t nb = std::max<int64_t>(1, (len + rpb - 1) / rpb);
+  const dim3 grid((unsigned)nb, (unsigned)((K + kCB - 1) / kCB));
+  launch_pdl(k_gemv_t, grid, dim3(kT), 0, s, true, Q, ld, len, ncols, v, with_norm ? 1 : 0, rpb,
+             K, rs.partial, out, rs.ticket, gate);
 }
 
 void gemv_n(const double* Q, int64_t ld, int64_t len, int64_t ncols, const double* c, double* v,
             double beta, double sign, bool norms, RedScratch& rs, double* out, cudaStream_t s,
             const int* gate) {
   if (len == 0 && !norms) return;
-  launch_pdl(k_gemv_n, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, Q, ld, len, ncols, c, v, beta, sign,
-                                                     norms ? 1 : 0, rpb_of(len), rs.partial, out,
-                                                     rs.ticket, gate);
+  const int64_t rpb = rpb_target(len, "GKB_GN_BLOCKS", 296);
+  const int64_t nb = std::max<int64_t>(1, (len + rpb - 1) / rpb);
+  launch_pdl(k_gemv_n, dim3((unsigned)nb), dim3(kT), 0, s, true, Q, ld, len, ncols, c, v, beta,
+             sign, norms ? 1 : 0, rpb, rs.partial, out, rs.ticket, gate);
 }
 
 void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
