@@ -138,11 +138,13 @@ def test_format_errors(gkb):
         gkb.GenotypeOperator.from_bed_payload(np.zeros(0, np.uint8), 0, 16)
 
 
-def test_pinned_buffers_and_out(gkb):
-    """gkb.pinned_empty + out= (page-locked host vectors) give the same bits as
-    pageable numpy vectors; out= validation follows the reference's
-    invalid_argument behaviour (ValueError)."""
-    p, n = 257, 1000
+@pytest.mark.parametrize("p,n", [(257, 1000), (3001, 5003)])
+def test_pinned_buffers_and_out(gkb, p, n):
+    """gkb.pinned_empty + out= (page-locked host vectors, used in place by the
+    kernels: K1's finish fused into the last CTA of each row block) give the
+    same bits as pageable numpy vectors (staged copies, separate reduce) --
+    also with several column ranges and row blocks; out= validation follows
+    the reference's invalid_argument behaviour (ValueError)."""
     payload, _ = random_payload(p, n, seed=5)
     op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
     x = np.random.default_rng(1).standard_normal(n)
