@@ -367,6 +367,7 @@ bool Lanczos::partial_reorth_update(Side side, const std::vector<double*>& cand,
 
 // deflate_right (gkl.cpp:178-204)
 void Lanczos::deflate_right() {
+  ++version_;
   const int64_t j = j_;
   const double lvl = eps_level(m_, n_);
   const int L = (int)ctx_->shards.size();
@@ -430,6 +431,7 @@ void Lanczos::launch_right(int64_t s, const std::vector<double*>& dres, int64_t 
 
 // bidiag_step (gkl.cpp:206-312)
 StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter) {
+  ++version_;
   const int64_t s = j_;
   if (s >= cap_ || s >= std::min(m_, n_))
     fail(GKB_ELOGIC, "bidiag_step: factorization cannot grow further");
@@ -793,6 +795,7 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
 }
 
 Lanczos::DevRun Lanczos::run_dev(const Options& o, int64_t nsteps, double* norm_scale) {
+  ++version_;
   using namespace dev::ctl;
   const int L = (int)ctx_->shards.size();
   if (ctl_d_.empty()) {
@@ -890,6 +893,7 @@ Ritz Lanczos::ritz_extract(double tol) const {
 
 // thick_restart (gkl.cpp:341-378)
 void Lanczos::thick_restart(int64_t keep, const Ritz* current) {
+  ++version_;
   const int64_t j = j_;
   if (keep < 1 || keep >= j) fail(GKB_EINVAL, "thick_restart: need 1 <= keep < steps");
   const int L = (int)ctx_->shards.size();
@@ -939,6 +943,7 @@ void Lanczos::thick_restart(int64_t keep, const Ritz* current) {
 
 // compress_exhausted (gkl.cpp:380-409)
 void Lanczos::compress_exhausted() {
+  ++version_;
   const int64_t j = j_;
   if (j == 0) return;
   const int L = (int)ctx_->shards.size();
@@ -996,6 +1001,12 @@ static void gather_left(Context* ctx, DevOp* op, const std::vector<double*>& src
     cudaFree(full);
     return;
   }
+  if (L == 1) {  // rows(0) == m: one contiguous block
+    ctx->set_device(0);
+    ctx->sync_all();
+    d2h_staged(ctx->shards[0], host, src[0], sizeof(double) * (size_t)(m * ncols));
+    return;
+  }
   for (int i = 0; i < L; ++i) {
     ctx->set_device(i);
     const int64_t r = op->rows(i);
@@ -1044,7 +1055,7 @@ void Lanczos::ritz_vectors(const Ritz& r, int64_t kc, double* outU, double* outV
   if (outU) gather_left(ctx_, op_, U2_, kc, outU);
   if (outV) {
     ctx_->set_device(0);
-    GKB_CUDA(cudaMemcpy(outV, V2_[0], sizeof(double) * (size_t)(n_ * kc), cudaMemcpyDeviceToHost));
+    d2h_staged(ctx_->shards[0], outV, V2_[0], sizeof(double) * (size_t)(n_ * kc));
   }
 }
 
@@ -1076,7 +1087,20 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
   double norm_scale = 0.0;
   Ritz ritz;
   int consecutive_breakdowns = 0;
+  int64_t ritz_version = -1;  // factorization version the current `ritz` was extracted from
   auto extract = [&]() {
+    if (ritz_version == f.version()) {  // unchanged since the last extraction: replay it
+      if (o.record_history) {
+        const size_t h = out.ritz_history.size();
+        for (int64_t i = 0; i < o.k; ++i) {
+          out.ritz_history.push_back(out.ritz_history[h - (size_t)o.k + (size_t)i]);
+          out.err_history.push_back(out.err_history[h - (size_t)o.k + (size_t)i]);
+        }
+        ++out.history_len;
+      }
+      return;
+    }
+    ritz_version = f.version();
     ritz = f.ritz_extract(o.tol);
     if (!ritz.values.empty()) norm_scale = std::max(norm_scale, ritz.values[0]);
     if (o.record_history) {
@@ -1174,6 +1198,7 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
     }
   }
 
+  const auto t_loop = std::chrono::steady_clock::now();
   extract();
   const int64_t j = f.steps();
   const int64_t count = std::min<int64_t>(o.k, j);
@@ -1184,7 +1209,9 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
   out.U.reset(new double[(size_t)std::max<int64_t>(m * count, 1)]);
   out.V.reset(new double[(size_t)std::max<int64_t>(n * count, 1)]);
   // Ritz vectors U W_L, V W_R, returned as-is (gkl.cpp:500-507).
+  const auto t_ext = std::chrono::steady_clock::now();
   f.ritz_vectors(ritz, count, out.U.get(), out.V.get());
+  const auto t_vec = std::chrono::steady_clock::now();
   out.all_converged = count == o.k && top_k_converged();
   out.mvps = mvps;
   ctx->set_device(0);
@@ -1198,9 +1225,14 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
   out.host_syncs = f.host_syncs;
   if (const char* e = getenv("GKB_VERBOSE"))
     if (e[0] == '1')
+    {
+      auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
       fprintf(stderr, "[gkb] svdl: %lld steps, host syncs %lld, speculative right half-steps kept %lld / "
-              "not used %lld\n", (long long)out.steps, (long long)f.host_syncs,
-              (long long)f.spec_hits, (long long)f.spec_misses);
+              "not used %lld; loop %.4f s, final extract %.4f s, Ritz vectors %.4f s\n",
+              (long long)out.steps, (long long)f.host_syncs, (long long)f.spec_hits,
+              (long long)f.spec_misses, sec(t_start, t_loop), sec(t_loop, t_ext),
+              sec(t_ext, t_vec));
+    }
   op->mvps += mvps;
   out.wall_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();

@@ -68,6 +68,8 @@ struct Shard {
 };
 
 constexpr int64_t kResCap = 1 << 16;
+// device -> pageable host copy through the shard's page-locked staging (synchronous)
+void d2h_staged(Shard& s, void* dst, const void* src, size_t bytes);
 
 struct Context {
   std::vector<Shard> shards;
@@ -222,6 +224,7 @@ class Lanczos {
   Lanczos(DevOp* op, int64_t capacity, const double* start_host, uint64_t rng_seed);
   ~Lanczos();
   int64_t steps() const { return j_; }
+  int64_t version() const { return version_; }  // bumped by every change of the factorization
   int64_t capacity() const { return cap_; }
   bool right_exhausted() const { return right_exhausted_; }
   StepInfo step(const Options& o, double norm_scale, int64_t* mvp_counter);
@@ -254,6 +257,7 @@ class Lanczos {
   DevOp* op_;
   Context* ctx_;
   int64_t m_, n_, cap_, j_ = 0;
+  int64_t version_ = 0;
   std::vector<double*> U_, V_, U2_, V2_, w_, z_, cbuf_;
   std::vector<double> B_, coupling_, mu_, nu_, mu_next_, nu_next_;
   bool right_exhausted_ = false;

@@ -398,42 +398,59 @@ class GenotypeOperator(LinearOperator):
         return {"nmissing": a.value, "packed_bytes": b.value, "device_bytes": c.value}
 
 
+class _OwnedArray(np.ndarray):
+    """A view of library-owned memory; `_owner` frees it with the last view."""
+
+
+class _SvdlResultOwner:
+    def __init__(self, res):
+        self.res = res
+
+    def __del__(self):
+        try:
+            check(lib.gkb_svdl_result_free(self.res))
+        except Exception:
+            pass
+
+
 def svdl(op: LinearOperator, opts: GklOptions) -> SvdlResult:
-    """svdl (gkl.hpp:196, gkl.cpp:416-514)."""
+    """svdl (gkl.hpp:196, gkl.cpp:416-514). U and V are Fortran-ordered views
+    of the library's result buffers (no copy); the buffers are released with
+    the last view."""
     o = opts._c()
     res = C.POINTER(_lib.gkb_svdl_result)()
     check(lib.gkb_svdl(op._h, C.byref(o), C.byref(res)))
-    try:
-        r = res.contents
-        cnt, m, n = r.count, r.m, r.n
+    owner = _SvdlResultOwner(res)
+    r = res.contents
+    cnt, m, n = r.count, r.m, r.n
 
-        def arr(p, k):
-            return np.ctypeslib.as_array(p, shape=(k,)).copy() if k > 0 else np.zeros(0)
+    def arr(p, k):
+        return np.ctypeslib.as_array(p, shape=(k,)).copy() if k > 0 else np.zeros(0)
 
-        singvals = arr(r.singvals, cnt)
-        def cols(p, rows):  # column-major rows x cnt: one copy, Fortran order
-            if not cnt:
-                return np.zeros((rows, 0))
-            return np.ctypeslib.as_array(p, shape=(cnt, rows)).T.copy(order="F")
+    def cols(p, rows):  # column-major rows x cnt, viewed in place
+        if not cnt:
+            return np.zeros((rows, 0))
+        v = np.ctypeslib.as_array(p, shape=(cnt, rows)).T.view(_OwnedArray)
+        v._owner = owner
+        return v
 
-        U = cols(r.U, m)
-        V = cols(r.V, n)
-        err = arr(r.err_estimates, cnt)
-        conv = (np.ctypeslib.as_array(r.converged, shape=(cnt,)).astype(bool).copy()
-                if cnt else np.zeros(0, dtype=bool))
-        st = SvdlStats(mvps=r.mvps, steps=r.steps, restarts=r.restarts,
-                       reorth_count=r.reorth_count, deflations=r.deflations,
-                       converged=bool(r.all_converged), wall_seconds=r.wall_seconds,
-                       device_seconds=r.device_seconds, host_syncs=r.host_syncs)
-        if r.history_len > 0:
-            k = int(opts.k)
-            h = arr(r.ritz_history, r.history_len * k).reshape(r.history_len, k)
-            e = arr(r.err_history, r.history_len * k).reshape(r.history_len, k)
-            st.ritz_history = [row[~np.isnan(row)] for row in h]
-            st.err_history = [row[~np.isnan(row)] for row in e]
-        return SvdlResult(singvals, U, V, err, conv, st)
-    finally:
-        check(lib.gkb_svdl_result_free(res))
+    singvals = arr(r.singvals, cnt)
+    U = cols(r.U, m)
+    V = cols(r.V, n)
+    err = arr(r.err_estimates, cnt)
+    conv = (np.ctypeslib.as_array(r.converged, shape=(cnt,)).astype(bool).copy()
+            if cnt else np.zeros(0, dtype=bool))
+    st = SvdlStats(mvps=r.mvps, steps=r.steps, restarts=r.restarts,
+                   reorth_count=r.reorth_count, deflations=r.deflations,
+                   converged=bool(r.all_converged), wall_seconds=r.wall_seconds,
+                   device_seconds=r.device_seconds, host_syncs=r.host_syncs)
+    if r.history_len > 0:
+        k = int(opts.k)
+        h = arr(r.ritz_history, r.history_len * k).reshape(r.history_len, k)
+        e = arr(r.err_history, r.history_len * k).reshape(r.history_len, k)
+        st.ritz_history = [row[~np.isnan(row)] for row in h]
+        st.err_history = [row[~np.isnan(row)] for row in e]
+    return SvdlResult(singvals, U, V, err, conv, st)
 
 
 @dataclass
