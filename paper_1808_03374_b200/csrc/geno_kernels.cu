@@ -54,6 +54,8 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kStripsPerWarp = GKB_SPW;  // row strips sharing each B fragment
 constexpr int kDepth = 2;                // tiles in flight per strip
+constexpr int kFullRange = 14;  // pm_plan's default kt_cta: fully unrolled main loop
+static_assert(kStripsPerWarp <= 2, "the unrolled full-range loop prefetches strips 0 and 1");
 constexpr int kRowsPerCta = 8 * kStripsPerWarp * 16;  // 256
 constexpr int kStripsPerCta = 8 * kStripsPerWarp;
 constexpr int kMinCtas = kStripsPerWarp <= 2 ? 4 : 3;  // per SM (register budget)
@@ -539,10 +541,34 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     bp += 64;                                                              \
     ++t;                                                                   \
   }
-  for (int t = 0; t < ktiles;) {
-    GKB_PM_STEP(bA, bC)
-    GKB_PM_STEP(bB, bA)
-    GKB_PM_STEP(bC, bB)
+  if (ktiles == kFullRange) {
+    // a full range: trip count known at compile time, fully unrolled -- no
+    // per-tile bound test, clamp or counter; prefetch offsets are constants
+    const uint4* p0 = src;
+    const uint4* p1 = src + KT * 32;
+#define GKB_PM_FULL(T, CUR, DST)                                           \
+    {                                                                      \
+      const uint4 b01 = bp[(T) * 64], b23 = bp[(T) * 64 + 32];             \
+      if ((T) + 2 < kFullRange) {                                          \
+        DST[0] = ld_stream(p0 + ((T) + 2) * 32);                           \
+        if (kStripsPerWarp > 1) DST[kStripsPerWarp - 1] = ld_stream(p1 + ((T) + 2) * 32); \
+      }                                                                    \
+      _Pragma("unroll") for (int r = 0; r < kStripsPerWarp; ++r)           \
+        mma_tile(acc[r], CUR[r], b01, b23);                                \
+    }
+#pragma unroll
+    for (int T = 0; T < kFullRange; T += 3) {
+      GKB_PM_FULL(T, bA, bC)
+      if (T + 1 < kFullRange) GKB_PM_FULL(T + 1, bB, bA)
+      if (T + 2 < kFullRange) GKB_PM_FULL(T + 2, bC, bB)
+    }
+#undef GKB_PM_FULL
+  } else {
+    for (int t = 0; t < ktiles;) {
+      GKB_PM_STEP(bA, bC)
+      GKB_PM_STEP(bB, bA)
+      GKB_PM_STEP(bC, bB)
+    }
   }
 #undef GKB_PM_STEP
   if (m_off) {
