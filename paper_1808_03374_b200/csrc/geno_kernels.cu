@@ -638,6 +638,215 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
 }
 
 
+// ---------------------------------------------------------------- two vectors per pass
+// Block products ("decode amortized over k"): the same
+// kernel for two coefficient vectors at once. Each tile is loaded and expanded
+// once; every group of four A registers feeds one MMA per vector. Digits,
+// integer sums, the epilogue and the list walk are the single-vector kernel's,
+// in the same order, so each column equals its single-vector product bit for
+// bit. 3 CTAs/SM (two digit sets and two coefficient stagings in shared memory).
+struct PM2Args {
+  const uint4* dig[2];
+  const int* dexp[2];
+  const double* dsum[2];
+  const double* cval[2];
+  double* part[2];
+};
+
+__device__ __forceinline__ void mma_tile2(int (&a0)[4], int (&a1)[4], const uint4 w,
+                                          const uint4 b01a, const uint4 b23a, const uint4 b01b,
+                                          const uint4 b23b) {
+  const uint32_t m0 = 0x03030303u, m1 = m0 << 2, m2 = m0 << 4, m3 = m0 << 6;
+  uint32_t p0 = w.x & m0, p1 = w.y & m0, p2 = w.x & m1, p3 = w.y & m1;
+  mma_u8s8(a0, p0, p1, p2, p3, b01a.x, b01a.y);
+  mma_u8s8(a1, p0, p1, p2, p3, b01b.x, b01b.y);
+  p0 = w.x & m2; p1 = w.y & m2; p2 = w.x & m3; p3 = w.y & m3;
+  mma_u8s8(a0, p0, p1, p2, p3, b01a.z, b01a.w);
+  mma_u8s8(a1, p0, p1, p2, p3, b01b.z, b01b.w);
+  p0 = w.z & m0; p1 = w.w & m0; p2 = w.z & m1; p3 = w.w & m1;
+  mma_u8s8(a0, p0, p1, p2, p3, b23a.x, b23a.y);
+  mma_u8s8(a1, p0, p1, p2, p3, b23b.x, b23b.y);
+  p0 = w.z & m2; p1 = w.w & m2; p2 = w.z & m3; p3 = w.w & m3;
+  mma_u8s8(a0, p0, p1, p2, p3, b23a.z, b23a.w);
+  mma_u8s8(a1, p0, p1, p2, p3, b23b.z, b23b.w);
+}
+
+// walk_list for two coefficient vectors (same entries, same order per vector)
+__device__ __forceinline__ void walk_list2(const uint16_t* __restrict__ ent, uint32_t k0,
+                                           uint32_t ke, const double* __restrict__ cva,
+                                           const double* __restrict__ cvb, double& ca,
+                                           double& cb) {
+  double sa = 0.0, sb = 0.0;
+  uint32_t k = k0;
+#pragma unroll 1
+  for (; k + 4 <= ke; k += 4) {
+    const int c0 = ent[k], c1 = ent[k + 1], c2 = ent[k + 2], c3 = ent[k + 3];
+    sa += cva[c0];
+    sa += cva[c1];
+    sa += cva[c2];
+    sa += cva[c3];
+    sb += cvb[c0];
+    sb += cvb[c1];
+    sb += cvb[c2];
+    sb += cvb[c3];
+  }
+#pragma unroll 1
+  for (; k < ke; ++k) {
+    const int c = ent[k];
+    sa += cva[c];
+    sb += cvb[c];
+  }
+  ca = sa;
+  cb = sb;
+}
+
+size_t pm2_smem_bytes(int kt_cta) {
+  return 2 * (size_t)kt_cta * 64 * 16 + kOffBytes + 2 * kEntCap + 16 + 2 * (size_t)kt_cta * 128 * 8;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
+    const uint4* __restrict__ lay, int64_t KT, int kt_cta, PM2Args a,
+    const double* __restrict__ mu, const double* __restrict__ mean,
+    const uint32_t* __restrict__ m_off, const int64_t* __restrict__ m_base,
+    const uint16_t* __restrict__ m_ent, int64_t rows_pad, int64_t C) {
+  extern __shared__ __align__(16) uint4 dg[];  // 2 x kt_cta * 64 digits, then list staging
+  const int kc = blockIdx.y;
+  const int64_t kt0 = (int64_t)kc * kt_cta;
+  const int ktiles = (int)min((int64_t)kt_cta, KT - kt0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tid = lane & 3;
+  const int64_t strip0 = ((int64_t)blockIdx.x * 8 + warp) * kStripsPerWarp;
+  const uint4* src = lay + (strip0 * KT + kt0) * 32 + lane;
+  const int64_t b = (int64_t)kc * gridDim.x + blockIdx.x;
+  const int64_t col0 = kt0 * 128;
+  const uint4 Z = make_uint4(0, 0, 0, 0);
+  int acc0[kStripsPerWarp][4], acc1[kStripsPerWarp][4];
+  uint4 bA[kStripsPerWarp], bB[kStripsPerWarp], bC[kStripsPerWarp];
+  const uint4* nxt[kStripsPerWarp];
+  pdl_trigger();
+#pragma unroll
+  for (int r = 0; r < kStripsPerWarp; ++r) {
+    acc0[r][0] = acc0[r][1] = acc0[r][2] = acc0[r][3] = 0;
+    acc1[r][0] = acc1[r][1] = acc1[r][2] = acc1[r][3] = 0;
+    const uint4* p = src + r * KT * 32;
+    bA[r] = ktiles > 0 ? ld_stream(p) : Z;
+    bB[r] = ktiles > 1 ? ld_stream(p + 32) : Z;
+    bC[r] = Z;
+    nxt[r] = p + 32 * min(2, max(ktiles - 1, 0));
+  }
+  uint4* dg1 = dg + kt_cta * 64;
+  uint8_t* stage = reinterpret_cast<uint8_t*>(dg + 2 * kt_cta * 64);
+  uint32_t* offs = reinterpret_cast<uint32_t*>(stage);
+  double* cvs0 = reinterpret_cast<double*>(stage + kOffBytes + 2 * kEntCap + 16);
+  double* cvs1 = cvs0 + kt_cta * 128;
+  int ent_shift = -1;
+  int64_t eb = 0;
+  if (m_off) {
+    for (int i = threadIdx.x; i <= kRowsPerCta; i += kThreads)
+      cp_async4(offs + i, m_off + b * (kRowsPerCta + 1) + i);
+    eb = m_base[b];
+    const int64_t ne = m_off[b * (kRowsPerCta + 1) + kRowsPerCta];
+    const int64_t a0 = (eb * 2) & ~int64_t(15), a1 = (eb * 2 + ne * 2 + 15) & ~int64_t(15);
+    if (a1 - a0 <= 2 * kEntCap) {
+      const uint8_t* esrc = reinterpret_cast<const uint8_t*>(m_ent) + a0;
+      for (int64_t i = threadIdx.x; i < (a1 - a0) / 16; i += kThreads)
+        cp_async16(stage + kOffBytes + 16 * i, esrc + 16 * i);
+      ent_shift = (int)(eb - a0 / 2);
+    }
+  }
+  pdl_wait();
+  if (m_off) {
+    const int ncol = (int)min((int64_t)ktiles * 128, C - col0);
+    for (int i = threadIdx.x; i < ncol; i += kThreads) {
+      cp_async8(cvs0 + i, a.cval[0] + col0 + i);
+      cp_async8(cvs1 + i, a.cval[1] + col0 + i);
+    }
+    cp_async_commit();
+  }
+  {
+    const uint4* gd0 = a.dig[0] + kt0 * 64;
+    const uint4* gd1 = a.dig[1] + kt0 * 64;
+    for (int i = threadIdx.x; i < ktiles * 64; i += kThreads) {
+      dg[i] = gd0[i];
+      dg1[i] = gd1[i];
+    }
+  }
+  __syncthreads();
+  const int sw = g ^ (2 * tid);
+  const uint4* bp = dg + tid * 8 + sw;
+#define GKB_PM2_STEP(CUR, DST)                                             \
+  if (t < ktiles) {                                                        \
+    const uint4 b01a = bp[0], b23a = bp[32];                               \
+    const uint4 b01b = bp[kt_cta * 64], b23b = bp[kt_cta * 64 + 32];       \
+    const bool adv = t + 2 < ktiles - 1;                                   \
+    _Pragma("unroll") for (int r = 0; r < kStripsPerWarp; ++r) {           \
+      DST[r] = ld_stream(nxt[r]);                                          \
+      nxt[r] += adv ? 32 : 0;                                              \
+      mma_tile2(acc0[r], acc1[r], CUR[r], b01a, b23a, b01b, b23b);         \
+    }                                                                      \
+    bp += 64;                                                              \
+    ++t;                                                                   \
+  }
+  for (int t = 0; t < ktiles;) {
+    GKB_PM2_STEP(bA, bC)
+    GKB_PM2_STEP(bB, bA)
+    GKB_PM2_STEP(bC, bB)
+  }
+#undef GKB_PM2_STEP
+  if (m_off) {
+    cp_async_wait_all();
+    __syncthreads();
+  }
+  const int E0 = a.dexp[0][kc], E1 = a.dexp[1][kc];
+  const double rs0 = a.dsum[0][kc], rs1 = a.dsum[1][kc];
+  const double p0 = pow2(16 * tid), p1 = pow2(16 * tid + 8);
+#pragma unroll
+  for (int r = 0; r < kStripsPerWarp; ++r) {
+    double u0 = (double)acc0[r][0] * p0 + (double)acc0[r][1] * p1;
+    double u1 = (double)acc0[r][2] * p0 + (double)acc0[r][3] * p1;
+    double v0 = (double)acc1[r][0] * p0 + (double)acc1[r][1] * p1;
+    double v1 = (double)acc1[r][2] * p0 + (double)acc1[r][3] * p1;
+    u0 += __shfl_xor_sync(0xffffffffu, u0, 1);
+    u0 += __shfl_xor_sync(0xffffffffu, u0, 2);
+    u1 += __shfl_xor_sync(0xffffffffu, u1, 1);
+    u1 += __shfl_xor_sync(0xffffffffu, u1, 2);
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+    const int hi = tid & 1;
+    const int64_t row = (strip0 + r) * 16 + g + 8 * hi;
+    const int rl = (int)(row - (int64_t)blockIdx.x * kRowsPerCta);
+    const double val0 = scalbn(hi ? u1 : u0, E0 - 62);
+    const double val1 = scalbn(hi ? v1 : v0, E1 - 62);
+    double c0 = 0.0, c1 = 0.0;
+    if (m_off) {
+      const uint32_t e0 = offs[rl], e1 = offs[rl + 1], mid = e0 + (e1 - e0) / 2;
+      const uint32_t k0 = (tid >> 1) ? mid : e0, ke = (tid >> 1) ? e1 : mid;
+      if (ent_shift >= 0)
+        walk_list2(reinterpret_cast<const uint16_t*>(stage + kOffBytes) + ent_shift, k0, ke, cvs0,
+                   cvs1, c0, c1);
+      else
+        walk_list2(m_ent + eb, k0, ke, cvs0, cvs1, c0, c1);
+      c0 += __shfl_xor_sync(0xffffffffu, c0, 2);
+      c1 += __shfl_xor_sync(0xffffffffu, c1, 2);
+    }
+    if ((tid >> 1) == 0) {
+      double o0, o1;
+      if (MODE == 0) {
+        o0 = val0 - mu[row] * rs0 - (3.0 - mean[row]) * c0;
+        o1 = val1 - mu[row] * rs1 - (3.0 - mean[row]) * c1;
+      } else {
+        o0 = val0 - rs0 - c0;
+        o1 = val1 - rs1 - c1;
+      }
+      a.part[0][(int64_t)kc * rows_pad + row] = o0;
+      a.part[1][(int64_t)kc * rows_pad + row] = o1;
+    }
+  }
+}
+
 // K1 finish: y_j = inv_s_j * sum_kc part[kc][j] (ranges in order)
 __global__ void k1_reduce(const double* __restrict__ part, int nkc, int64_t rows_pad,
                           int64_t p_loc, const double* __restrict__ inv_s,
@@ -824,6 +1033,74 @@ void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s) {
   launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, true);
   launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
              (const double*)g.s2.part, g.pl2.nkc, g.pl2.rows_pad, g.n, z);
+}
+
+// ---- two vectors per pass (block products) ------------------------------
+namespace {
+template <int MODE>
+void digitize_into(const GenoView& g, const PMPlan& pl, const double* v, const PMScratch& sc,
+                   cudaStream_t s, bool pdl) {
+  allow_smem(k_digitize<MODE>, pl.dig_smem);
+  if (MODE == 0)
+    launch_pdl(k_digitize<0>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, pdl, v,
+               (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, g.n,
+               pl.kt_cta, sc.dig, sc.dexp, sc.dsum, (double*)nullptr);
+  else
+    launch_pdl(k_digitize<1>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, pdl, v,
+               (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc,
+               pl.kt_cta, sc.dig, sc.dexp, sc.dsum, sc.cm);
+}
+
+template <int MODE>
+void launch_main2(const GenoView& g, const PMPlan& pl, const uint4* lay, const PMScratch& s0,
+                  const PMScratch& s1, const double* cv0, const double* cv1, const MissLists& ml,
+                  cudaStream_t s) {
+  const size_t smem = pm2_smem_bytes(pl.kt_cta);
+  allow_smem(k_pm_main2<MODE>, smem);
+  PM2Args a;
+  a.dig[0] = s0.dig;
+  a.dig[1] = s1.dig;
+  a.dexp[0] = s0.dexp;
+  a.dexp[1] = s1.dexp;
+  a.dsum[0] = s0.dsum;
+  a.dsum[1] = s1.dsum;
+  a.cval[0] = cv0;
+  a.cval[1] = cv1;
+  a.part[0] = s0.part;
+  a.part[1] = s1.part;
+  launch_pdl(k_pm_main2<MODE>, dim3((unsigned)pl.grid_x, (unsigned)pl.nkc), dim3(kThreads), smem,
+             s, true, lay, pl.KT, pl.kt_cta, a, (const double*)g.mu, (const double*)g.mean,
+             ml.off, ml.base, ml.ent, pl.rows_pad, pl.C);
+}
+}  // namespace
+
+void k1_apply2(const GenoView& g, const PMScratch& sb, const double* x0, const double* x1,
+               double* y0, double* y1, cudaStream_t s) {
+  if (g.p_loc == 0) return;
+  digitize_into<0>(g, g.pl1, x0, g.s1, s, true);
+  digitize_into<0>(g, g.pl1, x1, sb, s, true);
+  launch_main2<0>(g, g.pl1, g.lt1, g.s1, sb, x0, x1, g.m1, s);
+  for (int v = 0; v < 2; ++v)
+    launch_pdl(k1_reduce, dim3((unsigned)((g.p_loc + 255) / 256)), dim3(256), 0, s, true,
+               (const double*)(v ? sb.part : g.s1.part), g.pl1.nkc, g.pl1.rows_pad, g.p_loc,
+               (const double*)g.inv_s, v ? y1 : y0);
+}
+
+void k2_adjoint2(const GenoView& g, const PMScratch& sb, const double* y0, const double* y1,
+                 double* z0, double* z1, cudaStream_t s) {
+  if (g.n == 0) return;
+  if (g.p_loc == 0) {
+    cudaMemsetAsync(z0, 0, sizeof(double) * (size_t)g.n, s);
+    cudaMemsetAsync(z1, 0, sizeof(double) * (size_t)g.n, s);
+    return;
+  }
+  digitize_into<1>(g, g.pl2, y0, g.s2, s, true);
+  digitize_into<1>(g, g.pl2, y1, sb, s, true);
+  launch_main2<1>(g, g.pl2, g.lt2, g.s2, sb, g.s2.cm, sb.cm, g.m2, s);
+  for (int v = 0; v < 2; ++v)
+    launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
+               (const double*)(v ? sb.part : g.s2.part), g.pl2.nkc, g.pl2.rows_pad, g.n,
+               v ? z1 : z0);
 }
 
 }  // namespace dev

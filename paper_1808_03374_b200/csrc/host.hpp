@@ -121,6 +121,14 @@ struct DevOp {
   bool direct_io(const void* a, const void* b) const;
   // k columns per call (column-major host blocks): one H2D, k device products
   // back to back, one D2H (the block form subspace iteration uses)
+  // Device blocks, column-major per shard: X[i] n x k (ldx), Y[i] rows(i) x k
+  // (ldy[i]); the adjoint's Z[i] n x k (ldz) is summed across shards. Default:
+  // one column at a time; an operator may do several columns per pass.
+  virtual void apply_block_dev(const std::vector<const double*>& X, int64_t ldx, int64_t k,
+                               const std::vector<double*>& Y, const std::vector<int64_t>& ldy);
+  virtual void adjoint_block_dev(const std::vector<const double*>& Yb,
+                                 const std::vector<int64_t>& ldyb, int64_t k,
+                                 const std::vector<double*>& Z, int64_t ldz);
   void apply_block_host(const double* X, int64_t k, double* Y);
   void adjoint_block_host(const double* Y, int64_t k, double* Z);
   std::vector<double*> bin_, bout_;  // per shard block buffers (grow-only)
@@ -141,6 +149,7 @@ struct GenoShard {
   double* inv_s = nullptr;
   int64_t* counts = nullptr;  // device p_loc*4
   int64_t nmissing = 0;
+  dev::PMScratch s1b{}, s2b{};  // second scratch sets (two-vector block products), lazily
   // per-CTA missing lists of the two layouts (kernels.hpp MissLists)
   uint32_t* m1_off = nullptr;
   int64_t* m1_base = nullptr;
@@ -166,6 +175,10 @@ struct GenoOp : DevOp {
   void set_scaling(const double* mu, const double* inv_s);  // global p arrays
   void get_scaling(double* mu, double* inv_s);
   void apply_dev(const std::vector<const double*>& x, const std::vector<double*>& y) override;
+  void apply_block_dev(const std::vector<const double*>& X, int64_t ldx, int64_t k,
+                       const std::vector<double*>& Y, const std::vector<int64_t>& ldy) override;
+  void adjoint_block_dev(const std::vector<const double*>& Yb, const std::vector<int64_t>& ldyb,
+                         int64_t k, const std::vector<double*>& Z, int64_t ldz) override;
   void adjoint_dev(const std::vector<const double*>& y, const std::vector<double*>& z) override;
   int64_t packed_bytes() const;
   int64_t device_bytes() const;

@@ -91,6 +91,12 @@ void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s,
               bool stream_out = false);
 // K2 apply_adjoint (reference X^T*y, per-sample sum) over the local SNPs; z has n entries.
 void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s);
+// Two vectors per pass (block products): each column bitwise equal to the
+// single-vector product. `sb` is a second scratch set of the layout (vector 1).
+void k1_apply2(const GenoView& g, const PMScratch& sb, const double* x0, const double* x1,
+               double* y0, double* y1, cudaStream_t s);
+void k2_adjoint2(const GenoView& g, const PMScratch& sb, const double* y0, const double* y1,
+                 double* z0, double* z1, cudaStream_t s);
 // Pieces (for timing breakdowns): digitize, then the main tensor-core kernel.
 void k1_digitize(const GenoView& g, const double* x, cudaStream_t s);
 void k2_digitize(const GenoView& g, const double* y, cudaStream_t s);

@@ -154,6 +154,35 @@ void DevOp::ensure_block_buffers(int64_t in_doubles, int64_t out_doubles) {
   }
 }
 
+void DevOp::apply_block_dev(const std::vector<const double*>& X, int64_t ldx, int64_t k,
+                            const std::vector<double*>& Y, const std::vector<int64_t>& ldy) {
+  const int L = (int)ctx->shards.size();
+  for (int64_t c = 0; c < k; ++c) {
+    std::vector<const double*> xi(L);
+    std::vector<double*> yi(L);
+    for (int i = 0; i < L; ++i) {
+      xi[i] = X[i] + c * ldx;
+      yi[i] = Y[i] + c * ldy[i];
+    }
+    apply_dev(xi, yi);
+  }
+}
+
+void DevOp::adjoint_block_dev(const std::vector<const double*>& Yb,
+                              const std::vector<int64_t>& ldyb, int64_t k,
+                              const std::vector<double*>& Z, int64_t ldz) {
+  const int L = (int)ctx->shards.size();
+  for (int64_t c = 0; c < k; ++c) {
+    std::vector<const double*> yi(L);
+    std::vector<double*> zi(L);
+    for (int i = 0; i < L; ++i) {
+      yi[i] = Yb[i] + c * ldyb[i];
+      zi[i] = Z[i] + c * ldz;
+    }
+    adjoint_dev(yi, zi);
+  }
+}
+
 void DevOp::apply_block_host(const double* X, int64_t k, double* Y) {
   const int L = (int)ctx->shards.size();
   const bool spmd = ctx->use_nccl && ctx->nshards_total > 1;
@@ -167,14 +196,16 @@ void DevOp::apply_block_host(const double* X, int64_t k, double* Y) {
     GKB_CUDA(cudaMemcpyAsync(bin_[i], X, sizeof(double) * (size_t)(n * k), cudaMemcpyHostToDevice,
                              ctx->shards[i].stream));
   }
-  for (int64_t c = 0; c < k; ++c) {
-    std::vector<const double*> xi(L);
-    std::vector<double*> yi(L);
+  {
+    std::vector<const double*> xb(L);
+    std::vector<double*> yb(L);
+    std::vector<int64_t> ld(L);
     for (int i = 0; i < L; ++i) {
-      xi[i] = bin_[i] + c * n;
-      yi[i] = spmd ? bout_[i] + c * m + row0(i) : bout_[i] + c * rows(i);
+      xb[i] = bin_[i];
+      yb[i] = spmd ? bout_[i] + row0(i) : bout_[i];
+      ld[i] = spmd ? m : rows(i);
     }
-    apply_dev(xi, yi);
+    apply_block_dev(xb, n, k, yb, ld);
   }
   if (spmd) {
     // zero the other ranks' rows of every column, then one allreduce of m*k
@@ -215,14 +246,16 @@ void DevOp::adjoint_block_host(const double* Yh, int64_t k, double* Z) {
                                sizeof(double) * (size_t)m, sizeof(double) * (size_t)rows(i),
                                (size_t)k, cudaMemcpyHostToDevice, ctx->shards[i].stream));
   }
-  for (int64_t c = 0; c < k; ++c) {
-    std::vector<const double*> yi(L);
-    std::vector<double*> zi(L);
+  {
+    std::vector<const double*> yb(L);
+    std::vector<double*> zb(L);
+    std::vector<int64_t> ld(L);
     for (int i = 0; i < L; ++i) {
-      yi[i] = bin_[i] + c * rows(i);
-      zi[i] = bout_[i] + c * n;
+      yb[i] = bin_[i];
+      zb[i] = bout_[i];
+      ld[i] = rows(i);
     }
-    adjoint_dev(yi, zi);
+    adjoint_block_dev(yb, ld, k, zb, n);
   }
   ctx->set_device(0);
   GKB_CUDA(cudaMemcpyAsync(Z, bout_[0], sizeof(double) * (size_t)(n * k), cudaMemcpyDeviceToHost,
@@ -369,6 +402,8 @@ GenoOp::~GenoOp() {
       if (p) cudaFreeAsync(p, st);
     free_scratch(g.s1, st);
     free_scratch(g.s2, st);
+    free_scratch(g.s1b, st);
+    free_scratch(g.s2b, st);
     cudaStreamSynchronize(st);
   }
 }
@@ -742,6 +777,67 @@ void GenoOp::apply_dev(const std::vector<const double*>& x, const std::vector<do
     ctx->set_device((int)i);
     dev::k1_apply(gs[i].view(), x[i], y[i], ctx->shards[i].stream, host_out_);
     GKB_LAUNCH_CHECK();
+  }
+}
+
+// Column pairs through the two-vector kernel (each column bitwise the
+// single-vector product); an odd last column goes alone.
+void GenoOp::apply_block_dev(const std::vector<const double*>& X, int64_t ldx, int64_t k,
+                             const std::vector<double*>& Y, const std::vector<int64_t>& ldy) {
+  if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
+  int64_t c = 0;
+  for (; c + 2 <= k; c += 2)
+    for (size_t i = 0; i < gs.size(); ++i) {
+      ctx->set_device((int)i);
+      GenoShard& g = gs[i];
+      cudaStream_t st = ctx->shards[i].stream;
+      if (!g.s1b.part) alloc_scratch(g.pl1, false, g.s1b, st);
+      dev::k1_apply2(g.view(), g.s1b, X[i] + c * ldx, X[i] + (c + 1) * ldx, Y[i] + c * ldy[i],
+                     Y[i] + (c + 1) * ldy[i], st);
+      GKB_LAUNCH_CHECK();
+    }
+  if (c < k) {
+    const int L = (int)gs.size();
+    std::vector<const double*> xi(L);
+    std::vector<double*> yi(L);
+    for (int i = 0; i < L; ++i) {
+      xi[i] = X[i] + c * ldx;
+      yi[i] = Y[i] + c * ldy[i];
+    }
+    apply_dev(xi, yi);
+  }
+}
+
+void GenoOp::adjoint_block_dev(const std::vector<const double*>& Yb,
+                               const std::vector<int64_t>& ldyb, int64_t k,
+                               const std::vector<double*>& Z, int64_t ldz) {
+  if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
+  const int L = (int)gs.size();
+  int64_t c = 0;
+  for (; c + 2 <= k; c += 2) {
+    for (int i = 0; i < L; ++i) {
+      ctx->set_device(i);
+      GenoShard& g = gs[i];
+      cudaStream_t st = ctx->shards[i].stream;
+      if (!g.s2b.part) alloc_scratch(g.pl2, true, g.s2b, st);
+      dev::k2_adjoint2(g.view(), g.s2b, Yb[i] + c * ldyb[i], Yb[i] + (c + 1) * ldyb[i],
+                       Z[i] + c * ldz, Z[i] + (c + 1) * ldz, st);
+      GKB_LAUNCH_CHECK();
+    }
+    for (int64_t q = c; q < c + 2; ++q) {  // cross-shard sums, column by column
+      std::vector<double*> zq(L);
+      for (int i = 0; i < L; ++i) zq[i] = Z[i] + q * ldz;
+      ctx->allreduce(zq, n);
+    }
+  }
+  if (c < k) {
+    std::vector<const double*> yi(L);
+    std::vector<double*> zi(L);
+    for (int i = 0; i < L; ++i) {
+      yi[i] = Yb[i] + c * ldyb[i];
+      zi[i] = Z[i] + c * ldz;
+    }
+    adjoint_dev(yi, zi);
   }
 }
 

@@ -10,7 +10,8 @@
 // orthogonality. Cholesky's R has a positive diagonal, so Q is the same
 // sign-fixed factor up to rounding. The condition of the orthonormal Q follows
 // from the second pass on the host (Q^T Q = R2^-T G2 R2^-1). The gram pass
-// X X^T is k adjoint + k apply products back to back; the convergence test
+// X X^T is a k-column adjoint + apply block (two columns per pass on the
+// genotype operator); the convergence test
 // ||Y - Y_prev||_F is a device reduction. Per iteration the host reads two
 // k x k Gram matrices and one scalar.
 //
@@ -199,19 +200,18 @@ SubspaceOutput subspace_qr_device(DevOp* op, int64_t k, double tol, int64_t max_
     };
     int64_t mvps = 0;
     // X X^T on the block Y -> W, column by column (subspace.cpp:70-77)
+    // (block products: the operator may take several columns per pass)
     auto gram_apply = [&]() {
-      for (int64_t j = 0; j < k; ++j) {
-        std::vector<const double*> yin(L), zin(L);
-        std::vector<double*> zout(L), wout(L);
-        for (int i = 0; i < L; ++i) {
-          yin[i] = Y[i] + j * r[i];
-          zout[i] = Z[i] + j * n;
-          zin[i] = zout[i];
-          wout[i] = W[i] + j * r[i];
-        }
-        op->adjoint_dev(yin, zout);
-        op->apply_dev(zin, wout);
+      std::vector<const double*> yin(L), zin(L);
+      std::vector<double*> zout(L), wout(L);
+      for (int i = 0; i < L; ++i) {
+        yin[i] = Y[i];
+        zout[i] = Z[i];
+        zin[i] = Z[i];
+        wout[i] = W[i];
       }
+      op->adjoint_block_dev(yin, r, k, zout, n);
+      op->apply_block_dev(zin, n, k, wout, r);
       mvps += 2 * k;
     };
 
@@ -278,14 +278,14 @@ SubspaceOutput subspace_qr_device(DevOp* op, int64_t k, double tol, int64_t max_
     }
     out.rank_deficient = out.invcond_history.back() < 1e-12;
     // Rayleigh-Ritz: singular values of X^T Q (subspace.cpp:103-110)
-    for (int64_t j = 0; j < k; ++j) {
+    {
       std::vector<const double*> yin(L);
       std::vector<double*> zout(L);
       for (int i = 0; i < L; ++i) {
-        yin[i] = Y[i] + j * r[i];
-        zout[i] = Z[i] + j * n;
+        yin[i] = Y[i];
+        zout[i] = Z[i];
       }
-      op->adjoint_dev(yin, zout);
+      op->adjoint_block_dev(yin, r, k, zout, n);
     }
     mvps += k;
     std::vector<double> Zh((size_t)(n * k));

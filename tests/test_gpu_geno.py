@@ -178,3 +178,23 @@ def test_schemes_vs_oracle(gkb, orc, scheme):
     assert rel_err(op.apply(x), ref.apply(x)) <= 1e-12
     y = np.random.default_rng(scheme + 10).standard_normal(p)
     assert rel_err(op.apply_adjoint(y), ref.apply_adjoint(y)) <= 1e-12
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 6])
+def test_block_products_equal_single_columns(gkb, k):
+    """Block products (two columns per pass through the shared-expansion
+    kernel, an odd last column alone) give each column bit for bit the
+    single-vector product, with missing entries, several column ranges and
+    row blocks."""
+    p, n = 3001, 5003
+    payload, _ = random_payload(p, n, seed=23, missing=0.03)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
+    rng = np.random.default_rng(k)
+    X = rng.standard_normal((n, k))
+    Y = op.apply_block(X)
+    for c in range(k):
+        assert np.array_equal(Y[:, c], op.apply(X[:, c])), c
+    U = rng.standard_normal((p, k))
+    Z = op.apply_adjoint_block(U)
+    for c in range(k):
+        assert np.array_equal(Z[:, c], op.apply_adjoint(U[:, c])), c
