@@ -320,7 +320,7 @@ int gkb_op_bench(gkb_op* op, int which, int iters, int flush_l2, double* ms_per_
   return guarded([&] {
     need(op, "op");
     if (iters < 1) gkb::fail(GKB_EINVAL, "iters < 1");
-    if (which < 0 || which > 2) gkb::fail(GKB_EINVAL, "which must be 0, 1 or 2");
+    if (which < 0 || which > 3) gkb::fail(GKB_EINVAL, "which must be 0, 1, 2 or 3");
     gkb::Context& c = op->ctx->c;
     gkb::DevOp* d = op->op.get();
     const int L = (int)c.shards.size();
@@ -378,17 +378,38 @@ int gkb_op_bench(gkb_op* op, int which, int iters, int flush_l2, double* ms_per_
     };
     double flush_ms = 0.0;
     if (flush_l2) flush_ms = timed([&] { flush_all(); });
+    // which 3: a two-column block of each product (operator block path)
+    double *X2 = nullptr, *Y2 = nullptr, *Z2 = nullptr;
+    if (which == 3) {
+      if (L != 1) gkb::fail(GKB_EINVAL, "bench: which 3 needs a single shard");
+      c.set_device(0);
+      GKB_CUDA(cudaMalloc(&X2, sizeof(double) * (size_t)(2 * d->n)));
+      GKB_CUDA(cudaMalloc(&Y2, sizeof(double) * (size_t)(2 * std::max<int64_t>(d->m, 1))));
+      GKB_CUDA(cudaMalloc(&Z2, sizeof(double) * (size_t)(2 * d->n)));
+      for (int q = 0; q < 2; ++q)
+        GKB_CUDA(cudaMemcpy(X2 + q * d->n, xh.data(), sizeof(double) * (size_t)d->n,
+                            cudaMemcpyHostToDevice));
+    }
     // whole step: K1 (+reduce) and/or K2 (+reduce, +cross-shard sum)
     const double total = timed([&] {
       if (flush_l2) flush_all();
       if (which == 0 || which == 2) d->apply_dev(xi, yi);
       if (which == 1 || which == 2) d->adjoint_dev(yc, zi);
+      if (which == 3) {
+        d->apply_block_dev({X2}, d->n, 2, {Y2}, {d->m});
+        d->adjoint_block_dev({Y2}, {d->m}, 2, {Z2}, d->n);
+      }
     });
+    if (X2) cudaFree(X2);
+    if (Y2) cudaFree(Y2);
+    if (Z2) cudaFree(Z2);
     GKB_LAUNCH_CHECK();
     if (ms_per_iter) *ms_per_iter = (total - flush_ms) / iters;
     double main_ms = 0.0;
     int launches = 0;
-    if (op->geno) {
+    if (op->geno && which == 3) {
+      launches = 10 * L;  // per product pair: 2 digitize + 1 two-vector main + 2 reduce
+    } else if (op->geno) {
       gkb::GenoShard& g = op->geno->gs[0];
       const double t = timed([&] {
         if (flush_l2) flush_all();
