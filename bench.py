@@ -328,8 +328,9 @@ def run_ours(args):
                          "sample": "subspace_iterate kQr, k=10, tol 1e-8, max 40 iterations"},
             "regress": {"seconds": round(t_reg, 4), "markers": int(scan.beta.size),
                         "markers_per_s": round(scan.beta.size / t_reg, 1), "pcs": 10,
-                        "sample": "marker_scan: y ~ [1, m_i, Z] for every SNP (one 12-column "
-                                  "block product + host algebra)"},
+                        "sample": "marker_scan: y ~ [1, m_i, Z] for every SNP (12-column block "
+                                  "product, two columns per pass, and per-marker algebra on "
+                                  "the device)"},
         }
 
     peak, peak_src = load_peaks()

@@ -112,6 +112,15 @@ int gkb_geno_from_synth(gkb_ctx* ctx, const gkb_synth_spec* spec, gkb_op** op);
 
 /* Per-marker [n0, n1, n2, nmissing] (int64, p x 4), counted on the device. */
 int gkb_geno_counts(gkb_op* op, int64_t* counts);
+/* Per-marker PC-adjusted regression scan (the per-marker fits of gkpca
+ * regress, gkpca.cpp:554-680, with regress.cpp:10-65's estimates by
+ * Frisch-Waugh-Lovell): for every marker i, y ~ [1, m_i, Z] (Z: n x k,
+ * column-major, may be NULL for k = 0). Block product and per-marker algebra
+ * on the device; outputs of length p; dep[i] = 1 where the reference reports
+ * the rank-deficiency error for design column 1. */
+int gkb_geno_marker_scan(gkb_op* op, const double* y, const double* Z, int64_t k, int unbiased,
+                         double* beta, double* se, double* intercept, double* sigma2,
+                         int32_t* dep);
 /* scheme: 0 unit variance (genio.cpp:174-175), 1 binomial with clamp
  * (genio.cpp:176-180), 2 hwe sqrt(2f(1-f)) (BASELINE.json standardization),
  * 3 none (raw dosage, missing -> 0). Computes (mu, inv_s) from the device

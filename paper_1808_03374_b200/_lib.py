@@ -146,6 +146,7 @@ SIGNATURES = {
     "gkb_gkl_options_validate": (I, [C.POINTER(gkb_gkl_options), I64, I64]),
     "gkb_svdl": (I, [P, C.POINTER(gkb_gkl_options), C.POINTER(C.POINTER(gkb_svdl_result))]),
     "gkb_svdl_result_free": (I, [C.POINTER(gkb_svdl_result)]),
+    "gkb_geno_marker_scan": (I, [P, PD, PD, I64, I, PD, PD, PD, PD, C.POINTER(C.c_int32)]),
     "gkb_subspace_qr": (I, [P, I64, C.c_double, I64, C.c_uint64, I,
                             C.POINTER(C.POINTER(gkb_subspace_result))]),
     "gkb_subspace_result_free": (I, [C.POINTER(gkb_subspace_result)]),

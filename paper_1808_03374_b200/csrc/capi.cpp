@@ -202,6 +202,23 @@ int gkb_geno_counts(gkb_op* op, int64_t* counts) {
   });
 }
 
+int gkb_geno_marker_scan(gkb_op* op, const double* y, const double* Z, int64_t k, int unbiased,
+                         double* beta, double* se, double* intercept, double* sigma2,
+                         int32_t* dep) {
+  return guarded([&] {
+    auto* g = as_geno(op);
+    need(y, "y");
+    if (k < 0) gkb::fail(GKB_EINVAL, "marker_scan: k must be >= 0");
+    if (k > 0) need(Z, "Z");
+    need(beta, "beta");
+    need(se, "se");
+    need(intercept, "intercept");
+    need(sigma2, "sigma2");
+    need(dep, "dep");
+    g->marker_scan(y, Z, k, unbiased != 0, beta, se, intercept, sigma2, dep);
+  });
+}
+
 int gkb_geno_standardize(gkb_op* op, int scheme) {
   return guarded([&] {
     auto* g = as_geno(op);

@@ -847,6 +847,54 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
   }
 }
 
+// ---------------------------------------------------------------- marker scan
+// Per-marker fits y ~ [1, m_i, Z] (regress.cpp:10-65 per marker, by
+// Frisch-Waugh-Lovell -- paper_1808_03374_b200/regress.py): one thread per
+// marker i reads P[i, :] = [m_i.y, m_i.C] of the block product, the marker's
+// counts and scaling, and the shared nuisance algebra (A^-1 = (C'C)^-1, w = C'y,
+// y'y - w'A^-1 w), and writes beta, se, intercept, sigma2 and the dependency flag.
+__global__ void k_marker_scan(const double* __restrict__ P, int64_t ldp, int64_t rows, int K,
+                              const double* __restrict__ Ainv, const double* __restrict__ w,
+                              double yyc, double a0w, double denom,
+                              const int64_t* __restrict__ counts, const double* __restrict__ mu,
+                              const double* __restrict__ inv_s, const double* __restrict__ mean,
+                              double* __restrict__ beta, double* __restrict__ se,
+                              double* __restrict__ icpt, double* __restrict__ sig2,
+                              int* __restrict__ dep) {
+  extern __shared__ double ms[];  // Ainv (K x K) then w (K)
+  pdl_wait();
+  pdl_trigger();
+  for (int t = threadIdx.x; t < K * K + K; t += blockDim.x) ms[t] = t < K * K ? Ainv[t] : w[t - K * K];
+  __syncthreads();
+  const double* Ai = ms;
+  const double* ws = ms + K * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t* c = counts + 4 * i;
+    const double m = mu[i], is = inv_s[i], mn = mean[i];
+    const double q = ((double)c[0] * m * m + (double)c[1] * (1.0 - m) * (1.0 - m) +
+                      (double)c[2] * (2.0 - m) * (2.0 - m) + (double)c[3] * (mn - m) * (mn - m)) *
+                     (is * is);
+    double my = P[i], d = q, uw = 0.0, au0 = 0.0;
+    for (int a = 0; a < K; ++a) {  // AU_a = sum_b u_b Ainv[b, a];  d -= AU_a u_a
+      double au = 0.0;
+      for (int b = 0; b < K; ++b) au += P[(int64_t)(1 + b) * ldp + i] * Ai[b + a * K];
+      if (a == 0) au0 = au;
+      d -= au * P[(int64_t)(1 + a) * ldp + i];
+      uw += au * ws[a];
+    }
+    const int distinct = (c[0] > 0) + (c[1] > 0) + (c[2] > 0);
+    const double bt = (my - uw) / d;
+    const double rss = yyc - bt * bt * d;
+    const double s2 = rss / denom;
+    beta[i] = bt;
+    sig2[i] = s2;
+    se[i] = sqrt(s2 / d);
+    icpt[i] = a0w - bt * au0;
+    dep[i] = (distinct < 2 || is == 0.0 || !(d > 0.0)) ? 1 : 0;
+  }
+}
+
 // K1 finish: y_j = inv_s_j * sum_kc part[kc][j] (ranges in order)
 __global__ void k1_reduce(const double* __restrict__ part, int nkc, int64_t rows_pad,
                           int64_t p_loc, const double* __restrict__ inv_s,
@@ -1101,6 +1149,18 @@ void k2_adjoint2(const GenoView& g, const PMScratch& sb, const double* y0, const
     launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
                (const double*)(v ? sb.part : g.s2.part), g.pl2.nkc, g.pl2.rows_pad, g.n,
                v ? z1 : z0);
+}
+
+void marker_scan(const GenoView& g, const double* P, int64_t ldp, int K, const double* Ainv,
+                 const double* w, double yyc, double a0w, double denom, const int64_t* counts,
+                 double* beta, double* se, double* icpt, double* sig2, int* dep,
+                 cudaStream_t s) {
+  if (g.p_loc == 0) return;
+  const size_t sm = sizeof(double) * (size_t)(K * K + K);
+  launch_pdl(k_marker_scan, dim3((unsigned)std::min<int64_t>((g.p_loc + 255) / 256, 148 * 8)),
+             dim3(256), sm, s, true, P, ldp, g.p_loc, K, Ainv, w, yyc, a0w, denom, counts,
+             (const double*)g.mu, (const double*)g.inv_s, (const double*)g.mean, beta, se, icpt,
+             sig2, dep);
 }
 
 }  // namespace dev

@@ -182,6 +182,10 @@ struct GenoOp : DevOp {
   void adjoint_dev(const std::vector<const double*>& y, const std::vector<double*>& z) override;
   int64_t packed_bytes() const;
   int64_t device_bytes() const;
+  // per-marker regression scan (regress.py marker_scan) with the block product
+  // and the per-marker algebra on the device; host outputs of length m
+  void marker_scan(const double* y, const double* Z, int64_t k, bool unbiased, double* beta,
+                   double* se, double* icpt, double* sig2, int32_t* dep);
   void read_bed(int64_t row0, int64_t nrows, uint8_t* out);
 
  private:

@@ -97,6 +97,11 @@ void k1_apply2(const GenoView& g, const PMScratch& sb, const double* x0, const d
                double* y0, double* y1, cudaStream_t s);
 void k2_adjoint2(const GenoView& g, const PMScratch& sb, const double* y0, const double* y1,
                  double* z0, double* z1, cudaStream_t s);
+// Per-marker fits y ~ [1, m_i, Z] from the block product P = X [y, C] (rows x
+// (K+1), ldp) and the shared nuisance algebra (K = columns of C = [1, Z]).
+void marker_scan(const GenoView& g, const double* P, int64_t ldp, int K, const double* Ainv,
+                 const double* w, double yyc, double a0w, double denom, const int64_t* counts,
+                 double* beta, double* se, double* icpt, double* sig2, int* dep, cudaStream_t s);
 // Pieces (for timing breakdowns): digitize, then the main tensor-core kernel.
 void k1_digitize(const GenoView& g, const double* x, cudaStream_t s);
 void k2_digitize(const GenoView& g, const double* y, cudaStream_t s);

@@ -851,6 +851,107 @@ void GenoOp::adjoint_dev(const std::vector<const double*>& y, const std::vector<
   ctx->allreduce(z, n);
 }
 
+// Per-marker scan: [y, 1, Z] block product on the device (two columns per
+// pass), the (k+1) x (k+1) nuisance algebra on the host, one thread per marker.
+void GenoOp::marker_scan(const double* y, const double* Z, int64_t k, bool unbiased,
+                         double* beta, double* se, double* icpt, double* sig2, int32_t* dep) {
+  if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
+  if (ctx->use_nccl && ctx->nshards_total > 1)
+    fail(GKB_ELOGIC, "marker_scan: SPMD operators use the host scan");
+  const int K = (int)(k + 1);
+  const int64_t nn = n;
+  // C = [1, Z]; A = C'C, w = C'y, A^-1 (Gauss-Jordan with partial pivoting)
+  std::vector<double> A((size_t)(K * K), 0.0), wv((size_t)K, 0.0), X((size_t)(nn * (K + 1)));
+  auto Cv = [&](int64_t s2, int a) { return a == 0 ? 1.0 : Z[(int64_t)(a - 1) * nn + s2]; };
+  for (int64_t s2 = 0; s2 < nn; ++s2) {
+    X[s2] = y[s2];
+    for (int a = 0; a < K; ++a) {
+      const double ca = Cv(s2, a);
+      X[(int64_t)(1 + a) * nn + s2] = ca;
+      wv[a] += ca * y[s2];
+      for (int b = 0; b <= a; ++b) A[a + b * K] += ca * Cv(s2, b);
+    }
+  }
+  for (int a = 0; a < K; ++a)
+    for (int b = a + 1; b < K; ++b) A[a + b * K] = A[b + a * K];
+  std::vector<double> Ai((size_t)(K * K), 0.0), M(A);
+  for (int a = 0; a < K; ++a) Ai[a + a * K] = 1.0;
+  for (int c = 0; c < K; ++c) {
+    int piv = c;
+    for (int r2 = c + 1; r2 < K; ++r2)
+      if (std::fabs(M[r2 + c * K]) > std::fabs(M[piv + c * K])) piv = r2;
+    if (M[piv + c * K] == 0.0) fail(GKB_ELOGIC, "marker_scan: nuisance design is singular");
+    for (int j = 0; j < K; ++j) {
+      std::swap(M[c + j * K], M[piv + j * K]);
+      std::swap(Ai[c + j * K], Ai[piv + j * K]);
+    }
+    const double dv = M[c + c * K];
+    for (int j = 0; j < K; ++j) {
+      M[c + j * K] /= dv;
+      Ai[c + j * K] /= dv;
+    }
+    for (int r2 = 0; r2 < K; ++r2)
+      if (r2 != c) {
+        const double f = M[r2 + c * K];
+        if (f == 0.0) continue;
+        for (int j = 0; j < K; ++j) {
+          M[r2 + j * K] -= f * M[c + j * K];
+          Ai[r2 + j * K] -= f * Ai[c + j * K];
+        }
+      }
+  }
+  double yy = 0.0;
+  for (int64_t s2 = 0; s2 < nn; ++s2) yy += y[s2] * y[s2];
+  double wAw = 0.0, a0w = 0.0;
+  for (int a = 0; a < K; ++a)
+    for (int b = 0; b < K; ++b) {
+      wAw += wv[a] * Ai[a + b * K] * wv[b];
+      if (a == 0) a0w += Ai[0 + b * K] * wv[b];
+    }
+  const double yyc = yy - wAw;
+  const double denom = unbiased ? (double)(nn - (K + 1)) : (double)nn;
+  const int L = (int)gs.size();
+  int64_t rmax = 1;
+  for (int i = 0; i < L; ++i) rmax = std::max(rmax, rows(i));
+  ensure_block_buffers(nn * (K + 1), rmax * (K + 1) + 5 * rmax + 2 * (K * K + K));
+  std::vector<const double*> xb(L);
+  std::vector<double*> yb(L);
+  std::vector<int64_t> ld(L);
+  for (int i = 0; i < L; ++i) {
+    ctx->set_device(i);
+    GKB_CUDA(cudaMemcpyAsync(bin_[i], X.data(), sizeof(double) * (size_t)(nn * (K + 1)),
+                             cudaMemcpyHostToDevice, ctx->shards[i].stream));
+    xb[i] = bin_[i];
+    yb[i] = bout_[i];
+    ld[i] = rows(i);
+  }
+  apply_block_dev(xb, nn, K + 1, yb, ld);
+  std::vector<double> aw(Ai);
+  aw.insert(aw.end(), wv.begin(), wv.end());
+  for (int i = 0; i < L; ++i) {
+    ctx->set_device(i);
+    cudaStream_t st = ctx->shards[i].stream;
+    const int64_t r = rows(i);
+    double* base = bout_[i] + r * (K + 1);
+    double* dAi = base + 5 * rmax;
+    GKB_CUDA(cudaMemcpyAsync(dAi, aw.data(), sizeof(double) * aw.size(), cudaMemcpyHostToDevice, st));
+    int* ddep = reinterpret_cast<int*>(base + 4 * rmax);
+    dev::marker_scan(gs[i].view(), bout_[i], std::max<int64_t>(r, 1), K, dAi, dAi + K * K, yyc,
+                     a0w, denom, gs[i].counts, base, base + rmax, base + 2 * rmax, base + 3 * rmax,
+                     ddep, st);
+    GKB_LAUNCH_CHECK();
+    const int64_t r0 = row0(i);
+    Shard& sh = ctx->shards[i];
+    GKB_CUDA(cudaStreamSynchronize(st));
+    d2h_staged(sh, beta + r0, base, sizeof(double) * (size_t)r);
+    d2h_staged(sh, se + r0, base + rmax, sizeof(double) * (size_t)r);
+    d2h_staged(sh, icpt + r0, base + 2 * rmax, sizeof(double) * (size_t)r);
+    d2h_staged(sh, sig2 + r0, base + 3 * rmax, sizeof(double) * (size_t)r);
+    d2h_staged(sh, dep + r0, ddep, sizeof(int32_t) * (size_t)r);
+  }
+  mvps += K + 1;
+}
+
 int64_t GenoOp::packed_bytes() const {
   int64_t b = 0;
   const int64_t stride = (n + 3) / 4;

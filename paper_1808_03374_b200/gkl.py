@@ -381,6 +381,21 @@ class GenotypeOperator(LinearOperator):
         mu, inv_s = _f64(mu, self.p), _f64(inv_s, self.p)
         check(lib.gkb_geno_set_scaling(self._h, _pd(mu), _pd(inv_s)))
 
+    def marker_scan(self, y, Z=None, unbiased: bool = False):
+        """Per-marker fits y ~ [1, m_i, Z] on the device (gkb_geno_marker_scan):
+        (beta, se, intercept, sigma2, dependent) arrays of length p."""
+        y = _f64(y, self.n)
+        Zm = np.zeros((self.n, 0)) if Z is None else np.asfortranarray(
+            np.asarray(Z, dtype=np.float64).reshape(self.n, -1))
+        k = Zm.shape[1]
+        outs = [np.empty(self.p) for _ in range(4)]
+        dep = np.empty(self.p, dtype=np.int32)
+        zp = _pd(Zm) if k else C.POINTER(C.c_double)()
+        check(lib.gkb_geno_marker_scan(self._h, _pd(y), zp, k, int(bool(unbiased)),
+                                       *[_pd(o) for o in outs],
+                                       dep.ctypes.data_as(C.POINTER(C.c_int32))))
+        return (*outs, dep.astype(bool))
+
     def scaling(self):
         mu, inv_s = np.empty(self.p), np.empty(self.p)
         check(lib.gkb_geno_get_scaling(self._h, _pd(mu), _pd(inv_s)))

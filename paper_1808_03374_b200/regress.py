@@ -136,6 +136,14 @@ def marker_scan(op, y, Z: Optional[np.ndarray] = None, unbiased: bool = False,
     n = op.cols()
     if y.size != n:
         raise ValueError("marker_scan: phenotype length does not match samples")
+    if sumsq is None and constant is None and hasattr(op, "marker_scan"):
+        # genotype operator: block product and per-marker algebra on the device
+        try:
+            beta, se, icpt, s2, dep = op.marker_scan(y, Z, unbiased)
+            return MarkerScan(beta, se, icpt, s2, dep)
+        except Exception as e:  # SPMD operators keep the host algebra
+            if "SPMD" not in str(e):
+                raise
     Zm = np.zeros((n, 0)) if Z is None else np.asarray(Z, dtype=np.float64).reshape(n, -1)
     C = np.hstack([np.ones((n, 1)), Zm])                    # shared nuisance columns
     P = op.apply_block(np.hstack([y[:, None], C]))          # [m.y, m.1, m.Z] per marker
@@ -154,7 +162,8 @@ def marker_scan(op, y, Z: Optional[np.ndarray] = None, unbiased: bool = False,
         denom = float(n - kk) if unbiased else float(n)
         sigma2 = rss / denom
         se = np.sqrt(sigma2 / d)
-    intercept = (Ainv @ (w[:, None] - U.T * beta[None, :]))[0]
+    # [A^-1 (w - u_i beta_i)]_0 = (A^-1 w)_0 - beta_i (u_i' A^-1)_0  (A^-1 symmetric)
+    intercept = float(Ainv[0] @ w) - beta * AU[:, 0]
     dep = constant_markers(op) if constant is None else np.asarray(constant, dtype=bool)
     dep = dep | ~(d > 0)
     return MarkerScan(beta, se, intercept, sigma2, dep)

@@ -151,3 +151,26 @@ def test_device_scan_vs_reference_loop(gkb, R, scheme, k, unbiased):
         assert abs(scan.intercept[i] - ic) <= 1e-9 * max(1.0, abs(ic)), i
         assert abs(scan.sigma2[i] - s2) <= 1e-9 * s2, i
     assert scan.dependent[5] and scan.dependent[9]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,unbiased", [(0, False), (3, True), (10, False)])
+def test_device_marker_scan_matches_host_algebra(gkb, k, unbiased):
+    """gkb_geno_marker_scan (block product + one thread per marker on the
+    device) against the host Frisch-Waugh-Lovell algebra on the same block
+    product (regress.marker_scan with explicit sumsq/constant)."""
+    from paper_1808_03374_b200 import regress as R
+    from paper_1808_03374_b200 import synth
+    spec = synth.config_spec(2, scale=0.05)
+    op = gkb.GenotypeOperator.from_synth(spec, scheme=gkb.ScalingScheme.kHwe)
+    rng = np.random.default_rng(3 + k)
+    y = rng.standard_normal(spec.n)
+    Z = rng.standard_normal((spec.n, k)) if k else None
+    dev = R.marker_scan(op, y, Z, unbiased)
+    host = R.marker_scan(op, y, Z, unbiased, sumsq=R.marker_sumsq(op),
+                         constant=R.constant_markers(op))
+    assert np.array_equal(dev.dependent, host.dependent)
+    ok = ~host.dependent
+    for f in ("beta", "se", "intercept", "sigma2"):
+        a, b = getattr(dev, f)[ok], getattr(host, f)[ok]
+        assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)) <= 1e-8, f
