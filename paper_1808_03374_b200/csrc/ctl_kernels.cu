@@ -56,10 +56,7 @@ __device__ bool monitors_side(bool left, const Params& p, double norm_scale) {
   return left ? p.m <= p.n : p.n < p.m;
 }
 
-__global__ void __launch_bounds__(kCtlThreads) k_ctl(double* __restrict__ d, int* __restrict__ iv,
-                                                     Params p) {
-  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
-  pdl_trigger();
+__device__ void run_op(double* __restrict__ d, int* __restrict__ iv, const Params& p) {
   const Layout L = layout(p.cap);
   double* B = d + L.B;  // B(i, c) = B[i + c * cap]
   double* coup = d + L.coup;
@@ -271,6 +268,22 @@ __global__ void __launch_bounds__(kCtlThreads) k_ctl(double* __restrict__ d, int
     }
     default:
       return;
+  }
+}
+
+// One decision, or two back to back (then_op >= 0: e.g. the cgs2 end and the
+// half-step finalize, consecutive on the critical path) in one launch.
+__global__ void __launch_bounds__(kCtlThreads) k_ctl(double* __restrict__ d, int* __restrict__ iv,
+                                                     Params p) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
+  run_op(d, iv, p);
+  if (p.then_op >= 0) {
+    __syncthreads();  // the first decision's global writes are visible block-wide
+    Params q = p;
+    q.op = p.then_op;
+    q.then_op = -1;
+    run_op(d, iv, q);
   }
 }
 

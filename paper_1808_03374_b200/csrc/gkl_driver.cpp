@@ -624,13 +624,14 @@ dev::ctl::Params Lanczos::ctl_params(const Options& o, int op, int64_t s) const 
   p.eta = kCgs2Eta;
   p.eps = kEps;
   p.lo = p.hi = -1;
+  p.then_op = -1;
   return p;
 }
 
 // cgs2 (orth.hpp:19-44) with its second-pass test on the device; pass 1 runs
 // when the int at gate_slot is set (full mode: alive; partial: reorthogonalize).
 void Lanczos::cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec, int gate_slot,
-                       const Options& o, int64_t s) {
+                       const Options& o, int64_t s, int then_op) {
   using namespace dev::ctl;
   const int L = (int)ctx_->shards.size();
   const auto& Q = basis(side);
@@ -669,6 +670,7 @@ void Lanczos::cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec
     Params p = ctl_params(o, pass == 0 ? OP_CG_MID : OP_CG_END, s);
     p.ncols = ncols;
     p.side = side == kLeft ? 0 : 1;
+    if (pass == 1) p.then_op = then_op;  // e.g. the half-step finalize, same launch
     ctl(p);
   }
 }
@@ -702,9 +704,11 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
         dev::nrm2sq(w_[i], op_->rows(i), sh.rs, res(i, R_N), sh.stream, ci(i) + I_ALIVE);
       }
       reduce_left(R_N, 1);
-      ctl(ctl_params(o, OP_SQRT_L, s));
+      Params q = ctl_params(o, OP_SQRT_L, s);
+      q.then_op = OP_L_END;
+      ctl(q);
     } else {
-      cgs2_dev(kLeft, s, w_, I_ALIVE, o, s);
+      cgs2_dev(kLeft, s, w_, I_ALIVE, o, s, OP_L_END);
     }
   } else {
     const bool pat = lo >= 0;
@@ -748,10 +752,15 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
       }
       reduce_left(R_N, 1);
     }
-    ctl(ctl_params(o, OP_L_B, s));
-    if (s > 0) cgs2_dev(kLeft, s, w_, I_GRE, o, s);
+    if (s > 0) {
+      ctl(ctl_params(o, OP_L_B, s));
+      cgs2_dev(kLeft, s, w_, I_GRE, o, s, OP_L_END);
+    } else {  // no basis yet: the omega test has no rows
+      Params q = ctl_params(o, OP_L_B, s);
+      q.then_op = OP_L_END;
+      ctl(q);
+    }
   }
-  ctl(ctl_params(o, OP_L_END, s));
 
   // Right half-step: beta v_{s+1} = X^T u_{s+1} - alpha v_s.
   for (int i = 0; i < L; ++i) {
@@ -782,11 +791,10 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
       dev::nrm2sq(z_[i], n_, sh.rs, res(i, R_N), sh.stream, g);
     }
     ctl(ctl_params(o, OP_R_B, s));
-    cgs2_dev(kRight, s + 1, z_, I_GRE, o, s);
+    cgs2_dev(kRight, s + 1, z_, I_GRE, o, s, OP_R_END);
   } else {
-    cgs2_dev(kRight, s + 1, z_, I_ALIVE, o, s);
+    cgs2_dev(kRight, s + 1, z_, I_ALIVE, o, s, OP_R_END);
   }
-  ctl(ctl_params(o, OP_R_END, s));
   for (int i = 0; i < L; ++i) {
     ctx_->set_device(i);
     dev::div_copy_dv(z_[i], cd(i) + ctl_L_.sc + S_BETA, V_[i] + (s + 1) * n_, n_,

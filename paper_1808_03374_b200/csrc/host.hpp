@@ -317,7 +317,7 @@ class Lanczos {
   int* ci(int i) const { return reinterpret_cast<int*>(cd(i) + ctl_L_.nd); }
   void enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t hi);
   void cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec, int gate_slot,
-                const Options& o, int64_t s);
+                const Options& o, int64_t s, int then_op = -1);
   dev::ctl::Params ctl_params(const Options& o, int op, int64_t s) const;
 };
 

@@ -207,6 +207,7 @@ __host__ __device__ inline Layout layout(int64_t cap) {
 enum Op { OP_L_A, OP_L_B, OP_CG_MID, OP_CG_END, OP_L_END, OP_R_A, OP_R_B, OP_R_END, OP_SQRT_L };
 struct Params {
   int op, side, full, nidx, has_pattern, omega_rec, one_sided;
+  int then_op;  // a second decision in the same launch (-1: none)
   int64_t s, ncols, lo, hi, m, n, cap;
   double omega, lvl, bfac, guard, eta, eps;
 };
