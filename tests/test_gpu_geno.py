@@ -198,3 +198,23 @@ def test_block_products_equal_single_columns(gkb, k):
     Z = op.apply_adjoint_block(U)
     for c in range(k):
         assert np.array_equal(Z[:, c], op.apply_adjoint(U[:, c])), c
+
+
+@pytest.mark.parametrize("nshards,p", [(2, 3001), (3, 7)])
+def test_block_products_sharded(gkb, nshards, p):
+    """Two-column block products on a multi-shard context (rows split across
+    shards, possibly tiny or empty shards; the adjoint summed across shards)
+    equal the single-shard operator's columns bit for bit."""
+    n = 2051
+    payload, _ = random_payload(p, n, seed=31, missing=0.03)
+    one = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
+    ctx = gkb.Context([0] * nshards)
+    sh = gkb.GenotypeOperator.from_bed_payload(payload, p, n, ctx=ctx,
+                                               scheme=gkb.ScalingScheme.kHwe)
+    rng = np.random.default_rng(nshards)
+    X = rng.standard_normal((n, 4))
+    U = rng.standard_normal((p, 4))
+    assert np.array_equal(sh.apply_block(X), one.apply_block(X))
+    Za, Zb = sh.apply_adjoint_block(U), one.apply_adjoint_block(U)
+    # the adjoint's cross-shard sum adds per-shard partials (order differs from one shard)
+    assert np.max(np.abs(Za - Zb)) <= 1e-12 * np.max(np.abs(Zb))

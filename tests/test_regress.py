@@ -174,3 +174,22 @@ def test_device_marker_scan_matches_host_algebra(gkb, k, unbiased):
     for f in ("beta", "se", "intercept", "sigma2"):
         a, b = getattr(dev, f)[ok], getattr(host, f)[ok]
         assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)) <= 1e-8, f
+
+
+@pytest.mark.gpu
+def test_device_marker_scan_sharded(gkb):
+    """The device scan on a two-shard context gives every marker's fit exactly
+    as on one shard (each marker's row lives on one shard)."""
+    from paper_1808_03374_b200 import regress as R
+    from paper_1808_03374_b200 import synth
+    spec = synth.config_spec(2, scale=0.05)
+    one = gkb.GenotypeOperator.from_synth(spec, scheme=gkb.ScalingScheme.kHwe)
+    two = gkb.GenotypeOperator.from_synth(spec, ctx=gkb.Context([0, 0]),
+                                          scheme=gkb.ScalingScheme.kHwe)
+    rng = np.random.default_rng(9)
+    y = rng.standard_normal(spec.n)
+    Z = rng.standard_normal((spec.n, 4))
+    a, b = R.marker_scan(one, y, Z), R.marker_scan(two, y, Z)
+    assert np.array_equal(a.dependent, b.dependent)
+    for f in ("beta", "se", "intercept", "sigma2"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
