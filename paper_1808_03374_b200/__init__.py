@@ -9,13 +9,14 @@ from ._lib import FormatError, GkbError, LogicError, LIB_PATH
 from .gkl import (bed_check, Context, DenseOperator, GenotypeOperator, GklOptions, LanczosFactorization,
                   LinearOperator, ReorthMode, RestartMode, RitzSet, ScalingScheme, StepInfo,
                   StepStatus, SvdlResult, SvdlStats, cgs2, default_context, error_metric_l1,
-                  marker_scaling, partition_rows, pinned_empty, rng_uniform_symmetric, svd_small,
-                  svdl)
+                  marker_scaling, norm_estimate, adjoint_mismatch, partition_rows, pinned_empty,
+                  rng_uniform_symmetric, svd_small, svdl)
 
 __all__ = [
     "FormatError", "GkbError", "LogicError", "LIB_PATH", "Context", "DenseOperator",
     "GenotypeOperator", "GklOptions", "LanczosFactorization", "LinearOperator", "ReorthMode",
     "RestartMode", "RitzSet", "ScalingScheme", "StepInfo", "StepStatus", "SvdlResult", "SvdlStats",
     "cgs2", "default_context", "error_metric_l1", "marker_scaling", "partition_rows",
-    "pinned_empty", "rng_uniform_symmetric", "svd_small", "svdl", "bed_check",
+    "pinned_empty", "rng_uniform_symmetric", "svd_small", "svdl", "bed_check", "norm_estimate",
+    "adjoint_mismatch",
 ]

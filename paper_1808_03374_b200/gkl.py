@@ -28,6 +28,7 @@ __all__ = [
     "Context", "LinearOperator", "DenseOperator", "GenotypeOperator", "LanczosFactorization",
     "StepInfo", "StepStatus", "RitzSet", "svdl", "cgs2", "svd_small", "rng_uniform_symmetric",
     "partition_rows", "marker_scaling", "error_metric_l1", "pinned_empty", "bed_check", "rng_normal",
+    "norm_estimate", "adjoint_mismatch",
 ]
 
 
@@ -634,6 +635,39 @@ def rng_uniform_symmetric(seed: int, n: int) -> np.ndarray:
     out = np.empty(n)
     check(lib.gkb_rng_fill_symmetric(int(seed) & 0xFFFFFFFFFFFFFFFF, n, _pd(out)))
     return out
+
+
+def norm_estimate(op: LinearOperator, iters: int = 20, seed: int = 0x9E3779B97F4A7C15) -> float:
+    """norm_estimate (linop.hpp:122-123, linop.cpp:9-28): ||X z|| after `iters`
+    power iterations on X^T X from a seeded uniform start -- a lower estimate of
+    sigma_1. 2 iters + 1 products on the device operator."""
+    n = op.cols()
+    if n == 0 or op.rows() == 0:
+        return 0.0
+    z = rng_uniform_symmetric(seed, n)
+    zn = float(np.linalg.norm(z))
+    if zn == 0.0:
+        z[0] = zn = 1.0
+    z = z / zn
+    for _ in range(int(iters)):
+        w = op.apply_adjoint(op.apply(z))
+        wn = float(np.linalg.norm(w))
+        if wn == 0.0:  # z reached the null space exactly
+            return 0.0
+        z = w / wn
+    return float(np.linalg.norm(op.apply(z)))
+
+
+def adjoint_mismatch(op: LinearOperator, seed: int = 7) -> float:
+    """adjoint_mismatch (linop.hpp:125-127, linop.cpp:30-39): |u'(X v) - (X^T u)'v|
+    / (||u|| ||v||) on normal probes v (cols) then u (rows) from one stream."""
+    n, m = op.cols(), op.rows()
+    r = rng_normal(seed, n + m)
+    v, u = r[:n], r[n:]
+    left = float(u @ op.apply(v))
+    right = float(op.apply_adjoint(u) @ v)
+    scale = float(np.linalg.norm(u) * np.linalg.norm(v))
+    return 0.0 if scale == 0.0 else abs(left - right) / scale
 
 
 def rng_normal(seed: int, n: int) -> np.ndarray:

@@ -218,3 +218,16 @@ def test_block_products_sharded(gkb, nshards, p):
     Za, Zb = sh.apply_adjoint_block(U), one.apply_adjoint_block(U)
     # the adjoint's cross-shard sum adds per-shard partials (order differs from one shard)
     assert np.max(np.abs(Za - Zb)) <= 1e-12 * np.max(np.abs(Zb))
+
+
+def test_norm_estimate_and_adjoint_mismatch_vs_oracle(gkb, orc):
+    """norm_estimate / adjoint_mismatch (linop.cpp:9-39) on the device operator
+    against the oracle's restatement on the same payload and scaling."""
+    p, n = 1201, 903
+    payload, _ = random_payload(p, n, seed=41, missing=0.02)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
+    mu, inv_s = op.scaling()
+    ref = orc.GenoOracle(payload, p, n, mu, inv_s, nthreads=4)
+    a, b = gkb.norm_estimate(op, 20), orc.norm_estimate(ref, 20)
+    assert abs(a - b) <= 1e-11 * b
+    assert gkb.adjoint_mismatch(op) <= 1e-14 and orc.adjoint_mismatch(ref) <= 1e-14
