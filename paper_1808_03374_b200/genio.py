@@ -141,6 +141,19 @@ def write_csv_matrix(path: str, M: np.ndarray) -> None:
             f.write(",".join("%.17g" % v for v in M[i]) + "\n")
 
 
+def impute_mean(dosages: np.ndarray, return_all_missing: bool = False):
+    """impute_mean (genio.cpp:124-148): markers x samples dosages (3 = missing)
+    -> float64 with each missing entry replaced by its row's observed mean (0
+    for an all-missing row); optionally the all-missing row flags."""
+    d = np.asarray(dosages)
+    miss = d == 3
+    obs = (~miss).sum(axis=1)
+    sums = np.where(miss, 0, d).sum(axis=1, dtype=np.float64)
+    mean = np.where(obs > 0, sums / np.maximum(obs, 1), 0.0)
+    out = np.where(miss, mean[:, None], d.astype(np.float64))
+    return (out, obs == 0) if return_all_missing else out
+
+
 def standardize_dense(X: np.ndarray, scheme: str) -> np.ndarray:
     """standardize (genio.cpp:150-185) on a dense matrix: row mean, population
     variance over all n columns, zero-variance rows -> 0; unit: s = sqrt(var);

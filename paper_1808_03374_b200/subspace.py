@@ -54,6 +54,12 @@ def qr_thin(M: np.ndarray):
     return Q * s[None, :], R * s[:, None]
 
 
+def orthonormality_error(Q: np.ndarray) -> float:
+    """orthonormality_error (orth.cpp:23-29): max |Q^T Q - I|."""
+    Q = np.asarray(Q, dtype=np.float64)
+    return float(np.abs(Q.T @ Q - np.eye(Q.shape[1])).max()) if Q.shape[1] else 0.0
+
+
 def delta_criterion(prev: np.ndarray, curr: np.ndarray, scaled: bool = True) -> float:
     """subspace.cpp:13-21: ||curr - prev||_F (/ sqrt(rows*cols) when scaled)."""
     if prev.shape != curr.shape:

@@ -269,3 +269,17 @@ def test_bench_end_to_end(gkb, tmp_path, capsys):
     assert row[3] == "nan" and row[4] == "nan"
     assert run(["bench", pre + ".bed", "--seed", "5", "--algos", "gkl-xx", "--out",
                 str(out)]) == 4
+
+
+def test_impute_mean_and_orthonormality_error():
+    """genio.impute_mean (genio.cpp:124-148) against the oracle's decode/impute
+    semantics, and orthonormality_error (orth.cpp:23-29)."""
+    from paper_1808_03374_b200 import genio
+    from paper_1808_03374_b200.subspace import orthonormality_error
+    d = np.array([[0, 1, 3, 2], [3, 3, 3, 3], [2, 3, 2, 2]], dtype=np.uint8)
+    X, allm = genio.impute_mean(d, return_all_missing=True)
+    assert np.array_equal(X, [[0, 1, 1, 2], [0, 0, 0, 0], [2, 2, 2, 2]])
+    assert allm.tolist() == [False, True, False]
+    Q = np.linalg.qr(np.random.default_rng(0).standard_normal((20, 4)))[0]
+    assert orthonormality_error(Q) <= 1e-14
+    assert abs(orthonormality_error(2 * Q) - 3.0) <= 1e-12
