@@ -28,7 +28,9 @@ def random_payload(p, n, seed, missing=0.02, special_rows=True):
 
 
 SHAPES = [(1, 1), (4, 16), (5, 17), (7, 3), (33, 100), (130, 257), (257, 1000), (1031, 2049),
-          (64, 4099)]
+          (64, 4099),
+          # column-range boundaries (14 tiles = 1792 columns; the unrolled full-range loop)
+          (5, 1792), (5, 1793), (1792, 3), (1793, 1791)]
 
 
 @pytest.mark.parametrize("p,n", SHAPES)
