@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "ctl_ops.cuh"
 #include "kernels.hpp"
 #include "pdl.hpp"
 
@@ -50,16 +51,17 @@ __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 // last CTA to arrive sums them into out[k]. Order: segment s of the nblk
 // partials (fixed boundaries) summed sequentially, then the kSeg segment sums
 // in order -- a function of (nblk, K) only.
-__device__ void grid_finalize_cols(const double* partial, int nblk, int K, int kb, int ke,
+// Returns true in the last CTA (all of its threads see out[]).
+__device__ bool grid_finalize_cols(const double* partial, int nblk, int K, int kb, int ke,
                                    double* out, unsigned* ticket, unsigned nctas);
 
-__device__ void grid_finalize(const double* partial, int nblk, int K, double* out,
+__device__ bool grid_finalize(const double* partial, int nblk, int K, double* out,
                               unsigned* ticket, unsigned nctas) {
-  grid_finalize_cols(partial, nblk, K, 0, K, out, ticket, nctas);
+  return grid_finalize_cols(partial, nblk, K, 0, K, out, ticket, nctas);
 }
 
 // Columns [kb, ke) only; `ticket` counts the nctas CTAs that write them.
-__device__ void grid_finalize_cols(const double* partial, int nblk, int K, int kb, int ke,
+__device__ bool grid_finalize_cols(const double* partial, int nblk, int K, int kb, int ke,
                                    double* out, unsigned* ticket, unsigned nctas) {
   __shared__ bool last;
   __shared__ double seg[kSeg][33];
@@ -67,7 +69,7 @@ __device__ void grid_finalize_cols(const double* partial, int nblk, int K, int k
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == nctas - 1;
   __syncthreads();
-  if (!last) return;
+  if (!last) return false;
   __threadfence();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b0 = (int)((int64_t)nblk * warp / kSeg), b1 = (int)((int64_t)nblk * (warp + 1) / kSeg);
@@ -99,12 +101,13 @@ __device__ void grid_finalize_cols(const double* partial, int nblk, int K, int k
     __syncthreads();
   }
   if (threadIdx.x == 0) *ticket = 0u;  // ready for the next launch on this stream
+  return true;
 }
 
 // Reduces vals[0..K) across the CTA into partial[blockIdx.x * K + k] (warp
 // sums, then the kWarps warp sums in order), then the grid-level finalize.
 template <int K>
-__device__ void block_partial_finalize(double (&vals)[K], double* partial, double* out,
+__device__ bool block_partial_finalize(double (&vals)[K], double* partial, double* out,
                                        unsigned* ticket) {
   __shared__ double sred[K][kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -120,7 +123,18 @@ __device__ void block_partial_finalize(double (&vals)[K], double* partial, doubl
     for (int i = 0; i < kWarps; ++i) t += sred[threadIdx.x][i];
     partial[(int64_t)blockIdx.x * K + threadIdx.x] = t;
   }
-  grid_finalize(partial, gridDim.x, K, out, ticket, gridDim.x);
+  return grid_finalize(partial, gridDim.x, K, out, ticket, gridDim.x);
+}
+
+// The fused light decision (kernels.hpp ctl::Post): in the last CTA, or in
+// block 0 of a gated-off launch (the decision then clears its gates).
+__device__ __forceinline__ void run_post(const ctl::Post& post) {
+  if (post.p.op >= 0) ctl::run_light(post.d, post.iv, post.p, threadIdx.x, blockDim.x);
+}
+__device__ __forceinline__ bool gated_off_post(const int* gate, const ctl::Post& post) {
+  if (!gated_off(gate)) return false;
+  if (blockIdx.x == 0 && blockIdx.y == 0) run_post(post);
+  return true;
 }
 
 // Row chunk of CTA b: [b * rpb, min(len, (b + 1) * rpb)), rpb = kT * U.
@@ -203,11 +217,12 @@ __global__ void __launch_bounds__(kT) k_gemv_n(const double* __restrict__ Q, int
                                                int norms, int64_t rpb,
                                                double* __restrict__ partial,
                                                double* __restrict__ out,
-                                               unsigned* __restrict__ ticket, const int* gate) {
+                                               unsigned* __restrict__ ticket, const int* gate,
+                                               const ctl::Post post) {
   pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
   pdl_trigger();
   __shared__ double cs[1024];
-  if (gated_off(gate)) return;
+  if (gated_off_post(gate, post)) return;
   const Chunk ch = chunk(len, rpb);
   double nrm[2] = {0.0, 0.0};
   for (int64_t rb = ch.r0 + threadIdx.x; rb - threadIdx.x < ch.r1; rb += (int64_t)kT * kBatch) {
@@ -256,17 +271,18 @@ __global__ void __launch_bounds__(kT) k_gemv_n(const double* __restrict__ Q, int
       }
     }
   }
-  if (norms) block_partial_finalize<2>(nrm, partial, out, ticket);
+  if (norms && block_partial_finalize<2>(nrm, partial, out, ticket)) run_post(post);
 }
 
 __global__ void __launch_bounds__(kT) k_dot(const double* __restrict__ a,
                                             const double* __restrict__ b, int64_t len,
                                             int64_t rpb, double* __restrict__ partial,
                                             double* __restrict__ out,
-                                            unsigned* __restrict__ ticket, const int* gate) {
+                                            unsigned* __restrict__ ticket, const int* gate,
+                                            const ctl::Post post) {
   pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
   pdl_trigger();
-  if (gated_off(gate)) return;
+  if (gated_off_post(gate, post)) return;
   const Chunk ch = chunk(len, rpb);
   double acc[1] = {0.0};
   for (int64_t rb = ch.r0 + threadIdx.x; rb < ch.r1; rb += (int64_t)kT * kBatch) {
@@ -280,7 +296,7 @@ __global__ void __launch_bounds__(kT) k_dot(const double* __restrict__ a,
 #pragma unroll
     for (int i = 0; i < kBatch; ++i) acc[0] += x[i] * y[i];
   }
-  block_partial_finalize<1>(acc, partial, out, ticket);
+  if (block_partial_finalize<1>(acc, partial, out, ticket)) run_post(post);
 }
 
 // sum (a - b)^2 (subspace delta criterion)
@@ -325,10 +341,11 @@ __global__ void __launch_bounds__(kT) k_axpy_norms(double alpha, const double* _
                                                    double* __restrict__ v, int64_t len,
                                                    int64_t rpb, double* __restrict__ partial,
                                                    double* __restrict__ out,
-                                                   unsigned* __restrict__ ticket, const int* gate) {
+                                                   unsigned* __restrict__ ticket, const int* gate,
+                                                   const ctl::Post post) {
   pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
   pdl_trigger();
-  if (gated_off(gate)) return;
+  if (gated_off_post(gate, post)) return;
   if (dval) alpha = take_sqrt ? sqrt(*dval) : *dval;
   const Chunk ch = chunk(len, rpb);
   double acc[2] = {0.0, 0.0};
@@ -349,7 +366,7 @@ __global__ void __launch_bounds__(kT) k_axpy_norms(double alpha, const double* _
       acc[1] += nv * nv;
     }
   }
-  block_partial_finalize<2>(acc, partial, out, ticket);
+  if (block_partial_finalize<2>(acc, partial, out, ticket)) run_post(post);
 }
 
 __global__ void k_div_copy_dev(const double* __restrict__ src, const double* __restrict__ dval,
@@ -467,6 +484,16 @@ int64_t red_blocks(int64_t len) {
   return b > 0 ? b : 1;
 }
 
+namespace {
+ctl::Post post_of(const ctl::Post* p) {
+  if (p) return *p;
+  ctl::Post none;
+  none.p.op = -1;
+  return none;
+}
+
+}  // namespace
+
 void init_red_scratch(RedScratch& rs) {
   if (!rs.ticket) {  // one per gemv_t column group (K <= 8 * kTickets), [0] for the rest
     cudaMalloc(&rs.ticket, sizeof(unsigned) * kTickets);
@@ -495,23 +522,23 @@ void gemv_t(const double* Q, int64_t ld, int64_t len, int64_t ncols, const doubl
 
 void gemv_n(const double* Q, int64_t ld, int64_t len, int64_t ncols, const double* c, double* v,
             double beta, double sign, bool norms, RedScratch& rs, double* out, cudaStream_t s,
-            const int* gate) {
+            const int* gate, const ctl::Post* post) {
   if (len == 0 && !norms) return;
   const int64_t rpb = rpb_target(len, "GKB_GN_BLOCKS", 296);
   const int64_t nb = std::max<int64_t>(1, (len + rpb - 1) / rpb);
   launch_pdl(k_gemv_n, dim3((unsigned)nb), dim3(kT), 0, s, true, Q, ld, len, ncols, c, v, beta,
-             sign, norms ? 1 : 0, rpb, rs.partial, out, rs.ticket, gate);
+             sign, norms ? 1 : 0, rpb, rs.partial, out, rs.ticket, gate, post_of(post));
 }
 
 void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
-         const int* gate) {
-  launch_pdl(k_dot, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, a, b, len, rpb_of(len), rs.partial, out,
-                                                  rs.ticket, gate);
+         const int* gate, const ctl::Post* post) {
+  launch_pdl(k_dot, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, a, b, len, rpb_of(len),
+             rs.partial, out, rs.ticket, gate, post_of(post));
 }
 
 void nrm2sq(const double* a, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
-            const int* gate) {
-  dot(a, a, len, rs, out, s, gate);
+            const int* gate, const ctl::Post* post) {
+  dot(a, a, len, rs, out, s, gate, post);
 }
 
 void diff_nrm2sq(const double* a, const double* b, int64_t len, RedScratch& rs, double* out,
@@ -529,20 +556,19 @@ void axpy_dev(const double* dptr, const double* u, double* v, int64_t len, cudaS
 void axpy_norms(double alpha, const double* u, double* v, int64_t len, RedScratch& rs, double* out,
                 cudaStream_t s) {
   launch_pdl(k_axpy_norms, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, alpha, nullptr, 0, u, v, len,
-                                                         rpb_of(len), rs.partial, out, rs.ticket,
-                                                         nullptr);
+             rpb_of(len), rs.partial, out, rs.ticket, nullptr, post_of(nullptr));
 }
 
 void axpy_norms_dsq(const double* nrm2, const double* u, double* v, int64_t len, RedScratch& rs,
                     double* out, cudaStream_t s) {
   launch_pdl(k_axpy_norms, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, 0.0, nrm2, 1, u, v, len, rpb_of(len),
-                                                         rs.partial, out, rs.ticket, nullptr);
+             rs.partial, out, rs.ticket, nullptr, post_of(nullptr));
 }
 
 void axpy_norms_dv(const double* alpha, const double* u, double* v, int64_t len, RedScratch& rs,
-                   double* out, cudaStream_t s, const int* gate) {
+                   double* out, cudaStream_t s, const int* gate, const ctl::Post* post) {
   launch_pdl(k_axpy_norms, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, 0.0, alpha, 0, u, v, len, rpb_of(len),
-                                                         rs.partial, out, rs.ticket, gate);
+             rs.partial, out, rs.ticket, gate, post_of(post));
 }
 
 void div_copy_dsq(const double* src, const double* nrm2, double* dst, int64_t len,

@@ -22,6 +22,7 @@
 
 #include "kernels.hpp"
 #include "pdl.hpp"
+#include "ctl_ops.cuh"
 
 namespace gkb {
 namespace dev {
@@ -73,23 +74,9 @@ __device__ void run_op(double* __restrict__ d, int* __restrict__ iv, const Param
   const int64_t cg_o = R_CG + p.ncols + 3;  // second-pass slots (host cgs2: o = ncols + 3)
 
   switch (p.op) {
-    case OP_L_A: {  // norms of the left candidate -> local second pass?
-      if (!alive) {
-        if (t == 0) iv[I_G2P] = iv[I_GRE] = iv[I_GRE2] = 0;
-        for (int64_t c = t; c < cap; c += blockDim.x) iv[I_G2PC + c] = 0;
-        return;
-      }
-      const double w0 = sqrt(res[R_N]);
-      const double ac = sqrt(res[R_N + p.nidx]);
-      const bool f = ac < p.eta * w0;
-      for (int64_t c = t; c < cap; c += blockDim.x)
-        iv[I_G2PC + c] = (f && p.has_pattern && c >= p.lo && c <= p.hi && coup[c] != 0.0) ? 1 : 0;
-      if (t == 0) {
-        iv[I_G2P] = (f && p.has_pattern) ? 1 : 0;
-        sc[S_ACAND] = ac;
-      }
+    case OP_L_A:
+      run_light(d, iv, p, t, blockDim.x);
       return;
-    }
     case OP_L_B:    // after the second pass: omega (left) -> reorthogonalize?
     case OP_R_B: {  // same on the right
       const bool left = p.op == OP_L_B;
@@ -168,19 +155,9 @@ __device__ void run_op(double* __restrict__ d, int* __restrict__ iv, const Param
       }
       return;
     }
-    case OP_CG_MID: {  // cgs2 pass 1 done: second pass? (orth.hpp:30-33)
-      const bool on = p.full ? alive : (alive && iv[I_GRE] != 0);
-      if (t != 0) return;
-      if (!on) {
-        iv[I_GRE2] = 0;
-        return;
-      }
-      const double nb = sqrt(res[R_CG + p.ncols]);
-      const double na = sqrt(res[R_CG + p.ncols + 2]);
-      iv[I_GRE2] = (na < p.eta * nb) ? 1 : 0;
-      sc[S_NAFTER] = na;
+    case OP_CG_MID:
+      run_light(d, iv, p, t, blockDim.x);
       return;
-    }
     case OP_CG_END: {  // cgs2 done: its norm is the new candidate
       const bool on = p.full ? alive : (alive && iv[I_GRE] != 0);
       if (!on) return;
@@ -223,19 +200,9 @@ __device__ void run_op(double* __restrict__ d, int* __restrict__ iv, const Param
       }
       return;
     }
-    case OP_R_A: {  // norms of the right candidate -> local second pass? (partial)
-      if (!alive) {
-        if (t == 0) iv[I_G2P] = iv[I_GRE] = iv[I_GRE2] = 0;
-        return;
-      }
-      if (t == 0) {
-        const double z0 = sqrt(res[R_N]);
-        const double bc = sqrt(res[R_N + 1]);
-        iv[I_G2P] = (bc < p.eta * z0) ? 1 : 0;
-        sc[S_BCAND] = bc;
-      }
+    case OP_R_A:
+      run_light(d, iv, p, t, blockDim.x);
       return;
-    }
     case OP_R_END: {  // beta fixed: breakdown test, coupling, omega levels (gkl.cpp:292-311)
       if (!alive) return;
       const int64_t s = p.s;

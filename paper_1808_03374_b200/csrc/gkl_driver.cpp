@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -607,6 +608,17 @@ StepInfo Lanczos::step(const Options& o, double norm_scale, int64_t* mvp_counter
 // anything back: each decision is a ctl kernel (ctl_kernels.cu) writing gates,
 // and the kernels of both branches are enqueued with the gate that enables
 // them. Kernels and result slots are the host path's, so the values are too.
+// The light decisions (L_A, R_A, CG_MID) run inside the reduction that
+// produces their inputs (kernels.hpp ctl::Post) unless GKB_NO_CTL_FUSE is set;
+// on the left that needs the allreduce in between to be a no-op.
+bool Lanczos::fuse_ctl() {
+  static const bool on = getenv("GKB_NO_CTL_FUSE") == nullptr;
+  return on;
+}
+bool Lanczos::reduce_local() const {
+  return ctx_->use_nccl ? ctx_->nshards_total == 1 : ctx_->shards.size() == 1;
+}
+
 dev::ctl::Params Lanczos::ctl_params(const Options& o, int op, int64_t s) const {
   dev::ctl::Params p{};
   p.op = op;
@@ -660,18 +672,24 @@ void Lanczos::cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec
                   sh.stream, ci(i) + slot);
     }
     reduce(oc, ncols + (pass == 0 ? 1 : 0));
-    for (int i = 0; i < L; ++i) {
-      ctx_->set_device(i);
-      Shard& sh = ctx_->shards[i];
-      dev::gemv_n(Q[i], ld(side, i), len(side, i), ncols, res(i, oc), vec[i], 1.0, -1.0, true,
-                  sh.rs, res(i, on), sh.stream, ci(i) + slot);
-    }
-    reduce(on, 2);
     Params p = ctl_params(o, pass == 0 ? OP_CG_MID : OP_CG_END, s);
     p.ncols = ncols;
     p.side = side == kLeft ? 0 : 1;
     if (pass == 1) p.then_op = then_op;  // e.g. the half-step finalize, same launch
-    ctl(p);
+    // pass 1's decision runs in gemv_n's last CTA when no allreduce follows it
+    const bool fuse = pass == 0 && fuse_ctl() && (side != kLeft || reduce_local());
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      Shard& sh = ctx_->shards[i];
+      Post post;
+      post.d = cd(i);
+      post.iv = ci(i);
+      post.p = p;
+      dev::gemv_n(Q[i], ld(side, i), len(side, i), ncols, res(i, oc), vec[i], 1.0, -1.0, true,
+                  sh.rs, res(i, on), sh.stream, ci(i) + slot, fuse ? &post : nullptr);
+    }
+    reduce(on, 2);
+    if (!fuse) ctl(p);
   }
 }
 
@@ -712,23 +730,29 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
     }
   } else {
     const bool pat = lo >= 0;
-    for (int i = 0; i < L; ++i) {
-      ctx_->set_device(i);
-      Shard& sh = ctx_->shards[i];
-      const int64_t r = op_->rows(i);
-      if (pat)
-        dev::gemv_n(U_[i] + lo * r, r, r, hi - lo + 1, cd(i) + ctl_L_.coup + lo, w_[i], 1.0, -1.0,
-                    true, sh.rs, res(i, R_N), sh.stream, ci(i) + I_ALIVE);
-      else
-        dev::nrm2sq(w_[i], r, sh.rs, res(i, R_N), sh.stream, ci(i) + I_ALIVE);
-    }
-    reduce_left(R_N, pat ? 2 : 1);
     Params pa = ctl_params(o, OP_L_A, s);
     pa.nidx = pat ? 1 : 0;
     pa.has_pattern = pat ? 1 : 0;
     pa.lo = lo;
     pa.hi = hi;
-    ctl(pa);
+    const bool fuse = fuse_ctl() && reduce_local();  // decision in the reduction's last CTA
+    for (int i = 0; i < L; ++i) {
+      ctx_->set_device(i);
+      Shard& sh = ctx_->shards[i];
+      const int64_t r = op_->rows(i);
+      Post post;
+      post.d = cd(i);
+      post.iv = ci(i);
+      post.p = pa;
+      const Post* pp = fuse ? &post : nullptr;
+      if (pat)
+        dev::gemv_n(U_[i] + lo * r, r, r, hi - lo + 1, cd(i) + ctl_L_.coup + lo, w_[i], 1.0, -1.0,
+                    true, sh.rs, res(i, R_N), sh.stream, ci(i) + I_ALIVE, pp);
+      else
+        dev::nrm2sq(w_[i], r, sh.rs, res(i, R_N), sh.stream, ci(i) + I_ALIVE, pp);
+    }
+    reduce_left(R_N, pat ? 2 : 1);
+    if (!fuse) ctl(pa);
     if (pat) {  // local second pass over the structural pattern (gkl.cpp:233-242)
       for (int64_t c = lo; c <= hi; ++c) {
         for (int i = 0; i < L; ++i) {
@@ -775,13 +799,18 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
     op_->adjoint_dev(uin, z_);
   }
   if (!o.full) {
+    const bool fuse = fuse_ctl();  // right side: no allreduce before the decision
     for (int i = 0; i < L; ++i) {
       ctx_->set_device(i);
       Shard& sh = ctx_->shards[i];
+      Post post;
+      post.d = cd(i);
+      post.iv = ci(i);
+      post.p = ctl_params(o, OP_R_A, s);
       dev::axpy_norms_dv(cd(i) + ctl_L_.sc + S_ALPHA, V_[i] + s * n_, z_[i], n_, sh.rs,
-                         res(i, R_N), sh.stream, ci(i) + I_ALIVE);
+                         res(i, R_N), sh.stream, ci(i) + I_ALIVE, fuse ? &post : nullptr);
     }
-    ctl(ctl_params(o, OP_R_A, s));
+    if (!fuse) ctl(ctl_params(o, OP_R_A, s));
     for (int i = 0; i < L; ++i) {  // local second pass against v_s (gkl.cpp:277-284)
       ctx_->set_device(i);
       Shard& sh = ctx_->shards[i];

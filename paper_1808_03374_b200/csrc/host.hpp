@@ -318,6 +318,8 @@ class Lanczos {
   void enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t hi);
   void cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec, int gate_slot,
                 const Options& o, int64_t s, int then_op = -1);
+  static bool fuse_ctl();
+  bool reduce_local() const;
   dev::ctl::Params ctl_params(const Options& o, int op, int64_t s) const;
 };
 

@@ -111,6 +111,9 @@ void k2_main_only(const GenoView& g, cudaStream_t s);
 // ---- dense fp64 basis / operator kernels (K3-K6) -------------------------
 // Reduction scratch: per-CTA partials and the last-CTA ticket of the
 // single-launch reductions (one reduction in flight per stream).
+namespace ctl {
+struct Post;  // a light step decision run by the reduction's last CTA (below)
+}
 struct RedScratch {
   double* partial;
   int64_t cap;  // doubles
@@ -126,13 +129,13 @@ void gemv_t(const double* Q, int64_t ld, int64_t len, int64_t ncols, const doubl
 // (beta applies to v before the subtraction; used for dense apply with beta = 0 -> y = -Qc).
 void gemv_n(const double* Q, int64_t ld, int64_t len, int64_t ncols, const double* c, double* v,
             double beta, double sign, bool norms, RedScratch& rs, double* out, cudaStream_t s,
-            const int* gate = nullptr);
+            const int* gate = nullptr, const ctl::Post* post = nullptr);
 // out[0] = sum a*b ; (dot into device scalar)
 void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
-         const int* gate = nullptr);
+         const int* gate = nullptr, const ctl::Post* post = nullptr);
 // out[0] = ||a||^2
 void nrm2sq(const double* a, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
-            const int* gate = nullptr);
+            const int* gate = nullptr, const ctl::Post* post = nullptr);
 // out[0] = sum (a - b)^2
 void diff_nrm2sq(const double* a, const double* b, int64_t len, RedScratch& rs, double* out,
                  cudaStream_t s);
@@ -154,7 +157,7 @@ void axpy_norms_dsq(const double* nrm2, const double* u, double* v, int64_t len,
 // *divisor, no sqrt), gated: nothing happens when *gate == 0. Every kernel
 // above that takes a `gate` behaves the same way.
 void axpy_norms_dv(const double* alpha, const double* u, double* v, int64_t len, RedScratch& rs,
-                   double* out, cudaStream_t s, const int* gate);
+                   double* out, cudaStream_t s, const int* gate, const ctl::Post* post = nullptr);
 void div_copy_dv(const double* src, const double* divisor, double* dst, int64_t len,
                  cudaStream_t s, const int* gate);
 // dst[:, 0:kc] = Q[:, 0:j] * W (W is j x kc, ldw rows, on device); dst may not alias Q
@@ -212,6 +215,15 @@ struct Params {
   double omega, lvl, bfac, guard, eta, eps;
 };
 void launch(double* d, int* iv, const Params& p, cudaStream_t st);
+// A light decision (OP_L_A, OP_R_A, OP_CG_MID: ctl_ops.cuh) handed to the
+// reduction that produces its inputs: its last CTA runs it after the finalize
+// (block 0 when the reduction is gated off), saving the ctl launch. Only where
+// no allreduce sits between the two (right side, or one shard in total).
+struct Post {
+  double* d = nullptr;
+  int* iv = nullptr;
+  Params p{};
+};
 }  // namespace ctl
 
 // ---- synthetic generator ------------------------------------------------
