@@ -299,6 +299,57 @@ __global__ void __launch_bounds__(kT) k_dot(const double* __restrict__ a,
   if (block_partial_finalize<1>(acc, partial, out, ticket)) run_post(post);
 }
 
+// v -= (*dprev) * uprev (when `uprev` is set and agate is on), then
+// out[0] = sum unext * v (v itself when unext is null) when dgate is on: one
+// step of the sequential local second pass (gkl.cpp:233-242, :277-284) with
+// the next column's dot, or the final norm, in the same pass. Same chunking,
+// products and sum order as k_axpy_dev followed by k_dot, so the same bits.
+__global__ void __launch_bounds__(kT) k_axpy_dot(const double* __restrict__ dprev,
+                                                 const double* __restrict__ uprev,
+                                                 const int* agate,
+                                                 const double* __restrict__ unext,
+                                                 const int* dgate, double* __restrict__ v,
+                                                 int64_t len, int64_t rpb,
+                                                 double* __restrict__ partial,
+                                                 double* __restrict__ out,
+                                                 unsigned* __restrict__ ticket) {
+  pdl_wait();  // (pdl.hpp) nothing before this reads or writes global memory
+  pdl_trigger();
+  const bool aon = uprev != nullptr && !gated_off(agate);
+  const bool don = !gated_off(dgate);
+  if (!aon && !don) return;
+  const double a = aon ? *dprev : 0.0;
+  const Chunk ch = chunk(len, rpb);
+  double acc[1] = {0.0};
+  for (int64_t rb = ch.r0 + threadIdx.x; rb < ch.r1; rb += (int64_t)kT * kBatch) {
+    double x[kBatch], y[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int64_t r = rb + (int64_t)i * kT;
+      x[i] = r < ch.r1 ? v[r] : 0.0;
+      y[i] = (aon && r < ch.r1) ? uprev[r] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int64_t r = rb + (int64_t)i * kT;
+      if (aon && r < ch.r1) {
+        x[i] -= a * y[i];
+        v[r] = x[i];
+      }
+    }
+    if (don) {
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        const int64_t r = rb + (int64_t)i * kT;
+        y[i] = unext ? (r < ch.r1 ? unext[r] : 0.0) : x[i];
+      }
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) acc[0] += y[i] * x[i];
+    }
+  }
+  if (don) block_partial_finalize<1>(acc, partial, out, ticket);
+}
+
 // sum (a - b)^2 (subspace delta criterion)
 __global__ void __launch_bounds__(kT) k_diff_nrm2(const double* __restrict__ a,
                                                   const double* __restrict__ b, int64_t len,
@@ -539,6 +590,13 @@ void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* 
 void nrm2sq(const double* a, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
             const int* gate, const ctl::Post* post) {
   dot(a, a, len, rs, out, s, gate, post);
+}
+
+void axpy_dot(const double* dprev, const double* uprev, const int* agate, const double* unext,
+              const int* dgate, double* v, int64_t len, RedScratch& rs, double* out,
+              cudaStream_t s) {
+  launch_pdl(k_axpy_dot, dim3((unsigned)red_blocks(len)), dim3(kT), 0, s, true, dprev, uprev, agate,
+             unext, dgate, v, len, rpb_of(len), rs.partial, out, rs.ticket);
 }
 
 void diff_nrm2sq(const double* a, const double* b, int64_t len, RedScratch& rs, double* out,

@@ -753,7 +753,30 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
     }
     reduce_left(R_N, pat ? 2 : 1);
     if (!fuse) ctl(pa);
-    if (pat) {  // local second pass over the structural pattern (gkl.cpp:233-242)
+    if (pat && fuse_ctl()) {  // local second pass over the structural pattern (gkl.cpp:233-242)
+      // column c's axpy fused with column c+1's dot (or the final norm): the
+      // dot slots alternate so no CTA reads a slot the same launch writes
+      auto dslot = [&](int i, int64_t c) { return res(i, R_DOT + (c & 1)); };
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        Shard& sh = ctx_->shards[i];
+        const int64_t r = op_->rows(i);
+        dev::dot(U_[i] + lo * r, w_[i], r, sh.rs, dslot(i, lo), sh.stream, ci(i) + I_G2PC + lo);
+      }
+      reduce_left(R_DOT + (lo & 1), 1);
+      for (int64_t c = lo; c <= hi; ++c) {
+        const bool last = c == hi;
+        for (int i = 0; i < L; ++i) {
+          ctx_->set_device(i);
+          Shard& sh = ctx_->shards[i];
+          const int64_t r = op_->rows(i);
+          dev::axpy_dot(dslot(i, c), U_[i] + c * r, ci(i) + I_G2PC + c,
+                        last ? nullptr : U_[i] + (c + 1) * r, ci(i) + (last ? I_G2P : I_G2PC + c + 1),
+                        w_[i], r, sh.rs, last ? res(i, R_N) : dslot(i, c + 1), sh.stream);
+        }
+        reduce_left(last ? R_N : R_DOT + ((c + 1) & 1), 1);
+      }
+    } else if (pat) {
       for (int64_t c = lo; c <= hi; ++c) {
         for (int i = 0; i < L; ++i) {
           ctx_->set_device(i);
@@ -816,8 +839,13 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
       Shard& sh = ctx_->shards[i];
       const int* g = ci(i) + I_G2P;
       dev::dot(V_[i] + s * n_, z_[i], n_, sh.rs, res(i, R_DOT), sh.stream, g);
-      dev::axpy_dev(res(i, R_DOT), V_[i] + s * n_, z_[i], n_, sh.stream, g);
-      dev::nrm2sq(z_[i], n_, sh.rs, res(i, R_N), sh.stream, g);
+      if (fuse) {
+        dev::axpy_dot(res(i, R_DOT), V_[i] + s * n_, g, nullptr, g, z_[i], n_, sh.rs, res(i, R_N),
+                      sh.stream);
+      } else {
+        dev::axpy_dev(res(i, R_DOT), V_[i] + s * n_, z_[i], n_, sh.stream, g);
+        dev::nrm2sq(z_[i], n_, sh.rs, res(i, R_N), sh.stream, g);
+      }
     }
     ctl(ctl_params(o, OP_R_B, s));
     cgs2_dev(kRight, s + 1, z_, I_GRE, o, s, OP_R_END);

@@ -136,6 +136,11 @@ void dot(const double* a, const double* b, int64_t len, RedScratch& rs, double* 
 // out[0] = ||a||^2
 void nrm2sq(const double* a, int64_t len, RedScratch& rs, double* out, cudaStream_t s,
             const int* gate = nullptr, const ctl::Post* post = nullptr);
+// v -= (*dprev) * uprev (if uprev and agate on), then out[0] = sum unext * v
+// (||v||^2 when unext is null) if dgate on: axpy_dev + dot in one pass, same bits.
+void axpy_dot(const double* dprev, const double* uprev, const int* agate, const double* unext,
+              const int* dgate, double* v, int64_t len, RedScratch& rs, double* out,
+              cudaStream_t s);
 // out[0] = sum (a - b)^2
 void diff_nrm2sq(const double* a, const double* b, int64_t len, RedScratch& rs, double* out,
                  cudaStream_t s);
