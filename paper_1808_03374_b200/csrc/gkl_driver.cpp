@@ -860,6 +860,7 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
 }
 
 Lanczos::DevRun Lanczos::run_dev(const Options& o, int64_t nsteps, double* norm_scale) {
+  const auto t_run0 = std::chrono::steady_clock::now();
   ++version_;
   using namespace dev::ctl;
   const int L = (int)ctx_->shards.size();
@@ -904,7 +905,11 @@ Lanczos::DevRun Lanczos::run_dev(const Options& o, int64_t nsteps, double* norm_
   ctx_->set_device(0);
   Shard& s0 = ctx_->shards[0];
   GKB_CUDA(cudaMemcpyAsync(ctl_down_, ctl_d_[0], ctl_L_.bytes, cudaMemcpyDeviceToHost, s0.stream));
+  const auto t_enq = std::chrono::steady_clock::now();
   ctx_->sync_all();
+  const auto t_done = std::chrono::steady_clock::now();
+  t_enqueue += std::chrono::duration<double>(t_enq - t_run0).count();
+  t_wait += std::chrono::duration<double>(t_done - t_enq).count();
   ++host_syncs;
   const double* dd = reinterpret_cast<const double*>(ctl_down_);
   const int* di = reinterpret_cast<const int*>(dd + ctl_L_.nd);
@@ -1149,6 +1154,7 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
   GKB_CUDA(cudaEventRecord(e0, ctx->shards[0].stream));
 
   SvdlOutput out;
+  double t_extract = 0.0, t_restart = 0.0;  // host phases (GKB_VERBOSE)
   double norm_scale = 0.0;
   Ritz ritz;
   int consecutive_breakdowns = 0;
@@ -1223,10 +1229,14 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
         extract();
         if (top_k_converged()) break;
       } else if (f.steps() == o.max_subspace) {
+        const auto ta = std::chrono::steady_clock::now();
         extract();
+        const auto tb = std::chrono::steady_clock::now();
+        t_extract += std::chrono::duration<double>(tb - ta).count();
         if (top_k_converged()) break;
         if (mvps + 2 > o.max_mvps) break;
         f.thick_restart(o.keep, &ritz);
+        t_restart += std::chrono::duration<double>(std::chrono::steady_clock::now() - tb).count();
         ++out.restarts;
       }
       continue;
@@ -1297,6 +1307,8 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
               (long long)out.steps, (long long)f.host_syncs, (long long)f.spec_hits,
               (long long)f.spec_misses, sec(t_start, t_loop), sec(t_loop, t_ext),
               sec(t_ext, t_vec));
+      fprintf(stderr, "[gkb] svdl cycles: enqueue %.4f s, wait %.4f s, Ritz extract %.4f s, "
+              "thick restart %.4f s\n", f.t_enqueue, f.t_wait, t_extract, t_restart);
     }
   op->mvps += mvps;
   out.wall_seconds =

@@ -266,6 +266,7 @@ class Lanczos {
   };
   DevRun run_dev(const Options& o, int64_t nsteps, double* norm_scale);
   int64_t host_syncs = 0;
+  double t_enqueue = 0.0, t_wait = 0.0;  // run_dev host phases (GKB_VERBOSE)
   int64_t spec_hits = 0, spec_misses = 0;  // speculative right half-steps kept / not launched or redone
   Rng rng;
 

@@ -30,7 +30,12 @@ inline double dot4(const double* x, const double* y, int64_t r) {
   return (s0 + s1) + (s2 + s3);
 }
 
-// A (r x c, r >= c) -> U (r x c), s (c), V (c x c)
+// A (r x c, r >= c) -> U (r x c), s (c), V (c x c). An AVX2 clone where the
+// host has it: the loops vectorize lane-for-lane (dot4's four sums are the
+// four lanes, no FMA contraction), so both clones give the same bits. (A
+// round-robin ordering with the rounds shared among OpenMP threads was slower:
+// ~100 rounds per sweep of ~25 pairs at ~50 ns each do not pay two barriers.)
+__attribute__((target_clones("avx2", "default")))
 void jacobi_tall(const double* M, int64_t r, int64_t c, double* U, double* s, double* V) {
   std::vector<double> A(M, M + r * c), R((size_t)(c * c), 0.0);
   for (int64_t i = 0; i < c; ++i) R[i + i * c] = 1.0;
