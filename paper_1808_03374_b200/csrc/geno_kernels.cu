@@ -318,7 +318,10 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
                                                    int kt_cta, uint4* __restrict__ dig,
                                                    int* __restrict__ dexp,
                                                    double* __restrict__ dsum,
-                                                   double* __restrict__ cm) {
+                                                   double* __restrict__ cm,
+                                                   const double* __restrict__ div,
+                                                   double* __restrict__ store,
+                                                   const int* __restrict__ gate) {
   extern __shared__ uint4 dsm[];  // kt_cta * 64 uint4 (digits), then kt_cta * 128 doubles
   __shared__ double red[33];
   __shared__ int redi[33];
@@ -333,15 +336,24 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
   const int64_t c0 = (int64_t)kc * ncol;
   int emax = -1100;
   double part = 0.0;
+  // div: the input is v_in / *div (the Lanczos normalization w / alpha, z / beta,
+  // as k_div_copy_dev divides), stored to `store` unless *gate == 0
+  const double dv = div ? *div : 1.0;
+  const bool st = div && store && !(gate && *gate == 0);
   for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
     const int64_t c = c0 + t;
     double v = 0.0;
     if (c < C) {
+      double x = v_in[c];
+      if (div) {
+        x = x / dv;
+        if (st) store[c] = x;
+      }
       if (MODE == 0) {
-        v = v_in[c];
+        v = x;
         part += v;
       } else {
-        v = inv_s[c] * v_in[c];
+        v = inv_s[c] * x;
         part += v * mu[c];
         cm[c] = v * (3.0 - mean[c]);  // a missing entry holds the imputed mean (genio.cpp:144)
       }
@@ -1014,20 +1026,20 @@ void allow_smem(K kern, size_t bytes) {  // opt in above 48 KB
 }
 }  // namespace
 
-void k1_digitize(const GenoView& g, const double* x, cudaStream_t s) {
+void k1_digitize(const GenoView& g, const double* x, cudaStream_t s, const DivIn& di) {
   const PMPlan& pl = g.pl1;
   allow_smem(k_digitize<0>, pl.dig_smem);
   launch_pdl(k_digitize<0>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, true, x,
              (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, g.n, pl.kt_cta,
-             g.s1.dig, g.s1.dexp, g.s1.dsum, (double*)nullptr);
+             g.s1.dig, g.s1.dexp, g.s1.dsum, (double*)nullptr, di.div, di.store, di.gate);
 }
 
-void k2_digitize(const GenoView& g, const double* y, cudaStream_t s) {
+void k2_digitize(const GenoView& g, const double* y, cudaStream_t s, const DivIn& di) {
   const PMPlan& pl = g.pl2;
   allow_smem(k_digitize<1>, pl.dig_smem);
   launch_pdl(k_digitize<1>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, true, y,
              (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc,
-             pl.kt_cta, g.s2.dig, g.s2.dexp, g.s2.dsum, g.s2.cm);
+             pl.kt_cta, g.s2.dig, g.s2.dexp, g.s2.dsum, g.s2.cm, di.div, di.store, di.gate);
 }
 
 namespace {
@@ -1058,9 +1070,14 @@ void k2_main_only(const GenoView& g, cudaStream_t s) {
   launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, false);
 }
 
-void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s, bool stream_out) {
-  if (g.p_loc == 0) return;
-  k1_digitize(g, x, s);
+void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s, bool stream_out,
+              const DivIn& di) {
+  if (g.p_loc == 0) {
+    if (di.div) div_copy_dv(x, di.div, di.store, g.n, s, di.gate);
+    return;
+  }
+  k1_digitize(g, x, s, di);
+  if (di.div) x = di.store;  // the missing-entry terms read the stored quotient
   if (stream_out) {  // finish fused into the last CTA of each row block: y rows leave progressively
     launch_main<0>(g, g.pl1, g.lt1, g.s1, x, g.m1, s, true, y);
     return;
@@ -1071,13 +1088,13 @@ void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s, boo
              y);
 }
 
-void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s) {
-  if (g.n == 0) return;
-  if (g.p_loc == 0) {
-    cudaMemsetAsync(z, 0, sizeof(double) * (size_t)g.n, s);
+void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s, const DivIn& di) {
+  if (g.n == 0 || g.p_loc == 0) {
+    if (di.div) div_copy_dv(y, di.div, di.store, g.p_loc, s, di.gate);
+    if (g.n > 0) cudaMemsetAsync(z, 0, sizeof(double) * (size_t)g.n, s);
     return;
   }
-  k2_digitize(g, y, s);
+  k2_digitize(g, y, s, di);
   launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, true);
   launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
              (const double*)g.s2.part, g.pl2.nkc, g.pl2.rows_pad, g.n, z);
@@ -1092,11 +1109,13 @@ void digitize_into(const GenoView& g, const PMPlan& pl, const double* v, const P
   if (MODE == 0)
     launch_pdl(k_digitize<0>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, pdl, v,
                (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, g.n,
-               pl.kt_cta, sc.dig, sc.dexp, sc.dsum, (double*)nullptr);
+               pl.kt_cta, sc.dig, sc.dexp, sc.dsum, (double*)nullptr, (const double*)nullptr,
+               (double*)nullptr, (const int*)nullptr);
   else
     launch_pdl(k_digitize<1>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, pdl, v,
                (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc,
-               pl.kt_cta, sc.dig, sc.dexp, sc.dsum, sc.cm);
+               pl.kt_cta, sc.dig, sc.dexp, sc.dsum, sc.cm, (const double*)nullptr, (double*)nullptr,
+               (const int*)nullptr);
 }
 
 template <int MODE>

@@ -693,7 +693,7 @@ void Lanczos::cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec
   }
 }
 
-void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t hi) {
+void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t hi, bool last) {
   using namespace dev::ctl;
   const int L = (int)ctx_->shards.size();
   auto res = [&](int i, int64_t off) { return cd(i) + ctl_L_.res + off; };
@@ -708,11 +708,27 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
       launch(cd(i), ci(i), p, ctx_->shards[i].stream);
     }
   };
+  auto scal = [&](int slot) {
+    std::vector<const double*> d(L);
+    for (int i = 0; i < L; ++i) d[i] = cd(i) + ctl_L_.sc + slot;
+    return d;
+  };
+  auto alive_gates = [&]() {
+    std::vector<const int*> g(L);
+    for (int i = 0; i < L; ++i) g[i] = ci(i) + I_ALIVE;
+    return g;
+  };
   // Left half-step: alpha u_{s+1} = X v_s - U coupling.
   {
-    std::vector<const double*> vin(L);
-    for (int i = 0; i < L; ++i) vin[i] = V_[i] + s * n_;
-    op_->apply_dev(vin, w_);
+    std::vector<double*> vcol(L);
+    for (int i = 0; i < L; ++i) vcol[i] = V_[i] + s * n_;
+    if (v_pending_) {  // v_s = z / beta of the previous step, divided while digitized
+      std::vector<const double*> zr(z_.begin(), z_.end());
+      op_->apply_dev_div(zr, scal(S_BETA), alive_gates(), vcol, w_);
+      v_pending_ = false;
+    } else {
+      op_->apply_dev(std::vector<const double*>(vcol.begin(), vcol.end()), w_);
+    }
   }
   if (o.full) {
     if (s == 0) {
@@ -809,17 +825,22 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
     }
   }
 
-  // Right half-step: beta v_{s+1} = X^T u_{s+1} - alpha v_s.
-  for (int i = 0; i < L; ++i) {
-    ctx_->set_device(i);
-    const int64_t r = op_->rows(i);
-    dev::div_copy_dv(w_[i], cd(i) + ctl_L_.sc + S_ALPHA, U_[i] + s * r, r, ctx_->shards[i].stream,
-                     ci(i) + I_ALIVE);
-  }
+  // Right half-step: beta v_{s+1} = X^T u_{s+1} - alpha v_s, u_{s+1} = w / alpha
+  // (divided while the adjoint digitizes it unless GKB_NO_CTL_FUSE).
   {
-    std::vector<const double*> uin(L);
-    for (int i = 0; i < L; ++i) uin[i] = U_[i] + s * op_->rows(i);
-    op_->adjoint_dev(uin, z_);
+    std::vector<double*> ucol(L);
+    for (int i = 0; i < L; ++i) ucol[i] = U_[i] + s * op_->rows(i);
+    std::vector<const double*> wr(w_.begin(), w_.end());
+    if (fuse_ctl()) {
+      op_->adjoint_dev_div(wr, scal(S_ALPHA), alive_gates(), ucol, z_);
+    } else {
+      for (int i = 0; i < L; ++i) {
+        ctx_->set_device(i);
+        dev::div_copy_dv(w_[i], cd(i) + ctl_L_.sc + S_ALPHA, ucol[i], op_->rows(i),
+                         ctx_->shards[i].stream, ci(i) + I_ALIVE);
+      }
+      op_->adjoint_dev(std::vector<const double*>(ucol.begin(), ucol.end()), z_);
+    }
   }
   if (!o.full) {
     const bool fuse = fuse_ctl();  // right side: no allreduce before the decision
@@ -851,6 +872,10 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
     cgs2_dev(kRight, s + 1, z_, I_GRE, o, s, OP_R_END);
   } else {
     cgs2_dev(kRight, s + 1, z_, I_ALIVE, o, s, OP_R_END);
+  }
+  if (fuse_ctl() && !last) {  // v_{s+1} = z / beta: divided by the next step's apply
+    v_pending_ = true;
+    return;
   }
   for (int i = 0; i < L; ++i) {
     ctx_->set_device(i);
@@ -897,10 +922,11 @@ Lanczos::DevRun Lanczos::run_dev(const Options& o, int64_t nsteps, double* norm_
       if (lo < 0) lo = i;
       hi_c = i;
     }
+  v_pending_ = false;
   for (int64_t t = 0; t < nsteps; ++t) {
     const int64_t s = j_ + t;
     if (t > 0) lo = hi_c = s - 1;
-    enqueue_step_dev(o, s, lo, hi_c);
+    enqueue_step_dev(o, s, lo, hi_c, t + 1 == nsteps);
   }
   ctx_->set_device(0);
   Shard& s0 = ctx_->shards[0];

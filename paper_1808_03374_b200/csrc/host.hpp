@@ -115,6 +115,18 @@ struct DevOp {
   virtual void apply_dev(const std::vector<const double*>& x, const std::vector<double*>& y) = 0;
   // z (n) = sum_i X_i^T y_i, allreduced so every shard holds the full z.
   virtual void adjoint_dev(const std::vector<const double*>& y, const std::vector<double*>& z) = 0;
+  // The same products of x_raw / *div[i], the quotient stored to xs[i] unless
+  // *gate[i] == 0 (the Lanczos normalization before each product). Default:
+  // div_copy_dv, then the product; the genotype operator divides while it
+  // digitizes the input (one launch fewer, same bits).
+  virtual void apply_dev_div(const std::vector<const double*>& xraw,
+                             const std::vector<const double*>& div,
+                             const std::vector<const int*>& gate, const std::vector<double*>& xs,
+                             const std::vector<double*>& y);
+  virtual void adjoint_dev_div(const std::vector<const double*>& yraw,
+                               const std::vector<const double*>& div,
+                               const std::vector<const int*>& gate, const std::vector<double*>& ys,
+                               const std::vector<double*>& z);
   void alloc_host_api_buffers();
   void apply_host(const double* x, double* y);
   void adjoint_host(const double* y, double* z);
@@ -180,6 +192,12 @@ struct GenoOp : DevOp {
   void adjoint_block_dev(const std::vector<const double*>& Yb, const std::vector<int64_t>& ldyb,
                          int64_t k, const std::vector<double*>& Z, int64_t ldz) override;
   void adjoint_dev(const std::vector<const double*>& y, const std::vector<double*>& z) override;
+  void apply_dev_div(const std::vector<const double*>& xraw, const std::vector<const double*>& div,
+                     const std::vector<const int*>& gate, const std::vector<double*>& xs,
+                     const std::vector<double*>& y) override;
+  void adjoint_dev_div(const std::vector<const double*>& yraw,
+                       const std::vector<const double*>& div, const std::vector<const int*>& gate,
+                       const std::vector<double*>& ys, const std::vector<double*>& z) override;
   int64_t packed_bytes() const;
   int64_t device_bytes() const;
   // per-marker regression scan (regress.py marker_scan) with the block product
@@ -316,7 +334,8 @@ class Lanczos {
   void* ctl_down_ = nullptr;
   double* cd(int i) const { return reinterpret_cast<double*>(ctl_d_[i]); }
   int* ci(int i) const { return reinterpret_cast<int*>(cd(i) + ctl_L_.nd); }
-  void enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t hi);
+  void enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t hi, bool last);
+  bool v_pending_ = false;  // v_{s+1} = z / beta left to the next step's apply (same run)
   void cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec, int gate_slot,
                 const Options& o, int64_t s, int then_op = -1);
   static bool fuse_ctl();

@@ -87,10 +87,19 @@ void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int6
 // stream_out: y is written by the main kernel's last CTA of each row block (for
 // a page-locked host y: the rows cross PCIe while other blocks still stream);
 // otherwise by a separate fixed-order reduce (faster when y stays on the device).
+// di.div: the input is x / *di.div (the Lanczos normalization), divided inside
+// k_digitize and stored to di.store unless *di.gate == 0 -- what div_copy_dv
+// followed by the product does, bit for bit, one launch fewer.
+struct DivIn {
+  const double* div = nullptr;
+  double* store = nullptr;
+  const int* gate = nullptr;
+};
 void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s,
-              bool stream_out = false);
+              bool stream_out = false, const DivIn& di = DivIn());
 // K2 apply_adjoint (reference X^T*y, per-sample sum) over the local SNPs; z has n entries.
-void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s);
+void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s,
+                const DivIn& di = DivIn());
 // Two vectors per pass (block products): each column bitwise equal to the
 // single-vector product. `sb` is a second scratch set of the layout (vector 1).
 void k1_apply2(const GenoView& g, const PMScratch& sb, const double* x0, const double* x1,
@@ -103,8 +112,8 @@ void marker_scan(const GenoView& g, const double* P, int64_t ldp, int K, const d
                  const double* w, double yyc, double a0w, double denom, const int64_t* counts,
                  double* beta, double* se, double* icpt, double* sig2, int* dep, cudaStream_t s);
 // Pieces (for timing breakdowns): digitize, then the main tensor-core kernel.
-void k1_digitize(const GenoView& g, const double* x, cudaStream_t s);
-void k2_digitize(const GenoView& g, const double* y, cudaStream_t s);
+void k1_digitize(const GenoView& g, const double* x, cudaStream_t s, const DivIn& di = DivIn());
+void k2_digitize(const GenoView& g, const double* y, cudaStream_t s, const DivIn& di = DivIn());
 void k1_main_only(const GenoView& g, const double* x, cudaStream_t s);
 void k2_main_only(const GenoView& g, cudaStream_t s);
 

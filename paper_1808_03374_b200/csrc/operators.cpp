@@ -781,6 +781,30 @@ void GenoOp::get_scaling(double* mu, double* inv_s) {
   ctx->sync_all();
 }
 
+void DevOp::apply_dev_div(const std::vector<const double*>& xraw,
+                          const std::vector<const double*>& div,
+                          const std::vector<const int*>& gate, const std::vector<double*>& xs,
+                          const std::vector<double*>& y) {
+  for (size_t i = 0; i < ctx->shards.size(); ++i) {
+    ctx->set_device((int)i);
+    dev::div_copy_dv(xraw[i], div[i], xs[i], n, ctx->shards[i].stream, gate[i]);
+  }
+  std::vector<const double*> xc(xs.begin(), xs.end());
+  apply_dev(xc, y);
+}
+
+void DevOp::adjoint_dev_div(const std::vector<const double*>& yraw,
+                            const std::vector<const double*>& div,
+                            const std::vector<const int*>& gate, const std::vector<double*>& ys,
+                            const std::vector<double*>& z) {
+  for (size_t i = 0; i < ctx->shards.size(); ++i) {
+    ctx->set_device((int)i);
+    dev::div_copy_dv(yraw[i], div[i], ys[i], rows((int)i), ctx->shards[i].stream, gate[i]);
+  }
+  std::vector<const double*> yc(ys.begin(), ys.end());
+  adjoint_dev(yc, z);
+}
+
 void GenoOp::apply_dev(const std::vector<const double*>& x, const std::vector<double*>& y) {
   if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
   for (size_t i = 0; i < gs.size(); ++i) {
@@ -849,6 +873,39 @@ void GenoOp::adjoint_block_dev(const std::vector<const double*>& Yb,
     }
     adjoint_dev(yi, zi);
   }
+}
+
+void GenoOp::apply_dev_div(const std::vector<const double*>& xraw,
+                           const std::vector<const double*>& div,
+                           const std::vector<const int*>& gate, const std::vector<double*>& xs,
+                           const std::vector<double*>& y) {
+  if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
+  for (size_t i = 0; i < gs.size(); ++i) {
+    ctx->set_device((int)i);
+    dev::DivIn di;
+    di.div = div[i];
+    di.store = xs[i];
+    di.gate = gate[i];
+    dev::k1_apply(gs[i].view(), xraw[i], y[i], ctx->shards[i].stream, host_out_, di);
+    GKB_LAUNCH_CHECK();
+  }
+}
+
+void GenoOp::adjoint_dev_div(const std::vector<const double*>& yraw,
+                             const std::vector<const double*>& div,
+                             const std::vector<const int*>& gate, const std::vector<double*>& ys,
+                             const std::vector<double*>& z) {
+  if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
+  for (size_t i = 0; i < gs.size(); ++i) {
+    ctx->set_device((int)i);
+    dev::DivIn di;
+    di.div = div[i];
+    di.store = ys[i];
+    di.gate = gate[i];
+    dev::k2_adjoint(gs[i].view(), yraw[i], z[i], ctx->shards[i].stream, di);
+    GKB_LAUNCH_CHECK();
+  }
+  ctx->allreduce(z, n);
 }
 
 void GenoOp::adjoint_dev(const std::vector<const double*>& y, const std::vector<double*>& z) {
