@@ -105,7 +105,10 @@ __device__ void run_op(double* __restrict__ d, int* __restrict__ iv, const Param
         double* smu = sB + kStageJ * kStageJ;
         double* snu = smu + kStageJ + 2;
         double* scp = snu + kStageJ + 2;
-        for (int64_t e = t; e < j * j; e += blockDim.x) sB[e] = B[(e % j) + (e / j) * cap];
+        // warp w copies columns w, w + 4, ...; lanes the rows (no 64-bit div/mod)
+        const int jj = (int)j, lane = t & 31, nw = (int)(blockDim.x >> 5);
+        for (int c = t >> 5; c < jj; c += nw)
+          for (int i = lane; i < jj; i += 32) sB[i + c * jj] = B[i + (int64_t)c * cap];
         for (int64_t e = t; e <= j; e += blockDim.x) {
           smu[e] = mu[e];
           snu[e] = nu[e];
