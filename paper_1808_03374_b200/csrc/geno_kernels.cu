@@ -59,6 +59,9 @@ static_assert(kStripsPerWarp <= 2, "the unrolled full-range loop prefetches stri
 constexpr int kRowsPerCta = 8 * kStripsPerWarp * 16;  // 256
 constexpr int kStripsPerCta = 8 * kStripsPerWarp;
 constexpr int kMinCtas = kStripsPerWarp <= 2 ? 4 : 3;  // per SM (register budget)
+#ifndef GKB_EARLY_STAGE
+#define GKB_EARLY_STAGE 1  // k_pm_main: staging complete before the loop (no barrier after it)
+#endif
 
 // .bed 2-bit code -> dosage code r (r_hi = ~h, r_lo = l ^ h per field).
 __device__ __forceinline__ uint32_t bed_to_r(uint32_t c) {
@@ -532,6 +535,12 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     const uint4* gd = dig + kt0 * 64;
     for (int i = threadIdx.x; i < ktiles * 64; i += kThreads) dg[i] = gd[i];
   }
+#if GKB_EARLY_STAGE
+  // the coefficient and list copies land together with the digits (both from
+  // L2): one barrier, and each warp goes from its loop straight to its rows'
+  // epilogue instead of waiting there for the CTA's slowest warp
+  if (m_off) cp_async_wait_all();
+#endif
   __syncthreads();
   // swizzled digit slots: the 8 lanes of each quarter-warp hit 8 distinct 16-byte bank groups
   const int sw = g ^ (2 * tid);
@@ -583,10 +592,12 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     }
   }
 #undef GKB_PM_STEP
+#if !GKB_EARLY_STAGE
   if (m_off) {
     cp_async_wait_all();
     __syncthreads();
   }
+#endif
   // Epilogue. Thread (g, tid) holds digits (2 tid, 2 tid + 1) of rows g and
   // g + 8; 2^(16 tid) (D_2tid + 256 D_2tid+1) is exact in fp64, and the four
   // threads of the group add their parts by a butterfly (identical bits in
@@ -784,6 +795,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
       dg1[i] = gd1[i];
     }
   }
+#if GKB_EARLY_STAGE
+  if (m_off) cp_async_wait_all();  // as in k_pm_main
+#endif
   __syncthreads();
   const int sw = g ^ (2 * tid);
   const uint4* bp = dg + tid * 8 + sw;
@@ -806,10 +820,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
     GKB_PM2_STEP(bC, bB)
   }
 #undef GKB_PM2_STEP
+#if !GKB_EARLY_STAGE
   if (m_off) {
     cp_async_wait_all();
     __syncthreads();
   }
+#endif
   const int E0 = a.dexp[0][kc], E1 = a.dexp[1][kc];
   const double rs0 = a.dsum[0][kc], rs1 = a.dsum[1][kc];
   const double p0 = pow2(16 * tid), p1 = pow2(16 * tid + 8);
