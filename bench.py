@@ -101,7 +101,7 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-NCU_CAPTURE = "r1i_ncu_full_config2.json"  # ncu --set full of the current main kernels
+NCU_CAPTURE = "r1j_ncu_full_config2.json"  # ncu --set full of the current main kernels
 
 
 def ncu_traffic(kernel: str):

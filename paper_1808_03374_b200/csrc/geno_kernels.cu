@@ -445,6 +445,55 @@ __device__ __forceinline__ double walk_list(const uint16_t* __restrict__ ent, ui
   return corr;
 }
 
+// walk_list over two runs at once: each sum in its own sequential order (the
+// bits of two walk_list calls), the two runs' load latencies overlapped
+__device__ __forceinline__ void walk_list_pair(const uint16_t* __restrict__ ent, uint32_t ka,
+                                               uint32_t kea, uint32_t kb, uint32_t keb,
+                                               const double* __restrict__ cv, double& ca,
+                                               double& cb) {
+  double sa = 0.0, sb = 0.0;
+#pragma unroll 1
+  for (; ka + 4 <= kea && kb + 4 <= keb; ka += 4, kb += 4) {
+    const int a0 = ent[ka], a1 = ent[ka + 1], a2 = ent[ka + 2], a3 = ent[ka + 3];
+    const int b0 = ent[kb], b1 = ent[kb + 1], b2 = ent[kb + 2], b3 = ent[kb + 3];
+    const double x0 = cv[a0], x1 = cv[a1], x2 = cv[a2], x3 = cv[a3];
+    const double y0 = cv[b0], y1 = cv[b1], y2 = cv[b2], y3 = cv[b3];
+    sa += x0;
+    sb += y0;
+    sa += x1;
+    sb += y1;
+    sa += x2;
+    sb += y2;
+    sa += x3;
+    sb += y3;
+  }
+  // the rest of each run as walk_list continues it
+#pragma unroll 1
+  for (; ka + 4 <= kea; ka += 4) {
+    const int c0 = ent[ka], c1 = ent[ka + 1], c2 = ent[ka + 2], c3 = ent[ka + 3];
+    sa += cv[c0];
+    sa += cv[c1];
+    sa += cv[c2];
+    sa += cv[c3];
+  }
+#pragma unroll 1
+  for (; kb + 4 <= keb; kb += 4) {
+    const int c0 = ent[kb], c1 = ent[kb + 1], c2 = ent[kb + 2], c3 = ent[kb + 3];
+    sb += cv[c0];
+    sb += cv[c1];
+    sb += cv[c2];
+    sb += cv[c3];
+  }
+  // tails (< 4 each) interleaved
+#pragma unroll 1
+  for (; ka < kea || kb < keb; ++ka, ++kb) {
+    if (ka < kea) sa += cv[ent[ka]];
+    if (kb < keb) sb += cv[ent[kb]];
+  }
+  ca = sa;
+  cb = sb;
+}
+
 // Missing-list staging in shared memory (after the digits): 257 offsets and
 // up to kEntCap entries of the CTA's list (longer lists are read from global).
 constexpr int kEntCap = 4096 * kStripsPerWarp;
@@ -606,6 +655,9 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
   const int E = dexp[kc];
   const double rsum = dsum[kc];
   const double p0 = pow2(16 * tid), p1 = pow2(16 * tid + 8);
+  double val[kStripsPerWarp], corr[kStripsPerWarp];
+  int64_t rowr[kStripsPerWarp];
+  uint32_t k0[kStripsPerWarp], ke[kStripsPerWarp];
 #pragma unroll
   for (int r = 0; r < kStripsPerWarp; ++r) {
     double v0 = (double)acc[r][0] * p0 + (double)acc[r][1] * p1;
@@ -615,26 +667,42 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
     v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
     const int hi = tid & 1;
-    const int64_t row = (strip0 + r) * 16 + g + 8 * hi;
-    const int rl = (int)(row - (int64_t)bx * kRowsPerCta);
-    const double val = scalbn(hi ? v1 : v0, E - 62);
-    double corr = 0.0;
+    rowr[r] = (strip0 + r) * 16 + g + 8 * hi;
+    val[r] = scalbn(hi ? v1 : v0, E - 62);
+    corr[r] = 0.0;
     if (m_off) {
+      const int rl = (int)(rowr[r] - (int64_t)bx * kRowsPerCta);
       const uint32_t e0 = offs[rl], e1 = offs[rl + 1], mid = e0 + (e1 - e0) / 2;
-      const uint32_t k0 = (tid >> 1) ? mid : e0, ke = (tid >> 1) ? e1 : mid;
-      if (ent_shift >= 0)  // shared-memory run (pointer derived from the smem array: LDS)
-        corr = walk_list(reinterpret_cast<const uint16_t*>(stage + kOffBytes) + ent_shift, k0, ke,
-                         cvs);
-      else
-        corr = walk_list(m_ent + eb, k0, ke, cvs);
-      corr += __shfl_xor_sync(0xffffffffu, corr, 2);  // both halves, commutative -> same bits
+      k0[r] = (tid >> 1) ? mid : e0;
+      ke[r] = (tid >> 1) ? e1 : mid;
     }
+  }
+  if (m_off) {
+    if (ent_shift >= 0) {  // shared-memory runs (pointer derived from the smem array: LDS)
+      const uint16_t* ent = reinterpret_cast<const uint16_t*>(stage + kOffBytes) + ent_shift;
+      if (kStripsPerWarp == 2)  // both strips' runs walked together (latencies overlap)
+        walk_list_pair(ent, k0[0], ke[0], k0[kStripsPerWarp - 1], ke[kStripsPerWarp - 1], cvs,
+                       corr[0], corr[kStripsPerWarp - 1]);
+      else
+#pragma unroll
+        for (int r = 0; r < kStripsPerWarp; ++r) corr[r] = walk_list(ent, k0[r], ke[r], cvs);
+    } else {
+#pragma unroll
+      for (int r = 0; r < kStripsPerWarp; ++r) corr[r] = walk_list(m_ent + eb, k0[r], ke[r], cvs);
+    }
+#pragma unroll
+    for (int r = 0; r < kStripsPerWarp; ++r)  // both halves, commutative -> same bits
+      corr[r] += __shfl_xor_sync(0xffffffffu, corr[r], 2);
+  }
+#pragma unroll
+  for (int r = 0; r < kStripsPerWarp; ++r) {
     if ((tid >> 1) == 0) {
+      const int64_t row = rowr[r];
       double out;
       if (MODE == 0) {  // a missing entry holds the imputed mean (genio.cpp:144)
-        out = val - mu[row] * rsum - (3.0 - mean[row]) * corr;
+        out = val[r] - mu[row] * rsum - (3.0 - mean[row]) * corr[r];
       } else {
-        out = val - rsum - corr;
+        out = val[r] - rsum - corr[r];
       }
       part[(int64_t)kc * rows_pad + row] = out;
     }
