@@ -2,28 +2,35 @@
 """Benchmark of the B200 GKL hot path (BASELINE.json metric).
 
 Headline metric: packed genotype matvec HBM GB/s (A*v + A^T*u), plus seconds
-to the top-k singular triplets. Workload: BASELINE config 2 (n = 10,000
-individuals x p = 100,000 SNPs per GPU, Balding-Nichols, 5 subpopulations,
-1% missing, 50 related pairs; 250 MB packed), generated on the device with
-the seeded counter-based generator (synthetic data, same model as the
-config). A step is one reference apply (A^T u, per-SNP dot, kernel K1) plus
-one apply_adjoint (A v, per-sample sum, kernel K2) on device-resident
-vectors; `value` = 2 * packed bytes / step time, summed over ranks. Each
-product is three launches: k_digitize (coefficients -> fixed-point digits),
-k_pm_main (tensor-core packed product + missing/mean corrections) and a
-fixed-order partial-sum reduce.
+to the top-k singular triplets. Default workload: BASELINE config 4, the
+largest single-GPU config (n = 500,000 individuals x p = 100,000 SNPs,
+Dirichlet(0.5) admixture of 4 Balding-Nichols subpopulations, F = 0.01, 1%
+missing; 12.5 GB packed), generated on the device by the seeded
+counter-based generator (synthetic data of the config's model; BASELINE names
+no public dataset). `--config 3` selects config 3 (6.25 GB packed).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+A step is one reference apply (A^T u, per-SNP dot, kernel K1) plus one
+apply_adjoint (A v, per-sample sum, kernel K2) on device-resident vectors;
+`value` = 2 * packed bytes of the whole matrix / step time. Each product is
+digitize + main + a fixed-order partial-sum reduce.
 
-N > 1 runs under torchrun, one rank per GPU over NCCL; each rank holds a
-full config-2-sized SNP shard (weak scaling) and the adjoint's length-n
-partial sums are combined with ncclAllReduce. `--impl reference` times the
-reference algorithm's CPU implementation (the oracle restatement, all host
-threads) on the same workload.
+  python bench.py [--config 4] [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU over NCCL: STRONG scaling -- the
+config's SNPs are partitioned across the ranks (each owns ~p/N SNPs), K1 is
+shard-local and K2's length-n partial sums are combined with ncclAllReduce;
+`time_to_solution` is the sharded svdl.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle restatement in oracle/, the reference itself cannot be built here: no
+Eigen / vendor/) with all host threads on a bounded SNP sample of the SAME
+config, and never loads libgkb: the workload spec comes from
+paper_1808_03374_b200/workloads.py loaded by file path (pure numpy).
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
 import statistics
@@ -37,8 +44,25 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-CFG = 2
+DEFAULT_CFG = 4
 METRIC = "packed genotype matvec HBM GB/s (A·v+Aᵀ·u); seconds to top-k singular triplets"
+# ncu --set full captures of the main kernels per config (tools/ncu_summary.py)
+NCU_CAPTURE = {4: "r2_ncu_full_config4.json", 3: "r2_ncu_full_config3.json",
+               2: "r1j_ncu_full_config2.json"}
+
+
+def load_workloads():
+    """paper_1808_03374_b200/workloads.py by path: the package (and libgkb)
+    is never imported on the reference arm."""
+    name = "_gkb_workloads"
+    if name in sys.modules:
+        return sys.modules[name]
+    spec = importlib.util.spec_from_file_location(
+        name, os.path.join(ROOT, "paper_1808_03374_b200", "workloads.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
 
 
 def load_peaks():
@@ -101,31 +125,24 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-NCU_CAPTURE = "r1j_ncu_full_config2.json"  # ncu --set full of the current main kernels
-
-
-def ncu_traffic(kernel: str):
+def ncu_traffic(cfg: int, kernel: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
     the committed `ncu --set full` capture of this workload (profiles/)."""
-    import glob
-    best = None
-    # the current capture last (the glob order is only a fallback for older ones)
-    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_config2.json")))
-    cur = os.path.join(ROOT, "profiles", NCU_CAPTURE)
-    paths = [q for q in paths if q != cur] + ([cur] if os.path.exists(cur) else [])
-    for p in paths:
-        try:
-            with open(p) as f:
-                d = json.load(f)
-            m = d[kernel]
-            def mb(s):
-                v, u = s.split()[:2]
-                return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
-            best = (int(mb(m["dram__bytes_read.sum"]) + mb(m["dram__bytes_write.sum"])),
-                    os.path.basename(p))
-        except Exception:
-            continue
-    return best
+    name = NCU_CAPTURE.get(cfg)
+    if not name:
+        return None
+    p = os.path.join(ROOT, "profiles", name)
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        m = d[kernel]
+
+        def mb(s):
+            v, u = s.split()[:2]
+            return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
+        return (int(mb(m["dram__bytes_read.sum"]) + mb(m["dram__bytes_write.sum"])), name)
+    except Exception:
+        return None
 
 
 def dist_env():
@@ -135,11 +152,23 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_port_sample(spec, rows: int, nthreads: int, min_seconds: float, max_steps: int = 1000):
-    """Times the oracle's packed operator (apply + apply_adjoint) on the
-    first `rows` SNPs of the workload. Returns (GB/s, steps, seconds)."""
+def config_block(W, cfg, spec, ws):
+    """The `config` object; identical on both arms (same workload)."""
+    return {"workload": W.CONFIG_TEXT[cfg] + ", hwe standardization (g-2f)/sqrt(2f(1-f))",
+            "config_index": cfg, "n": spec.n, "p": spec.p,
+            "packed_bytes": spec.p * ((spec.n + 3) // 4),
+            "options": W.OPTIONS_TEXT[cfg],
+            "l2": "inputs larger than L2 (two multi-GB tile layouts alternate; no flush)",
+            "parallelism": f"snp-shard{ws}"}
+
+
+# ---------------------------------------------------------------- CPU legs
+def cpu_port_sample(W, spec, rows: int, nthreads: int, min_seconds: float,
+                    max_steps: int = 1000, row0: int = 0):
+    """Times the oracle's packed operator (apply + apply_adjoint) on SNPs
+    [row0, row0 + rows) of the workload. Returns (GB/s, steps, seconds)."""
     import oracle
-    payload = oracle.synth_bed(spec, 0, rows)
+    payload = oracle.synth_bed(spec, row0, row0 + rows)
     counts = oracle.marker_counts(payload, rows, spec.n)
     mu, inv_s = oracle.marker_scaling(counts, spec.n, 2)
     g = oracle.GenoOracle(payload, rows, spec.n, mu, inv_s, nthreads=nthreads)
@@ -158,42 +187,88 @@ def cpu_port_sample(spec, rows: int, nthreads: int, min_seconds: float, max_step
     return bytes_step * steps / el / 1e9, steps, el
 
 
+def cpu_dense_svdl(W, cfg: int):
+    """The reference's literal CPU path on config `cfg` (1 thread, as the
+    reference runs): .bed bytes -> dense fp64 impute_mean + standardize
+    (load_matrix, gkpca.cpp:89-108; genio.cpp:124-185) -> DenseOperator
+    (linop.hpp:43-64) -> svdl (gkl.cpp:416-514), restated in oracle/."""
+    import oracle
+    spec = W.config_spec(cfg)
+    payload = oracle.synth_bed(spec)
+    counts = oracle.marker_counts(payload, spec.p, spec.n)
+    mu, inv_s = oracle.marker_scaling(counts, spec.n, 2)
+    t0 = time.perf_counter()
+    X = oracle.dense_standardized(payload, spec.p, spec.n, mu, inv_s)
+    t_pre = time.perf_counter() - t0
+    opts = oracle.Options(**W.CONFIG_OPTIONS[cfg])
+    t0 = time.perf_counter()
+    r = oracle.svdl(oracle.DenseOracle(X), opts)
+    t = time.perf_counter() - t0
+    return {"config": cfg, "seconds": round(t, 3), "preprocess_seconds": round(t_pre, 3),
+            "mvps": r.mvps, "steps": r.steps, "restarts": r.restarts,
+            "converged": bool(r.all_converged), "cores": 1,
+            "sigma_1": float(r.singvals[0]) if r.singvals.size else None,
+            "path": "oracle dense (densified fp64 matrix, column-major GEMV) svdl, 1 thread"}
+
+
 def run_reference(args):
+    """CPU reference arm: the oracle restatement of the reference's operator,
+    all host threads, on a bounded SNP sample of the same config."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    from paper_1808_03374_b200 import synth
-    spec = synth.config_spec(CFG)
+    W = load_workloads()
+    cfg = args.config
+    spec = W.config_spec(cfg)
     cores = os.cpu_count() or 1
-    rows = 8000
+    stride = (spec.n + 3) // 4
+    # ~1 GB of packed rows per product: a step is ~1 s of 16-core CPU work
+    rows = max(64, min(spec.p, int(1e9 // stride)))
     vals = []
     for _ in range(args.warmup):
-        cpu_port_sample(spec, rows, cores, 0.0, max_steps=1)
+        cpu_port_sample(W, spec, min(rows, 256), cores, 0.0, max_steps=1)
+    import oracle
+    payload = oracle.synth_bed(spec, 0, rows)
+    counts = oracle.marker_counts(payload, rows, spec.n)
+    mu, inv_s = oracle.marker_scaling(counts, spec.n, 2)
+    g = oracle.GenoOracle(payload, rows, spec.n, mu, inv_s, nthreads=cores)
+    x = oracle.rng_fill_symmetric(7, spec.n)
+    x /= np.linalg.norm(x)
+    g.apply_adjoint(g.apply(x))
+    t_all = time.perf_counter()
     for _ in range(args.steps):
-        gbs, _, _ = cpu_port_sample(spec, rows, cores, 1.0)
-        vals.append(gbs)
-    v = statistics.median(vals)
+        t0 = time.perf_counter()
+        y = g.apply(x)
+        g.apply_adjoint(y)
+        vals.append(2 * rows * stride / (time.perf_counter() - t0) / 1e9)
+    el = time.perf_counter() - t_all
+    v = 2 * rows * stride * args.steps / el / 1e9
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GB/s",
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(2 * rows * ((spec.n + 3) // 4) / (v * 1e9) * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Balding-Nichols, BASELINE config 2 model)",
-        "config": {"workload": f"config {CFG}: n=10000 x p=100000 (sample: first {rows} SNPs)",
-                   "n": spec.n, "p": spec.p},
-        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle packed operator apply+apply_adjoint on SNPs "
-                                   f"[0,{rows}) of config {CFG}, OpenMP {cores} threads"},
-        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+        "ms_per_step": round(el / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based generator of the config's BASELINE model)",
+        "config": config_block(W, cfg, spec, ws),
+        "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"oracle packed operator apply+apply_adjoint (OpenMP, {cores} "
+                                   f"threads) on SNPs [0,{rows}) of config {cfg} "
+                                   f"({2 * rows * stride / 1e9:.2f} GB per step); the full "
+                                   f"config is {spec.p} SNPs", "step_gbs_median":
+                                   round(statistics.median(vals), 4)},
+        "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- GPU arm
 def run_ours(args):
     import paper_1808_03374_b200 as gkb
     from paper_1808_03374_b200 import synth
 
+    W = load_workloads()
+    cfg = args.config
     ws, rank, local = dist_env()
     dist = None
     if ws > 1:
@@ -210,54 +285,54 @@ def run_ours(args):
     else:
         ctx = gkb.Context((0,))
 
-    base = synth.config_spec(CFG)
-    # weak scaling: every rank holds p=100,000 SNPs; the global matrix is
-    # n x (p * ws) drawn from one seeded model
-    spec = synth.balding_nichols(base.n, base.p * ws, 5, 0.01, seed=2, missing_rate=0.01,
-                                 related_pairs=50, name=f"C2x{ws}") if ws > 1 else base
+    def barrier():
+        ctx.synchronize()
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if not dist:
+            return v
+        import torch
+        tt = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    # strong scaling: the config's SNPs partitioned across the ranks
+    spec = synth.config_spec(cfg)
     t_build = time.perf_counter()
     op = gkb.GenotypeOperator.from_synth(spec, ctx=ctx, scheme=gkb.ScalingScheme.kHwe)
     ctx.synchronize()
     t_build = time.perf_counter() - t_build
     info = op.info()
     packed_local = info["packed_bytes"]
-
-    def barrier():
-        ctx.synchronize()
-        if dist:
-            dist.barrier()
+    packed_total = spec.p * ((spec.n + 3) // 4)
 
     # warm-up steps, then per-kernel timings (device events on the library's
     # stream) and the timed region; nvidia-smi samples clocks across this whole
-    # window (>= ~1 s of the same kernels) so the timed region is covered.
-    op.bench(2, max(1, args.warmup), flush_l2=False)
+    # window (the same kernels back to back) so the timed region is covered.
+    op.bench(2, args.warmup, flush_l2=False)
     barrier()
     with ClockSampler(local) as clk:
-        iters_k = max(args.steps, int(0.5 / max(1e-6, 0.15e-3 * packed_local / 250e6)))
+        iters_k = max(args.steps, int(0.4 / max(1e-6, 0.15e-3 * packed_local / 250e6)))
         k1_ms, k1_main, _ = op.bench(0, iters_k, flush_l2=False)
         k2_ms, k2_main, _ = op.bench(1, iters_k, flush_l2=False)
         barrier()
         step_ms, main_ms, launches = op.bench(2, args.steps, flush_l2=False)
         barrier()
     clocks = clk.summary()
-    # max over ranks
-    if dist:
-        import torch
-        tt = torch.tensor([step_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        step_ms = float(tt.item())
-    packed_total = packed_local * ws
+    step_ms = max_over_ranks(step_ms)
     value = 2 * packed_total / (step_ms * 1e-3) / 1e9
 
     # e2e through the public API with host buffers (H2D inputs, D2H results)
-    # (pinned host buffers: page-locked numpy arrays from gkb.pinned_empty)
+    # (page-locked numpy arrays from gkb.pinned_empty, used in place)
     rng = np.random.default_rng(7)
     x = gkb.pinned_empty(spec.n)
     x[:] = rng.standard_normal(spec.n)
     x /= np.linalg.norm(x)
     y = gkb.pinned_empty(spec.p)
     z = gkb.pinned_empty(spec.n)
-    for _ in range(max(1, args.warmup)):
+    for _ in range(args.warmup):
         op.apply(x, out=y)
         op.apply_adjoint(y, out=z)
     barrier()
@@ -266,26 +341,22 @@ def run_ours(args):
         op.apply(x, out=y)
         op.apply_adjoint(y, out=z)
     barrier()
-    e2e_s = (time.perf_counter() - t0) / args.steps
-    if dist:
-        import torch
-        tt = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
     e2e = 2 * packed_total / e2e_s / 1e9
-    h2d = 8 * (spec.n + spec.p)   # x (n) for apply, y (p) for the adjoint
-    d2h = 8 * (spec.p + spec.n)   # y (p) and z (n) read back
+    h2d = 8 * (spec.n + spec.p) * ws   # x (n) for apply, y (p) for the adjoint, every rank
+    d2h = 8 * (spec.p + spec.n) * ws   # y (p) and z (n) read back
 
-    # .bed file -> HBM ingest: the workload's payload written
-    # as a PLINK fileset, then streamed back through gkb_geno_from_bed_file
-    # (page-cache-warm file; both layouts + counts + missing lists built)
+    # .bed file -> HBM ingest on a leading SNP block of the
+    # workload written as a PLINK fileset (page-cache-warm file)
     ingest = None
     if rank == 0 and ws == 1 and not args.no_ingest:
         import tempfile
         from paper_1808_03374_b200 import genio
+        rows = min(spec.p, max(4096, int(1.0e9 // ((spec.n + 3) // 4))))
         with tempfile.TemporaryDirectory() as td:
-            pre = os.path.join(td, "c2")
-            genio.write_bed(op.read_bed(), spec.p, spec.n, pre + ".bed", pre + ".bim", pre + ".fam")
+            pre = os.path.join(td, "blk")
+            genio.write_bed(op.read_bed(0, rows), rows, spec.n, pre + ".bed", pre + ".bim",
+                            pre + ".fam")
             op_f = gkb.GenotypeOperator.from_bed_file(pre, ctx=ctx)  # warm the page cache
             op_f.close()
             t0 = time.perf_counter()
@@ -293,23 +364,24 @@ def run_ours(args):
             ctx.synchronize()
             t_in = time.perf_counter() - t0
             op_f.close()
-        fbytes = packed_local + 3
+        fbytes = rows * ((spec.n + 3) // 4) + 3
         ingest = {"seconds": round(t_in, 4), "bytes": fbytes, "gbs": round(fbytes / t_in / 1e9, 2),
-                  "note": "page-cache-warm .bed -> HBM: header/size checks, streamed positional "
-                          "reads + both tile layouts, marker counts, missing lists, scaling"}
+                  "note": f"page-cache-warm .bed of SNPs [0,{rows}) of the workload -> HBM: "
+                          "header/size checks, streamed positional reads + both tile layouts, "
+                          "marker counts, missing lists, scaling"}
 
-    # time to top-k triplets (BASELINE config-2 options)
-    opts = synth.config_options(CFG)
+    # time to top-k triplets (the config's BASELINE options)
+    opts = synth.config_options(cfg)
     barrier()
     t0 = time.perf_counter()
     res = gkb.svdl(op, opts)
-    tts_first = time.perf_counter() - t0  # includes the solver's one-time buffers
+    tts_first = max_over_ranks(time.perf_counter() - t0)  # includes the solver's buffers
     barrier()
     t0 = time.perf_counter()
     res = gkb.svdl(op, opts)
-    tts = time.perf_counter() - t0
+    tts = max_over_ranks(time.perf_counter() - t0)
 
-    # widened rows (SURVEY §8f 3-4) on the same operator: subspace iteration
+    # widened rows (SURVEY 8f 3-4) on the same operator: subspace iteration
     # (QR variant, device-resident blocks; a bounded 40-iteration sample) and
     # the per-marker PC-adjusted regression scan with the solve's first 10 PCs
     widened = None
@@ -341,31 +413,46 @@ def run_ours(args):
     b_mvp = packed_local
     k1_gbs = b_mvp / (k1_main * 1e-3) / 1e9
     k2_gbs = b_mvp / (k2_main * 1e-3) / 1e9
-    # dominant kernel = the slower of the two tensor-core main kernels
-    # (k_pm_main<1> = K2 apply_adjoint, k_pm_main<0> = K1 apply); main_ms is
-    # its average launch duration from CUDA events on the library's stream
+    # dominant kernel = the slower of the two main kernels (k_pm_main<1> = K2
+    # apply_adjoint, k_pm_main<0> = K1 apply); its average launch duration
+    # from CUDA events on the library's stream
     dom = ("K2 apply_adjoint (A·v): k_pm_main<1>", k2_gbs, k2_main, "k_pm_main<1>") \
         if k2_main >= k1_main else ("K1 apply (Aᵀ·u): k_pm_main<0>", k1_gbs, k1_main, "k_pm_main<0>")
-    traffic = ncu_traffic(dom[3]) if ws == 1 else None
+    traffic = ncu_traffic(cfg, dom[3]) if ws == 1 else None
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        gbs, steps, el = cpu_port_sample(spec, 2000, 1, 10.0)
+        # faithful configuration: 1 thread (the reference's Eigen GEMV is
+        # single-threaded; no OpenMP in proj/CMakeLists.txt)
+        rows = max(64, int(2.5e8 // ((spec.n + 3) // 4)))
+        gbs, steps, el = cpu_port_sample(W, spec, rows, 1, 10.0)
         cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port",
                "sample": f"oracle packed operator (1 thread), apply+apply_adjoint on SNPs "
-                         f"[0,2000) of config {CFG}, {steps} steps in {el:.1f}s"}
+                         f"[0,{rows}) of config {cfg}, {steps} steps in {el:.1f}s"}
+        if not args.no_cpu_svdl:
+            # time to solution on the reference's literal dense path (config 1),
+            # beside the GPU solve of the same config
+            sv = cpu_dense_svdl(W, 1)
+            op1 = gkb.GenotypeOperator.from_synth(synth.config_spec(1), ctx=ctx,
+                                                  scheme=gkb.ScalingScheme.kHwe)
+            o1 = synth.config_options(1)
+            gkb.svdl(op1, o1)
+            t0 = time.perf_counter()
+            r1 = gkb.svdl(op1, o1)
+            sv["gpu_seconds"] = round(time.perf_counter() - t0, 4)
+            sv["gpu_mvps"] = r1.stats.mvps
+            sv["gpu_sigma_1"] = float(r1.singvals[0])
+            op1.close()
+            cpu["svdl"] = sv
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded Balding-Nichols, BASELINE config 2 model, device-generated)",
-            "config": {"workload": f"config {CFG}: n={spec.n} x p={base.p} SNPs per GPU, 5 subpops, "
-                                   f"F=0.01, 1% missing, 50 related pairs, hwe standardization",
-                       "n": spec.n, "p_total": spec.p, "packed_bytes_per_gpu": packed_local,
-                       "l2": "inputs larger than L2 (2 x 250 MB layouts alternate; no flush)",
-                       "parallelism": f"snp-shard{ws}"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based generator of the config's BASELINE model, "
+                    "device-generated)",
+            "config": config_block(W, cfg, spec, ws),
             "gpu_launches": launches * args.steps,
             "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": round(dom[1], 1),
                          "peak": peak, "unit": "GB/s", "frac": round(dom[1] / peak, 4),
@@ -375,6 +462,7 @@ def run_ours(args):
                          "peak_source": peak_src,
                          "k1_apply_gbs": round(k1_gbs, 1), "k2_adjoint_gbs": round(k2_gbs, 1),
                          "k1_main_ms": round(k1_main, 5), "k2_main_ms": round(k2_main, 5),
+                         "k1_step_ms": round(k1_ms, 5), "k2_step_ms": round(k2_ms, 5),
                          "algorithmic_bytes_per_launch": b_mvp},
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -383,10 +471,11 @@ def run_ours(args):
                                  "steps": res.stats.steps, "restarts": res.stats.restarts,
                                  "converged": res.stats.converged, "k": opts.k,
                                  "host_syncs": res.stats.host_syncs,
+                                 "solve_gbs": round(res.stats.mvps * packed_total / tts / 1e9, 1),
                                  "first_call_seconds": round(tts_first, 4),
                                  "note": "second solve on the same operator; the first call also "
                                          "allocates the solver's device/pinned buffers",
-                                 "options": "partial reorth w=1e-8, thick restart 50/25, tol 1e-10"},
+                                 "options": W.OPTIONS_TEXT[cfg]},
             "clocks": clocks,
             "build_seconds": round(t_build, 3),
         }
@@ -407,8 +496,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=DEFAULT_CFG, choices=[1, 2, 3, 4])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
+    ap.add_argument("--no-cpu-svdl", action="store_true",
+                    help="skip the CPU time-to-solution leg (config 1, dense, 1 thread)")
     ap.add_argument("--no-ingest", action="store_true", help="skip the .bed ingest timing")
     ap.add_argument("--no-widen", action="store_true",
                     help="skip the subspace / regression timings")

@@ -263,6 +263,25 @@ class GenoOracle:
         return z
 
 
+def dense_standardized(payload, p, n, mu, inv_s) -> np.ndarray:
+    """The reference's literal preprocessing (load_matrix, gkpca.cpp:89-108):
+    .bed decode (genio.cpp:33,53-83) -> impute_mean (missing -> observed
+    row mean, genio.cpp:124-148) -> affine standardization with the given
+    (mu, 1/s) (genio.cpp:150-185). Returns the dense p x n fp64 matrix in
+    column-major order (the layout DenseOperator's Eigen GEMV reads)."""
+    d = bed_decode(payload, p, n)
+    mean = marker_means(marker_counts(payload, p, n))
+    X = np.empty((p, n), dtype=np.float64, order="F")
+    step = max(1, (1 << 27) // max(n, 1))
+    for j0 in range(0, p, step):  # row blocks: bounded temporaries
+        j1 = min(p, j0 + step)
+        blk = d[j0:j1].astype(np.float64)
+        miss = d[j0:j1] == 3
+        blk[miss] = np.broadcast_to(mean[j0:j1, None], blk.shape)[miss]
+        X[j0:j1] = (blk - np.asarray(mu)[j0:j1, None]) * np.asarray(inv_s)[j0:j1, None]
+    return X
+
+
 class DenseOracle:
     def __init__(self, X):
         self.X = np.asfortranarray(np.asarray(X, dtype=np.float64))

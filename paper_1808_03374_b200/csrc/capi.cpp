@@ -646,9 +646,14 @@ int gkb_cgs2(gkb_ctx* ctx, const double* basis, int64_t len, int64_t ncols, doub
     gkb::Context& c = ctx->c;
     c.set_device(0);
     gkb::Shard& s = c.shards[0];
-    double *Q = nullptr, *dv = nullptr;
-    GKB_CUDA(cudaMalloc(&Q, sizeof(double) * (size_t)std::max<int64_t>(len * ncols, 1)));
-    GKB_CUDA(cudaMalloc(&dv, sizeof(double) * (size_t)std::max<int64_t>(len, 1)));
+    if (len < 0 || ncols < 0) gkb::fail(GKB_EINVAL, "cgs2: negative size");
+    // result slots: ncols + 3 (first pass) + ncols + 2 (second pass)
+    s.ensure_res(2 * ncols + 8);
+    gkb::DevScratch Qh, dvh;
+    GKB_CUDA(cudaMalloc(&Qh.p, sizeof(double) * (size_t)std::max<int64_t>(len * ncols, 1)));
+    GKB_CUDA(cudaMalloc(&dvh.p, sizeof(double) * (size_t)std::max<int64_t>(len, 1)));
+    double* Q = Qh.as<double>();
+    double* dv = dvh.as<double>();
     if (ncols > 0)
       GKB_CUDA(cudaMemcpy(Q, basis, sizeof(double) * (size_t)(len * ncols), cudaMemcpyHostToDevice));
     GKB_CUDA(cudaMemcpy(dv, v, sizeof(double) * (size_t)len, cudaMemcpyHostToDevice));
@@ -688,8 +693,6 @@ int gkb_cgs2(gkb_ctx* ctx, const double* basis, int64_t len, int64_t ncols, doub
     if (coeffs)
       for (int64_t i = 0; i < ncols; ++i) coeffs[i] += cf[i];
     if (norm_after) *norm_after = na;
-    cudaFree(Q);
-    cudaFree(dv);
   });
 }
 

@@ -24,6 +24,25 @@ void Shard::ensure_partial(int64_t doubles) {
   rs.cap = cap;
 }
 
+void Shard::ensure_res(int64_t doubles) {
+  if (res_cap >= doubles) return;
+  GKB_CUDA(cudaSetDevice(dev));
+  if (stream) GKB_CUDA(cudaStreamSynchronize(stream));
+  const int64_t cap = std::max<int64_t>(doubles, kResCap);
+  double* d = nullptr;
+  double* h = nullptr;
+  GKB_CUDA(cudaMalloc(&d, sizeof(double) * (size_t)cap));
+  if (cudaMallocHost(&h, sizeof(double) * (size_t)cap) != cudaSuccess) {
+    cudaFree(d);
+    fail(GKB_EOOM, "ensure_res: cudaMallocHost failed");
+  }
+  if (dres) cudaFree(dres);
+  if (hres) cudaFreeHost(hres);
+  dres = d;
+  hres = h;
+  res_cap = cap;
+}
+
 uint8_t* Shard::pinned_stage(int k, size_t bytes) {
   if (bytes > hstage_bytes) {
     for (int q = 0; q < 2; ++q) {
@@ -84,8 +103,7 @@ static void init_shard(Shard& s, int index, int dev) {
     uint64_t keep = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
-  GKB_CUDA(cudaMalloc(&s.dres, sizeof(double) * kResCap));
-  GKB_CUDA(cudaMallocHost(&s.hres, sizeof(double) * kResCap));
+  s.ensure_res(kResCap);
   GKB_CUDA(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
   s.ensure_partial(1 << 16);
   dev::init_red_scratch(s.rs);

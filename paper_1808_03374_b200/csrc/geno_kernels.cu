@@ -11,10 +11,10 @@
 //   DenseOperator apply/adjoint linop.hpp:50-58
 //
 // Arithmetic: exact fixed-point digits on the tensor
-// cores. For one CTA's column range (2048 columns) the fp64 coefficients v_c
-// are rounded to 62-bit fixed point relative to the range's largest exponent
-// E, M_c = rn(v_c 2^(62-E)), and split into 8 balanced base-256 digits
-// d_i(c) in [-128, 127]. The 2-bit dosage codes a_rc in {0,1,2,3} (3 =
+// cores. For one CTA's column range (kt_cta tiles of 128 columns; 14 tiles =
+// 1792 columns by default) the fp64 coefficients v_c are rounded to 62-bit
+// fixed point relative to the range's largest exponent E, M_c = rn(v_c 2^(62-E)),
+// and split into 8 balanced base-256 digits d_i(c) in [-128, 127]. The 2-bit dosage codes a_rc in {0,1,2,3} (3 =
 // missing) are expanded to u8 fragment registers and
 //   D_i(r) = sum_c a_rc d_i(c)
 // is accumulated EXACTLY in int32 by mma.sync.m16n8k32 (u8 x s8 -> s32; the

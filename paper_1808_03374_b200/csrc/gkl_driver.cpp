@@ -107,6 +107,8 @@ Lanczos::Lanczos(DevOp* op, int64_t capacity, const double* start, uint64_t rng_
     pool_alloc(&cbuf_[i], (size_t)(cap_ + 2));
     const int64_t need = dev::red_blocks(std::max<int64_t>(op_->rows(i), n_)) * (cap_ + 4) + 64;
     ctx_->shards[i].ensure_partial(need);
+    // result slots: cgs2 against up to cap + 1 columns writes 2 (cap + 1) + 5
+    ctx_->shards[i].ensure_res(2 * cap_ + 64);
   }
   B_.assign((size_t)(cap_ * cap_), 0.0);
   coupling_.assign((size_t)cap_, 0.0);

@@ -18,6 +18,33 @@
 
 namespace gkb {
 
+// RAII holders for scratch allocations on error paths (a GKB_CUDA throw
+// inside guarded() must not leak device memory or events).
+struct DevScratch {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;  // non-null: stream-ordered (cudaFreeAsync)
+  DevScratch() = default;
+  DevScratch(const DevScratch&) = delete;
+  DevScratch& operator=(const DevScratch&) = delete;
+  ~DevScratch() {
+    if (p) {
+      if (st) cudaFreeAsync(p, st);
+      else cudaFree(p);
+    }
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+struct EventHolder {
+  cudaEvent_t e = nullptr;
+  EventHolder() = default;
+  EventHolder(const EventHolder&) = delete;
+  EventHolder& operator=(const EventHolder&) = delete;
+  ~EventHolder() {
+    if (e) cudaEventDestroy(e);
+  }
+};
+
 // Rng (rng.hpp:17-62): std::mt19937_64 with the reference's draw algorithms.
 class Rng {
  public:
@@ -55,12 +82,16 @@ struct Shard {
   int dev = 0;
   cudaStream_t stream = nullptr;
   dev::RedScratch rs{nullptr, 0};
-  double* dres = nullptr;  // device results (kResCap doubles)
+  double* dres = nullptr;  // device results (res_cap doubles, >= kResCap)
   double* hres = nullptr;  // pinned host mirror
+  int64_t res_cap = 0;
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
   cudaEvent_t ev = nullptr;
   void ensure_partial(int64_t doubles);
+  // grow dres / hres to hold `doubles` results (synchronizes the stream when it
+  // reallocates; callers must re-read s.dres / s.hres afterwards)
+  void ensure_res(int64_t doubles);
   // pinned host staging for file ingest (two buffers, grow-only, kept)
   uint8_t* hstage[2] = {nullptr, nullptr};
   size_t hstage_bytes = 0;

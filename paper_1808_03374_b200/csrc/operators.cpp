@@ -340,7 +340,11 @@ static int64_t build_block_lists(const uint32_t* lay, const dev::PMPlan& pl, cud
   pool(base, sizeof(int64_t) * (size_t)nblk);
   GKB_CUDA(cudaMemcpyAsync(*base, h.data(), sizeof(int64_t) * (size_t)nblk, cudaMemcpyHostToDevice,
                            st));
-  pool(ent, sizeof(uint16_t) * (size_t)std::max<int64_t>(total, 1));
+  // padded to whole 16-byte chunks plus one: the main kernels stage a run with
+  // 16-byte cp.async copies whose end is rounded up (tail zeroed, never used)
+  const int64_t ent_alloc = (total + 7) / 8 * 8 + 8;
+  pool(ent, sizeof(uint16_t) * (size_t)ent_alloc);
+  GKB_CUDA(cudaMemsetAsync(*ent + total, 0, sizeof(uint16_t) * (size_t)(ent_alloc - total), st));
   dev::miss_lists(lay, pl, true, nullptr, *off, *base, *ent, st);
   GKB_LAUNCH_CHECK();
   *bytes += (int64_t)(sizeof(uint32_t) * nblk * (span + 1) + sizeof(int64_t) * nblk +
@@ -564,14 +568,19 @@ void GenoOp::build_from_bed_file(const char* bed, int64_t p, int64_t nn) {
       if (const char* e = std::getenv("GKB_STAGE_MB")) budget = std::max<int64_t>(1, atoll(e)) << 20;
       const int64_t br = staging_rows(stride, budget, pr);
       const int nthr = (int)std::max(1u, std::min(read_threads(), std::thread::hardware_concurrency()));
+      // scratch held by RAII so a short read or a CUDA error does not leak it
+      DevScratch dhold[2];
+      EventHolder ehold[2];
       uint8_t* dstage[2] = {nullptr, nullptr};
       uint8_t* hstage[2] = {nullptr, nullptr};
       cudaEvent_t ev[2] = {nullptr, nullptr};
       for (int k = 0; k < 2; ++k) {
-        GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dstage[k]), (size_t)(br * stride),
-                                 sh.stream));
+        dhold[k].st = sh.stream;
+        GKB_CUDA(cudaMallocAsync(&dhold[k].p, (size_t)(br * stride), sh.stream));
+        dstage[k] = dhold[k].as<uint8_t>();
         hstage[k] = sh.pinned_stage(k, (size_t)(br * stride));  // cached across loads
-        GKB_CUDA(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+        GKB_CUDA(cudaEventCreateWithFlags(&ehold[k].e, cudaEventDisableTiming));
+        ev[k] = ehold[k].e;
       }
       t_alloc += now_s() - ta;
       int k = 0;
@@ -616,9 +625,7 @@ void GenoOp::build_from_bed_file(const char* bed, int64_t p, int64_t nn) {
         GKB_LAUNCH_CHECK();
         GKB_CUDA(cudaEventRecord(ev[k], sh.stream));
       }
-      for (int kk = 0; kk < 2; ++kk) cudaFreeAsync(dstage[kk], sh.stream);
-      GKB_CUDA(cudaStreamSynchronize(sh.stream));
-      for (int kk = 0; kk < 2; ++kk) cudaEventDestroy(ev[kk]);
+      GKB_CUDA(cudaStreamSynchronize(sh.stream));  // staging freed / events destroyed by RAII
     }
   } catch (...) {
     ::close(fd);

@@ -131,6 +131,7 @@ SubspaceOutput subspace_qr_device(DevOp* op, int64_t k, double tol, int64_t max_
   SubspaceOutput out;
   try {
     // k x k Gram of the block B (rows(i) x k per shard), summed across shards
+    for (int i = 0; i < L; ++i) ctx->shards[i].ensure_res(k * k + 64);
     auto gram = [&](const std::vector<double*>& B) {
       for (int i = 0; i < L; ++i) {
         ctx->set_device(i);
