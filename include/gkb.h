@@ -259,6 +259,10 @@ int gkb_ritz_extract(gkb_lanczos* lz, double tol, double* values, double* WL, do
                      double* err, double* err_crude, int32_t* converged);
 int gkb_thick_restart(gkb_lanczos* lz, int64_t keep);     /* gkl.cpp:341-378 */
 int gkb_compress_exhausted(gkb_lanczos* lz);              /* gkl.cpp:380-409 */
+/* deflate_right (gkl.cpp:178-204): a fresh right vector drawn from the
+ * factorization's Rng (seeded at gkb_lanczos_create) and orthogonalized
+ * against V by cgs2, up to 4 attempts; else the right side is exhausted. */
+int gkb_deflate_right(gkb_lanczos* lz);
 
 /* ---- primitives -------------------------------------------------------- */
 /* cgs2 (orth.hpp:19-44) run on the device: basis len x ncols (host, column-

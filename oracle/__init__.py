@@ -454,6 +454,24 @@ class Lanczos:
     def coupling(self):
         return np.ctypeslib.as_array(self.f.coupling, shape=(self.f.cap,))[: self.f.j].copy()
 
+    def compress_exhausted(self):  # gkl.cpp:380-409
+        _o.orc_compress_exhausted(C.byref(self.f))
+
+    def deflate_right(self):  # gkl.cpp:178-204
+        _o.orc_deflate_right(C.byref(self.f), C.byref(self.rng))
+
+    @property
+    def right_exhausted(self):
+        return bool(self.f.right_exhausted)
+
+    def error_metric_l1(self, tol, k):  # gkl.cpp:411-414
+        r = orc_ritz()
+        _o.orc_ritz_extract(C.byref(self.f), float(tol), C.byref(r))
+        try:
+            return _o.orc_error_metric_l1(C.byref(r), int(k))
+        finally:
+            _o.orc_ritz_free(C.byref(r))
+
     def ritz(self, tol):
         r = orc_ritz()
         _o.orc_ritz_extract(C.byref(self.f), float(tol), C.byref(r))

@@ -159,6 +159,7 @@ SIGNATURES = {
     "gkb_ritz_extract": (I, [P, D, PD, PD, PD, PD, PD, PI32]),
     "gkb_thick_restart": (I, [P, I64]),
     "gkb_compress_exhausted": (I, [P]),
+    "gkb_deflate_right": (I, [P]),
     "gkb_cgs2": (I, [P, PD, I64, I64, PD, PD, PD]),
     "gkb_svd_small": (I, [PD, I64, I64, PD, PD, PD]),
     "gkb_rng_fill_symmetric": (I, [C.c_uint64, I64, PD]),

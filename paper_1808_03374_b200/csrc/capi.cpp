@@ -637,6 +637,13 @@ int gkb_compress_exhausted(gkb_lanczos* lz) {
   });
 }
 
+int gkb_deflate_right(gkb_lanczos* lz) {
+  return guarded([&] {
+    need(lz, "lz");
+    lz->lz->deflate_right();
+  });
+}
+
 int gkb_cgs2(gkb_ctx* ctx, const double* basis, int64_t len, int64_t ncols, double* v,
              double* coeffs, double* norm_after) {
   return guarded([&] {

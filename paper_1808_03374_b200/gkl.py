@@ -588,6 +588,9 @@ class LanczosFactorization:
     def compress_exhausted(self) -> None:
         check(lib.gkb_compress_exhausted(self._h))
 
+    def deflate_right(self) -> None:  # gkl.cpp:178-204 (draws from this factorization's Rng)
+        check(lib.gkb_deflate_right(self._h))
+
     def close(self):
         if self._h:
             check(lib.gkb_lanczos_destroy(self._h))

@@ -27,8 +27,21 @@ def orc():
 
 
 def rel_err(a, b):
+    """Max-norm relative error of a vector (normalised by max|b|): for
+    matvec outputs and bases; singular values use sigma_rel_err."""
     a, b = np.asarray(a), np.asarray(b)
     return float(np.max(np.abs(a - b)) / max(1e-300, np.max(np.abs(b))))
+
+
+def sigma_rel_err(a, b):
+    """Largest per-value relative error max_i |a_i - b_i| / |b_i| (BASELINE:
+    "top-k singular values within 1e-9 relative" -- every sigma, not
+    normalised by sigma_1)."""
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    if a.size == 0:
+        return 0.0
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
 
 
 def principal_angles(A, B):

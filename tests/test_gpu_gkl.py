@@ -5,7 +5,7 @@ within 1e-9 relative, principal angles < 1e-6, restarts within +-1)."""
 import numpy as np
 import pytest
 
-from conftest import principal_angles, rel_err
+from conftest import principal_angles, rel_err, sigma_rel_err
 
 pytestmark = pytest.mark.gpu
 EPS = np.finfo(float).eps
@@ -238,7 +238,7 @@ def test_svdl_parity_vs_oracle(gkb, orc, cfg, scale):
     o = orc.svdl(ref, orc.Options.from_gkl(opts))
     k = opts.k
     assert g.singvals.size == k and o.singvals.size == k
-    assert rel_err(g.singvals, o.singvals) <= 1e-9
+    assert sigma_rel_err(g.singvals, o.singvals) <= 1e-9
     assert principal_angles(g.U, o.U) < 1e-6
     assert principal_angles(g.V, o.V) < 1e-6
     assert abs(g.stats.restarts - o.restarts) <= 1
@@ -252,7 +252,7 @@ def test_svdl_sharded_matches(gkb, orc):
     op1, _ = _geno_pair(gkb, orc, spec)
     op3, _ = _geno_pair(gkb, orc, spec, nshards=3)
     a, b = gkb.svdl(op1, opts), gkb.svdl(op3, opts)
-    assert rel_err(a.singvals, b.singvals) <= 1e-9
+    assert sigma_rel_err(a.singvals, b.singvals) <= 1e-9
     assert principal_angles(a.V, b.V) < 1e-6
     assert principal_angles(a.U, b.U) < 1e-6
 
