@@ -58,6 +58,18 @@ const char* gkb_version(void);
 int gkb_init(int nshards, const int* devices, gkb_ctx** ctx);
 int gkb_nccl_unique_id(uint8_t id_out[128]);
 int gkb_init_nccl(int device, const uint8_t id[128], int nranks, int rank, gkb_ctx** ctx);
+/* gkb_init_host_comm: SPMD like gkb_init_nccl, with the sums done by the
+ * caller: `fn(user, buf, count)` must replace the page-locked host buffer
+ * buf[0..count) by its elementwise sum over all ranks (a collective: every
+ * rank makes the same calls in the same order). It runs on a CUDA host-
+ * function thread between a D2H and an H2D copy on the shard's stream, so it
+ * must not call CUDA. Used to run the multi-process path of the library as
+ * several processes on ONE GPU (e.g. an allreduce over torch.distributed /
+ * gloo), since NCCL cannot place two ranks on one device; no kernel waits
+ * on another process. */
+typedef void (*gkb_host_allreduce_fn)(void* user, double* buf, int64_t count);
+int gkb_init_host_comm(int device, int nranks, int rank, gkb_host_allreduce_fn fn, void* user,
+                       gkb_ctx** ctx);
 int gkb_destroy(gkb_ctx* ctx);
 /* nshards local to this process, world size, this process's first shard index */
 int gkb_ctx_info(gkb_ctx* ctx, int* nshards_local, int* nshards_total, int* first_shard);

@@ -109,6 +109,9 @@ I = C.c_int
 I64 = C.c_int64
 D = C.c_double
 
+# gkb_host_allreduce_fn: void (*)(void* user, double* buf, int64_t count)
+HOST_ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+
 # name -> (restype, argtypes); every symbol declared in include/gkb.h
 SIGNATURES = {
     "gkb_last_error": (C.c_char_p, []),
@@ -116,6 +119,7 @@ SIGNATURES = {
     "gkb_init": (I, [I, C.POINTER(C.c_int), C.POINTER(P)]),
     "gkb_nccl_unique_id": (I, [PU8]),
     "gkb_init_nccl": (I, [I, PU8, I, I, C.POINTER(P)]),
+    "gkb_init_host_comm": (I, [I, I, I, HOST_ALLREDUCE_FN, P, C.POINTER(P)]),
     "gkb_destroy": (I, [P]),
     "gkb_ctx_info": (I, [P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "gkb_synchronize": (I, [P]),

@@ -95,6 +95,16 @@ int gkb_init_nccl(int device, const uint8_t id[128], int nranks, int rank, gkb_c
   });
 }
 
+int gkb_init_host_comm(int device, int nranks, int rank, gkb_host_allreduce_fn fn, void* user,
+                       gkb_ctx** ctx) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    auto c = std::make_unique<gkb_ctx>();
+    c->c.init_host(device, nranks, rank, fn, user);
+    *ctx = c.release();
+  });
+}
+
 int gkb_destroy(gkb_ctx* ctx) {
   return guarded([&] { delete ctx; });
 }

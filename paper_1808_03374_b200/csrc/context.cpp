@@ -120,7 +120,7 @@ void Context::init_local(const std::vector<int>& devices) {
   }
   nshards_total = (int)devices.size();
   first_shard = 0;
-  use_nccl = false;
+  spmd_mode = false;
 }
 
 void Context::init_nccl(int device, const ncclUniqueId& id, int nranks, int rank) {
@@ -129,10 +129,36 @@ void Context::init_nccl(int device, const ncclUniqueId& id, int nranks, int rank
   init_shard(shards[0], rank, device);
   nshards_total = nranks;
   first_shard = rank;
-  use_nccl = true;
+  spmd_mode = true;
   GKB_CUDA(cudaSetDevice(device));
   check_nccl(ncclCommInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
 }
+
+void Context::init_host(int device, int nranks, int rank, gkb_host_allreduce_fn fn, void* user) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(GKB_EINVAL, "gkb_init_host_comm: bad rank");
+  if (!fn) fail(GKB_EINVAL, "gkb_init_host_comm: null allreduce function");
+  shards.resize(1);
+  init_shard(shards[0], rank, device);
+  nshards_total = nranks;
+  first_shard = rank;
+  spmd_mode = true;
+  host_fn = fn;
+  host_user = user;
+}
+
+namespace {
+struct HostAllreduce {
+  gkb_host_allreduce_fn fn;
+  void* user;
+  double* buf;
+  int64_t count;
+};
+void CUDART_CB host_allreduce_tramp(void* p) {
+  const HostAllreduce* a = static_cast<const HostAllreduce*>(p);
+  a->fn(a->user, a->buf, a->count);
+  delete a;
+}
+}  // namespace
 
 Context::~Context() {
   for (auto& s : shards) {
@@ -146,6 +172,7 @@ Context::~Context() {
       if (s.hstage[q]) cudaFreeHost(s.hstage[q]);
     if (s.flush_buf) cudaFree(s.flush_buf);
     if (s.ev) cudaEventDestroy(s.ev);
+    if (host_buf) cudaFreeHost(host_buf);
     if (s.stream) cudaStreamDestroy(s.stream);
   }
   if (stage && !shards.empty()) {
@@ -166,10 +193,28 @@ void Context::sync_all() {
 
 void Context::allreduce(const std::vector<double*>& bufs, int64_t count) {
   if (count == 0) return;
-  if (use_nccl) {
+  if (spmd_mode) {
     if (nshards_total == 1) return;
     Shard& s = shards[0];
     GKB_CUDA(cudaSetDevice(s.dev));
+    if (host_fn) {
+      // stream-ordered: the host function runs after the D2H copy and before
+      // the H2D copy on the shard's stream (it must not call CUDA); one
+      // staging buffer serves every call since the stream serializes them
+      const size_t bytes = sizeof(double) * (size_t)count;
+      if (host_cap < count) {
+        GKB_CUDA(cudaStreamSynchronize(s.stream));
+        if (host_buf) GKB_CUDA(cudaFreeHost(host_buf));
+        host_buf = nullptr;
+        host_cap = std::max<int64_t>(count, 1 << 12);
+        GKB_CUDA(cudaMallocHost(&host_buf, sizeof(double) * (size_t)host_cap));
+      }
+      GKB_CUDA(cudaMemcpyAsync(host_buf, bufs[0], bytes, cudaMemcpyDeviceToHost, s.stream));
+      GKB_CUDA(cudaLaunchHostFunc(s.stream, host_allreduce_tramp,
+                                  new HostAllreduce{host_fn, host_user, host_buf, count}));
+      GKB_CUDA(cudaMemcpyAsync(bufs[0], host_buf, bytes, cudaMemcpyHostToDevice, s.stream));
+      return;
+    }
     check_nccl(ncclAllReduce(bufs[0], bufs[0], (size_t)count, ncclDouble, ncclSum, comm, s.stream),
                "ncclAllReduce");
     return;

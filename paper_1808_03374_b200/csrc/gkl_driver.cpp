@@ -618,7 +618,7 @@ bool Lanczos::fuse_ctl() {
   return on;
 }
 bool Lanczos::reduce_local() const {
-  return ctx_->use_nccl ? ctx_->nshards_total == 1 : ctx_->shards.size() == 1;
+  return ctx_->spmd_mode ? ctx_->nshards_total == 1 : ctx_->shards.size() == 1;
 }
 
 dev::ctl::Params Lanczos::ctl_params(const Options& o, int op, int64_t s) const {
@@ -1081,7 +1081,7 @@ static void gather_left(Context* ctx, DevOp* op, const std::vector<double*>& src
   const int L = (int)ctx->shards.size();
   const int64_t m = op->m;
   if (ncols == 0) return;
-  if (ctx->use_nccl && ctx->nshards_total > 1) {
+  if (ctx->spmd_mode && ctx->nshards_total > 1) {
     ctx->set_device(0);
     Shard& s = ctx->shards[0];
     double* full = nullptr;

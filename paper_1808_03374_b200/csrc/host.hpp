@@ -106,8 +106,16 @@ struct Context {
   std::vector<Shard> shards;
   int nshards_total = 1;
   int first_shard = 0;
-  bool use_nccl = false;
+  // SPMD: one shard per process, collectives across processes -- over NCCL
+  // (gkb_init_nccl), or through a caller-supplied host allreduce
+  // (gkb_init_host_comm: stream-ordered D2H -> host function -> H2D, used to
+  // run the SPMD path as several processes on one GPU, e.g. over gloo)
+  bool spmd_mode = false;
   ncclComm_t comm = nullptr;
+  gkb_host_allreduce_fn host_fn = nullptr;
+  void* host_user = nullptr;
+  double* host_buf = nullptr;  // page-locked staging of the host allreduce
+  int64_t host_cap = 0;
   // local-mode allreduce staging on shard 0's device
   double* stage = nullptr;
   int64_t stage_cap = 0;
@@ -115,6 +123,7 @@ struct Context {
   ~Context();
   void init_local(const std::vector<int>& devices);
   void init_nccl(int device, const ncclUniqueId& id, int nranks, int rank);
+  void init_host(int device, int nranks, int rank, gkb_host_allreduce_fn fn, void* user);
   // In-place sum over all shards (all processes). bufs: one device pointer per
   // local shard. Result identical on every shard.
   void allreduce(const std::vector<double*>& bufs, int64_t count);

@@ -42,7 +42,7 @@ void DevOp::alloc_host_api_buffers() {
     GKB_CUDA(cudaMalloc(&xbuf[i], sizeof(double) * (size_t)std::max<int64_t>(n, 1)));
     GKB_CUDA(cudaMalloc(&ybuf[i], sizeof(double) * (size_t)std::max<int64_t>(rows(i), 1)));
     GKB_CUDA(cudaMalloc(&zbuf[i], sizeof(double) * (size_t)std::max<int64_t>(n, 1)));
-    if (ctx->use_nccl && ctx->nshards_total > 1)
+    if (ctx->spmd_mode && ctx->nshards_total > 1)
       GKB_CUDA(cudaMalloc(&yfull[i], sizeof(double) * (size_t)std::max<int64_t>(m, 1)));
   }
 }
@@ -61,7 +61,7 @@ static bool device_accessible(const void* p) {
 // One local shard (no cross-shard sum) and an operator whose result kernels
 // write each element once: page-locked host buffers are used in place.
 bool DevOp::direct_io(const void* a, const void* b) const {
-  if (!direct_host_io || ctx->shards.size() != 1 || (ctx->use_nccl && ctx->nshards_total > 1))
+  if (!direct_host_io || ctx->shards.size() != 1 || (ctx->spmd_mode && ctx->nshards_total > 1))
     return false;
   return device_accessible(a) && (!b || device_accessible(b));
 }
@@ -91,7 +91,7 @@ void DevOp::apply_host(const double* x, double* y) {
     xi[i] = xbuf[i];
   }
   apply_dev(xi, ybuf);
-  if (ctx->use_nccl && ctx->nshards_total > 1) {
+  if (ctx->spmd_mode && ctx->nshards_total > 1) {
     Shard& s = ctx->shards[0];
     GKB_CUDA(cudaSetDevice(s.dev));
     GKB_CUDA(cudaMemsetAsync(yfull[0], 0, sizeof(double) * (size_t)m, s.stream));
@@ -185,7 +185,7 @@ void DevOp::adjoint_block_dev(const std::vector<const double*>& Yb,
 
 void DevOp::apply_block_host(const double* X, int64_t k, double* Y) {
   const int L = (int)ctx->shards.size();
-  const bool spmd = ctx->use_nccl && ctx->nshards_total > 1;
+  const bool spmd = ctx->spmd_mode && ctx->nshards_total > 1;
   int64_t rmax = 1;
   for (int i = 0; i < L; ++i) rmax = std::max(rmax, rows(i));
   // SPMD: every rank assembles the full m x k block for one allreduce;
@@ -741,7 +741,7 @@ void GenoOp::finish_build() {
     alloc_scratch(g.pl2, true, g.s2, sh.stream);
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
   }
-  if (ctx->use_nccl && ctx->nshards_total > 1) {
+  if (ctx->spmd_mode && ctx->nshards_total > 1) {
     // gather global counts: exact in fp64 (counts < 2^53)
     Shard& s = ctx->shards[0];
     ctx->set_device(0);
@@ -930,7 +930,7 @@ void GenoOp::adjoint_dev(const std::vector<const double*>& y, const std::vector<
 void GenoOp::marker_scan(const double* y, const double* Z, int64_t k, bool unbiased,
                          double* beta, double* se, double* icpt, double* sig2, int32_t* dep) {
   if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
-  if (ctx->use_nccl && ctx->nshards_total > 1)
+  if (ctx->spmd_mode && ctx->nshards_total > 1)
     fail(GKB_ELOGIC, "marker_scan: SPMD operators use the host scan");
   const int K = (int)(k + 1);
   const int64_t nn = n;

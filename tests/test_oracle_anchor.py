@@ -67,7 +67,7 @@ def test_default_recurrence_matches_dense_svd(cfg, scale):
     assert principal_angles(r.V, Vt[:k].T) < ANCHOR_ANGLE
 
 
-@pytest.mark.parametrize("cfg,scale", [(3, 0.01), (5, 0.005), (4, 0.01), (1, 0.1)])
+@pytest.mark.parametrize("cfg,scale", [(3, 0.005), (3, 0.01), (5, 0.005), (4, 0.01), (1, 0.1)])
 def test_literal_recurrence_matches_dense_where_it_converges(cfg, scale):
     spec, X, g = _case(cfg, scale)
     s = np.linalg.svd(X, compute_uv=False)
