@@ -786,6 +786,22 @@ void GenoOp::get_scaling(double* mu, double* inv_s) {
                              cudaMemcpyDeviceToHost, ctx->shards[i].stream));
   }
   ctx->sync_all();
+  if (ctx->spmd_mode && ctx->nshards_total > 1) {
+    // every rank returns the full vectors: zero-padded rows summed over ranks
+    Shard& s = ctx->shards[0];
+    ctx->set_device(0);
+    DevScratch buf;
+    GKB_CUDA(cudaMalloc(&buf.p, sizeof(double) * (size_t)(2 * m)));
+    double* d = buf.as<double>();
+    GKB_CUDA(cudaMemcpyAsync(d, mu, sizeof(double) * (size_t)m, cudaMemcpyHostToDevice, s.stream));
+    GKB_CUDA(cudaMemcpyAsync(d + m, inv_s, sizeof(double) * (size_t)m, cudaMemcpyHostToDevice,
+                             s.stream));
+    ctx->allreduce({d}, 2 * m);
+    GKB_CUDA(cudaMemcpyAsync(mu, d, sizeof(double) * (size_t)m, cudaMemcpyDeviceToHost, s.stream));
+    GKB_CUDA(cudaMemcpyAsync(inv_s, d + m, sizeof(double) * (size_t)m, cudaMemcpyDeviceToHost,
+                             s.stream));
+    GKB_CUDA(cudaStreamSynchronize(s.stream));
+  }
 }
 
 void DevOp::apply_dev_div(const std::vector<const double*>& xraw,
