@@ -271,7 +271,23 @@ def run_ours(args):
     cfg = args.config
     ws, rank, local = dist_env()
     dist = None
-    if ws > 1:
+    host_comm = os.environ.get("GKB_BENCH_HOST_COMM") == "1"
+    if ws > 1 and host_comm:
+        # test mode for the N > 1 harness on a box with fewer GPUs than ranks:
+        # every rank on device 0, the library's sums over gloo through
+        # gkb_init_host_comm (timings are not NVLink numbers)
+        import torch
+        import torch.distributed as tdist
+        local = 0
+        torch.cuda.set_device(0)
+        tdist.init_process_group("gloo")
+        sum_group = tdist.new_group(backend="gloo")
+
+        def host_allreduce(a):
+            tdist.all_reduce(torch.from_numpy(a), group=sum_group)
+        ctx = gkb.Context(host_comm=(0, ws, rank, host_allreduce))
+        dist = tdist
+    elif ws > 1:
         import torch
         import torch.distributed as tdist
         torch.cuda.set_device(local)
@@ -294,7 +310,8 @@ def run_ours(args):
         if not dist:
             return v
         import torch
-        tt = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        tt = torch.tensor([v], dtype=torch.float64,
+                          device="cpu" if host_comm else f"cuda:{local}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
 

@@ -59,6 +59,9 @@ static_assert(kStripsPerWarp <= 2, "the unrolled full-range loop prefetches stri
 constexpr int kRowsPerCta = 8 * kStripsPerWarp * 16;  // 256
 constexpr int kStripsPerCta = 8 * kStripsPerWarp;
 constexpr int kMinCtas = kStripsPerWarp <= 2 ? 4 : 3;  // per SM (register budget)
+#ifndef GKB_BULK_STAGE
+#define GKB_BULK_STAGE 1  // k_pm_main: bulk-copy (TMA engine) staging on an mbarrier
+#endif
 #ifndef GKB_EARLY_STAGE
 #define GKB_EARLY_STAGE 1  // k_pm_main: staging complete before the loop (no barrier after it)
 #endif
@@ -423,6 +426,42 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+
+// Bulk copies on the TMA engine (cp.async.bulk, SASS UBLKCP) completing on an
+// mbarrier: one thread stages a CTA's contiguous inputs (digits, correction
+// coefficients, missing-list run and offsets) with a handful of instructions
+// instead of every thread looping over 4-16 byte copies.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "GKB_MBAR_WAIT%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra GKB_MBAR_WAIT%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// dst, src 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
@@ -551,8 +590,66 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     nxt[r] = p + 32 * min(2, max(ktiles - 1, 0));
   }
   uint8_t* stage = reinterpret_cast<uint8_t*>(dg + kt_cta * 64);
-  uint32_t* offs = reinterpret_cast<uint32_t*>(stage);
   double* cvs = reinterpret_cast<double*>(stage + kOffBytes + 2 * kEntCap + 16);
+#if GKB_BULK_STAGE
+  // One thread stages the CTA's contiguous inputs with bulk copies on the TMA
+  // engine, completing on one mbarrier: the block's list offsets (a 16-byte
+  // aligned superset, oshift = the offsets' position in it) and list run
+  // (immutable, before the PDL wait), then the range's correction
+  // coefficients and digits (the predecessor's outputs, after it).
+  __shared__ __align__(8) uint64_t sbar;
+  if (threadIdx.x == 0) mbar_init(&sbar, 1);
+  const uint32_t* offs = reinterpret_cast<const uint32_t*>(stage);
+  int ent_shift = -1;
+  int64_t eb = 0;
+  uint32_t obytes = 0, ebytes = 0;
+  const uint8_t* osrc = nullptr;
+  const uint8_t* esrc = nullptr;
+  if (m_off) {
+    const uint32_t* orow = m_off + b * (kRowsPerCta + 1);
+    osrc = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(orow) & ~uintptr_t(15));
+    const uint32_t oshift = (uint32_t)(reinterpret_cast<const uint8_t*>(orow) - osrc);
+    obytes = (oshift + 4 * (kRowsPerCta + 1) + 15) & ~15u;
+    offs += oshift / 4;
+    eb = m_base[b];
+    const int64_t ne = orow[kRowsPerCta];
+    const int64_t a0 = (eb * 2) & ~int64_t(15), a1 = (eb * 2 + ne * 2 + 15) & ~int64_t(15);
+    if (a1 - a0 <= 2 * kEntCap) {
+      esrc = reinterpret_cast<const uint8_t*>(m_ent) + a0;
+      ebytes = (uint32_t)(a1 - a0);
+      ent_shift = (int)(eb - a0 / 2);
+    }
+  }
+  const int ncol = m_off ? (int)min((int64_t)ktiles * 128, C - col0) : 0;
+  const double* csrc = cval + col0;
+  // x may be a Krylov-basis column with an odd leading dimension: bulk only
+  // when 16-byte aligned (an odd count's last element by a plain copy)
+  const bool cbulk = m_off && ((reinterpret_cast<uintptr_t>(csrc) & 15) == 0);
+  const uint32_t cbytes = cbulk ? (uint32_t)(ncol & ~1) * 8u : 0u;
+  const uint32_t dbytes = (uint32_t)ktiles * 1024u;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&sbar, obytes + ebytes + cbytes + dbytes);
+    if (obytes) bulk_g2s(stage, osrc, obytes, &sbar);
+    if (ebytes) bulk_g2s(stage + kOffBytes, esrc, ebytes, &sbar);
+  }
+  // everything above reads only the layout and the missing lists; from here
+  // on the predecessor's outputs (digits, x / cm) are used
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    if (cbytes) bulk_g2s(cvs, csrc, cbytes, &sbar);
+    bulk_g2s(dg, dig + kt0 * 64, dbytes, &sbar);
+  }
+  if (m_off && !cbulk) {
+    for (int i = threadIdx.x; i < ncol; i += kThreads) cp_async8(cvs + i, csrc + i);
+    cp_async_commit();
+    cp_async_wait_all();
+  } else if (cbulk && (ncol & 1) && threadIdx.x == kThreads - 1) {
+    cvs[ncol - 1] = csrc[ncol - 1];
+  }
+  __syncthreads();  // the mbarrier's init, the plain copies
+  mbar_wait(&sbar, 0);
+#else
+  uint32_t* offs = reinterpret_cast<uint32_t*>(stage);
   // list entries: staged into shared memory (ent_shift = offset of the run's
   // first entry in the staged 16-byte-aligned copy), or -- a block denser in
   // missing entries than kEntCap -- walked in global memory (ent_shift < 0)
@@ -591,6 +688,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
   if (m_off) cp_async_wait_all();
 #endif
   __syncthreads();
+#endif
   // swizzled digit slots: the 8 lanes of each quarter-warp hit 8 distinct 16-byte bank groups
   const int sw = g ^ (2 * tid);
   const uint4* bp = dg + tid * 8 + sw;  // this thread's B fragments of tile t (64 uint4 per tile)
@@ -641,7 +739,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     }
   }
 #undef GKB_PM_STEP
-#if !GKB_EARLY_STAGE
+#if !GKB_EARLY_STAGE && !GKB_BULK_STAGE
   if (m_off) {
     cp_async_wait_all();
     __syncthreads();

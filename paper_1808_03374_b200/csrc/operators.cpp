@@ -321,7 +321,8 @@ static int64_t build_block_lists(const uint32_t* lay, const dev::PMPlan& pl, cud
   };
   pool(&cnt, sizeof(uint32_t) * (size_t)(nblk * span));
   pool(&tot, sizeof(int64_t) * (size_t)nblk);
-  pool(off, sizeof(uint32_t) * (size_t)(nblk * (span + 1)));
+  // + 4: the main kernels bulk-copy a 16-byte-aligned superset of a block's offsets
+  pool(off, sizeof(uint32_t) * (size_t)(nblk * (span + 1) + 4));
   dev::miss_lists(lay, pl, false, cnt, nullptr, nullptr, nullptr, st);
   GKB_LAUNCH_CHECK();
   dev::block_scan(cnt, nblk, span, *off, tot, st);
