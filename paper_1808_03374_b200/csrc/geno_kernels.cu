@@ -926,9 +926,70 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
   }
   uint4* dg1 = dg + kt_cta * 64;
   uint8_t* stage = reinterpret_cast<uint8_t*>(dg + 2 * kt_cta * 64);
-  uint32_t* offs = reinterpret_cast<uint32_t*>(stage);
   double* cvs0 = reinterpret_cast<double*>(stage + kOffBytes + 2 * kEntCap + 16);
   double* cvs1 = cvs0 + kt_cta * 128;
+#if GKB_BULK_STAGE
+  // bulk-copy staging on one mbarrier, as in k_pm_main (two digit sets and
+  // two coefficient vectors)
+  __shared__ __align__(8) uint64_t sbar;
+  if (threadIdx.x == 0) mbar_init(&sbar, 1);
+  const uint32_t* offs = reinterpret_cast<const uint32_t*>(stage);
+  int ent_shift = -1;
+  int64_t eb = 0;
+  uint32_t obytes = 0, ebytes = 0;
+  const uint8_t* osrc = nullptr;
+  const uint8_t* esrc = nullptr;
+  if (m_off) {
+    const uint32_t* orow = m_off + b * (kRowsPerCta + 1);
+    osrc = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(orow) & ~uintptr_t(15));
+    const uint32_t oshift = (uint32_t)(reinterpret_cast<const uint8_t*>(orow) - osrc);
+    obytes = (oshift + 4 * (kRowsPerCta + 1) + 15) & ~15u;
+    offs += oshift / 4;
+    eb = m_base[b];
+    const int64_t ne = orow[kRowsPerCta];
+    const int64_t a0 = (eb * 2) & ~int64_t(15), a1 = (eb * 2 + ne * 2 + 15) & ~int64_t(15);
+    if (a1 - a0 <= 2 * kEntCap) {
+      esrc = reinterpret_cast<const uint8_t*>(m_ent) + a0;
+      ebytes = (uint32_t)(a1 - a0);
+      ent_shift = (int)(eb - a0 / 2);
+    }
+  }
+  const int ncol = m_off ? (int)min((int64_t)ktiles * 128, C - col0) : 0;
+  const double* csrc0 = a.cval[0] + col0;
+  const double* csrc1 = a.cval[1] + col0;
+  const bool cbulk = m_off && ((reinterpret_cast<uintptr_t>(csrc0) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(csrc1) & 15) == 0);
+  const uint32_t cbytes = cbulk ? (uint32_t)(ncol & ~1) * 8u : 0u;
+  const uint32_t dbytes = (uint32_t)ktiles * 1024u;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&sbar, obytes + ebytes + 2 * cbytes + 2 * dbytes);
+    if (obytes) bulk_g2s(stage, osrc, obytes, &sbar);
+    if (ebytes) bulk_g2s(stage + kOffBytes, esrc, ebytes, &sbar);
+  }
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    if (cbytes) {
+      bulk_g2s(cvs0, csrc0, cbytes, &sbar);
+      bulk_g2s(cvs1, csrc1, cbytes, &sbar);
+    }
+    bulk_g2s(dg, a.dig[0] + kt0 * 64, dbytes, &sbar);
+    bulk_g2s(dg1, a.dig[1] + kt0 * 64, dbytes, &sbar);
+  }
+  if (m_off && !cbulk) {
+    for (int i = threadIdx.x; i < ncol; i += kThreads) {
+      cp_async8(cvs0 + i, csrc0 + i);
+      cp_async8(cvs1 + i, csrc1 + i);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+  } else if (cbulk && (ncol & 1) && threadIdx.x == kThreads - 1) {
+    cvs0[ncol - 1] = csrc0[ncol - 1];
+    cvs1[ncol - 1] = csrc1[ncol - 1];
+  }
+  __syncthreads();  // the mbarrier's init, the plain copies
+  mbar_wait(&sbar, 0);
+#else
+  uint32_t* offs = reinterpret_cast<uint32_t*>(stage);
   int ent_shift = -1;
   int64_t eb = 0;
   if (m_off) {
@@ -965,6 +1026,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
   if (m_off) cp_async_wait_all();  // as in k_pm_main
 #endif
   __syncthreads();
+#endif
   const int sw = g ^ (2 * tid);
   const uint4* bp = dg + tid * 8 + sw;
 #define GKB_PM2_STEP(CUR, DST)                                             \
@@ -986,7 +1048,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
     GKB_PM2_STEP(bC, bB)
   }
 #undef GKB_PM2_STEP
-#if !GKB_EARLY_STAGE
+#if !GKB_EARLY_STAGE && !GKB_BULK_STAGE
   if (m_off) {
     cp_async_wait_all();
     __syncthreads();
