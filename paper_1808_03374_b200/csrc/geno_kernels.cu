@@ -150,6 +150,12 @@ __device__ __forceinline__ double pow2(int k) {  // exact 2^k, -1022 <= k <= 102
   return __hiloint2double((1023 + k) << 20, 0);
 }
 
+// scalbn(v, k) with one DMUL when 2^k is a normal double (then v * 2^k is the
+// exact product rounded once, like scalbn); the library call otherwise
+__device__ __forceinline__ double scale2(double v, int k) {
+  return (k >= -1022 && k <= 1023) ? v * pow2(k) : scalbn(v, k);
+}
+
 // ---------------------------------------------------------------- K8 / K7
 // .bed records of one staging block (rows [row0, row0+rows) of the shard)
 // -> layout 1 (rows = SNPs): thread per (SNP row, word of 16 samples).
@@ -597,8 +603,13 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
   // aligned superset, oshift = the offsets' position in it) and list run
   // (immutable, before the PDL wait), then the range's correction
   // coefficients and digits (the predecessor's outputs, after it).
-  __shared__ __align__(8) uint64_t sbar;
-  if (threadIdx.x == 0) mbar_init(&sbar, 1);
+  // two mbarriers: [0] the digits (waited for before the loop), [1] the
+  // epilogue's inputs (waited for after it, by each warp on its own)
+  __shared__ __align__(8) uint64_t sbar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&sbar[0], 1);
+    mbar_init(&sbar[1], 1);
+  }
   const uint32_t* offs = reinterpret_cast<const uint32_t*>(stage);
   int ent_shift = -1;
   int64_t eb = 0;
@@ -628,16 +639,17 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
   const uint32_t cbytes = cbulk ? (uint32_t)(ncol & ~1) * 8u : 0u;
   const uint32_t dbytes = (uint32_t)ktiles * 1024u;
   if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&sbar, obytes + ebytes + cbytes + dbytes);
-    if (obytes) bulk_g2s(stage, osrc, obytes, &sbar);
-    if (ebytes) bulk_g2s(stage + kOffBytes, esrc, ebytes, &sbar);
+    mbar_arrive_expect_tx(&sbar[0], dbytes);
+    mbar_arrive_expect_tx(&sbar[1], obytes + ebytes + cbytes);
+    if (obytes) bulk_g2s(stage, osrc, obytes, &sbar[1]);
+    if (ebytes) bulk_g2s(stage + kOffBytes, esrc, ebytes, &sbar[1]);
   }
   // everything above reads only the layout and the missing lists; from here
   // on the predecessor's outputs (digits, x / cm) are used
   pdl_wait();
   if (threadIdx.x == 0) {
-    if (cbytes) bulk_g2s(cvs, csrc, cbytes, &sbar);
-    bulk_g2s(dg, dig + kt0 * 64, dbytes, &sbar);
+    bulk_g2s(dg, dig + kt0 * 64, dbytes, &sbar[0]);
+    if (cbytes) bulk_g2s(cvs, csrc, cbytes, &sbar[1]);
   }
   if (m_off && !cbulk) {
     for (int i = threadIdx.x; i < ncol; i += kThreads) cp_async8(cvs + i, csrc + i);
@@ -646,8 +658,8 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
   } else if (cbulk && (ncol & 1) && threadIdx.x == kThreads - 1) {
     cvs[ncol - 1] = csrc[ncol - 1];
   }
-  __syncthreads();  // the mbarrier's init, the plain copies
-  mbar_wait(&sbar, 0);
+  __syncthreads();  // the mbarriers' init, the plain copies
+  mbar_wait(&sbar[0], 0);
 #else
   uint32_t* offs = reinterpret_cast<uint32_t*>(stage);
   // list entries: staged into shared memory (ent_shift = offset of the run's
@@ -744,6 +756,9 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     cp_async_wait_all();
     __syncthreads();
   }
+#endif
+#if GKB_BULK_STAGE
+  mbar_wait(&sbar[1], 0);  // the list run, offsets and coefficients
 #endif
   // Epilogue. Thread (g, tid) holds digits (2 tid, 2 tid + 1) of rows g and
   // g + 8; 2^(16 tid) (D_2tid + 256 D_2tid+1) is exact in fp64, and the four
