@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
   for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
     const int wc = t >> 4, k = t & 15, q = k & 3, e = k >> 2;
     // group-q columns meet codes pre-multiplied by 4^q in the MMA (mma_tile)
-    long long M = __double2ll_rn(scalbn(vals[t], 62 - E - 2 * q));
+    long long M = __double2ll_rn(scale2(vals[t], 62 - E - 2 * q));
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int d = (int)(signed char)(M & 0xFF);
@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
     const int hi = tid & 1;
     rowr[r] = (strip0 + r) * 16 + g + 8 * hi;
-    val[r] = scalbn(hi ? v1 : v0, E - 62);
+    val[r] = scale2(hi ? v1 : v0, E - 62);
     corr[r] = 0.0;
     if (m_off) {
       const int rl = (int)(rowr[r] - (int64_t)bx * kRowsPerCta);
@@ -1089,8 +1089,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
     const int hi = tid & 1;
     const int64_t row = (strip0 + r) * 16 + g + 8 * hi;
     const int rl = (int)(row - (int64_t)blockIdx.x * kRowsPerCta);
-    const double val0 = scalbn(hi ? u1 : u0, E0 - 62);
-    const double val1 = scalbn(hi ? v1 : v0, E1 - 62);
+    const double val0 = scale2(hi ? u1 : u0, E0 - 62);
+    const double val1 = scale2(hi ? v1 : v0, E1 - 62);
     double c0 = 0.0, c1 = 0.0;
     if (m_off) {
       const uint32_t e0 = offs[rl], e1 = offs[rl + 1], mid = e0 + (e1 - e0) / 2;
