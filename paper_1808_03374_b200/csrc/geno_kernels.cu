@@ -842,6 +842,129 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
 }
 
 
+// ---------------------------------------------------------------- dense-missing mode
+// Main kernel for shards with many missing entries (DESIGN.md section 4,
+// "Missing data"): no lists. The missing indicator of a word, t = w & (w >> 1)
+// & 0x5555... (code 3 = missing), is expanded exactly like the codes (one LOP3
+// per fragment register: 0 or 4^q per byte) and multiplied on the tensor
+// cores with a digit set into a second exact accumulator:
+//   K1 (MODE 0): the same digits (of x): corr_j = sum_{s miss} x_s,
+//                y_j = inv_s_j (val_j - mu_j X - (3 - m_j) corr_j);
+//   K2 (MODE 1): the digits of cm_j = c_j (3 - m_j) (dig2):
+//                z_s = val_s - sum_j c_j mu_j - sum_{j miss} cm_j.
+// Both corrections are exact integer sums scaled like the main sum (the
+// list walk's fp64 sums are replaced by exact ones), and the kernel's cost
+// does not depend on the missing rate.
+__device__ __forceinline__ uint4 miss_ind(const uint4 w) {
+  uint4 t;
+  t.x = w.x & (w.x >> 1) & 0x55555555u;
+  t.y = w.y & (w.y >> 1) & 0x55555555u;
+  t.z = w.z & (w.z >> 1) & 0x55555555u;
+  t.w = w.w & (w.w >> 1) & 0x55555555u;
+  return t;
+}
+
+size_t pmi_smem_bytes(int kt_cta, int mode) {
+  return (size_t)kt_cta * 64 * 16 * (mode ? 2 : 1);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 3) k_pm_ind(
+    const uint4* __restrict__ lay, int64_t KT, int kt_cta, const uint4* __restrict__ dig,
+    const int* __restrict__ dexp, const double* __restrict__ dsum,
+    const uint4* __restrict__ dig2, const int* __restrict__ dexp2,
+    const double* __restrict__ mu, const double* __restrict__ mean, int64_t rows_pad,
+    double* __restrict__ part) {
+  extern __shared__ __align__(16) uint4 dg[];  // kt_cta * 64 digits [, K2: kt_cta * 64 of cm]
+  const int kc = blockIdx.y, bx = blockIdx.x;
+  const int64_t kt0 = (int64_t)kc * kt_cta;
+  const int ktiles = (int)min((int64_t)kt_cta, KT - kt0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tid = lane & 3;
+  const int64_t strip0 = ((int64_t)bx * 8 + warp) * kStripsPerWarp;
+  const uint4* src = lay + (strip0 * KT + kt0) * 32 + lane;
+  const uint4 Z = make_uint4(0, 0, 0, 0);
+  int acc[kStripsPerWarp][4], accm[kStripsPerWarp][4];
+  uint4 bA[kStripsPerWarp], bB[kStripsPerWarp], bC[kStripsPerWarp];
+  const uint4* nxt[kStripsPerWarp];
+  pdl_trigger();
+#pragma unroll
+  for (int r = 0; r < kStripsPerWarp; ++r) {
+    acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0;
+    accm[r][0] = accm[r][1] = accm[r][2] = accm[r][3] = 0;
+    const uint4* p = src + r * KT * 32;
+    bA[r] = ktiles > 0 ? ld_stream(p) : Z;
+    bB[r] = ktiles > 1 ? ld_stream(p + 32) : Z;
+    bC[r] = Z;
+    nxt[r] = p + 32 * min(2, max(ktiles - 1, 0));
+  }
+  __shared__ __align__(8) uint64_t sbar;
+  if (threadIdx.x == 0) mbar_init(&sbar, 1);
+  const uint32_t dbytes = (uint32_t)ktiles * 1024u;
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&sbar, MODE ? 2 * dbytes : dbytes);
+    bulk_g2s(dg, dig + kt0 * 64, dbytes, &sbar);
+    if (MODE) bulk_g2s(dg + kt_cta * 64, dig2 + kt0 * 64, dbytes, &sbar);
+  }
+  __syncthreads();  // the mbarrier's init
+  mbar_wait(&sbar, 0);
+  const int sw = g ^ (2 * tid);
+  const uint4* bp = dg + tid * 8 + sw;
+  const int m2 = MODE ? kt_cta * 64 : 0;  // K2: the cm digits' offset
+#define GKB_PMI_STEP(CUR, DST)                                             \
+  if (t < ktiles) {                                                        \
+    const uint4 b01 = bp[0], b23 = bp[32];                                 \
+    const uint4 c01 = MODE ? bp[m2] : b01, c23 = MODE ? bp[m2 + 32] : b23; \
+    const bool adv = t + 2 < ktiles - 1;                                   \
+    _Pragma("unroll") for (int r = 0; r < kStripsPerWarp; ++r) {           \
+      DST[r] = ld_stream(nxt[r]);                                          \
+      nxt[r] += adv ? 32 : 0;                                              \
+      mma_tile(acc[r], CUR[r], b01, b23);                                  \
+      mma_tile(accm[r], miss_ind(CUR[r]), c01, c23);                       \
+    }                                                                      \
+    bp += 64;                                                              \
+    ++t;                                                                   \
+  }
+  for (int t = 0; t < ktiles;) {
+    GKB_PMI_STEP(bA, bC)
+    GKB_PMI_STEP(bB, bA)
+    GKB_PMI_STEP(bC, bB)
+  }
+#undef GKB_PMI_STEP
+  const int E = dexp[kc], Em = MODE ? dexp2[kc] : E;
+  const double rsum = dsum[kc];
+  const double p0 = pow2(16 * tid), p1 = pow2(16 * tid + 8);
+  const int hi = tid & 1;
+#pragma unroll
+  for (int r = 0; r < kStripsPerWarp; ++r) {
+    double v0 = (double)acc[r][0] * p0 + (double)acc[r][1] * p1;
+    double v1 = (double)acc[r][2] * p0 + (double)acc[r][3] * p1;
+    double u0 = (double)accm[r][0] * p0 + (double)accm[r][1] * p1;
+    double u1 = (double)accm[r][2] * p0 + (double)accm[r][3] * p1;
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+    u0 += __shfl_xor_sync(0xffffffffu, u0, 1);
+    u0 += __shfl_xor_sync(0xffffffffu, u0, 2);
+    u1 += __shfl_xor_sync(0xffffffffu, u1, 1);
+    u1 += __shfl_xor_sync(0xffffffffu, u1, 2);
+    if ((tid >> 1) == 0) {
+      const int64_t row = (strip0 + r) * 16 + g + 8 * hi;
+      const double val = scale2(hi ? v1 : v0, E - 62);
+      const double cor = scale2(hi ? u1 : u0, Em - 62);
+      double out;
+      if (MODE == 0) {  // a missing entry holds the imputed mean (genio.cpp:144)
+        out = val - mu[row] * rsum - (3.0 - mean[row]) * cor;
+      } else {
+        out = val - rsum - cor;
+      }
+      part[(int64_t)kc * rows_pad + row] = out;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- two vectors per pass
 // Block products ("decode amortized over k"): the same
 // kernel for two coefficient vectors at once. Each tile is loaded and expanded
@@ -1320,12 +1443,44 @@ void launch_main(const GenoView& g, const PMPlan& pl, const uint4* lay, const PM
 }
 }  // namespace
 
+namespace {
+// dense-missing mode: no lists; K2 also needs the digits of cm (s2m)
+template <int MODE>
+void launch_ind(const GenoView& g, const PMPlan& pl, const uint4* lay, const PMScratch& sc,
+                cudaStream_t s, bool pdl) {
+  auto kern = k_pm_ind<MODE>;
+  const size_t smem = pmi_smem_bytes(pl.kt_cta, MODE);
+  allow_smem(kern, smem);
+  launch_pdl(kern, dim3((unsigned)pl.grid_x, (unsigned)pl.nkc), dim3(kThreads), smem, s, pdl,
+             lay, pl.KT, pl.kt_cta, (const uint4*)sc.dig, (const int*)sc.dexp,
+             (const double*)sc.dsum, (const uint4*)g.s2m.dig, (const int*)g.s2m.dexp,
+             (const double*)g.mu, (const double*)g.mean, pl.rows_pad, sc.part);
+}
+// digits of cm_j = c_j (3 - m_j) (written by k_digitize<1>) for the K2 indicator MMA
+void digitize_cm(const GenoView& g, cudaStream_t s, bool pdl) {
+  const PMPlan& pl = g.pl2;
+  allow_smem(k_digitize<0>, pl.dig_smem);
+  launch_pdl(k_digitize<0>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, pdl,
+             (const double*)g.s2.cm, (const double*)nullptr, (const double*)nullptr,
+             (const double*)nullptr, g.p_loc, pl.kt_cta, g.s2m.dig, g.s2m.dexp, g.s2m.dsum,
+             (double*)nullptr, (const double*)nullptr, (double*)nullptr, (const int*)nullptr);
+}
+}  // namespace
+
 // main kernel alone, fully serialized (the roofline timing in gkb_op_bench)
 void k1_main_only(const GenoView& g, const double* x, cudaStream_t s) {
+  if (g.ind) {
+    launch_ind<0>(g, g.pl1, g.lt1, g.s1, s, false);
+    return;
+  }
   launch_main<0>(g, g.pl1, g.lt1, g.s1, x, g.m1, s, false);
 }
 
 void k2_main_only(const GenoView& g, cudaStream_t s) {
+  if (g.ind) {
+    launch_ind<1>(g, g.pl2, g.lt2, g.s2, s, false);
+    return;
+  }
   launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, false);
 }
 
@@ -1337,6 +1492,13 @@ void k1_apply(const GenoView& g, const double* x, double* y, cudaStream_t s, boo
   }
   k1_digitize(g, x, s, di);
   if (di.div) x = di.store;  // the missing-entry terms read the stored quotient
+  if (g.ind) {
+    launch_ind<0>(g, g.pl1, g.lt1, g.s1, s, true);
+    launch_pdl(k1_reduce, dim3((unsigned)((g.p_loc + 255) / 256)), dim3(256), 0, s, true,
+               (const double*)g.s1.part, g.pl1.nkc, g.pl1.rows_pad, g.p_loc,
+               (const double*)g.inv_s, y);
+    return;
+  }
   if (stream_out) {  // finish fused into the last CTA of each row block: y rows leave progressively
     launch_main<0>(g, g.pl1, g.lt1, g.s1, x, g.m1, s, true, y);
     return;
@@ -1354,7 +1516,12 @@ void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s, c
     return;
   }
   k2_digitize(g, y, s, di);
-  launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, true);
+  if (g.ind) {
+    digitize_cm(g, s, true);
+    launch_ind<1>(g, g.pl2, g.lt2, g.s2, s, true);
+  } else {
+    launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, true);
+  }
   launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
              (const double*)g.s2.part, g.pl2.nkc, g.pl2.rows_pad, g.n, z);
 }
@@ -1403,6 +1570,11 @@ void launch_main2(const GenoView& g, const PMPlan& pl, const uint4* lay, const P
 void k1_apply2(const GenoView& g, const PMScratch& sb, const double* x0, const double* x1,
                double* y0, double* y1, cudaStream_t s) {
   if (g.p_loc == 0) return;
+  if (g.ind) {  // dense-missing mode: two single-vector products
+    k1_apply(g, x0, y0, s, false, DivIn{});
+    k1_apply(g, x1, y1, s, false, DivIn{});
+    return;
+  }
   digitize_into<0>(g, g.pl1, x0, g.s1, s, true);
   digitize_into<0>(g, g.pl1, x1, sb, s, true);
   launch_main2<0>(g, g.pl1, g.lt1, g.s1, sb, x0, x1, g.m1, s);
@@ -1418,6 +1590,11 @@ void k2_adjoint2(const GenoView& g, const PMScratch& sb, const double* y0, const
   if (g.p_loc == 0) {
     cudaMemsetAsync(z0, 0, sizeof(double) * (size_t)g.n, s);
     cudaMemsetAsync(z1, 0, sizeof(double) * (size_t)g.n, s);
+    return;
+  }
+  if (g.ind) {  // dense-missing mode: two single-vector products
+    k2_adjoint(g, y0, z0, s, DivIn{});
+    k2_adjoint(g, y1, z1, s, DivIn{});
     return;
   }
   digitize_into<1>(g, g.pl2, y0, g.s2, s, true);

@@ -211,6 +211,10 @@ struct GenoShard {
   uint16_t* m2_ent = nullptr;
   int64_t list_bytes = 0;
   dev::PMScratch s1{}, s2{};
+  // dense-missing mode (kernels.hpp GenoView::ind): chosen at build from the
+  // shard's missing fraction (GKB_MISS_MODE=list|ind|auto)
+  bool ind = false;
+  dev::PMScratch s2m{};
   dev::GenoView view() const;
 };
 

@@ -62,6 +62,10 @@ struct GenoView {
   MissLists m1, m2;
   PMScratch s1, s2;
   int64_t nmissing;
+  // dense-missing mode (no lists; indicator MMAs, k_pm_ind): s2m holds the
+  // digits of K2's cm_j = c_j (3 - m_j)
+  bool ind = false;
+  PMScratch s2m{};
 };
 
 // K8: .bed records of a staging block (rows [row0, row0+rows) of the shard) -> layouts.

@@ -391,6 +391,8 @@ dev::GenoView GenoShard::view() const {
   v.s1 = s1;
   v.s2 = s2;
   v.nmissing = nmissing;
+  v.ind = ind;
+  v.s2m = s2m;
   return v;
 }
 
@@ -409,6 +411,7 @@ GenoOp::~GenoOp() {
     free_scratch(g.s2, st);
     free_scratch(g.s1b, st);
     free_scratch(g.s2b, st);
+    free_scratch(g.s2m, st);
     cudaStreamSynchronize(st);
   }
 }
@@ -703,6 +706,19 @@ void GenoOp::build_from_synth(const dev::SynthDev& sp_in, const gkb_synth_spec* 
   finish_build();
 }
 
+// Missing-data handling of a shard: per-CTA lists walked in the epilogue
+// (cost grows with the missing count) below the threshold fraction, indicator
+// MMAs (flat cost, no list bytes) above it. GKB_MISS_MODE=list|ind forces one.
+static bool dense_missing(int64_t nmissing, int64_t p_loc, int64_t n) {
+  if (const char* e = std::getenv("GKB_MISS_MODE")) {
+    if (std::strcmp(e, "ind") == 0) return true;
+    if (std::strcmp(e, "list") == 0) return false;
+  }
+  double thr = 0.015;
+  if (const char* e = std::getenv("GKB_MISS_THRESHOLD")) thr = std::atof(e);
+  return (double)nmissing > thr * (double)p_loc * (double)n;
+}
+
 void GenoOp::finish_build() {
   const int L = (int)ctx->shards.size();
   counts_host.assign((size_t)(4 * m), 0);
@@ -731,7 +747,15 @@ void GenoOp::finish_build() {
                                cudaMemcpyHostToDevice, sh.stream));
     }
     g.list_bytes = 0;
-    if (g.nmissing > 0) {
+    g.ind = g.nmissing > 0 && dense_missing(g.nmissing, g.p_loc, g.n);
+    if (g.ind) {  // indicator MMAs instead of lists; K2's cm digits
+      auto pool = [&](auto** ptr, size_t bytes) {
+        GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, sh.stream));
+      };
+      pool(&g.s2m.dig, sizeof(uint4) * (size_t)(g.pl2.nkc * g.pl2.kt_cta * 64));
+      pool(&g.s2m.dexp, sizeof(int) * (size_t)g.pl2.nkc);
+      pool(&g.s2m.dsum, sizeof(double) * (size_t)g.pl2.nkc);
+    } else if (g.nmissing > 0) {
       const int64_t t1 = build_block_lists(g.lt1, g.pl1, sh.stream, &g.m1_off, &g.m1_base,
                                            &g.m1_ent, &g.list_bytes);
       const int64_t t2 = build_block_lists(g.lt2, g.pl2, sh.stream, &g.m2_off, &g.m2_base,
