@@ -140,6 +140,18 @@ int gkb_geno_marker_scan(gkb_op* op, const double* y, const double* Z, int64_t k
 int gkb_geno_standardize(gkb_op* op, int scheme);
 int gkb_geno_set_scaling(gkb_op* op, const double* mu, const double* inv_s);
 int gkb_geno_get_scaling(gkb_op* op, double* mu, double* inv_s);
+/* Device-memory plan of one shard of p_loc SNPs x n samples at a missing
+ * fraction: both tile layouts (one per product) when they fit in free_bytes,
+ * else layout 1 only (the adjoint then reads layout 1: single-layout mode,
+ * e.g. config 5 at 2 GPUs, 125 GB per layout per GPU). Host-only; the
+ * operator builders apply it with the device's free memory (GKB_LAYOUTS=1|2
+ * forces a mode). */
+int gkb_geno_plan(int64_t p_loc, int64_t n, double missing_fraction, int64_t free_bytes,
+                  int* layouts, int64_t* dual_bytes, int64_t* single_bytes);
+/* The modes an operator's shards were built in: layouts 1 or 2, and whether
+ * the missing entries are handled by indicator MMAs (dense_missing = 1, above
+ * 1.5% missing; GKB_MISS_MODE=list|ind forces) instead of per-CTA lists. */
+int gkb_geno_layouts(gkb_op* op, int* layouts, int* dense_missing);
 /* Reads rows [row0, row0+nrows) back from HBM as .bed records (layout round
  * trip; pads written 00 as write_bed does, genio.cpp:100). */
 int gkb_geno_read_bed(gkb_op* op, int64_t row0, int64_t nrows, uint8_t* payload_out);

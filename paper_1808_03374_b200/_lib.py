@@ -164,6 +164,8 @@ SIGNATURES = {
     "gkb_thick_restart": (I, [P, I64]),
     "gkb_compress_exhausted": (I, [P]),
     "gkb_deflate_right": (I, [P]),
+    "gkb_geno_plan": (I, [I64, I64, D, I64, C.POINTER(C.c_int), PI64, PI64]),
+    "gkb_geno_layouts": (I, [P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "gkb_cgs2": (I, [P, PD, I64, I64, PD, PD, PD]),
     "gkb_svd_small": (I, [PD, I64, I64, PD, PD, PD]),
     "gkb_rng_fill_symmetric": (I, [C.c_uint64, I64, PD]),

@@ -647,6 +647,30 @@ int gkb_compress_exhausted(gkb_lanczos* lz) {
   });
 }
 
+int gkb_geno_plan(int64_t p_loc, int64_t n, double missing_fraction, int64_t free_bytes,
+                  int* layouts, int64_t* dual_bytes, int64_t* single_bytes) {
+  return guarded([&] {
+    if (p_loc < 0 || n < 0) gkb::fail(GKB_EINVAL, "gkb_geno_plan: negative size");
+    const gkb::LayoutPlan pl = gkb::plan_layouts(p_loc, n, missing_fraction, free_bytes);
+    if (layouts) *layouts = pl.layouts;
+    if (dual_bytes) *dual_bytes = pl.dual_bytes;
+    if (single_bytes) *single_bytes = pl.single_bytes;
+  });
+}
+
+int gkb_geno_layouts(gkb_op* op, int* layouts, int* dense_missing) {
+  return guarded([&] {
+    auto* g = as_geno(op);
+    int l = 2, d = 0;
+    for (const auto& sh : g->gs) {
+      if (sh.single) l = 1;
+      if (sh.ind) d = 1;
+    }
+    if (layouts) *layouts = l;
+    if (dense_missing) *dense_missing = d;
+  });
+}
+
 int gkb_deflate_right(gkb_lanczos* lz) {
   return guarded([&] {
     need(lz, "lz");

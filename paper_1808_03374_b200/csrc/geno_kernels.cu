@@ -319,6 +319,8 @@ __global__ void __launch_bounds__(512) k_block_scan(const uint32_t* __restrict__
 // One CTA per column range kc (kt_cta * 128 columns): coefficients v_c
 //   MODE 0 (K1): v_c = x_c,            sum = sum_c v_c           (X of the range)
 //   MODE 1 (K2): v_c = inv_s_c * y_c,  sum = sum_c v_c mu_c, cm_c = v_c (3 - mean_c)
+//   MODE 2 (K2 from layout 1, single-layout mode): as MODE 1, digits in the
+//          k_pm_adj_l1 fragment order
 // -> E (largest exponent), 8 balanced base-256 digits of rn(v 2^(62-E)) in
 // mma B-fragment order: uint4 (word-column wc, digit i) holds, in 32-bit word
 // q, byte e = digit i of column 16 wc + 4 e + q.
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
       if (MODE == 0) {
         v = x;
         part += v;
-      } else {
+      } else {  // MODE 1 and 2: the adjoint's coefficients
         v = inv_s[c] * x;
         part += v * mu[c];
         cm[c] = v * (3.0 - mean[c]);  // a missing entry holds the imputed mean (genio.cpp:144)
@@ -376,6 +378,20 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
   const int E = block_max_int(emax, redi);
   const double s = block_sum(part, red);
   for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
+    if (MODE == 2) {
+      // K2 from layout 1 (k_pm_adj_l1): no column prescale (the 4^q scale sits
+      // on the output rows); SNP r of a 16-SNP strip is k-group (r & 7) >> 1,
+      // position (r & 1) + 2 (r >> 3); 128 bytes per strip = [digit][group][pos]
+      const int sg = t >> 4, r = t & 15, grp = (r & 7) >> 1, pos = (r & 1) + 2 * (r >> 3);
+      long long M = __double2ll_rn(scale2(vals[t], 62 - E));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int d = (int)(signed char)(M & 0xFF);
+        M = (M - d) >> 8;
+        db[sg * 128 + i * 16 + grp * 4 + pos] = (uint8_t)d;
+      }
+      continue;
+    }
     const int wc = t >> 4, k = t & 15, q = k & 3, e = k >> 2;
     // group-q columns meet codes pre-multiplied by 4^q in the MMA (mma_tile)
     long long M = __double2ll_rn(scale2(vals[t], 62 - E - 2 * q));
@@ -841,6 +857,263 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
   }
 }
 
+
+// ---------------------------------------------------------------- single-layout mode
+// K2 (reference apply_adjoint, z = X^T y) read from layout 1 (rows = SNPs),
+// for shards whose two layouts do not fit in HBM (config 5 at 2 GPUs: 125 GB
+// per layout per GPU). The contraction runs over SNPs, but a layout-1 word
+// holds 16 samples of ONE SNP, so a lane first gathers 4 SNPs' words of the
+// same 16 samples (two 8-byte loads from the tile's fragment order) and
+// byte-transposes them (8 PRMT): z_b byte i = SNP i's 4 codes of samples
+// 4b..4b+3. The shift-free mask z_b & (0x03030303 << 2q) is then a
+// register of 4 SNPs (k) for ONE sample (4b + q) scaled by 4^q, i.e. an A
+// fragment of mma.m16n8k16 (k-group = the lane's 4 SNPs, rows = samples).
+// The 4^q scale is per output row and undone exactly in the epilogue. Per
+// 512-byte tile: 2 LDG.64, 8 PRMT, 16 LOP3, 8 IMMA (vs 4 IMMA + 16 LOP3 in
+// the two-layout kernel). CTA = 8 warps x one 128-sample tile column each
+// (1024 samples) x a range of 112 SNP strips (1792 SNPs); per lane 8
+// accumulator sets (16 samples x 2 digits).
+constexpr int kL1tStrips = 112;               // SNP strips per range (1792 SNPs)
+constexpr int kL1tRows = 1024;                // samples per CTA
+constexpr int kL1tOffBytes = ((kL1tRows + 1) * 4 + 15) / 16 * 16;
+constexpr int kL1tEntBytes = 40 * 1024;       // staged list bytes (longer: walked in global)
+size_t l1t_smem_bytes() {
+  return (size_t)kL1tStrips * 128 + (size_t)kL1tStrips * 16 * 8 + kL1tOffBytes + kL1tEntBytes + 16;
+}
+
+__device__ __forceinline__ void mma16_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0));
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+__device__ __forceinline__ uint2 ld_stream8(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p));
+  return v;
+}
+
+// one tile: words w (SNPs 2t, 2t+8 of word-column g) and v (SNPs 2t+1, 2t+9)
+__device__ __forceinline__ void mma_tile_l1t(int (&acc)[8][4], const uint2 w, const uint2 v,
+                                             const uint32_t bd) {
+  // k order i = 0..3 <-> SNPs 2t, 2t+1, 2t+8, 2t+9 (k_digitize<2>'s positions)
+  const uint32_t t0 = prmt(w.x, v.x, 0x5140u), t1 = prmt(w.x, v.x, 0x7362u);
+  const uint32_t t2 = prmt(w.y, v.y, 0x5140u), t3 = prmt(w.y, v.y, 0x7362u);
+  const uint32_t z[4] = {prmt(t0, t2, 0x5410u), prmt(t0, t2, 0x7632u), prmt(t1, t3, 0x5410u),
+                         prmt(t1, t3, 0x7632u)};
+  const uint32_t m0 = 0x03030303u, m1 = m0 << 2, m2 = m0 << 4, m3 = m0 << 6;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    mma16_u8s8(acc[2 * b], z[b] & m0, z[b] & m1, bd);      // samples 4b, 4b+1 (x1, x4)
+    mma16_u8s8(acc[2 * b + 1], z[b] & m2, z[b] & m3, bd);  // samples 4b+2, 4b+3 (x16, x64)
+  }
+}
+
+// grid (sample blocks, SNP ranges). Writes part[kc][sample] = the range's
+// exact partial of z_s = sum_j c_j a_js - sum_j c_j mu_j - sum_{j miss} cm_j.
+__global__ void __launch_bounds__(kThreads, 3) k_pm_adj_l1(
+    const uint32_t* __restrict__ lay, int64_t KT, int64_t S1, const uint32_t* __restrict__ dig,
+    const int* __restrict__ dexp, const double* __restrict__ dsum,
+    const double* __restrict__ cval, const uint32_t* __restrict__ m_off,
+    const int64_t* __restrict__ m_base, const uint16_t* __restrict__ m_ent, int64_t rows_pad,
+    double* __restrict__ part) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint32_t* dgs = reinterpret_cast<uint32_t*>(sm);                      // 112 strips x 32 words
+  double* cvs = reinterpret_cast<double*>(sm + kL1tStrips * 128);        // 1792 cm values
+  uint8_t* stage = sm + kL1tStrips * 128 + kL1tStrips * 16 * 8;          // offsets, then entries
+  const int kc = blockIdx.y, bx = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t kt = (int64_t)bx * 8 + warp;
+  const bool live = kt < KT;
+  const int64_t s0 = (int64_t)kc * kL1tStrips;
+  const int ns = (int)min((int64_t)kL1tStrips, S1 - s0);
+  const int64_t b = (int64_t)kc * gridDim.x + bx;
+  // this lane's two 8-byte halves of the tile (fragment order, word_index):
+  // uint4 #(8t + (g & 3)) and #(8t + 4 + (g & 3)), half g >> 2
+  const uint2* lay2 = reinterpret_cast<const uint2*>(lay);
+  const int64_t o1 = (int64_t)(8 * t + (g & 3)) * 2 + (g >> 2), o2 = o1 + 8;
+  const uint2* pw = lay2 + ((s0 * KT + (live ? kt : 0)) * 32) * 2 + o1;
+  const int64_t sstride = KT * 64;  // uint2 per strip
+  int acc[8][4];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0;
+  const uint2 Z = make_uint2(0, 0);
+  uint2 wA = ns > 0 ? ld_stream8(pw) : Z, vA = ns > 0 ? ld_stream8(pw + (o2 - o1)) : Z;
+  uint2 wB = ns > 1 ? ld_stream8(pw + sstride) : Z,
+        vB = ns > 1 ? ld_stream8(pw + sstride + (o2 - o1)) : Z;
+  uint2 wC = Z, vC = Z;
+  const uint2* nx = pw + sstride * min(2, max(ns - 1, 0));
+  pdl_trigger();
+  __shared__ __align__(8) uint64_t sbar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&sbar[0], 1);
+    mbar_init(&sbar[1], 1);
+  }
+  // staging: offsets (aligned superset) + list run before the PDL wait,
+  // digits (barrier 0) and cm values (barrier 1) after it
+  const uint32_t* offs = reinterpret_cast<const uint32_t*>(stage);
+  int ent_shift = -1;
+  int64_t eb = 0;
+  uint32_t obytes = 0, ebytes = 0;
+  const uint8_t* osrc = nullptr;
+  const uint8_t* esrc = nullptr;
+  if (m_off) {
+    const uint32_t* orow = m_off + b * (kL1tRows + 1);
+    osrc = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(orow) & ~uintptr_t(15));
+    const uint32_t oshift = (uint32_t)(reinterpret_cast<const uint8_t*>(orow) - osrc);
+    obytes = (oshift + 4 * (kL1tRows + 1) + 15) & ~15u;
+    offs += oshift / 4;
+    eb = m_base[b];
+    const int64_t ne = orow[kL1tRows];
+    const int64_t a0 = (eb * 2) & ~int64_t(15), a1 = (eb * 2 + ne * 2 + 15) & ~int64_t(15);
+    if (a1 - a0 <= kL1tEntBytes) {
+      esrc = reinterpret_cast<const uint8_t*>(m_ent) + a0;
+      ebytes = (uint32_t)(a1 - a0);
+      ent_shift = (int)(eb - a0 / 2);
+    }
+  }
+  const uint32_t dbytes = (uint32_t)kL1tStrips * 128u;
+  const uint32_t cbytes = m_off ? (uint32_t)kL1tStrips * 16u * 8u : 0u;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&sbar[0], dbytes);
+    mbar_arrive_expect_tx(&sbar[1], obytes + ebytes + cbytes);
+    if (obytes) bulk_g2s(stage, osrc, obytes, &sbar[1]);
+    if (ebytes) bulk_g2s(stage + kL1tOffBytes, esrc, ebytes, &sbar[1]);
+  }
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    bulk_g2s(dgs, dig + (int64_t)kc * kL1tStrips * 32, dbytes, &sbar[0]);
+    if (cbytes) bulk_g2s(cvs, cval + (int64_t)kc * kL1tStrips * 16, cbytes, &sbar[1]);
+  }
+  __syncthreads();  // the mbarriers' init
+  mbar_wait(&sbar[0], 0);
+  const uint32_t* bq = dgs + g * 4 + t;  // digit g of the lane's k-group, strip by strip
+#define GKB_L1T_STEP(CW, CV, DW, DV)                                       \
+  if (s < ns) {                                                            \
+    const uint32_t bd = bq[32 * s];                                        \
+    DW = ld_stream8(nx);                                                   \
+    DV = ld_stream8(nx + (o2 - o1));                                       \
+    nx += (s + 2 < ns - 1) ? sstride : 0;                                  \
+    mma_tile_l1t(acc, CW, CV, bd);                                         \
+    ++s;                                                                   \
+  }
+  for (int s = 0; s < ns;) {
+    GKB_L1T_STEP(wA, vA, wC, vC)
+    GKB_L1T_STEP(wB, vB, wA, vA)
+    GKB_L1T_STEP(wC, vC, wB, vB)
+  }
+#undef GKB_L1T_STEP
+  mbar_wait(&sbar[1], 0);  // offsets, list run, cm values
+  // Epilogue. Lane (g, t) holds digits (2t, 2t+1) of 16 samples of word-column
+  // g: MMA 2b + h -> rows g / g + 8 = samples 4b + 2h / 4b + 2h + 1. A
+  // reduce-scatter over the 4 lanes of the group (xor 1, then xor 2: the tree
+  // of the two-layout kernel's butterfly) leaves lane t the sums of samples
+  // 4t..4t+3 (q = 0..3).
+  const double p0 = pow2(16 * t), p1 = pow2(16 * t + 8);
+  double V[4][4];
+#pragma unroll
+  for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      V[bb][2 * h] = (double)acc[2 * bb + h][0] * p0 + (double)acc[2 * bb + h][1] * p1;
+      V[bb][2 * h + 1] = (double)acc[2 * bb + h][2] * p0 + (double)acc[2 * bb + h][3] * p1;
+    }
+  double W[2][4];
+  const bool odd = t & 1;
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double keep = odd ? V[2 * k + 1][q] : V[2 * k][q];
+      const double send = odd ? V[2 * k][q] : V[2 * k + 1][q];
+      W[k][q] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+  double S[4];
+  const bool hi2 = t & 2;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double keep = hi2 ? W[1][q] : W[0][q];
+    const double send = hi2 ? W[0][q] : W[1][q];
+    S[q] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  if (!live) return;
+  const int E = dexp[kc];
+  const double rsum = dsum[kc];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int rl = warp * 128 + 16 * g + 4 * t + q;  // block-local sample row
+    double corr = 0.0;
+    if (m_off) {
+      const uint32_t e0 = offs[rl], e1 = offs[rl + 1];
+      corr = ent_shift >= 0
+                 ? walk_list(reinterpret_cast<const uint16_t*>(stage + kL1tOffBytes) + ent_shift,
+                             e0, e1, cvs)
+                 : walk_list(m_ent + eb, e0, e1, cvs);
+    }
+    const double val = scale2(S[q], E - 62 - 2 * q);
+    part[(int64_t)kc * rows_pad + (int64_t)bx * kL1tRows + rl] = val - rsum - corr;
+  }
+}
+
+// Missing lists of the single-layout K2 blocks (1024 samples x 1792 SNPs),
+// read from layout 1: thread per sample row; entries = block-local SNP
+// indices (ascending). Count pass / fill pass as k_miss_tiles.
+template <bool kFill>
+__global__ void __launch_bounds__(kL1tRows) k_miss_l1t(const uint32_t* __restrict__ lay,
+                                                     int64_t KT, int64_t p_loc, int64_t n,
+                                                     uint32_t* __restrict__ cnt,
+                                                     const uint32_t* __restrict__ off,
+                                                     const int64_t* __restrict__ base,
+                                                     uint16_t* __restrict__ ent) {
+  const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int r = threadIdx.x;
+  const int64_t smp = (int64_t)blockIdx.x * kL1tRows + r;
+  const int64_t j0 = (int64_t)blockIdx.y * kL1tStrips * 16;
+  const int64_t j1 = min(p_loc, j0 + (int64_t)kL1tStrips * 16);
+  uint32_t c = 0;
+  int64_t pos = kFill ? base[b] + off[b * (kL1tRows + 1) + r] : 0;
+  if (smp < n) {
+    const int64_t wc = smp >> 4;
+    const int sh = 2 * (int)(smp & 15);
+    for (int64_t j = j0; j < j1; ++j) {
+      const uint32_t code = (lay[word_index(KT, j, wc)] >> sh) & 3u;
+      if (code == 3u) {
+        if (kFill) ent[pos++] = (uint16_t)(j - j0);
+        else ++c;
+      }
+    }
+  }
+  if (!kFill) cnt[b * kL1tRows + r] = c;
+}
+
+// CTA per block: exclusive scan of 1024 row counts -> off, block total -> tot.
+__global__ void __launch_bounds__(kL1tRows) k_block_scan_1024(const uint32_t* __restrict__ cnt,
+                                                            uint32_t* __restrict__ off,
+                                                            int64_t* __restrict__ tot) {
+  __shared__ uint32_t sc[kL1tRows];
+  const int64_t b = blockIdx.x;
+  const int t = threadIdx.x;
+  sc[t] = cnt[b * kL1tRows + t];
+  __syncthreads();
+  for (int o = 1; o < kL1tRows; o <<= 1) {
+    const uint32_t v = t >= o ? sc[t - o] : 0u;
+    __syncthreads();
+    sc[t] += v;
+    __syncthreads();
+  }
+  if (t == 0) off[b * (kL1tRows + 1)] = 0;
+  off[b * (kL1tRows + 1) + t + 1] = sc[t];
+  if (t == kL1tRows - 1) tot[b] = sc[t];
+}
 
 // ---------------------------------------------------------------- dense-missing mode
 // Main kernel for shards with many missing entries (DESIGN.md section 4,
@@ -1400,6 +1673,32 @@ void block_scan(const uint32_t* cnt, int64_t nblk, int span, uint32_t* off, int6
   k_block_scan<<<(unsigned)nblk, 512, 0, s>>>(cnt, span, off, tot);
 }
 
+L1TPlan l1t_plan(const PMPlan& pl1, int64_t p_loc) {
+  L1TPlan lt;
+  lt.grid_x = (pl1.KT + 7) / 8;  // 8 tiles (1024 samples) per CTA
+  lt.nkc = std::max<int64_t>(1, (p_loc + kL1tStrips * 16 - 1) / (kL1tStrips * 16));
+  lt.rows_pad = lt.grid_x * kL1tRows;
+  return lt;
+}
+
+size_t l1t_dig_bytes() { return (size_t)kL1tStrips * 128; }
+
+void miss_lists_l1t(const uint32_t* lay1, const PMPlan& pl1, const L1TPlan& lt, int64_t p_loc,
+                    int64_t n, bool fill, uint32_t* cnt, const uint32_t* off, const int64_t* base,
+                    uint16_t* ent, cudaStream_t s) {
+  dim3 grid((unsigned)lt.grid_x, (unsigned)lt.nkc);
+  if (fill)
+    k_miss_l1t<true><<<grid, kL1tRows, 0, s>>>(lay1, pl1.KT, p_loc, n, cnt, off, base, ent);
+  else
+    k_miss_l1t<false><<<grid, kL1tRows, 0, s>>>(lay1, pl1.KT, p_loc, n, cnt, off, base, ent);
+}
+
+void block_scan_1024(const uint32_t* cnt, int64_t nblk, uint32_t* off, int64_t* tot,
+                     cudaStream_t s) {
+  if (nblk == 0) return;
+  k_block_scan_1024<<<(unsigned)nblk, kL1tRows, 0, s>>>(cnt, off, tot);
+}
+
 namespace {
 template <class K>
 void allow_smem(K kern, size_t bytes) {  // opt in above 48 KB
@@ -1467,6 +1766,26 @@ void digitize_cm(const GenoView& g, cudaStream_t s, bool pdl) {
 }
 }  // namespace
 
+namespace {
+// single-layout mode: K2's digitize (digits in k_pm_adj_l1 order) and main kernel
+void digitize_l1t(const GenoView& g, const double* y, cudaStream_t s, const DivIn& di) {
+  const size_t smem = (size_t)14 * 64 * sizeof(uint4) + (size_t)14 * 128 * sizeof(double);
+  allow_smem(k_digitize<2>, smem);
+  launch_pdl(k_digitize<2>, dim3((unsigned)g.l1t_nkc), dim3(1024), smem, s, true, y,
+             (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc, 14,
+             g.s2.dig, g.s2.dexp, g.s2.dsum, g.s2.cm, di.div, di.store, di.gate);
+}
+void launch_adj_l1(const GenoView& g, cudaStream_t s, bool pdl) {
+  const size_t smem = l1t_smem_bytes();
+  allow_smem(k_pm_adj_l1, smem);
+  launch_pdl(k_pm_adj_l1, dim3((unsigned)g.l1t_grid, (unsigned)g.l1t_nkc), dim3(kThreads), smem,
+             s, pdl, reinterpret_cast<const uint32_t*>(g.lt1), g.pl1.KT, g.pl1.S,
+             reinterpret_cast<const uint32_t*>(g.s2.dig), (const int*)g.s2.dexp,
+             (const double*)g.s2.dsum, (const double*)g.s2.cm, g.m2.off, g.m2.base, g.m2.ent,
+             g.l1t_rows_pad, g.s2.part);
+}
+}  // namespace
+
 // main kernel alone, fully serialized (the roofline timing in gkb_op_bench)
 void k1_main_only(const GenoView& g, const double* x, cudaStream_t s) {
   if (g.ind) {
@@ -1477,6 +1796,10 @@ void k1_main_only(const GenoView& g, const double* x, cudaStream_t s) {
 }
 
 void k2_main_only(const GenoView& g, cudaStream_t s) {
+  if (g.single) {
+    launch_adj_l1(g, s, false);
+    return;
+  }
   if (g.ind) {
     launch_ind<1>(g, g.pl2, g.lt2, g.s2, s, false);
     return;
@@ -1513,6 +1836,13 @@ void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s, c
   if (g.n == 0 || g.p_loc == 0) {
     if (di.div) div_copy_dv(y, di.div, di.store, g.p_loc, s, di.gate);
     if (g.n > 0) cudaMemsetAsync(z, 0, sizeof(double) * (size_t)g.n, s);
+    return;
+  }
+  if (g.single) {  // K2 from layout 1
+    digitize_l1t(g, y, s, di);
+    launch_adj_l1(g, s, true);
+    launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
+               (const double*)g.s2.part, (int)g.l1t_nkc, g.l1t_rows_pad, g.n, z);
     return;
   }
   k2_digitize(g, y, s, di);
@@ -1592,7 +1922,7 @@ void k2_adjoint2(const GenoView& g, const PMScratch& sb, const double* y0, const
     cudaMemsetAsync(z1, 0, sizeof(double) * (size_t)g.n, s);
     return;
   }
-  if (g.ind) {  // dense-missing mode: two single-vector products
+  if (g.ind || g.single) {  // dense-missing / single-layout mode: two single-vector products
     k2_adjoint(g, y0, z0, s, DivIn{});
     k2_adjoint(g, y1, z1, s, DivIn{});
     return;

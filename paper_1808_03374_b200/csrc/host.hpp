@@ -215,14 +215,28 @@ struct GenoShard {
   // shard's missing fraction (GKB_MISS_MODE=list|ind|auto)
   bool ind = false;
   dev::PMScratch s2m{};
+  // single-layout mode (kernels.hpp GenoView::single): chosen at allocation
+  // by plan_layouts (GKB_LAYOUTS=1|2 forces)
+  bool single = false;
+  dev::L1TPlan plt{};
   dev::GenoView view() const;
 };
+
+// Device-memory plan of one shard (p_loc SNPs x n samples): both tile
+// layouts when they fit in `free_bytes` (with the lists, scratch and a solver
+// headroom), else layout 1 only (K2 by k_pm_adj_l1).
+struct LayoutPlan {
+  int layouts = 2;
+  int64_t dual_bytes = 0, single_bytes = 0;
+};
+LayoutPlan plan_layouts(int64_t p_loc, int64_t n, double missing_fraction, int64_t free_bytes);
 
 struct GenoOp : DevOp {
   GenoOp() { direct_host_io = true; }  // k1_reduce writes y, k_digitize<1> reads y, k2_reduce writes z
   std::vector<GenoShard> gs;
   std::vector<int64_t> counts_host;  // p*4 (local rows only in SPMD mode, zero elsewhere)
   bool scaled = false;
+  double plan_missing = 0.02;  // missing fraction assumed by the layout plan (synth: the spec's)
   ~GenoOp() override;
   void build_from_payload(const uint8_t* payload, int64_t p, int64_t n);
   void build_from_bed_file(const char* bed, int64_t p, int64_t n);  // after bed_check

@@ -66,7 +66,22 @@ struct GenoView {
   // digits of K2's cm_j = c_j (3 - m_j)
   bool ind = false;
   PMScratch s2m{};
+  // single-layout mode (no layout 2; K2 read from layout 1 by k_pm_adj_l1):
+  // blocks of 1024 samples x 1792 SNPs; m2 / s2 are sized for this geometry
+  bool single = false;
+  int64_t l1t_grid = 0, l1t_nkc = 0, l1t_rows_pad = 0;
 };
+// single-layout K2 geometry of a shard (p_loc SNPs x n samples)
+struct L1TPlan {
+  int64_t grid_x, nkc, rows_pad;
+};
+L1TPlan l1t_plan(const PMPlan& pl1, int64_t p_loc);
+void miss_lists_l1t(const uint32_t* lay1, const PMPlan& pl1, const L1TPlan& lt, int64_t p_loc,
+                    int64_t n, bool fill, uint32_t* cnt, const uint32_t* off, const int64_t* base,
+                    uint16_t* ent, cudaStream_t s);
+void block_scan_1024(const uint32_t* cnt, int64_t nblk, uint32_t* off, int64_t* tot,
+                     cudaStream_t s);
+size_t l1t_dig_bytes();  // digits per range
 
 // K8: .bed records of a staging block (rows [row0, row0+rows) of the shard) -> layouts.
 void build_lt1(const uint8_t* bed, int64_t stride_bytes, int64_t rows, int64_t row0, int64_t n,

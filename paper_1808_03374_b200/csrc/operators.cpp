@@ -353,6 +353,49 @@ static int64_t build_block_lists(const uint32_t* lay, const dev::PMPlan& pl, cud
   return total;
 }
 
+// Missing lists of the single-layout K2 blocks (1024 samples x 1792 SNPs,
+// dev::miss_lists_l1t), into the shard's m2 fields. Returns the entry count.
+static int64_t build_l1t_lists(GenoShard& g, cudaStream_t st) {
+  const dev::L1TPlan& lt = g.plt;
+  const int span = 1024;
+  const int64_t nblk = lt.grid_x * lt.nkc;
+  uint32_t* cnt = nullptr;
+  int64_t* tot = nullptr;
+  auto pool = [&](auto** ptr, size_t bytes) {
+    GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, st));
+  };
+  pool(&cnt, sizeof(uint32_t) * (size_t)(nblk * span));
+  pool(&tot, sizeof(int64_t) * (size_t)nblk);
+  pool(&g.m2_off, sizeof(uint32_t) * (size_t)(nblk * (span + 1) + 4));
+  dev::miss_lists_l1t(g.lt1, g.pl1, lt, g.p_loc, g.n, false, cnt, nullptr, nullptr, nullptr, st);
+  GKB_LAUNCH_CHECK();
+  dev::block_scan_1024(cnt, nblk, g.m2_off, tot, st);
+  GKB_LAUNCH_CHECK();
+  std::vector<int64_t> h((size_t)nblk);
+  GKB_CUDA(cudaMemcpyAsync(h.data(), tot, sizeof(int64_t) * (size_t)nblk, cudaMemcpyDeviceToHost, st));
+  GKB_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(cnt, st);
+  cudaFreeAsync(tot, st);
+  int64_t total = 0;
+  for (int64_t bb = 0; bb < nblk; ++bb) {
+    const int64_t c = h[bb];
+    h[bb] = total;
+    total += c;
+  }
+  pool(&g.m2_base, sizeof(int64_t) * (size_t)nblk);
+  GKB_CUDA(cudaMemcpyAsync(g.m2_base, h.data(), sizeof(int64_t) * (size_t)nblk,
+                           cudaMemcpyHostToDevice, st));
+  const int64_t ent_alloc = (total + 7) / 8 * 8 + 8;
+  pool(&g.m2_ent, sizeof(uint16_t) * (size_t)ent_alloc);
+  GKB_CUDA(cudaMemsetAsync(g.m2_ent + total, 0, sizeof(uint16_t) * (size_t)(ent_alloc - total), st));
+  dev::miss_lists_l1t(g.lt1, g.pl1, lt, g.p_loc, g.n, true, nullptr, g.m2_off, g.m2_base, g.m2_ent,
+                      st);
+  GKB_LAUNCH_CHECK();
+  g.list_bytes += (int64_t)(sizeof(uint32_t) * nblk * (span + 1) + sizeof(int64_t) * nblk +
+                            sizeof(uint16_t) * total);
+  return total;
+}
+
 static void alloc_scratch(const dev::PMPlan& pl, bool with_cm, dev::PMScratch& sc,
                           cudaStream_t st) {
   auto pool = [&](auto** ptr, size_t bytes) {
@@ -393,6 +436,10 @@ dev::GenoView GenoShard::view() const {
   v.nmissing = nmissing;
   v.ind = ind;
   v.s2m = s2m;
+  v.single = single;
+  v.l1t_grid = plt.grid_x;
+  v.l1t_nkc = plt.nkc;
+  v.l1t_rows_pad = plt.rows_pad;
   return v;
 }
 
@@ -416,20 +463,58 @@ GenoOp::~GenoOp() {
   }
 }
 
+LayoutPlan plan_layouts(int64_t p_loc, int64_t n, double missing_fraction, int64_t free_bytes) {
+  const dev::PMPlan pl1 = dev::pm_plan(p_loc, n), pl2 = dev::pm_plan(n, p_loc);
+  const dev::L1TPlan lt = dev::l1t_plan(pl1, p_loc);
+  const double nm = std::max(0.0, missing_fraction) * (double)p_loc * (double)n;
+  auto lists = [&](int64_t blocks, int64_t span) {  // 16-bit entries + offsets + bases
+    return (int64_t)(2.0 * nm) + blocks * ((span + 1) * 4 + 8);
+  };
+  const int64_t lay1 = 4 * dev::pm_words(pl1), lay2 = 4 * dev::pm_words(pl2);
+  const int64_t l1 = lists(pl1.grid_x * pl1.nkc, 256), l2 = lists(pl2.grid_x * pl2.nkc, 256);
+  const int64_t l2t = lists(lt.grid_x * lt.nkc, 1024);
+  const int64_t part1 = 8 * pl1.nkc * pl1.rows_pad, part2 = 8 * pl2.nkc * pl2.rows_pad;
+  const int64_t part2t = 8 * lt.nkc * lt.rows_pad;
+  const int64_t vecs = 8 * 3 * pl1.rows_pad + 8 * (int64_t)(n + p_loc) * 8;
+  // svdl's double-buffered bases at a 64-vector subspace
+  const int64_t solver = 2 * 8 * 65 * (p_loc + n);
+  LayoutPlan pl;
+  pl.dual_bytes = lay1 + lay2 + l1 + l2 + part1 + part2 + vecs + solver;
+  pl.single_bytes = lay1 + l1 + l2t + part1 + part2t + vecs + solver;
+  pl.layouts = pl.dual_bytes <= free_bytes ? 2 : 1;
+  return pl;
+}
+
 void GenoOp::alloc_shard(int i, int64_t p_loc, int64_t nn) {
   GenoShard& g = gs[i];
   g.p_loc = p_loc;
   g.n = nn;
   g.pl1 = dev::pm_plan(p_loc, nn);
   g.pl2 = dev::pm_plan(nn, p_loc);
+  g.plt = dev::l1t_plan(g.pl1, p_loc);
   ctx->set_device(i);
   cudaStream_t st = ctx->shards[i].stream;
+  {  // one layout or two (GKB_LAYOUTS=1|2 forces; else the device-memory plan)
+    const char* e = std::getenv("GKB_LAYOUTS");
+    if (e && std::strcmp(e, "1") == 0) {
+      g.single = true;
+    } else if (e && std::strcmp(e, "2") == 0) {
+      g.single = false;
+    } else {
+      size_t fr = 0, tot = 0;
+      GKB_CUDA(cudaMemGetInfo(&fr, &tot));
+      const int64_t margin = (int64_t)2 << 30;
+      g.single = plan_layouts(p_loc, nn, plan_missing, (int64_t)fr - margin).layouts == 1;
+    }
+  }
   const size_t w1 = (size_t)dev::pm_words(g.pl1), w2 = (size_t)dev::pm_words(g.pl2);
   // the two layouts are the large allocations: stream-ordered from the pool
   GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g.lt1), sizeof(uint32_t) * w1, st));
-  GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g.lt2), sizeof(uint32_t) * w2, st));
   GKB_CUDA(cudaMemsetAsync(g.lt1, 0, sizeof(uint32_t) * w1, st));
-  GKB_CUDA(cudaMemsetAsync(g.lt2, 0, sizeof(uint32_t) * w2, st));
+  if (!g.single) {
+    GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g.lt2), sizeof(uint32_t) * w2, st));
+    GKB_CUDA(cudaMemsetAsync(g.lt2, 0, sizeof(uint32_t) * w2, st));
+  }
   const size_t pp = (size_t)g.pl1.rows_pad;
   // everything else too: no implicit device synchronization during ingest
   auto pool = [&](auto** ptr, size_t bytes) {
@@ -476,7 +561,7 @@ void GenoOp::build_from_payload(const uint8_t* payload, int64_t p, int64_t nn) {
                                sh.stream));
       dev::build_lt1(dstage, stride, rb, b0, nn, gs[i].pl1, gs[i].lt1, sh.stream);
       GKB_LAUNCH_CHECK();
-      dev::build_lt2(dstage, stride, rb, b0, nn, gs[i].pl2, gs[i].lt2, sh.stream);
+      if (!gs[i].single) dev::build_lt2(dstage, stride, rb, b0, nn, gs[i].pl2, gs[i].lt2, sh.stream);
       GKB_LAUNCH_CHECK();
     }
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
@@ -625,7 +710,7 @@ void GenoOp::build_from_bed_file(const char* bed, int64_t p, int64_t nn) {
                                  sh.stream));
         dev::build_lt1(dstage[k], stride, rb, b0, nn, gs[i].pl1, gs[i].lt1, sh.stream);
         GKB_LAUNCH_CHECK();
-        dev::build_lt2(dstage[k], stride, rb, b0, nn, gs[i].pl2, gs[i].lt2, sh.stream);
+        if (!gs[i].single) dev::build_lt2(dstage[k], stride, rb, b0, nn, gs[i].pl2, gs[i].lt2, sh.stream);
         GKB_LAUNCH_CHECK();
         GKB_CUDA(cudaEventRecord(ev[k], sh.stream));
       }
@@ -656,6 +741,7 @@ void GenoOp::build_from_synth(const dev::SynthDev& sp_in, const gkb_synth_spec* 
   gs.resize(L);
   const int64_t stride = (nn + 3) / 4;
   (void)sp_in;
+  plan_missing = spec->missing_rate;
   for (int i = 0; i < L; ++i) {
     const int64_t r0 = row0(i), pr = rows(i);
     alloc_shard(i, pr, nn);
@@ -693,7 +779,7 @@ void GenoOp::build_from_synth(const dev::SynthDev& sp_in, const gkb_synth_spec* 
       GKB_LAUNCH_CHECK();
       dev::build_lt1(dstage, stride, rb, b0, nn, gs[i].pl1, gs[i].lt1, sh.stream);
       GKB_LAUNCH_CHECK();
-      dev::build_lt2(dstage, stride, rb, b0, nn, gs[i].pl2, gs[i].lt2, sh.stream);
+      if (!gs[i].single) dev::build_lt2(dstage, stride, rb, b0, nn, gs[i].pl2, gs[i].lt2, sh.stream);
       GKB_LAUNCH_CHECK();
     }
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
@@ -748,22 +834,40 @@ void GenoOp::finish_build() {
     }
     g.list_bytes = 0;
     g.ind = g.nmissing > 0 && dense_missing(g.nmissing, g.p_loc, g.n);
-    if (g.ind) {  // indicator MMAs instead of lists; K2's cm digits
-      auto pool = [&](auto** ptr, size_t bytes) {
-        GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, sh.stream));
-      };
+    auto pool = [&](auto** ptr, size_t bytes) {
+      GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, sh.stream));
+    };
+    if (g.ind && !g.single) {  // indicator MMAs instead of lists; K2's cm digits
       pool(&g.s2m.dig, sizeof(uint4) * (size_t)(g.pl2.nkc * g.pl2.kt_cta * 64));
       pool(&g.s2m.dexp, sizeof(int) * (size_t)g.pl2.nkc);
       pool(&g.s2m.dsum, sizeof(double) * (size_t)g.pl2.nkc);
-    } else if (g.nmissing > 0) {
+    }
+    if (g.nmissing > 0 && !g.ind) {
       const int64_t t1 = build_block_lists(g.lt1, g.pl1, sh.stream, &g.m1_off, &g.m1_base,
                                            &g.m1_ent, &g.list_bytes);
+      if (t1 != g.nmissing) fail(GKB_ECUDA, "missing-list count mismatch (layout 1)");
+    }
+    if (g.nmissing > 0 && !g.ind && !g.single) {
       const int64_t t2 = build_block_lists(g.lt2, g.pl2, sh.stream, &g.m2_off, &g.m2_base,
                                            &g.m2_ent, &g.list_bytes);
-      if (t1 != g.nmissing || t2 != g.nmissing) fail(GKB_ECUDA, "missing-list count mismatch");
+      if (t2 != g.nmissing) fail(GKB_ECUDA, "missing-list count mismatch (layout 2)");
+    }
+    if (g.nmissing > 0 && g.single) {  // K2 from layout 1 always walks lists
+      const int64_t t2 = build_l1t_lists(g, sh.stream);
+      if (t2 != g.nmissing) fail(GKB_ECUDA, "missing-list count mismatch (single layout)");
     }
     alloc_scratch(g.pl1, false, g.s1, sh.stream);
-    alloc_scratch(g.pl2, true, g.s2, sh.stream);
+    if (g.single) {  // K2's scratch in the single-layout geometry
+      const dev::L1TPlan& lt = g.plt;
+      pool(&g.s2.dig, dev::l1t_dig_bytes() * (size_t)lt.nkc);
+      pool(&g.s2.dexp, sizeof(int) * (size_t)lt.nkc);
+      pool(&g.s2.dsum, sizeof(double) * (size_t)lt.nkc);
+      pool(&g.s2.part, sizeof(double) * (size_t)(lt.nkc * lt.rows_pad));
+      pool(&g.s2.cm, sizeof(double) * (size_t)(lt.nkc * 1792));
+      pool(&g.s2.tick, sizeof(unsigned));
+    } else {
+      alloc_scratch(g.pl2, true, g.s2, sh.stream);
+    }
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
   }
   if (ctx->spmd_mode && ctx->nshards_total > 1) {
@@ -873,7 +977,7 @@ void GenoOp::apply_block_dev(const std::vector<const double*>& X, int64_t ldx, i
       ctx->set_device((int)i);
       GenoShard& g = gs[i];
       cudaStream_t st = ctx->shards[i].stream;
-      if (!g.s1b.part) alloc_scratch(g.pl1, false, g.s1b, st);
+      if (!g.s1b.part && !g.ind) alloc_scratch(g.pl1, false, g.s1b, st);
       dev::k1_apply2(g.view(), g.s1b, X[i] + c * ldx, X[i] + (c + 1) * ldx, Y[i] + c * ldy[i],
                      Y[i] + (c + 1) * ldy[i], st);
       GKB_LAUNCH_CHECK();
@@ -901,7 +1005,7 @@ void GenoOp::adjoint_block_dev(const std::vector<const double*>& Yb,
       ctx->set_device(i);
       GenoShard& g = gs[i];
       cudaStream_t st = ctx->shards[i].stream;
-      if (!g.s2b.part) alloc_scratch(g.pl2, true, g.s2b, st);
+      if (!g.s2b.part && !g.ind && !g.single) alloc_scratch(g.pl2, true, g.s2b, st);
       dev::k2_adjoint2(g.view(), g.s2b, Yb[i] + c * ldyb[i], Yb[i] + (c + 1) * ldyb[i],
                        Z[i] + c * ldz, Z[i] + (c + 1) * ldz, st);
       GKB_LAUNCH_CHECK();
@@ -1077,7 +1181,7 @@ int64_t GenoOp::packed_bytes() const {
 int64_t GenoOp::device_bytes() const {
   int64_t b = 0;
   for (const auto& g : gs) {
-    b += 4 * (dev::pm_words(g.pl1) + dev::pm_words(g.pl2));
+    b += 4 * (dev::pm_words(g.pl1) + (g.single ? 0 : dev::pm_words(g.pl2)));
     b += g.list_bytes + 16 * g.pl1.rows_pad;  // missing lists, mu + inv_s
   }
   return b;

@@ -432,6 +432,13 @@ class GenotypeOperator(LinearOperator):
         check(lib.gkb_geno_read_bed(self._h, row0, nrows, out.ctypes.data_as(C.POINTER(C.c_uint8))))
         return out
 
+    def modes(self):
+        """(layouts, dense_missing): 2 = both tile layouts, 1 = single-layout
+        mode; dense_missing = indicator MMAs instead of per-CTA lists."""
+        a, b = C.c_int(), C.c_int()
+        check(lib.gkb_geno_layouts(self._h, C.byref(a), C.byref(b)))
+        return a.value, bool(b.value)
+
     def info(self):
         a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
         check(lib.gkb_geno_info(self._h, C.byref(a), C.byref(b), C.byref(c)))
@@ -625,6 +632,14 @@ class LanczosFactorization:
             self.close()
         except Exception:
             pass
+
+
+def geno_plan(p_loc: int, n: int, missing_fraction: float, free_bytes: int):
+    """Layout plan of one shard (gkb_geno_plan): (layouts, dual_bytes, single_bytes)."""
+    a, b, c = C.c_int(), C.c_int64(), C.c_int64()
+    check(lib.gkb_geno_plan(int(p_loc), int(n), float(missing_fraction), int(free_bytes),
+                            C.byref(a), C.byref(b), C.byref(c)))
+    return a.value, b.value, c.value
 
 
 def error_metric_l1(ritz: RitzSet, k: int) -> float:  # gkl.cpp:411-414

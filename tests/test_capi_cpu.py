@@ -136,3 +136,17 @@ def test_genio_roundtrip(tmp_path):
         f.write(b"\x00")
     with pytest.raises(gkb.FormatError):
         genio.read_bed(bed, bim, fam)
+
+
+def test_layout_planner():
+    """gkb_geno_plan (host-only): config 5 at 2 GPUs (500,000 SNPs x 1,000,000
+    samples per GPU, 1% missing) does not fit two 125 GB layouts in a B200's
+    HBM and plans one (~154 GB); config 4 on one GPU keeps both."""
+    import paper_1808_03374_b200 as gkb
+    hbm = 178 << 30
+    layouts, dual, single = gkb.geno_plan(500_000, 1_000_000, 0.01, hbm)
+    assert layouts == 1 and dual > hbm and single < hbm
+    assert single >= 125_000_000_000
+    layouts, dual, single = gkb.geno_plan(100_000, 500_000, 0.01, hbm)
+    assert layouts == 2 and dual < hbm
+    assert gkb.geno_plan(250_000, 1_000_000, 0.01, hbm)[0] == 2   # config 5 at 4 GPUs
