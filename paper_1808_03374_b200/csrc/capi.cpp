@@ -366,13 +366,13 @@ int gkb_op_bench(gkb_op* op, int which, int iters, int flush_l2, double* ms_per_
     std::vector<double*> yi(L), zi(L);
     for (int i = 0; i < L; ++i) {
       c.set_device(i);
-      GKB_CUDA(cudaMemcpy(d->xbuf[i], xh.data(), sizeof(double) * (size_t)d->n,
-                          cudaMemcpyHostToDevice));
+      gkb::Shard& s = c.shards[i];
+      GKB_CUDA(cudaMemcpyAsync(d->xbuf[i], xh.data(), sizeof(double) * (size_t)d->n,
+                               cudaMemcpyHostToDevice, s.stream));
       xi[i] = d->xbuf[i];
       yi[i] = d->ybuf[i];
       yc[i] = d->ybuf[i];
       zi[i] = d->zbuf[i];
-      gkb::Shard& s = c.shards[i];
       if (flush_l2 && !s.flush_buf) {
         s.flush_bytes = (size_t)256 << 20;  // 2x the 126 MB L2
         GKB_CUDA(cudaMalloc(&s.flush_buf, s.flush_bytes));
@@ -414,8 +414,8 @@ int gkb_op_bench(gkb_op* op, int which, int iters, int flush_l2, double* ms_per_
       GKB_CUDA(cudaMalloc(&Y2, sizeof(double) * (size_t)(2 * std::max<int64_t>(d->m, 1))));
       GKB_CUDA(cudaMalloc(&Z2, sizeof(double) * (size_t)(2 * d->n)));
       for (int q = 0; q < 2; ++q)
-        GKB_CUDA(cudaMemcpy(X2 + q * d->n, xh.data(), sizeof(double) * (size_t)d->n,
-                            cudaMemcpyHostToDevice));
+        GKB_CUDA(cudaMemcpyAsync(X2 + q * d->n, xh.data(), sizeof(double) * (size_t)d->n,
+                                 cudaMemcpyHostToDevice, c.shards[0].stream));
     }
     // whole step: K1 (+reduce) and/or K2 (+reduce, +cross-shard sum)
     const double total = timed([&] {
@@ -696,8 +696,10 @@ int gkb_cgs2(gkb_ctx* ctx, const double* basis, int64_t len, int64_t ncols, doub
     double* Q = Qh.as<double>();
     double* dv = dvh.as<double>();
     if (ncols > 0)
-      GKB_CUDA(cudaMemcpy(Q, basis, sizeof(double) * (size_t)(len * ncols), cudaMemcpyHostToDevice));
-    GKB_CUDA(cudaMemcpy(dv, v, sizeof(double) * (size_t)len, cudaMemcpyHostToDevice));
+      GKB_CUDA(cudaMemcpyAsync(Q, basis, sizeof(double) * (size_t)(len * ncols),
+                               cudaMemcpyHostToDevice, s.stream));
+    GKB_CUDA(cudaMemcpyAsync(dv, v, sizeof(double) * (size_t)len, cudaMemcpyHostToDevice,
+                             s.stream));
     s.ensure_partial(gkb::dev::red_blocks(len) * (ncols + 4) + 64);
     const double eta = 0.70710678118654752440;
     double na;
@@ -730,7 +732,9 @@ int gkb_cgs2(gkb_ctx* ctx, const double* basis, int64_t len, int64_t ncols, doub
       }
     }
     GKB_LAUNCH_CHECK();
-    GKB_CUDA(cudaMemcpy(v, dv, sizeof(double) * (size_t)len, cudaMemcpyDeviceToHost));
+    GKB_CUDA(cudaMemcpyAsync(v, dv, sizeof(double) * (size_t)len, cudaMemcpyDeviceToHost,
+                             s.stream));
+    GKB_CUDA(cudaStreamSynchronize(s.stream));
     if (coeffs)
       for (int64_t i = 0; i < ncols; ++i) coeffs[i] += cf[i];
     if (norm_after) *norm_after = na;

@@ -1123,7 +1123,9 @@ void Lanczos::get(double* U, double* V, double* B, double* coupling, double* om_
   if (U) gather_left(ctx_, op_, U_, j, U);
   if (V) {
     ctx_->set_device(0);
-    GKB_CUDA(cudaMemcpy(V, V_[0], sizeof(double) * (size_t)(n_ * (j + 1)), cudaMemcpyDeviceToHost));
+    GKB_CUDA(cudaMemcpyAsync(V, V_[0], sizeof(double) * (size_t)(n_ * (j + 1)),
+                             cudaMemcpyDeviceToHost, ctx_->shards[0].stream));
+    GKB_CUDA(cudaStreamSynchronize(ctx_->shards[0].stream));
   }
   if (B)
     for (int64_t c = 0; c < j; ++c)

@@ -753,20 +753,23 @@ void GenoOp::build_from_synth(const dev::SynthDev& sp_in, const gkb_synth_spec* 
     double* dadmix = nullptr;
     int32_t* dcopy = nullptr;
     GKB_CUDA(cudaMalloc(&dfreq, sizeof(double) * (size_t)(spec->npop * p)));
-    GKB_CUDA(cudaMemcpy(dfreq, spec->freq, sizeof(double) * (size_t)(spec->npop * p),
-                        cudaMemcpyHostToDevice));
+    // stream-ordered copies: a synchronous cudaMemcpy from pageable memory may
+    // return before its DMA lands, and the shard stream does not wait for it
+    GKB_CUDA(cudaMemcpyAsync(dfreq, spec->freq, sizeof(double) * (size_t)(spec->npop * p),
+                             cudaMemcpyHostToDevice, sh.stream));
     if (spec->pop) {
       GKB_CUDA(cudaMalloc(&dpop, sizeof(int32_t) * (size_t)nn));
-      GKB_CUDA(cudaMemcpy(dpop, spec->pop, sizeof(int32_t) * (size_t)nn, cudaMemcpyHostToDevice));
+      GKB_CUDA(cudaMemcpyAsync(dpop, spec->pop, sizeof(int32_t) * (size_t)nn,
+                               cudaMemcpyHostToDevice, sh.stream));
     } else {
       GKB_CUDA(cudaMalloc(&dadmix, sizeof(double) * (size_t)(nn * spec->npop)));
-      GKB_CUDA(cudaMemcpy(dadmix, spec->admix, sizeof(double) * (size_t)(nn * spec->npop),
-                          cudaMemcpyHostToDevice));
+      GKB_CUDA(cudaMemcpyAsync(dadmix, spec->admix, sizeof(double) * (size_t)(nn * spec->npop),
+                               cudaMemcpyHostToDevice, sh.stream));
     }
     if (spec->copy_from) {
       GKB_CUDA(cudaMalloc(&dcopy, sizeof(int32_t) * (size_t)nn));
-      GKB_CUDA(cudaMemcpy(dcopy, spec->copy_from, sizeof(int32_t) * (size_t)nn,
-                          cudaMemcpyHostToDevice));
+      GKB_CUDA(cudaMemcpyAsync(dcopy, spec->copy_from, sizeof(int32_t) * (size_t)nn,
+                               cudaMemcpyHostToDevice, sh.stream));
     }
     dev::SynthDev sd{p, nn, spec->seed, spec->npop, dfreq, dpop, dadmix, spec->missing_rate, dcopy,
                      spec->copy_prob};
@@ -877,7 +880,11 @@ void GenoOp::finish_build() {
     std::vector<double> hc(counts_host.begin(), counts_host.end());
     double* dc = nullptr;
     GKB_CUDA(cudaMalloc(&dc, sizeof(double) * hc.size()));
-    GKB_CUDA(cudaMemcpy(dc, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice));
+    // stream-ordered: a synchronous cudaMemcpy from pageable memory may return
+    // before its DMA lands, and the allreduce on the shard stream (a
+    // non-blocking stream) would read stale counts
+    GKB_CUDA(cudaMemcpyAsync(dc, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice,
+                             s.stream));
     ctx->allreduce({dc}, (int64_t)hc.size());
     GKB_CUDA(cudaMemcpyAsync(hc.data(), dc, sizeof(double) * hc.size(), cudaMemcpyDeviceToHost,
                              s.stream));
