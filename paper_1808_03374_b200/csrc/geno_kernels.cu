@@ -901,25 +901,39 @@ __device__ __forceinline__ uint2 ld_stream8(const uint2* p) {
   return v;
 }
 
-// one tile: words w (SNPs 2t, 2t+8 of word-column g) and v (SNPs 2t+1, 2t+9)
-__device__ __forceinline__ void mma_tile_l1t(int (&acc)[8][4], const uint2 w, const uint2 v,
-                                             const uint32_t bd) {
+// two strips (A, B) of one tile column: per strip, words w (SNPs 2t, 2t+8 of
+// word-column g) and v (SNPs 2t+1, 2t+9); strip A is the MMA's k-group t and
+// strip B the k-group 4 + t of mma.m16n8k32 (bd: digit g of both)
+__device__ __forceinline__ void l1t_transpose(const uint2 w, const uint2 v, uint32_t (&z)[4]) {
   // k order i = 0..3 <-> SNPs 2t, 2t+1, 2t+8, 2t+9 (k_digitize<2>'s positions)
   const uint32_t t0 = prmt(w.x, v.x, 0x5140u), t1 = prmt(w.x, v.x, 0x7362u);
   const uint32_t t2 = prmt(w.y, v.y, 0x5140u), t3 = prmt(w.y, v.y, 0x7362u);
-  const uint32_t z[4] = {prmt(t0, t2, 0x5410u), prmt(t0, t2, 0x7632u), prmt(t1, t3, 0x5410u),
-                         prmt(t1, t3, 0x7632u)};
+  z[0] = prmt(t0, t2, 0x5410u);
+  z[1] = prmt(t0, t2, 0x7632u);
+  z[2] = prmt(t1, t3, 0x5410u);
+  z[3] = prmt(t1, t3, 0x7632u);
+}
+__device__ __forceinline__ void mma_tile_l1t(int (&acc)[8][4], const uint2 wa, const uint2 va,
+                                             const uint2 wb, const uint2 vb, const uint32_t bda,
+                                             const uint32_t bdb) {
+  uint32_t za[4], zb[4];
+  l1t_transpose(wa, va, za);
+  l1t_transpose(wb, vb, zb);
   const uint32_t m0 = 0x03030303u, m1 = m0 << 2, m2 = m0 << 4, m3 = m0 << 6;
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    mma16_u8s8(acc[2 * b], z[b] & m0, z[b] & m1, bd);      // samples 4b, 4b+1 (x1, x4)
-    mma16_u8s8(acc[2 * b + 1], z[b] & m2, z[b] & m3, bd);  // samples 4b+2, 4b+3 (x16, x64)
+    // samples 4b, 4b+1 (x1, x4) and 4b+2, 4b+3 (x16, x64); rows g / g + 8
+    mma_u8s8(acc[2 * b], za[b] & m0, za[b] & m1, zb[b] & m0, zb[b] & m1, bda, bdb);
+    mma_u8s8(acc[2 * b + 1], za[b] & m2, za[b] & m3, zb[b] & m2, zb[b] & m3, bda, bdb);
   }
 }
 
 // grid (sample blocks, SNP ranges). Writes part[kc][sample] = the range's
 // exact partial of z_s = sum_j c_j a_js - sum_j c_j mu_j - sum_{j miss} cm_j.
-__global__ void __launch_bounds__(kThreads, 3) k_pm_adj_l1(
+#ifndef GKB_L1T_MINB
+#define GKB_L1T_MINB 2  // CTAs per SM (register budget of the strip-pair loop)
+#endif
+__global__ void __launch_bounds__(kThreads, GKB_L1T_MINB) k_pm_adj_l1(
     const uint32_t* __restrict__ lay, int64_t KT, int64_t S1, const uint32_t* __restrict__ dig,
     const int* __restrict__ dexp, const double* __restrict__ dsum,
     const double* __restrict__ cval, const uint32_t* __restrict__ m_off,
@@ -947,11 +961,28 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_adj_l1(
 #pragma unroll
   for (int m = 0; m < 8; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0;
   const uint2 Z = make_uint2(0, 0);
-  uint2 wA = ns > 0 ? ld_stream8(pw) : Z, vA = ns > 0 ? ld_stream8(pw + (o2 - o1)) : Z;
-  uint2 wB = ns > 1 ? ld_stream8(pw + sstride) : Z,
-        vB = ns > 1 ? ld_stream8(pw + sstride + (o2 - o1)) : Z;
-  uint2 wC = Z, vC = Z;
-  const uint2* nx = pw + sstride * min(2, max(ns - 1, 0));
+  // strip pairs (s, s + 1): a pair's second strip beyond the layout rereads
+  // the first (its digits are zero: rows >= p_loc)
+  const int np = (ns + 1) / 2;
+  const int64_t d12 = o2 - o1;
+  auto pair_ptr = [&](int q) { return pw + sstride * (2 * (int64_t)q); };
+  auto second = [&](int q) { return 2 * q + 1 < ns ? sstride : 0; };
+  uint2 aw0 = Z, av0 = Z, bw0 = Z, bv0 = Z, aw1 = Z, av1 = Z, bw1 = Z, bv1 = Z;
+  if (np > 0) {
+    const uint2* p = pair_ptr(0);
+    aw0 = ld_stream8(p);
+    av0 = ld_stream8(p + d12);
+    bw0 = ld_stream8(p + second(0));
+    bv0 = ld_stream8(p + second(0) + d12);
+  }
+  if (np > 1) {
+    const uint2* p = pair_ptr(1);
+    aw1 = ld_stream8(p);
+    av1 = ld_stream8(p + d12);
+    bw1 = ld_stream8(p + second(1));
+    bv1 = ld_stream8(p + second(1) + d12);
+  }
+  uint2 aw2 = Z, av2 = Z, bw2 = Z, bv2 = Z;
   pdl_trigger();
   __shared__ __align__(8) uint64_t sbar[2];
   if (threadIdx.x == 0) {
@@ -997,19 +1028,24 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_adj_l1(
   __syncthreads();  // the mbarriers' init
   mbar_wait(&sbar[0], 0);
   const uint32_t* bq = dgs + g * 4 + t;  // digit g of the lane's k-group, strip by strip
-#define GKB_L1T_STEP(CW, CV, DW, DV)                                       \
-  if (s < ns) {                                                            \
-    const uint32_t bd = bq[32 * s];                                        \
-    DW = ld_stream8(nx);                                                   \
-    DV = ld_stream8(nx + (o2 - o1));                                       \
-    nx += (s + 2 < ns - 1) ? sstride : 0;                                  \
-    mma_tile_l1t(acc, CW, CV, bd);                                         \
-    ++s;                                                                   \
+  // pair q in buffer (q mod 3); pair q + 2 prefetched into the buffer of q - 1
+#define GKB_L1T_STEP(AW, AV, BW, BV, NAW, NAV, NBW, NBV)                   \
+  if (q < np) {                                                            \
+    const uint32_t bda = bq[64 * q], bdb = bq[64 * q + 32];                \
+    if (q + 2 < np) {                                                      \
+      const uint2* p = pair_ptr(q + 2);                                    \
+      NAW = ld_stream8(p);                                                 \
+      NAV = ld_stream8(p + d12);                                           \
+      NBW = ld_stream8(p + second(q + 2));                                 \
+      NBV = ld_stream8(p + second(q + 2) + d12);                           \
+    }                                                                      \
+    mma_tile_l1t(acc, AW, AV, BW, BV, bda, bdb);                           \
+    ++q;                                                                   \
   }
-  for (int s = 0; s < ns;) {
-    GKB_L1T_STEP(wA, vA, wC, vC)
-    GKB_L1T_STEP(wB, vB, wA, vA)
-    GKB_L1T_STEP(wC, vC, wB, vB)
+  for (int q = 0; q < np;) {
+    GKB_L1T_STEP(aw0, av0, bw0, bv0, aw2, av2, bw2, bv2)
+    GKB_L1T_STEP(aw1, av1, bw1, bv1, aw0, av0, bw0, bv0)
+    GKB_L1T_STEP(aw2, av2, bw2, bv2, aw1, av1, bw1, bv1)
   }
 #undef GKB_L1T_STEP
   mbar_wait(&sbar[1], 0);  // offsets, list run, cm values
