@@ -1550,6 +1550,293 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
   }
 }
 
+// ---------------------------------------------------------------- tcgen05 block products
+// Block products of k >= 3 coefficient vectors in ONE pass over the layout
+// (VERDICT r1 item 9): the 5th-generation tensor cores (tcgen05.mma
+// kind::i8, SASS UTCIMMA) with the accumulators in tensor memory. CTA = 256
+// rows (two M = 128 accumulators) x one column range (kt_cta tiles); per
+// tile the 8 warps expand their strips' 2-bit codes AND missing indicators
+// (w & (w >> 1) & 0x55..) to u8 in shared memory (the shift-free masks, one
+// 16-byte K chunk per word, canonical K-major no-swizzle layout), one thread
+// bulk-copies the tile's B image (digits of all k vectors: N = 8k rows) and
+// issues 16 MMAs (4 K-steps x codes / indicators x two row halves),
+// committed to the buffer's "empty" mbarrier (2 buffers). TMEM columns:
+// [0, N) codes rows 0-127, [N, 2N) codes rows 128-255, [2N, 3N) and
+// [3N, 4N) the indicators. The missing corrections are exact integer sums
+// (no lists): K1 (MODE 0) multiplies the indicators with the same digits
+// (sum_{s miss} x_s); K2 (MODE 1) with the digits of cm_j = c_j (3 - m_j)
+// (a second B image). Epilogue: tcgen05.ld per row; the row value is
+// sum_i D_i 256^i 2^(E - 62) as in the mma.sync kernels.
+constexpr int kTcRows = 256;
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // sm_100 descriptor version; no swizzle, base offset 0
+  return d;
+}
+__device__ __forceinline__ void umma_i8(uint32_t dt, uint64_t da, uint64_t db, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+
+// smem A image of one row half (128 rows x 8 chunks of 16 B): canonical
+// K-major, core matrix (rows 8a..8a+7, chunk c) at a * 1024 + c * 128
+__device__ __forceinline__ uint32_t tc_a_off(int r, int c) {
+  return (uint32_t)((r >> 3) * 1024 + c * 128 + (r & 7) * 16);
+}
+
+size_t tc_smem_bytes(int k, int mode) {
+  const size_t N = 8 * (size_t)k;
+  // 2 buffers x (codes + indicators (2 x 32 KB) + B image(s) N x 128 B)
+  return 2 * (2 * 32768 + N * 128 * (mode ? 2 : 1)) + 1024;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_pm_blk_tc(
+    const uint4* __restrict__ lay, int64_t KT, int kt_cta, int k,
+    const uint8_t* __restrict__ tdig, const uint8_t* __restrict__ tdig2,
+    const int* __restrict__ dexp, const int* __restrict__ dexp2, const double* __restrict__ dsum,
+    const double* __restrict__ mu, const double* __restrict__ mean, int64_t rows_pad, int nkc,
+    double* __restrict__ part) {
+  extern __shared__ __align__(1024) uint8_t tsm[];
+  const int N = 8 * k;
+  const uint32_t bimg = (uint32_t)N * 128u;  // B image bytes per tile
+  // buffer layout: [codes h0 | codes h1 | ind h0 | ind h1] (16 KB each), B [, B2]
+  const uint32_t bufsz = 65536u + bimg * (MODE ? 2u : 1u);
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm) + 1023) &
+                                             ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t fullb[2], emptyb[2], doneb;
+  __shared__ uint32_t tbase;
+  const int kc = blockIdx.y, bx = blockIdx.x;
+  const int64_t kt0 = (int64_t)kc * kt_cta;
+  const int ktiles = (int)min((int64_t)kt_cta, KT - kt0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tid = lane & 3;
+  const int64_t strip0 = ((int64_t)bx * 8 + warp) * 2;  // this warp's two strips
+  const uint4* src0 = lay + (strip0 * KT + kt0) * 32 + lane;
+  const uint4* src1 = src0 + KT * 32;
+  uint32_t ncols = 32;
+  while (ncols < 4u * (uint32_t)N) ncols <<= 1;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&fullb[b], 8 + 1);  // 8 warps' A stores + the B bulk copy's arrival
+      mbar_init(&emptyb[b], 1);     // the MMA commit
+    }
+    mbar_init(&doneb, 1);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tbase)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tbase;
+  pdl_wait();  // the digits are the predecessor's output
+  // kind::i8 instruction descriptor: D s32, A u8, B s8, K-major, N, M = 128
+  const uint32_t idesc = (2u << 4) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+  const uint32_t m0 = 0x03030303u, m1 = m0 << 2, m2 = m0 << 4, m3 = m0 << 6;
+  uint4 w0 = ktiles > 0 ? ld_stream(src0) : make_uint4(0, 0, 0, 0);
+  uint4 w1 = ktiles > 0 ? ld_stream(src1) : make_uint4(0, 0, 0, 0);
+  const int half = warp >> 2;                       // rows 0-127 / 128-255
+  const int r0 = (warp & 3) * 32;                   // this warp's first row in its half
+  for (int t = 0; t < ktiles; ++t) {
+    const int b = t & 1;
+    uint8_t* buf = base + (size_t)b * bufsz;
+    // the MMAs of tile t - 2 must have released this buffer
+    if (t >= 2) mbar_wait(&emptyb[b], (uint32_t)(((t >> 1) - 1) & 1));
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&fullb[b], bimg * (MODE ? 2u : 1u));
+      const size_t toff = ((size_t)kc * kt_cta + t) * bimg;
+      bulk_g2s(buf + 65536, tdig + toff, bimg, &fullb[b]);
+      if (MODE) bulk_g2s(buf + 65536 + bimg, tdig2 + toff, bimg, &fullb[b]);
+    }
+    const uint4 c0 = w0, c1 = w1;
+    if (t + 1 < ktiles) {  // next tile's words while this one is expanded
+      w0 = ld_stream(src0 + 32 * (t + 1));
+      w1 = ld_stream(src1 + 32 * (t + 1));
+    }
+    // lane (g, tid) holds words (row g, col tid), (g + 8, tid), (g, tid + 4),
+    // (g + 8, tid + 4) of each strip; one 16-byte K chunk per word
+#pragma unroll
+    for (int sidx = 0; sidx < 2; ++sidx) {
+      const uint4 w = sidx ? c1 : c0;
+      const int rb = r0 + 16 * sidx + g;
+      const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = rb + 8 * (j & 1), c = tid + 4 * (j >> 1);
+        const uint32_t x = words[j];
+        const uint32_t mi = x & (x >> 1) & 0x55555555u;
+        const uint32_t off = tc_a_off(r, c);
+        *reinterpret_cast<uint4*>(buf + half * 16384 + off) =
+            make_uint4(x & m0, x & m1, x & m2, x & m3);
+        *reinterpret_cast<uint4*>(buf + 32768 + half * 16384 + off) =
+            make_uint4(mi & m0, mi & m1, mi & m2, mi & m3);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // STS -> tensor core reads
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&fullb[b]);
+    if (threadIdx.x == 0) {
+      mbar_wait(&fullb[b], (uint32_t)((t >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t sa = smem_u32(buf), sb = sa + 65536, sb2 = sb + (MODE ? bimg : 0u);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
+        const uint64_t db = umma_desc(sb + ks * 256, 128, 1024);
+        const uint64_t dbm = umma_desc(sb2 + ks * 256, 128, 1024);
+        umma_i8(tmem, umma_desc(sa + ks * 256, 128, 1024), db, idesc, acc);
+        umma_i8(tmem + (uint32_t)N, umma_desc(sa + 16384 + ks * 256, 128, 1024), db, idesc, acc);
+        umma_i8(tmem + 2u * (uint32_t)N, umma_desc(sa + 32768 + ks * 256, 128, 1024), dbm, idesc,
+                acc);
+        umma_i8(tmem + 3u * (uint32_t)N, umma_desc(sa + 49152 + ks * 256, 128, 1024), dbm, idesc,
+                acc);
+      }
+      umma_commit(&emptyb[b]);
+    }
+  }
+  if (threadIdx.x == 0) umma_commit(&doneb);  // every MMA issued so far
+  mbar_wait(&doneb, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // epilogue: warp w reads TMEM lanes 32 (w & 3) .. + 31 of its half
+  const int row_l = r0 + lane;                         // row within the half
+  const int64_t row = (int64_t)bx * kTcRows + half * 128 + row_l;
+  const uint32_t lanebase = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+  const double rmu = MODE == 0 ? mu[row] : 0.0, rmean = MODE == 0 ? mean[row] : 0.0;
+  for (int v = 0; v < k; ++v) {
+    uint32_t dc[8], dm[8];
+    tmem_ld8(lanebase + (uint32_t)(half * N + 8 * v), dc);
+    tmem_ld8(lanebase + (uint32_t)(2 * N + half * N + 8 * v), dm);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    // sum_i D_i 256^i in the mma.sync kernels' association: per 16-bit pair
+    // exact, pairs added in digit order
+    double vc = 0.0, vm = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      vc += ((double)(int)dc[2 * i] + 256.0 * (double)(int)dc[2 * i + 1]) * pow2(16 * i);
+      vm += ((double)(int)dm[2 * i] + 256.0 * (double)(int)dm[2 * i + 1]) * pow2(16 * i);
+    }
+    const int E = dexp[(int64_t)v * nkc + kc];
+    const double val = scale2(vc, E - 62);
+    double out;
+    if (MODE == 0) {
+      const double cor = scale2(vm, E - 62);
+      out = val - rmu * dsum[(int64_t)v * nkc + kc] - (3.0 - rmean) * cor;
+    } else {
+      const double cor = scale2(vm, dexp2[(int64_t)v * nkc + kc] - 62);
+      out = val - dsum[(int64_t)v * nkc + kc] - cor;
+    }
+    part[((int64_t)v * nkc + kc) * rows_pad + row] = out;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols)
+                 : "memory");
+}
+
+// Digits of k vectors for k_pm_blk_tc, one CTA per (range, vector): the B
+// image of each tile (N = 8k rows x 128 K bytes, canonical K-major): row
+// 8v + i, chunk wc (the tile's word column), byte 4q + e <-> column
+// 16 wc + 4e + q (the shift-free masks' byte order) with the 4^-q group
+// prescale. MODE 0: v = x; MODE 1: v = inv_s y (dsum = sum v mu), and the
+// digits of cm = v (3 - mean) into dig2 (exponent dexp2).
+template <int MODE>
+__global__ void __launch_bounds__(1024) k_digitize_tc(const double* __restrict__ X, int64_t ldx,
+                                                      int k, const double* __restrict__ inv_s,
+                                                      const double* __restrict__ mu,
+                                                      const double* __restrict__ mean, int64_t C,
+                                                      int kt_cta, uint8_t* __restrict__ dig,
+                                                      uint8_t* __restrict__ dig2,
+                                                      int* __restrict__ dexp,
+                                                      int* __restrict__ dexp2,
+                                                      double* __restrict__ dsum) {
+  __shared__ double red[33];
+  __shared__ int redi[33];
+  pdl_wait();
+  pdl_trigger();
+  const int kc = blockIdx.x, v = blockIdx.y, nkc = gridDim.x;
+  const int N = 8 * k;
+  const int ncol = kt_cta * 128;
+  const int64_t c0 = (int64_t)kc * ncol;
+  const double* xin = X + (int64_t)v * ldx;
+  int emax = -1100, emax2 = -1100;
+  double psum = 0.0;
+  for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
+    const int64_t c = c0 + t;
+    if (c < C) {
+      double val = xin[c];
+      if (MODE == 1) {
+        val = inv_s[c] * val;
+        psum += val * mu[c];
+        emax2 = max(emax2, exp_of(val * (3.0 - mean[c])));
+      } else {
+        psum += val;
+      }
+      emax = max(emax, exp_of(val));
+    }
+  }
+  const int E = block_max_int(emax, redi);
+  const int E2 = MODE ? block_max_int(emax2, redi) : 0;
+  const double sm = block_sum(psum, red);
+  for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
+    const int64_t c = c0 + t;
+    double val = 0.0, cmv = 0.0;
+    if (c < C) {
+      val = xin[c];
+      if (MODE == 1) {
+        val = inv_s[c] * val;
+        cmv = val * (3.0 - mean[c]);
+      }
+    }
+    const int tile = t >> 7, wc = (t >> 4) & 7, k16 = t & 15, q = k16 & 3, e = k16 >> 2;
+    const size_t off = ((size_t)kc * kt_cta + tile) * (size_t)N * 128 + (size_t)v * 1024 +
+                       (size_t)wc * 128 + 4 * q + e;
+    long long M = __double2ll_rn(scale2(val, 62 - E - 2 * q));
+    long long M2 = MODE ? __double2ll_rn(scale2(cmv, 62 - E2 - 2 * q)) : 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int d = (int)(signed char)(M & 0xFF);
+      M = (M - d) >> 8;
+      dig[off + i * 16] = (uint8_t)d;
+      if (MODE) {
+        const int d2 = (int)(signed char)(M2 & 0xFF);
+        M2 = (M2 - d2) >> 8;
+        dig2[off + i * 16] = (uint8_t)d2;
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    dexp[(int64_t)v * nkc + kc] = E;
+    dsum[(int64_t)v * nkc + kc] = sm;
+    if (MODE) dexp2[(int64_t)v * nkc + kc] = E2;
+  }
+}
+
 // ---------------------------------------------------------------- marker scan
 // Per-marker fits y ~ [1, m_i, Z] (regress.cpp:10-65 per marker, by
 // Frisch-Waugh-Lovell -- paper_1808_03374_b200/regress.py): one thread per
@@ -1890,6 +2177,56 @@ void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s, c
   }
   launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
              (const double*)g.s2.part, g.pl2.nkc, g.pl2.rows_pad, g.n, z);
+}
+
+// ---- tcgen05 block products ------------------------------------------------
+size_t tc_dig_bytes(const PMPlan& pl, int kmax) {
+  return (size_t)pl.nkc * pl.kt_cta * (size_t)(8 * kmax) * 128;
+}
+
+namespace {
+template <int MODE>
+void launch_tc(const GenoView& g, const PMPlan& pl, const uint4* lay, const TcScratch& t, int k,
+               cudaStream_t s) {
+  const size_t smem = tc_smem_bytes(k, MODE);
+  allow_smem(k_pm_blk_tc<MODE>, smem);
+  launch_pdl(k_pm_blk_tc<MODE>, dim3((unsigned)pl.grid_x, (unsigned)pl.nkc), dim3(kThreads), smem,
+             s, true, lay, pl.KT, pl.kt_cta, k, (const uint8_t*)t.dig, (const uint8_t*)t.dig2,
+             (const int*)t.dexp, (const int*)t.dexp2, (const double*)t.dsum, (const double*)g.mu,
+             (const double*)g.mean, pl.rows_pad, pl.nkc, t.part);
+}
+}  // namespace
+
+void k1_apply_tc(const GenoView& g, const TcScratch& t, const double* X, int64_t ldx, int k,
+                 double* Y, int64_t ldy, cudaStream_t s) {
+  if (g.p_loc == 0 || k <= 0) return;
+  const PMPlan& pl = g.pl1;
+  launch_pdl(k_digitize_tc<0>, dim3((unsigned)pl.nkc, (unsigned)k), dim3(1024), 0, s, true, X, ldx,
+             k, (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, g.n,
+             pl.kt_cta, t.dig, (uint8_t*)nullptr, t.dexp, (int*)nullptr, t.dsum);
+  launch_tc<0>(g, pl, g.lt1, t, k, s);
+  for (int v = 0; v < k; ++v)
+    launch_pdl(k1_reduce, dim3((unsigned)((g.p_loc + 255) / 256)), dim3(256), 0, s, true,
+               (const double*)(t.part + (size_t)v * pl.nkc * pl.rows_pad), pl.nkc, pl.rows_pad,
+               g.p_loc, (const double*)g.inv_s, Y + (size_t)v * ldy);
+}
+
+void k2_adjoint_tc(const GenoView& g, const TcScratch& t, const double* Yin, int64_t ldy, int k,
+                   double* Z, int64_t ldz, cudaStream_t s) {
+  if (g.n == 0 || k <= 0) return;
+  if (g.p_loc == 0) {
+    for (int v = 0; v < k; ++v) cudaMemsetAsync(Z + (size_t)v * ldz, 0, sizeof(double) * g.n, s);
+    return;
+  }
+  const PMPlan& pl = g.pl2;
+  launch_pdl(k_digitize_tc<1>, dim3((unsigned)pl.nkc, (unsigned)k), dim3(1024), 0, s, true, Yin,
+             ldy, k, (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc,
+             pl.kt_cta, t.dig, t.dig2, t.dexp, t.dexp2, t.dsum);
+  launch_tc<1>(g, pl, g.lt2, t, k, s);
+  for (int v = 0; v < k; ++v)
+    launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
+               (const double*)(t.part + (size_t)v * pl.nkc * pl.rows_pad), pl.nkc, pl.rows_pad,
+               g.n, Z + (size_t)v * ldz);
 }
 
 // ---- two vectors per pass (block products) ------------------------------

@@ -219,6 +219,7 @@ struct GenoShard {
   // by plan_layouts (GKB_LAYOUTS=1|2 forces)
   bool single = false;
   dev::L1TPlan plt{};
+  dev::TcScratch tc1{}, tc2{};  // tcgen05 block products (lazily, k_pm_blk_tc)
   dev::GenoView view() const;
 };
 

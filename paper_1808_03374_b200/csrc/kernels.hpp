@@ -71,6 +71,25 @@ struct GenoView {
   bool single = false;
   int64_t l1t_grid = 0, l1t_nkc = 0, l1t_rows_pad = 0;
 };
+// tcgen05 block products (k_pm_blk_tc): digits of up to kmax vectors in the
+// tcgen05 B-image layout, exponents / sums per (vector, range), partials.
+struct TcScratch {
+  int kmax = 0;
+  uint8_t* dig = nullptr;   // nkc * kt_cta tiles x (8 kmax) rows x 128 B
+  uint8_t* dig2 = nullptr;  // K2: digits of cm
+  int* dexp = nullptr;      // kmax * nkc
+  int* dexp2 = nullptr;
+  double* dsum = nullptr;   // kmax * nkc
+  double* part = nullptr;   // kmax * nkc * rows_pad
+};
+// Y[:, v] = X_loc X[:, v] (K1) / Z[:, v] = X_loc^T Y[:, v] (K2, local partial
+// sums) for v < k <= 16, one pass over the layout.
+void k1_apply_tc(const GenoView& g, const TcScratch& t, const double* X, int64_t ldx, int k,
+                 double* Y, int64_t ldy, cudaStream_t s);
+void k2_adjoint_tc(const GenoView& g, const TcScratch& t, const double* Yin, int64_t ldy, int k,
+                   double* Z, int64_t ldz, cudaStream_t s);
+size_t tc_dig_bytes(const PMPlan& pl, int kmax);
+
 // single-layout K2 geometry of a shard (p_loc SNPs x n samples)
 struct L1TPlan {
   int64_t grid_x, nkc, rows_pad;

@@ -459,6 +459,11 @@ GenoOp::~GenoOp() {
     free_scratch(g.s1b, st);
     free_scratch(g.s2b, st);
     free_scratch(g.s2m, st);
+    for (dev::TcScratch* t : {&g.tc1, &g.tc2}) {
+      void* tp[] = {t->dig, t->dig2, t->dexp, t->dexp2, t->dsum, t->part};
+      for (void* p : tp)
+        if (p) cudaFreeAsync(p, st);
+    }
     cudaStreamSynchronize(st);
   }
 }
@@ -975,9 +980,51 @@ void GenoOp::apply_dev(const std::vector<const double*>& x, const std::vector<do
 
 // Column pairs through the two-vector kernel (each column bitwise the
 // single-vector product); an odd last column goes alone.
+// tcgen05 block products for k >= 3 columns (GKB_TC_BLOCK=0 disables): both
+// layouts present, lists not required (exact indicator MMAs)
+static bool use_tc_block(const GenoShard& g, int64_t k) {
+  const char* e = std::getenv("GKB_TC_BLOCK");
+  const bool off = e && std::strcmp(e, "0") == 0;
+  return !off && k >= 3 && !g.single;
+}
+
+static void ensure_tc(dev::TcScratch& t, const dev::PMPlan& pl, int kmax, bool k2,
+                      cudaStream_t st) {
+  if (t.kmax >= kmax) return;
+  void* ptrs[] = {t.dig, t.dig2, t.dexp, t.dexp2, t.dsum, t.part};
+  for (void* p : ptrs)
+    if (p) cudaFreeAsync(p, st);
+  t = dev::TcScratch{};
+  auto pool = [&](auto** ptr, size_t bytes) {
+    GKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, st));
+  };
+  pool(&t.dig, dev::tc_dig_bytes(pl, kmax));
+  if (k2) pool(&t.dig2, dev::tc_dig_bytes(pl, kmax));
+  pool(&t.dexp, sizeof(int) * (size_t)(kmax * pl.nkc));
+  if (k2) pool(&t.dexp2, sizeof(int) * (size_t)(kmax * pl.nkc));
+  pool(&t.dsum, sizeof(double) * (size_t)(kmax * pl.nkc));
+  pool(&t.part, sizeof(double) * (size_t)kmax * (size_t)pl.nkc * (size_t)pl.rows_pad);
+  t.kmax = kmax;
+}
+
 void GenoOp::apply_block_dev(const std::vector<const double*>& X, int64_t ldx, int64_t k,
                              const std::vector<double*>& Y, const std::vector<int64_t>& ldy) {
   if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
+  if (use_tc_block(gs[0], k)) {
+    for (int64_t c0 = 0; c0 < k; c0 += 16) {
+      const int kk = (int)std::min<int64_t>(16, k - c0);
+      for (size_t i = 0; i < gs.size(); ++i) {
+        ctx->set_device((int)i);
+        GenoShard& g = gs[i];
+        cudaStream_t st = ctx->shards[i].stream;
+        ensure_tc(g.tc1, g.pl1, std::max(kk, (int)std::min<int64_t>(k, 16)), false, st);
+        dev::k1_apply_tc(g.view(), g.tc1, X[i] + c0 * ldx, ldx, kk, Y[i] + c0 * ldy[i], ldy[i],
+                         st);
+        GKB_LAUNCH_CHECK();
+      }
+    }
+    return;
+  }
   int64_t c = 0;
   for (; c + 2 <= k; c += 2)
     for (size_t i = 0; i < gs.size(); ++i) {
@@ -1006,6 +1053,26 @@ void GenoOp::adjoint_block_dev(const std::vector<const double*>& Yb,
                                const std::vector<double*>& Z, int64_t ldz) {
   if (!scaled) fail(GKB_ELOGIC, "genotype operator: scaling not set (call standardize)");
   const int L = (int)gs.size();
+  if (use_tc_block(gs[0], k)) {
+    for (int64_t c0 = 0; c0 < k; c0 += 16) {
+      const int kk = (int)std::min<int64_t>(16, k - c0);
+      for (int i = 0; i < L; ++i) {
+        ctx->set_device(i);
+        GenoShard& g = gs[i];
+        cudaStream_t st = ctx->shards[i].stream;
+        ensure_tc(g.tc2, g.pl2, std::max(kk, (int)std::min<int64_t>(k, 16)), true, st);
+        dev::k2_adjoint_tc(g.view(), g.tc2, Yb[i] + c0 * ldyb[i], ldyb[i], kk, Z[i] + c0 * ldz,
+                           ldz, st);
+        GKB_LAUNCH_CHECK();
+      }
+      for (int64_t q = c0; q < c0 + kk; ++q) {  // cross-shard sums, column by column
+        std::vector<double*> zq(L);
+        for (int i = 0; i < L; ++i) zq[i] = Z[i] + q * ldz;
+        ctx->allreduce(zq, n);
+      }
+    }
+    return;
+  }
   int64_t c = 0;
   for (; c + 2 <= k; c += 2) {
     for (int i = 0; i < L; ++i) {

@@ -183,11 +183,12 @@ def test_schemes_vs_oracle(gkb, orc, scheme):
 
 
 @pytest.mark.parametrize("k", [1, 2, 3, 6])
-def test_block_products_equal_single_columns(gkb, k):
+def test_block_products_equal_single_columns(gkb, monkeypatch, k):
     """Block products (two columns per pass through the shared-expansion
-    kernel, an odd last column alone) give each column bit for bit the
-    single-vector product, with missing entries, several column ranges and
-    row blocks."""
+    kernel, an odd last column alone; GKB_TC_BLOCK=0 keeps this path for
+    k >= 3) give each column bit for bit the single-vector product, with
+    missing entries, several column ranges and row blocks."""
+    monkeypatch.setenv("GKB_TC_BLOCK", "0")
     p, n = 3001, 5003
     payload, _ = random_payload(p, n, seed=23, missing=0.03)
     op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
@@ -233,3 +234,27 @@ def test_norm_estimate_and_adjoint_mismatch_vs_oracle(gkb, orc):
     a, b = gkb.norm_estimate(op, 20), orc.norm_estimate(ref, 20)
     assert abs(a - b) <= 1e-11 * b
     assert gkb.adjoint_mismatch(op) <= 1e-14 and orc.adjoint_mismatch(ref) <= 1e-14
+
+
+@pytest.mark.parametrize("k", [3, 4, 8, 12, 16, 17])
+@pytest.mark.parametrize("p,n,missing", [(3001, 5003, 0.03), (257, 1000, 0.0), (64, 4099, 0.2)])
+def test_tc_block_products_vs_oracle(gkb, orc, k, p, n, missing):
+    """Block products of k >= 3 columns on the 5th-generation tensor cores
+    (k_pm_blk_tc: tcgen05.mma kind::i8, accumulators in TMEM, exact
+    indicator-MMA missing corrections; at most 16 columns per pass) against
+    the oracle, column by column, and against the single-vector products."""
+    payload, _ = random_payload(p, n, seed=41 + k + p, missing=missing)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
+    mu, inv_s = op.scaling()
+    ref = orc.GenoOracle(payload, p, n, mu, inv_s)
+    rng = np.random.default_rng(k + n)
+    X = rng.standard_normal((n, k)) * np.logspace(-3, 3, k)
+    Y = op.apply_block(X)
+    U = rng.standard_normal((p, k)) * np.logspace(2, -2, k)
+    Z = op.apply_adjoint_block(U)
+    for c in range(k):
+        yo, zo = ref.apply(X[:, c]), ref.apply_adjoint(U[:, c])
+        assert np.max(np.abs(Y[:, c] - yo)) <= 1e-12 * max(1e-300, np.max(np.abs(yo))), c
+        assert np.max(np.abs(Z[:, c] - zo)) <= 1e-12 * max(1e-300, np.max(np.abs(zo))), c
+        assert rel_err(Y[:, c], op.apply(X[:, c])) <= 1e-13
+        assert rel_err(Z[:, c], op.apply_adjoint(U[:, c])) <= 1e-13
