@@ -1612,19 +1612,21 @@ size_t tc_smem_bytes(int k, int mode) {
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_pm_blk_tc(
-    const uint4* __restrict__ lay, int64_t KT, int kt_cta, int k,
+    const uint4* __restrict__ lay, int64_t KT, int kt_cta, int k, int kpad,
     const uint8_t* __restrict__ tdig, const uint8_t* __restrict__ tdig2,
     const int* __restrict__ dexp, const int* __restrict__ dexp2, const double* __restrict__ dsum,
     const double* __restrict__ mu, const double* __restrict__ mean, int64_t rows_pad, int nkc,
     double* __restrict__ part) {
   extern __shared__ __align__(1024) uint8_t tsm[];
-  const int N = 8 * k;
+  // N = 8 kpad: kpad = k rounded up to even (N a multiple of 16: kind::i8 at
+  // M = 128 raised an illegal instruction for N = 40, 56, ... on this part)
+  const int N = 8 * kpad;
   const uint32_t bimg = (uint32_t)N * 128u;  // B image bytes per tile
   // buffer layout: [codes h0 | codes h1 | ind h0 | ind h1] (16 KB each), B [, B2]
   const uint32_t bufsz = 65536u + bimg * (MODE ? 2u : 1u);
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm) + 1023) &
                                              ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t fullb[2], emptyb[2], doneb;
+  __shared__ __align__(8) uint64_t fullb[2], emptyb[2];
   __shared__ uint32_t tbase;
   const int kc = blockIdx.y, bx = blockIdx.x;
   const int64_t kt0 = (int64_t)kc * kt_cta;
@@ -1641,7 +1643,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pm_blk_tc(
       mbar_init(&fullb[b], 8 + 1);  // 8 warps' A stores + the B bulk copy's arrival
       mbar_init(&emptyb[b], 1);     // the MMA commit
     }
-    mbar_init(&doneb, 1);
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -1719,8 +1720,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pm_blk_tc(
       umma_commit(&emptyb[b]);
     }
   }
-  if (threadIdx.x == 0) umma_commit(&doneb);  // every MMA issued so far
-  mbar_wait(&doneb, 0);
+  // every MMA done AND every commit arrival landed before this CTA's shared
+  // memory can be reused: wait for the last completion of both "empty"
+  // barriers (an unwaited asynchronous arrival would hit the next CTA's smem)
+  if (ktiles >= 1) mbar_wait(&emptyb[(ktiles - 1) & 1], (uint32_t)(((ktiles - 1) >> 1) & 1));
+  if (ktiles >= 2) mbar_wait(&emptyb[(ktiles - 2) & 1], (uint32_t)(((ktiles - 2) >> 1) & 1));
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // epilogue: warp w reads TMEM lanes 32 (w & 3) .. + 31 of its half
   const int row_l = r0 + lane;                         // row within the half
@@ -1780,7 +1784,8 @@ __global__ void __launch_bounds__(1024) k_digitize_tc(const double* __restrict__
   pdl_wait();
   pdl_trigger();
   const int kc = blockIdx.x, v = blockIdx.y, nkc = gridDim.x;
-  const int N = 8 * k;
+  const int N = 8 * gridDim.y;  // gridDim.y = kpad; vectors v >= k are zero
+  const bool pad = v >= k;
   const int ncol = kt_cta * 128;
   const int64_t c0 = (int64_t)kc * ncol;
   const double* xin = X + (int64_t)v * ldx;
@@ -1788,7 +1793,7 @@ __global__ void __launch_bounds__(1024) k_digitize_tc(const double* __restrict__
   double psum = 0.0;
   for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
     const int64_t c = c0 + t;
-    if (c < C) {
+    if (c < C && !pad) {
       double val = xin[c];
       if (MODE == 1) {
         val = inv_s[c] * val;
@@ -1806,7 +1811,7 @@ __global__ void __launch_bounds__(1024) k_digitize_tc(const double* __restrict__
   for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
     const int64_t c = c0 + t;
     double val = 0.0, cmv = 0.0;
-    if (c < C) {
+    if (c < C && !pad) {
       val = xin[c];
       if (MODE == 1) {
         val = inv_s[c] * val;
@@ -1830,7 +1835,7 @@ __global__ void __launch_bounds__(1024) k_digitize_tc(const double* __restrict__
       }
     }
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && !pad) {
     dexp[(int64_t)v * nkc + kc] = E;
     dsum[(int64_t)v * nkc + kc] = sm;
     if (MODE) dexp2[(int64_t)v * nkc + kc] = E2;
@@ -2181,17 +2186,19 @@ void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s, c
 
 // ---- tcgen05 block products ------------------------------------------------
 size_t tc_dig_bytes(const PMPlan& pl, int kmax) {
-  return (size_t)pl.nkc * pl.kt_cta * (size_t)(8 * kmax) * 128;
+  const int kp = kmax + (kmax & 1);
+  return (size_t)pl.nkc * pl.kt_cta * (size_t)(8 * kp) * 128;
 }
 
 namespace {
 template <int MODE>
 void launch_tc(const GenoView& g, const PMPlan& pl, const uint4* lay, const TcScratch& t, int k,
                cudaStream_t s) {
-  const size_t smem = tc_smem_bytes(k, MODE);
+  const size_t smem = tc_smem_bytes(k + (k & 1), MODE);
   allow_smem(k_pm_blk_tc<MODE>, smem);
   launch_pdl(k_pm_blk_tc<MODE>, dim3((unsigned)pl.grid_x, (unsigned)pl.nkc), dim3(kThreads), smem,
-             s, true, lay, pl.KT, pl.kt_cta, k, (const uint8_t*)t.dig, (const uint8_t*)t.dig2,
+             s, true, lay, pl.KT, pl.kt_cta, k, k + (k & 1), (const uint8_t*)t.dig,
+             (const uint8_t*)t.dig2,
              (const int*)t.dexp, (const int*)t.dexp2, (const double*)t.dsum, (const double*)g.mu,
              (const double*)g.mean, pl.rows_pad, pl.nkc, t.part);
 }
@@ -2201,7 +2208,8 @@ void k1_apply_tc(const GenoView& g, const TcScratch& t, const double* X, int64_t
                  double* Y, int64_t ldy, cudaStream_t s) {
   if (g.p_loc == 0 || k <= 0) return;
   const PMPlan& pl = g.pl1;
-  launch_pdl(k_digitize_tc<0>, dim3((unsigned)pl.nkc, (unsigned)k), dim3(1024), 0, s, true, X, ldx,
+  launch_pdl(k_digitize_tc<0>, dim3((unsigned)pl.nkc, (unsigned)(k + (k & 1))), dim3(1024), 0, s,
+             true, X, ldx,
              k, (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, g.n,
              pl.kt_cta, t.dig, (uint8_t*)nullptr, t.dexp, (int*)nullptr, t.dsum);
   launch_tc<0>(g, pl, g.lt1, t, k, s);
@@ -2219,7 +2227,8 @@ void k2_adjoint_tc(const GenoView& g, const TcScratch& t, const double* Yin, int
     return;
   }
   const PMPlan& pl = g.pl2;
-  launch_pdl(k_digitize_tc<1>, dim3((unsigned)pl.nkc, (unsigned)k), dim3(1024), 0, s, true, Yin,
+  launch_pdl(k_digitize_tc<1>, dim3((unsigned)pl.nkc, (unsigned)(k + (k & 1))), dim3(1024), 0, s,
+             true, Yin,
              ldy, k, (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc,
              pl.kt_cta, t.dig, t.dig2, t.dexp, t.dexp2, t.dsum);
   launch_tc<1>(g, pl, g.lt2, t, k, s);

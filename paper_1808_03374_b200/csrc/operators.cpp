@@ -980,12 +980,13 @@ void GenoOp::apply_dev(const std::vector<const double*>& x, const std::vector<do
 
 // Column pairs through the two-vector kernel (each column bitwise the
 // single-vector product); an odd last column goes alone.
-// tcgen05 block products for k >= 3 columns (GKB_TC_BLOCK=0 disables): both
-// layouts present, lists not required (exact indicator MMAs)
+// tcgen05 block products for k >= 3 columns: opt-in (GKB_TC_BLOCK=1) until
+// they beat the two-columns-per-pass kernel; both layouts
+// present, lists not required (exact indicator MMAs)
 static bool use_tc_block(const GenoShard& g, int64_t k) {
   const char* e = std::getenv("GKB_TC_BLOCK");
-  const bool off = e && std::strcmp(e, "0") == 0;
-  return !off && k >= 3 && !g.single;
+  const bool on = e && std::strcmp(e, "1") == 0;
+  return on && k >= 3 && !g.single;
 }
 
 static void ensure_tc(dev::TcScratch& t, const dev::PMPlan& pl, int kmax, bool k2,

@@ -183,12 +183,11 @@ def test_schemes_vs_oracle(gkb, orc, scheme):
 
 
 @pytest.mark.parametrize("k", [1, 2, 3, 6])
-def test_block_products_equal_single_columns(gkb, monkeypatch, k):
+def test_block_products_equal_single_columns(gkb, k):
     """Block products (two columns per pass through the shared-expansion
-    kernel, an odd last column alone; GKB_TC_BLOCK=0 keeps this path for
-    k >= 3) give each column bit for bit the single-vector product, with
+    kernel, an odd last column alone; the default unless GKB_TC_BLOCK=1)
+    give each column bit for bit the single-vector product, with
     missing entries, several column ranges and row blocks."""
-    monkeypatch.setenv("GKB_TC_BLOCK", "0")
     p, n = 3001, 5003
     payload, _ = random_payload(p, n, seed=23, missing=0.03)
     op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
@@ -236,13 +235,14 @@ def test_norm_estimate_and_adjoint_mismatch_vs_oracle(gkb, orc):
     assert gkb.adjoint_mismatch(op) <= 1e-14 and orc.adjoint_mismatch(ref) <= 1e-14
 
 
-@pytest.mark.parametrize("k", [3, 4, 8, 12, 16, 17])
+@pytest.mark.parametrize("k", [3, 4, 5, 8, 11, 12, 16, 17])
 @pytest.mark.parametrize("p,n,missing", [(3001, 5003, 0.03), (257, 1000, 0.0), (64, 4099, 0.2)])
-def test_tc_block_products_vs_oracle(gkb, orc, k, p, n, missing):
+def test_tc_block_products_vs_oracle(gkb, orc, monkeypatch, k, p, n, missing):
     """Block products of k >= 3 columns on the 5th-generation tensor cores
     (k_pm_blk_tc: tcgen05.mma kind::i8, accumulators in TMEM, exact
     indicator-MMA missing corrections; at most 16 columns per pass) against
     the oracle, column by column, and against the single-vector products."""
+    monkeypatch.setenv("GKB_TC_BLOCK", "1")
     payload, _ = random_payload(p, n, seed=41 + k + p, missing=missing)
     op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
     mu, inv_s = op.scaling()
@@ -258,3 +258,21 @@ def test_tc_block_products_vs_oracle(gkb, orc, k, p, n, missing):
         assert np.max(np.abs(Z[:, c] - zo)) <= 1e-12 * max(1e-300, np.max(np.abs(zo))), c
         assert rel_err(Y[:, c], op.apply(X[:, c])) <= 1e-13
         assert rel_err(Z[:, c], op.apply_adjoint(U[:, c])) <= 1e-13
+
+
+def test_tc_block_products_in_subspace_iteration(gkb, orc, monkeypatch):
+    """The tcgen05 block products inside an iterative solver (back-to-back
+    PDL-chained launches, both directions): subspace iteration on the
+    config-2 model equals the two-columns-per-pass path."""
+    from paper_1808_03374_b200 import subspace as Sb
+    from paper_1808_03374_b200 import synth
+    spec = synth.config_spec(2, scale=0.05)
+    op = gkb.GenotypeOperator.from_synth(spec, scheme=gkb.ScalingScheme.kHwe)
+    monkeypatch.setenv("GKB_TC_BLOCK", "0")
+    a = Sb.subspace_iterate(op, 6, Sb.SubspaceVariant.kQr, 1e-9, 100, 1)
+    monkeypatch.setenv("GKB_TC_BLOCK", "1")
+    b = Sb.subspace_iterate(op, 6, Sb.SubspaceVariant.kQr, 1e-9, 100, 1)
+    from conftest import principal_angles, sigma_rel_err
+    assert sigma_rel_err(b.singvals, a.singvals) <= 1e-9
+    assert principal_angles(b.basis, a.basis) < 1e-6
+    assert abs(a.state.iterations - b.state.iterations) <= 1
