@@ -1568,13 +1568,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
 // (a second B image). Epilogue: tcgen05.ld per row; the row value is
 // sum_i D_i 256^i 2^(E - 62) as in the mma.sync kernels.
 constexpr int kTcRows = 256;
-__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = (uint64_t)((addr & 0x3FFFF) >> 4);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // sm_100 descriptor version; no swizzle, base offset 0
-  return d;
-}
 __device__ __forceinline__ void umma_i8(uint32_t dt, uint64_t da, uint64_t db, uint32_t idesc,
                                         uint32_t acc) {
   asm volatile(
@@ -1598,20 +1591,31 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
                : "r"(taddr));
 }
 
-// smem A image of one row half (128 rows x 8 chunks of 16 B): canonical
-// K-major, core matrix (rows 8a..8a+7, chunk c) at a * 1024 + c * 128
-__device__ __forceinline__ uint32_t tc_a_off(int r, int c) {
-  return (uint32_t)((r >> 3) * 1024 + c * 128 + (r & 7) * 16);
+// smem A / B images: canonical K-major with the 128-byte swizzle (atoms of
+// 8 rows x 128 B, 1024-byte aligned; row r's 16-byte chunk c at
+// (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) * 16)): one tile's K
+// (128 bytes per row) is one atom row, and the producers' quarter-warps
+// store to 8 distinct bank groups
+__device__ __host__ __forceinline__ uint32_t tc_sw_off(int r, int c) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t addr) {
+  uint64_t d = (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;           // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset: 8-row atoms
+  d |= (uint64_t)1 << 46;            // sm_100 descriptor version
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
 }
 
 size_t tc_smem_bytes(int k, int mode) {
   const size_t N = 8 * (size_t)k;
-  // 2 buffers x (codes + indicators (2 x 32 KB) + B image(s) N x 128 B)
+  // 2 buffers x (codes + indicators (2 x 32 KB) + B image(s) N x 128 B), 1 KB alignment slack
   return 2 * (2 * 32768 + N * 128 * (mode ? 2 : 1)) + 1024;
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 1) k_pm_blk_tc(
+__global__ void __launch_bounds__(kThreads + 32, 1) k_pm_blk_tc(
     const uint4* __restrict__ lay, int64_t KT, int kt_cta, int k, int kpad,
     const uint8_t* __restrict__ tdig, const uint8_t* __restrict__ tdig2,
     const int* __restrict__ dexp, const int* __restrict__ dexp2, const double* __restrict__ dsum,
@@ -1622,7 +1626,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pm_blk_tc(
   // M = 128 raised an illegal instruction for N = 40, 56, ... on this part)
   const int N = 8 * kpad;
   const uint32_t bimg = (uint32_t)N * 128u;  // B image bytes per tile
-  // buffer layout: [codes h0 | codes h1 | ind h0 | ind h1] (16 KB each), B [, B2]
+  // buffer: [codes h0 | codes h1 | ind h0 | ind h1] (16 KB each), B [, B2]
   const uint32_t bufsz = 65536u + bimg * (MODE ? 2u : 1u);
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm) + 1023) &
                                              ~uintptr_t(1023));
@@ -1632,19 +1636,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_pm_blk_tc(
   const int64_t kt0 = (int64_t)kc * kt_cta;
   const int ktiles = (int)min((int64_t)kt_cta, KT - kt0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, tid = lane & 3;
-  const int64_t strip0 = ((int64_t)bx * 8 + warp) * 2;  // this warp's two strips
-  const uint4* src0 = lay + (strip0 * KT + kt0) * 32 + lane;
-  const uint4* src1 = src0 + KT * 32;
+  const bool mma_warp = warp == 8;  // warps 0-7 produce, warp 8 issues the MMAs
   uint32_t ncols = 32;
   while (ncols < 4u * (uint32_t)N) ncols <<= 1;
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&fullb[b], 8 + 1);  // 8 warps' A stores + the B bulk copy's arrival
+      mbar_init(&fullb[b], 8 + 1);  // 8 producer warps + the B bulk copy's arrival
       mbar_init(&emptyb[b], 1);     // the MMA commit
     }
   }
-  if (warp == 0) {
+  if (mma_warp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tbase)),
                  "r"(ncols)
@@ -1656,68 +1657,97 @@ __global__ void __launch_bounds__(kThreads, 1) k_pm_blk_tc(
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tbase;
   pdl_wait();  // the digits are the predecessor's output
-  // kind::i8 instruction descriptor: D s32, A u8, B s8, K-major, N, M = 128
-  const uint32_t idesc = (2u << 4) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
-  const uint32_t m0 = 0x03030303u, m1 = m0 << 2, m2 = m0 << 4, m3 = m0 << 6;
-  uint4 w0 = ktiles > 0 ? ld_stream(src0) : make_uint4(0, 0, 0, 0);
-  uint4 w1 = ktiles > 0 ? ld_stream(src1) : make_uint4(0, 0, 0, 0);
-  const int half = warp >> 2;                       // rows 0-127 / 128-255
-  const int r0 = (warp & 3) * 32;                   // this warp's first row in its half
-  for (int t = 0; t < ktiles; ++t) {
-    const int b = t & 1;
-    uint8_t* buf = base + (size_t)b * bufsz;
-    // the MMAs of tile t - 2 must have released this buffer
-    if (t >= 2) mbar_wait(&emptyb[b], (uint32_t)(((t >> 1) - 1) & 1));
-    if (threadIdx.x == 0) {
-      mbar_arrive_expect_tx(&fullb[b], bimg * (MODE ? 2u : 1u));
-      const size_t toff = ((size_t)kc * kt_cta + t) * bimg;
-      bulk_g2s(buf + 65536, tdig + toff, bimg, &fullb[b]);
-      if (MODE) bulk_g2s(buf + 65536 + bimg, tdig2 + toff, bimg, &fullb[b]);
-    }
-    const uint4 c0 = w0, c1 = w1;
-    if (t + 1 < ktiles) {  // next tile's words while this one is expanded
-      w0 = ld_stream(src0 + 32 * (t + 1));
-      w1 = ld_stream(src1 + 32 * (t + 1));
-    }
-    // lane (g, tid) holds words (row g, col tid), (g + 8, tid), (g, tid + 4),
-    // (g + 8, tid + 4) of each strip; one 16-byte K chunk per word
+  if (mma_warp) {
+    if (lane == 0) {
+      // kind::i8 instruction descriptor: D s32, A u8, B s8, K-major, N, M = 128
+      const uint32_t idesc = (2u << 4) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+      for (int t = 0; t < ktiles; ++t) {
+        const int b = t & 1;
+        mbar_wait(&fullb[b], (uint32_t)((t >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sa = smem_u32(base + (size_t)b * bufsz), sb = sa + 65536;
+        const uint32_t sb2 = sb + (MODE ? bimg : 0u);
 #pragma unroll
-    for (int sidx = 0; sidx < 2; ++sidx) {
-      const uint4 w = sidx ? c1 : c0;
-      const int rb = r0 + 16 * sidx + g;
-      const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = rb + 8 * (j & 1), c = tid + 4 * (j >> 1);
-        const uint32_t x = words[j];
-        const uint32_t mi = x & (x >> 1) & 0x55555555u;
-        const uint32_t off = tc_a_off(r, c);
-        *reinterpret_cast<uint4*>(buf + half * 16384 + off) =
-            make_uint4(x & m0, x & m1, x & m2, x & m3);
-        *reinterpret_cast<uint4*>(buf + 32768 + half * 16384 + off) =
-            make_uint4(mi & m0, mi & m1, mi & m2, mi & m3);
+        for (int ks = 0; ks < 4; ++ks) {  // K = 32 bytes per MMA: 32 B into the atom rows
+          const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
+          const uint64_t db = umma_desc_sw128(sb + ks * 32);
+          const uint64_t dbm = umma_desc_sw128(sb2 + ks * 32);
+          umma_i8(tmem, umma_desc_sw128(sa + ks * 32), db, idesc, acc);
+          umma_i8(tmem + (uint32_t)N, umma_desc_sw128(sa + 16384 + ks * 32), db, idesc, acc);
+          umma_i8(tmem + 2u * (uint32_t)N, umma_desc_sw128(sa + 32768 + ks * 32), dbm, idesc,
+                  acc);
+          umma_i8(tmem + 3u * (uint32_t)N, umma_desc_sw128(sa + 49152 + ks * 32), dbm, idesc,
+                  acc);
+        }
+        umma_commit(&emptyb[b]);
       }
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // STS -> tensor core reads
     __syncwarp();
-    if (lane == 0) mbar_arrive(&fullb[b]);
-    if (threadIdx.x == 0) {
-      mbar_wait(&fullb[b], (uint32_t)((t >> 1) & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t sa = smem_u32(buf), sb = sa + 65536, sb2 = sb + (MODE ? bimg : 0u);
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
-        const uint64_t db = umma_desc(sb + ks * 256, 128, 1024);
-        const uint64_t dbm = umma_desc(sb2 + ks * 256, 128, 1024);
-        umma_i8(tmem, umma_desc(sa + ks * 256, 128, 1024), db, idesc, acc);
-        umma_i8(tmem + (uint32_t)N, umma_desc(sa + 16384 + ks * 256, 128, 1024), db, idesc, acc);
-        umma_i8(tmem + 2u * (uint32_t)N, umma_desc(sa + 32768 + ks * 256, 128, 1024), dbm, idesc,
-                acc);
-        umma_i8(tmem + 3u * (uint32_t)N, umma_desc(sa + 49152 + ks * 256, 128, 1024), dbm, idesc,
-                acc);
+  } else {
+    const int g = lane >> 2, tid = lane & 3;
+    const int64_t strip0 = ((int64_t)bx * 8 + warp) * 2;  // this warp's two strips
+    const uint4* src0 = lay + (strip0 * KT + kt0) * 32 + lane;
+    const uint4* src1 = src0 + KT * 32;
+    const uint32_t m0 = 0x03030303u, m1 = m0 << 2, m2 = m0 << 4, m3 = m0 << 6;
+    const uint4 Z = make_uint4(0, 0, 0, 0);
+    // three register buffers: tiles t + 1 and t + 2 in flight while t is stored
+    uint4 pa0 = ktiles > 0 ? ld_stream(src0) : Z, pa1 = ktiles > 0 ? ld_stream(src1) : Z;
+    uint4 pb0 = ktiles > 1 ? ld_stream(src0 + 32) : Z, pb1 = ktiles > 1 ? ld_stream(src1 + 32) : Z;
+    uint4 pc0 = Z, pc1 = Z;
+    const int half = warp >> 2;      // rows 0-127 / 128-255
+    const int r0 = (warp & 3) * 32;  // this warp's first row in its half
+    const int sw = (g & 1) ? 2 : 0;  // odd rows store their c + 4 chunks first: 8 bank groups
+    auto stage = [&](int t, const uint4& c0, const uint4& c1) {
+      const int b = t & 1;
+      uint8_t* buf = base + (size_t)b * bufsz;
+      // the MMAs of tile t - 2 must have released this buffer
+      if (t >= 2) mbar_wait(&emptyb[b], (uint32_t)(((t >> 1) - 1) & 1));
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&fullb[b], bimg * (MODE ? 2u : 1u));
+        const size_t toff = ((size_t)kc * kt_cta + t) * bimg;
+        bulk_g2s(buf + 65536, tdig + toff, bimg, &fullb[b]);
+        if (MODE) bulk_g2s(buf + 65536 + bimg, tdig2 + toff, bimg, &fullb[b]);
       }
-      umma_commit(&emptyb[b]);
+      // lane (g, tid) holds words (row g, col tid), (g + 8, tid), (g, tid + 4),
+      // (g + 8, tid + 4) of each strip; one 16-byte K chunk per word
+#pragma unroll
+      for (int sidx = 0; sidx < 2; ++sidx) {
+        const uint4 w = sidx ? c1 : c0;
+        // words j = (row g, col tid), (g + 8, tid), (g, tid + 4), (g + 8, tid + 4),
+        // taken in the order jj ^ sw (selects, no local-memory array)
+        const uint32_t lo0 = sw ? w.z : w.x, lo1 = sw ? w.w : w.y;
+        const uint32_t hi0 = sw ? w.x : w.z, hi1 = sw ? w.y : w.w;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = jj ^ sw;
+          const int r = r0 + 16 * sidx + g + 8 * (j & 1), c = tid + 4 * (j >> 1);
+          const uint32_t x = jj == 0 ? lo0 : jj == 1 ? lo1 : jj == 2 ? hi0 : hi1;
+          const uint32_t mi = x & (x >> 1) & 0x55555555u;
+          const uint32_t off = tc_sw_off(r, c);
+          *reinterpret_cast<uint4*>(buf + half * 16384 + off) =
+              make_uint4(x & m0, x & m1, x & m2, x & m3);
+          *reinterpret_cast<uint4*>(buf + 32768 + half * 16384 + off) =
+              make_uint4(mi & m0, mi & m1, mi & m2, mi & m3);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // STS -> tensor core reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fullb[b]);
+    };
+    for (int t = 0; t < ktiles;) {
+#define GKB_TC_STEP(C0, C1, N0, N1)                                       \
+      if (t < ktiles) {                                                   \
+        if (t + 2 < ktiles) {                                             \
+          N0 = ld_stream(src0 + 32 * (t + 2));                            \
+          N1 = ld_stream(src1 + 32 * (t + 2));                            \
+        }                                                                 \
+        stage(t, C0, C1);                                                 \
+        ++t;                                                              \
+      }
+      GKB_TC_STEP(pa0, pa1, pc0, pc1)
+      GKB_TC_STEP(pb0, pb1, pa0, pa1)
+      GKB_TC_STEP(pc0, pc1, pb0, pb1)
+#undef GKB_TC_STEP
     }
   }
   // every MMA done AND every commit arrival landed before this CTA's shared
@@ -1726,49 +1756,52 @@ __global__ void __launch_bounds__(kThreads, 1) k_pm_blk_tc(
   if (ktiles >= 1) mbar_wait(&emptyb[(ktiles - 1) & 1], (uint32_t)(((ktiles - 1) >> 1) & 1));
   if (ktiles >= 2) mbar_wait(&emptyb[(ktiles - 2) & 1], (uint32_t)(((ktiles - 2) >> 1) & 1));
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // epilogue: warp w reads TMEM lanes 32 (w & 3) .. + 31 of its half
-  const int row_l = r0 + lane;                         // row within the half
-  const int64_t row = (int64_t)bx * kTcRows + half * 128 + row_l;
-  const uint32_t lanebase = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-  const double rmu = MODE == 0 ? mu[row] : 0.0, rmean = MODE == 0 ? mean[row] : 0.0;
-  for (int v = 0; v < k; ++v) {
-    uint32_t dc[8], dm[8];
-    tmem_ld8(lanebase + (uint32_t)(half * N + 8 * v), dc);
-    tmem_ld8(lanebase + (uint32_t)(2 * N + half * N + 8 * v), dm);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    // sum_i D_i 256^i in the mma.sync kernels' association: per 16-bit pair
-    // exact, pairs added in digit order
-    double vc = 0.0, vm = 0.0;
+  if (!mma_warp) {
+    // epilogue: warp w reads TMEM lanes 32 (w & 3) .. + 31 of its half
+    const int half = warp >> 2, r0 = (warp & 3) * 32;
+    const int64_t row = (int64_t)bx * kTcRows + half * 128 + r0 + lane;
+    const uint32_t lanebase = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    const double rmu = MODE == 0 ? mu[row] : 0.0, rmean = MODE == 0 ? mean[row] : 0.0;
+    for (int v = 0; v < k; ++v) {
+      uint32_t dc[8], dm[8];
+      tmem_ld8(lanebase + (uint32_t)(half * N + 8 * v), dc);
+      tmem_ld8(lanebase + (uint32_t)(2 * N + half * N + 8 * v), dm);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // sum_i D_i 256^i: per 16-bit pair exact, pairs added in digit order
+      double vc = 0.0, vm = 0.0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      vc += ((double)(int)dc[2 * i] + 256.0 * (double)(int)dc[2 * i + 1]) * pow2(16 * i);
-      vm += ((double)(int)dm[2 * i] + 256.0 * (double)(int)dm[2 * i + 1]) * pow2(16 * i);
+      for (int i = 0; i < 4; ++i) {
+        vc += ((double)(int)dc[2 * i] + 256.0 * (double)(int)dc[2 * i + 1]) * pow2(16 * i);
+        vm += ((double)(int)dm[2 * i] + 256.0 * (double)(int)dm[2 * i + 1]) * pow2(16 * i);
+      }
+      const int E = dexp[(int64_t)v * nkc + kc];
+      const double val = scale2(vc, E - 62);
+      double out;
+      if (MODE == 0) {
+        const double cor = scale2(vm, E - 62);
+        out = val - rmu * dsum[(int64_t)v * nkc + kc] - (3.0 - rmean) * cor;
+      } else {
+        const double cor = scale2(vm, dexp2[(int64_t)v * nkc + kc] - 62);
+        out = val - dsum[(int64_t)v * nkc + kc] - cor;
+      }
+      part[((int64_t)v * nkc + kc) * rows_pad + row] = out;
     }
-    const int E = dexp[(int64_t)v * nkc + kc];
-    const double val = scale2(vc, E - 62);
-    double out;
-    if (MODE == 0) {
-      const double cor = scale2(vm, E - 62);
-      out = val - rmu * dsum[(int64_t)v * nkc + kc] - (3.0 - rmean) * cor;
-    } else {
-      const double cor = scale2(vm, dexp2[(int64_t)v * nkc + kc] - 62);
-      out = val - dsum[(int64_t)v * nkc + kc] - cor;
-    }
-    part[((int64_t)v * nkc + kc) * rows_pad + row] = out;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0)
+  if (mma_warp)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols)
                  : "memory");
 }
 
-// Digits of k vectors for k_pm_blk_tc, one CTA per (range, vector): the B
-// image of each tile (N = 8k rows x 128 K bytes, canonical K-major): row
+// Digits of k vectors for k_pm_blk_tc, one CTA per (span, vector): the B
+// image of each tile (N = 8 kpad rows x 128 K bytes, 128-byte swizzle): row
 // 8v + i, chunk wc (the tile's word column), byte 4q + e <-> column
 // 16 wc + 4e + q (the shift-free masks' byte order) with the 4^-q group
 // prescale. MODE 0: v = x; MODE 1: v = inv_s y (dsum = sum v mu), and the
-// digits of cm = v (3 - mean) into dig2 (exponent dexp2).
+// digits of cm = v (3 - mean) into dig2 (exponent dexp2). A vector's 1 KB of
+// each tile is staged in shared memory and written out with 16-byte stores.
+constexpr int kTcSpan = 56;  // tiles per span (7168 columns): |D| <= 192 x 127 x 7168 < 2^31
 template <int MODE>
 __global__ void __launch_bounds__(1024) k_digitize_tc(const double* __restrict__ X, int64_t ldx,
                                                       int k, const double* __restrict__ inv_s,
@@ -1779,6 +1812,7 @@ __global__ void __launch_bounds__(1024) k_digitize_tc(const double* __restrict__
                                                       int* __restrict__ dexp,
                                                       int* __restrict__ dexp2,
                                                       double* __restrict__ dsum) {
+  extern __shared__ __align__(16) uint8_t dsh[];  // kt_cta KB [, MODE 1: + kt_cta KB]
   __shared__ double red[33];
   __shared__ int redi[33];
   pdl_wait();
@@ -1788,7 +1822,7 @@ __global__ void __launch_bounds__(1024) k_digitize_tc(const double* __restrict__
   const bool pad = v >= k;
   const int ncol = kt_cta * 128;
   const int64_t c0 = (int64_t)kc * ncol;
-  const double* xin = X + (int64_t)v * ldx;
+  const double* xin = X + (int64_t)(pad ? 0 : v) * ldx;
   int emax = -1100, emax2 = -1100;
   double psum = 0.0;
   for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
@@ -1808,6 +1842,7 @@ __global__ void __launch_bounds__(1024) k_digitize_tc(const double* __restrict__
   const int E = block_max_int(emax, redi);
   const int E2 = MODE ? block_max_int(emax2, redi) : 0;
   const double sm = block_sum(psum, red);
+  uint8_t* sd2 = dsh + (size_t)kt_cta * 1024;
   for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
     const int64_t c = c0 + t;
     double val = 0.0, cmv = 0.0;
@@ -1819,21 +1854,30 @@ __global__ void __launch_bounds__(1024) k_digitize_tc(const double* __restrict__
       }
     }
     const int tile = t >> 7, wc = (t >> 4) & 7, k16 = t & 15, q = k16 & 3, e = k16 >> 2;
-    const size_t off = ((size_t)kc * kt_cta + tile) * (size_t)N * 128 + (size_t)v * 1024 +
-                       (size_t)wc * 128 + 4 * q + e;
+    // rows 8v + i of the tile's B image (128-byte swizzle, tc_sw_off): this
+    // vector's 1 KB block of the tile, staged
+    const int off0 = tile * 1024 + 4 * q + e;
     long long M = __double2ll_rn(scale2(val, 62 - E - 2 * q));
     long long M2 = MODE ? __double2ll_rn(scale2(cmv, 62 - E2 - 2 * q)) : 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
+      const int off = off0 + i * 128 + ((wc ^ i) << 4);
       const int d = (int)(signed char)(M & 0xFF);
       M = (M - d) >> 8;
-      dig[off + i * 16] = (uint8_t)d;
+      dsh[off] = (uint8_t)d;
       if (MODE) {
         const int d2 = (int)(signed char)(M2 & 0xFF);
         M2 = (M2 - d2) >> 8;
-        dig2[off + i * 16] = (uint8_t)d2;
+        sd2[off] = (uint8_t)d2;
       }
     }
+  }
+  __syncthreads();
+  for (int u = threadIdx.x; u < kt_cta * 64; u += blockDim.x) {  // 16-byte units
+    const int tile = u >> 6, w = u & 63;
+    const size_t dst = ((size_t)kc * kt_cta + tile) * (size_t)N * 128 + (size_t)v * 1024 + 16 * w;
+    *reinterpret_cast<uint4*>(dig + dst) = reinterpret_cast<const uint4*>(dsh)[u];
+    if (MODE) *reinterpret_cast<uint4*>(dig2 + dst) = reinterpret_cast<const uint4*>(sd2)[u];
   }
   if (threadIdx.x == 0 && !pad) {
     dexp[(int64_t)v * nkc + kc] = E;
@@ -2185,9 +2229,11 @@ void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s, c
 }
 
 // ---- tcgen05 block products ------------------------------------------------
+int tc_nkc(const PMPlan& pl) { return (int)((pl.KT + kTcSpan - 1) / kTcSpan); }
+
 size_t tc_dig_bytes(const PMPlan& pl, int kmax) {
   const int kp = kmax + (kmax & 1);
-  return (size_t)pl.nkc * pl.kt_cta * (size_t)(8 * kp) * 128;
+  return (size_t)tc_nkc(pl) * kTcSpan * (size_t)(8 * kp) * 128;
 }
 
 namespace {
@@ -2196,11 +2242,12 @@ void launch_tc(const GenoView& g, const PMPlan& pl, const uint4* lay, const TcSc
                cudaStream_t s) {
   const size_t smem = tc_smem_bytes(k + (k & 1), MODE);
   allow_smem(k_pm_blk_tc<MODE>, smem);
-  launch_pdl(k_pm_blk_tc<MODE>, dim3((unsigned)pl.grid_x, (unsigned)pl.nkc), dim3(kThreads), smem,
-             s, true, lay, pl.KT, pl.kt_cta, k, k + (k & 1), (const uint8_t*)t.dig,
-             (const uint8_t*)t.dig2,
-             (const int*)t.dexp, (const int*)t.dexp2, (const double*)t.dsum, (const double*)g.mu,
-             (const double*)g.mean, pl.rows_pad, pl.nkc, t.part);
+  const int nkc = tc_nkc(pl);
+  launch_pdl(k_pm_blk_tc<MODE>, dim3((unsigned)pl.grid_x, (unsigned)nkc), dim3(kThreads + 32),
+             smem, s, true, lay, pl.KT, kTcSpan, k, k + (k & 1), (const uint8_t*)t.dig,
+             (const uint8_t*)t.dig2, (const int*)t.dexp, (const int*)t.dexp2,
+             (const double*)t.dsum, (const double*)g.mu, (const double*)g.mean, pl.rows_pad, nkc,
+             t.part);
 }
 }  // namespace
 
@@ -2208,14 +2255,17 @@ void k1_apply_tc(const GenoView& g, const TcScratch& t, const double* X, int64_t
                  double* Y, int64_t ldy, cudaStream_t s) {
   if (g.p_loc == 0 || k <= 0) return;
   const PMPlan& pl = g.pl1;
-  launch_pdl(k_digitize_tc<0>, dim3((unsigned)pl.nkc, (unsigned)(k + (k & 1))), dim3(1024), 0, s,
-             true, X, ldx,
-             k, (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, g.n,
-             pl.kt_cta, t.dig, (uint8_t*)nullptr, t.dexp, (int*)nullptr, t.dsum);
+  const int nkc = tc_nkc(pl);
+  const size_t dsm = (size_t)kTcSpan * 1024;
+  allow_smem(k_digitize_tc<0>, dsm);
+  launch_pdl(k_digitize_tc<0>, dim3((unsigned)nkc, (unsigned)(k + (k & 1))), dim3(1024), dsm, s,
+             true, X, ldx, k, (const double*)nullptr, (const double*)nullptr,
+             (const double*)nullptr, g.n, kTcSpan, t.dig, (uint8_t*)nullptr, t.dexp, (int*)nullptr,
+             t.dsum);
   launch_tc<0>(g, pl, g.lt1, t, k, s);
   for (int v = 0; v < k; ++v)
     launch_pdl(k1_reduce, dim3((unsigned)((g.p_loc + 255) / 256)), dim3(256), 0, s, true,
-               (const double*)(t.part + (size_t)v * pl.nkc * pl.rows_pad), pl.nkc, pl.rows_pad,
+               (const double*)(t.part + (size_t)v * nkc * pl.rows_pad), nkc, pl.rows_pad,
                g.p_loc, (const double*)g.inv_s, Y + (size_t)v * ldy);
 }
 
@@ -2227,15 +2277,17 @@ void k2_adjoint_tc(const GenoView& g, const TcScratch& t, const double* Yin, int
     return;
   }
   const PMPlan& pl = g.pl2;
-  launch_pdl(k_digitize_tc<1>, dim3((unsigned)pl.nkc, (unsigned)(k + (k & 1))), dim3(1024), 0, s,
-             true, Yin,
-             ldy, k, (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc,
-             pl.kt_cta, t.dig, t.dig2, t.dexp, t.dexp2, t.dsum);
+  const int nkc = tc_nkc(pl);
+  const size_t dsm = (size_t)kTcSpan * 2048;
+  allow_smem(k_digitize_tc<1>, dsm);
+  launch_pdl(k_digitize_tc<1>, dim3((unsigned)nkc, (unsigned)(k + (k & 1))), dim3(1024), dsm, s,
+             true, Yin, ldy, k, (const double*)g.inv_s, (const double*)g.mu,
+             (const double*)g.mean, g.p_loc, kTcSpan, t.dig, t.dig2, t.dexp, t.dexp2, t.dsum);
   launch_tc<1>(g, pl, g.lt2, t, k, s);
   for (int v = 0; v < k; ++v)
     launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
-               (const double*)(t.part + (size_t)v * pl.nkc * pl.rows_pad), pl.nkc, pl.rows_pad,
-               g.n, Z + (size_t)v * ldz);
+               (const double*)(t.part + (size_t)v * nkc * pl.rows_pad), nkc, pl.rows_pad, g.n,
+               Z + (size_t)v * ldz);
 }
 
 // ---- two vectors per pass (block products) ------------------------------

@@ -89,6 +89,7 @@ void k1_apply_tc(const GenoView& g, const TcScratch& t, const double* X, int64_t
 void k2_adjoint_tc(const GenoView& g, const TcScratch& t, const double* Yin, int64_t ldy, int k,
                    double* Z, int64_t ldz, cudaStream_t s);
 size_t tc_dig_bytes(const PMPlan& pl, int kmax);
+int tc_nkc(const PMPlan& pl);  // tcgen05 spans (56 tiles) of a layout
 
 // single-layout K2 geometry of a shard (p_loc SNPs x n samples)
 struct L1TPlan {

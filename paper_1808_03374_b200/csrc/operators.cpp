@@ -980,13 +980,15 @@ void GenoOp::apply_dev(const std::vector<const double*>& x, const std::vector<do
 
 // Column pairs through the two-vector kernel (each column bitwise the
 // single-vector product); an odd last column goes alone.
-// tcgen05 block products for k >= 3 columns: opt-in (GKB_TC_BLOCK=1) until
-// they beat the two-columns-per-pass kernel; both layouts
-// present, lists not required (exact indicator MMAs)
+// tcgen05 block products (k_pm_blk_tc) for k >= 6 columns, where one pass
+// beats ceil(k/2) passes of the two-column kernel;
+// GKB_TC_BLOCK=0 disables, =1 uses them from k = 3. Both layouts present;
+// lists not required (exact indicator MMAs).
 static bool use_tc_block(const GenoShard& g, int64_t k) {
   const char* e = std::getenv("GKB_TC_BLOCK");
-  const bool on = e && std::strcmp(e, "1") == 0;
-  return on && k >= 3 && !g.single;
+  if (e && std::strcmp(e, "0") == 0) return false;
+  const int64_t kmin = (e && std::strcmp(e, "1") == 0) ? 3 : 6;
+  return k >= kmin && !g.single;
 }
 
 static void ensure_tc(dev::TcScratch& t, const dev::PMPlan& pl, int kmax, bool k2,
@@ -1001,10 +1003,11 @@ static void ensure_tc(dev::TcScratch& t, const dev::PMPlan& pl, int kmax, bool k
   };
   pool(&t.dig, dev::tc_dig_bytes(pl, kmax));
   if (k2) pool(&t.dig2, dev::tc_dig_bytes(pl, kmax));
-  pool(&t.dexp, sizeof(int) * (size_t)(kmax * pl.nkc));
-  if (k2) pool(&t.dexp2, sizeof(int) * (size_t)(kmax * pl.nkc));
-  pool(&t.dsum, sizeof(double) * (size_t)(kmax * pl.nkc));
-  pool(&t.part, sizeof(double) * (size_t)kmax * (size_t)pl.nkc * (size_t)pl.rows_pad);
+  const int64_t nkc = dev::tc_nkc(pl);
+  pool(&t.dexp, sizeof(int) * (size_t)(kmax * nkc));
+  if (k2) pool(&t.dexp2, sizeof(int) * (size_t)(kmax * nkc));
+  pool(&t.dsum, sizeof(double) * (size_t)(kmax * nkc));
+  pool(&t.part, sizeof(double) * (size_t)kmax * (size_t)nkc * (size_t)pl.rows_pad);
   t.kmax = kmax;
 }
 
