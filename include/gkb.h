@@ -209,8 +209,9 @@ typedef struct {
    * 0 = exactly as written in gkl.cpp:127-136 (omits the |coupling|*nu
    *     previous-level term, so the estimates can under-run the true loss of
    *     orthogonality; the reference's own test_gkl.cpp:124-171 fails);
-   * 1 = complete recurrence (default): adds the term, mirroring the right
-   *     side's alpha_last*mu term (gkl.cpp:155-160). DESIGN.md section 6. */
+   * 1 = complete recurrence (default here, NOT the reference's algorithm):
+   *     adds the term, mirroring the right side's alpha_last*mu term
+   *     (gkl.cpp:155-160); anchored to dense LAPACK SVDs. DESIGN.md section 5. */
   int omega_recurrence;
 } gkb_gkl_options;
 

@@ -103,7 +103,12 @@ class StepStatus(enum.IntEnum):  # gkl.hpp:111-116
 
 @dataclass
 class GklOptions:
-    """GklOptions (gkl.hpp:17-33); same field names and defaults."""
+    """GklOptions (gkl.hpp:17-33): the reference's field names and defaults,
+    plus one field the reference does not have: `omega_recurrence`. Its
+    default 1 is NOT the reference's algorithm -- it adds the |coupling| nu
+    term that the left recurrence of gkl.cpp:127-136 omits (the
+    literal recurrence loses orthogonality on the config-2 model); 0 runs
+    gkl.cpp:127-136 as written."""
     k: int = 10
     tol: float = 1e-8
     max_mvps: int = 1000000
