@@ -1621,7 +1621,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) k_pm_blk_tc(
     const int* __restrict__ dexp, const int* __restrict__ dexp2, const double* __restrict__ dsum,
     const double* __restrict__ mu, const double* __restrict__ mean, int64_t rows_pad, int nkc,
     double* __restrict__ part) {
-  extern __shared__ __align__(1024) uint8_t tsm[];
+  extern __shared__ __align__(16) uint8_t tsm[];  // aligned to 1024 below
   // N = 8 kpad: kpad = k rounded up to even (N a multiple of 16: kind::i8 at
   // M = 128 raised an illegal instruction for N = 40, 56, ... on this part)
   const int N = 8 * kpad;
