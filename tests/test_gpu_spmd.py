@@ -31,13 +31,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, host_step):
+def _worker(rank, world, port, q, host_step, env=None):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     if host_step:
         os.environ["GKB_HOST_STEP"] = "1"
+    os.environ.update(env or {})
     import torch
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -82,11 +83,13 @@ def _worker(rank, world, port, q, host_step):
         dist.destroy_process_group()
 
 
-def _single(gkb, cfg, scale, host_step, monkeypatch):
+def _single(gkb, cfg, scale, host_step, monkeypatch, env=None):
     from paper_1808_03374_b200 import subspace as Sb
     from paper_1808_03374_b200 import synth
     if host_step:
         monkeypatch.setenv("GKB_HOST_STEP", "1")
+    for key, val in (env or {}).items():
+        monkeypatch.setenv(key, val)
     spec = synth.config_spec(cfg, scale=scale)
     op = gkb.GenotypeOperator.from_synth(spec, scheme=gkb.ScalingScheme.kHwe)
     rng = np.random.default_rng(cfg)
@@ -103,14 +106,19 @@ def _single(gkb, cfg, scale, host_step, monkeypatch):
                                else sres.singvals), sub_mvps=sres.mvps)
 
 
+MODES = [(False, {}), (True, {}),
+         # single-layout adjoint, dense-missing indicator MMAs, tcgen05 block products
+         (False, {"GKB_LAYOUTS": "1", "GKB_MISS_MODE": "ind", "GKB_TC_BLOCK": "1"})]
+
+
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("host_step", [False, True])
-def test_two_process_spmd_equals_single_process(gkb, monkeypatch, host_step):
+@pytest.mark.parametrize("host_step,env", MODES, ids=["device-step", "host-step", "modes"])
+def test_two_process_spmd_equals_single_process(gkb, monkeypatch, host_step, env):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, host_step)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, host_step, env)) for r in range(2)]
     for pr in procs:
         pr.start()
     got = q.get(timeout=540)
@@ -119,7 +127,7 @@ def test_two_process_spmd_equals_single_process(gkb, monkeypatch, host_step):
         assert pr.exitcode == 0
     assert got is not None
     for cfg, scale in [(2, 0.05), (3, 0.01)]:
-        a, b = got[cfg], _single(gkb, cfg, scale, host_step, monkeypatch)
+        a, b = got[cfg], _single(gkb, cfg, scale, host_step, monkeypatch, env)
         assert np.array_equal(a["mu"], b["mu"])            # global marker counts -> same scaling
         assert np.array_equal(a["y"], b["y"])              # K1 is shard-local: bitwise
         assert rel_err(a["z"], b["z"]) <= 1e-14            # K2 partials + allreduce
@@ -130,3 +138,5 @@ def test_two_process_spmd_equals_single_process(gkb, monkeypatch, host_step):
         assert abs(a["restarts"] - b["restarts"]) <= 1
         assert sigma_rel_err(a["sub_s"], b["sub_s"]) <= 1e-9
         assert a["sub_mvps"] == b["sub_mvps"]
+    for key in (env or {}):
+        monkeypatch.delenv(key, raising=False)
