@@ -54,7 +54,10 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kStripsPerWarp = GKB_SPW;  // row strips sharing each B fragment
 constexpr int kDepth = 2;                // tiles in flight per strip
-constexpr int kFullRange = 14;  // pm_plan's default kt_cta: fully unrolled main loop
+#ifndef GKB_FULL
+#define GKB_FULL 14
+#endif
+constexpr int kFullRange = GKB_FULL;  // pm_plan's default kt_cta: fully unrolled main loop
 static_assert(kStripsPerWarp <= 2, "the unrolled full-range loop prefetches strips 0 and 1");
 constexpr int kRowsPerCta = 8 * kStripsPerWarp * 16;  // 256
 constexpr int kStripsPerCta = 8 * kStripsPerWarp;
@@ -1987,7 +1990,7 @@ PMPlan pm_plan(int64_t R, int64_t C) {
   if (pl.S < kStripsPerCta) pl.S = kStripsPerCta;
   pl.KT = (C + 127) / 128;
   if (pl.KT < 1) pl.KT = 1;
-  pl.kt_cta = 14;  // 1792 columns per CTA (14 KB of digits); 12-20 swept, 14 best (config 2 and 3)
+  pl.kt_cta = kFullRange;  // 1792 columns per CTA (14 KB of digits); 12-20 swept, 14 best (config 2 and 3)
   if (const char* e = std::getenv("GKB_KT_CTA")) pl.kt_cta = std::max(1, std::atoi(e));  // sweeps
   pl.nkc = (int)((pl.KT + pl.kt_cta - 1) / pl.kt_cta);
   pl.grid_x = pl.S / kStripsPerCta;
