@@ -1238,10 +1238,38 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_ind(
     bp += 64;                                                              \
     ++t;                                                                   \
   }
-  for (int t = 0; t < ktiles;) {
-    GKB_PMI_STEP(bA, bC)
-    GKB_PMI_STEP(bB, bA)
-    GKB_PMI_STEP(bC, bB)
+  if (ktiles == kFullRange) {
+    // a full range: fully unrolled, constant prefetch offsets (as k_pm_main)
+    const uint4* p0 = src;
+    const uint4* p1 = src + KT * 32;
+#define GKB_PMI_FULL(T, CUR, DST)                                          \
+    {                                                                      \
+      const uint4 b01 = bp[(T) * 64], b23 = bp[(T) * 64 + 32];             \
+      const uint4 c01 = MODE ? bp[(T) * 64 + m2] : b01;                    \
+      const uint4 c23 = MODE ? bp[(T) * 64 + m2 + 32] : b23;               \
+      if ((T) + 2 < kFullRange) {                                          \
+        DST[0] = ld_stream(p0 + ((T) + 2) * 32);                           \
+        DST[kStripsPerWarp - 1] = ld_stream(p1 + ((T) + 2) * 32);          \
+      }                                                                    \
+      _Pragma("unroll") for (int r = 0; r < kStripsPerWarp; ++r) {         \
+        mma_tile(acc[r], CUR[r], b01, b23);                                \
+        mma_tile(accm[r], miss_ind(CUR[r]), c01, c23);                     \
+      }                                                                    \
+    }
+    static_assert(kStripsPerWarp == 2, "the unrolled loop prefetches strips 0 and 1");
+#pragma unroll
+    for (int T = 0; T < kFullRange; T += 3) {
+      GKB_PMI_FULL(T, bA, bC)
+      if (T + 1 < kFullRange) GKB_PMI_FULL(T + 1, bB, bA)
+      if (T + 2 < kFullRange) GKB_PMI_FULL(T + 2, bC, bB)
+    }
+#undef GKB_PMI_FULL
+  } else {
+    for (int t = 0; t < ktiles;) {
+      GKB_PMI_STEP(bA, bC)
+      GKB_PMI_STEP(bB, bA)
+      GKB_PMI_STEP(bC, bB)
+    }
   }
 #undef GKB_PMI_STEP
   const int E = dexp[kc], Em = MODE ? dexp2[kc] : E;
