@@ -232,6 +232,7 @@ typedef struct {
   /* device-side accounting (not in the reference) */
   double device_seconds;    /* CUDA-event time of the solve on shard 0 */
   int64_t host_syncs;       /* device->host scalar round trips */
+  int64_t fused_tails;      /* right half-steps run as one fused cluster launch */
 } gkb_svdl_result;
 
 void gkb_gkl_options_default(gkb_gkl_options* o);

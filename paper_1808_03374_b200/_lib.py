@@ -66,6 +66,7 @@ class gkb_svdl_result(C.Structure):
         ("err_history", C.POINTER(C.c_double)),
         ("device_seconds", C.c_double),
         ("host_syncs", C.c_int64),
+        ("fused_tails", C.c_int64),
     ]
 
 

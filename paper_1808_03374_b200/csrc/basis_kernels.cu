@@ -4,6 +4,10 @@
 // (gkl.cpp:233-242, :277-284), thick-restart / compress recombination
 // (gkl.cpp:355-359, :396-400) and the final Ritz vectors (:503-507).
 //
+// The products and sums that the unfused device step and the fused right tail
+// (ctl_kernels.cu, compiled without contraction) must agree on are explicit
+// __fma_rn / __dmul_rn (the forms the compiler contracted them to before).
+//
 // All of them stream a few vectors of 10^4..10^6 doubles: HBM/L2 bound and,
 // at these lengths, latency bound. Each kernel therefore works on row chunks
 // of kT * U rows per CTA (U rows per thread, loads of a batch issued together)
@@ -183,11 +187,11 @@ __global__ void __launch_bounds__(kT) k_gemv_t(const double* __restrict__ Q, int
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
           const int64_t r = rb + (int64_t)i * kT;
-          if (r < ch.r1) acc[k] += q[r] * vr[i];
+          if (r < ch.r1) acc[k] = __fma_rn(q[r], vr[i], acc[k]);
         }
       } else if (c == ncols && with_norm) {
 #pragma unroll
-        for (int i = 0; i < kBatch; ++i) acc[k] += vr[i] * vr[i];
+        for (int i = 0; i < kBatch; ++i) acc[k] = __fma_rn(vr[i], vr[i], acc[k]);
       }
     }
   }
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(kT) k_gemv_n(const double* __restrict__ Q, int
 #pragma unroll
         for (int k = 0; k < kCB; ++k)
 #pragma unroll
-          for (int i = 0; i < kBatch; ++i) s[i] += q[k][i] * cs[l + k];
+          for (int i = 0; i < kBatch; ++i) s[i] = __fma_rn(q[k][i], cs[l + k], s[i]);
       }
       for (; l < cn; ++l) {
         const double* q0 = Q + (cb + l) * ld;
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(kT) k_gemv_n(const double* __restrict__ Q, int
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
           const int64_t r = rb + (int64_t)i * kT;
-          if (r < ch.r1) s[i] += q0[r] * w0;
+          if (r < ch.r1) s[i] = __fma_rn(q0[r], w0, s[i]);
         }
       }
     }
@@ -264,10 +268,11 @@ __global__ void __launch_bounds__(kT) k_gemv_n(const double* __restrict__ Q, int
       const int64_t r = rb + (int64_t)i * kT;
       if (r < ch.r1) {
         const double old = v[r];
-        const double nv = beta == 0.0 ? sign * s[i] : beta * old + sign * s[i];
+        const double nv = beta == 0.0 ? __dmul_rn(sign, s[i])
+                                      : __fma_rn(beta, old, __dmul_rn(sign, s[i]));
         v[r] = nv;
-        nrm[0] += old * old;
-        nrm[1] += nv * nv;
+        nrm[0] = __fma_rn(old, old, nrm[0]);
+        nrm[1] = __fma_rn(nv, nv, nrm[1]);
       }
     }
   }
@@ -294,7 +299,7 @@ __global__ void __launch_bounds__(kT) k_dot(const double* __restrict__ a,
       y[i] = r < ch.r1 ? b[r] : 0.0;
     }
 #pragma unroll
-    for (int i = 0; i < kBatch; ++i) acc[0] += x[i] * y[i];
+    for (int i = 0; i < kBatch; ++i) acc[0] = __fma_rn(x[i], y[i], acc[0]);
   }
   if (block_partial_finalize<1>(acc, partial, out, ticket)) run_post(post);
 }
@@ -333,7 +338,7 @@ __global__ void __launch_bounds__(kT) k_axpy_dot(const double* __restrict__ dpre
     for (int i = 0; i < kBatch; ++i) {
       const int64_t r = rb + (int64_t)i * kT;
       if (aon && r < ch.r1) {
-        x[i] -= a * y[i];
+        x[i] = __fma_rn(-a, y[i], x[i]);
         v[r] = x[i];
       }
     }
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(kT) k_axpy_dot(const double* __restrict__ dpre
         y[i] = unext ? (r < ch.r1 ? unext[r] : 0.0) : x[i];
       }
 #pragma unroll
-      for (int i = 0; i < kBatch; ++i) acc[0] += y[i] * x[i];
+      for (int i = 0; i < kBatch; ++i) acc[0] = __fma_rn(y[i], x[i], acc[0]);
     }
   }
   if (don) block_partial_finalize<1>(acc, partial, out, ticket);
@@ -411,10 +416,10 @@ __global__ void __launch_bounds__(kT) k_axpy_norms(double alpha, const double* _
 #pragma unroll
     for (int i = 0; i < kBatch; ++i) {
       const int64_t r = rb + (int64_t)i * kT;
-      const double nv = x[i] - alpha * y[i];
+      const double nv = __fma_rn(-alpha, y[i], x[i]);
       if (r < ch.r1) v[r] = nv;
-      acc[0] += x[i] * x[i];
-      acc[1] += nv * nv;
+      acc[0] = __fma_rn(x[i], x[i], acc[0]);
+      acc[1] = __fma_rn(nv, nv, acc[1]);
     }
   }
   if (block_partial_finalize<2>(acc, partial, out, ticket)) run_post(post);

@@ -513,6 +513,7 @@ int gkb_svdl(gkb_op* op, const gkb_gkl_options* o, gkb_svdl_result** res) {
     r->err_history = dup(out.err_history);
     r->device_seconds = out.device_seconds;
     r->host_syncs = out.host_syncs;
+    r->fused_tails = out.fused_tails;
     *res = r;
   });
 }

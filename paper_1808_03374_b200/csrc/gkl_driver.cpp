@@ -152,6 +152,20 @@ Lanczos::~Lanczos() {
     if (e) cudaEventDestroy(e);
   if (ev_left_) cudaEventDestroy(ev_left_);
   if (ev_right_) cudaEventDestroy(ev_right_);
+  if (tlog_) {  // GKB_RTAIL_TLOG: mean SM cycles per phase of the fused right tail
+    unsigned long long h[16] = {};
+    cudaSetDevice(ctx_->shards[0].dev);
+    cudaMemcpy(h, tlog_, sizeof(h), cudaMemcpyDeviceToHost);
+    static const char* names[] = {"load", "partials", "barrier", "finalize", "second pass",
+                                  "omega", "gt", "gt-bar", "end", "gt-fin", "gn", "gn-bar+fin",
+                                  "pass2", "#cgs2", "#pass2"};
+    fprintf(stderr, "[gkb] fused right tail, %llu launches, mean cycles per phase:", h[15]);
+    for (int k = 0; k < 15; ++k)
+      fprintf(stderr, " %s %.0f", names[k],
+              k >= 13 ? (double)h[k] : (h[15] ? (double)h[k] / (double)h[15] : 0.0));
+    fprintf(stderr, "\n");
+    cudaFree(tlog_);
+  }
 }
 
 // Small host->device uploads (coupling coefficients, restart matrices, start
@@ -695,6 +709,30 @@ void Lanczos::cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec
   }
 }
 
+// The right half-step's tail fused into one launch per shard (the right
+// side is replicated: no collective inside it). All shards or none.
+bool Lanczos::right_tail_dev(const Options& o, int64_t s) {
+  const int L = (int)ctx_->shards.size();
+  for (int i = 0; i < L; ++i) {
+    ctx_->set_device(i);
+    Shard& sh = ctx_->shards[i];
+    dev::ctl::TailArgs a{cd(i), ci(i), ctl_params(o, dev::ctl::OP_R_B, s), V_[i], z_[i], n_};
+    if (i == 0 && getenv("GKB_RTAIL_TLOG")) {  // debug: per-phase cycles of the fused tail
+      if (!tlog_) {
+        GKB_CUDA(cudaMalloc(&tlog_, 16 * sizeof(unsigned long long)));
+        GKB_CUDA(cudaMemset(tlog_, 0, 16 * sizeof(unsigned long long)));
+      }
+      a.tlog = tlog_;
+    }
+    if (!dev::ctl::right_tail(a, sh.stream)) {
+      if (i == 0) return false;
+      fail(GKB_ELOGIC, "fused right tail launched on some shards only");
+    }
+  }
+  ++fused_tails;
+  return true;
+}
+
 void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t hi, bool last) {
   using namespace dev::ctl;
   const int L = (int)ctx_->shards.size();
@@ -844,7 +882,9 @@ void Lanczos::enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t 
       op_->adjoint_dev(std::vector<const double*>(ucol.begin(), ucol.end()), z_);
     }
   }
-  if (!o.full) {
+  if (fuse_ctl() && right_tail_dev(o, s)) {
+    // the whole sequence below in one cluster launch (ctl_kernels.cu k_right_tail)
+  } else if (!o.full) {
     const bool fuse = fuse_ctl();  // right side: no allreduce before the decision
     for (int i = 0; i < L; ++i) {
       ctx_->set_device(i);
@@ -1328,6 +1368,7 @@ SvdlOutput svdl(DevOp* op, const Options& o) {
   cudaEventDestroy(e1);
   out.device_seconds = ms * 1e-3;
   out.host_syncs = f.host_syncs;
+  out.fused_tails = f.fused_tails;
   if (const char* e = getenv("GKB_VERBOSE"))
     if (e[0] == '1')
     {

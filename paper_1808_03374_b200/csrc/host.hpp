@@ -343,6 +343,8 @@ class Lanczos {
   };
   DevRun run_dev(const Options& o, int64_t nsteps, double* norm_scale);
   int64_t host_syncs = 0;
+  int64_t fused_tails = 0;  // right_tail_dev launches
+  unsigned long long* tlog_ = nullptr;  // GKB_RTAIL_TLOG (debug; printed and freed at destruction)
   double t_enqueue = 0.0, t_wait = 0.0;  // run_dev host phases (GKB_VERBOSE)
   int64_t spec_hits = 0, spec_misses = 0;  // speculative right half-steps kept / not launched or redone
   Rng rng;
@@ -393,6 +395,7 @@ class Lanczos {
   void* ctl_down_ = nullptr;
   double* cd(int i) const { return reinterpret_cast<double*>(ctl_d_[i]); }
   int* ci(int i) const { return reinterpret_cast<int*>(cd(i) + ctl_L_.nd); }
+  bool right_tail_dev(const Options& o, int64_t s);
   void enqueue_step_dev(const Options& o, int64_t s, int64_t lo, int64_t hi, bool last);
   bool v_pending_ = false;  // v_{s+1} = z / beta left to the next step's apply (same run)
   void cgs2_dev(Side side, int64_t ncols, const std::vector<double*>& vec, int gate_slot,
@@ -412,7 +415,7 @@ struct SvdlOutput {
   int restarts = 0, reorth_count = 0, deflations = 0;
   bool all_converged = false;
   double wall_seconds = 0.0, device_seconds = 0.0;
-  int64_t host_syncs = 0;
+  int64_t host_syncs = 0, fused_tails = 0;
   std::vector<double> ritz_history, err_history;
   int64_t history_len = 0;
 };

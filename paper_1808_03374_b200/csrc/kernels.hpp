@@ -268,6 +268,23 @@ struct Params {
   double omega, lvl, bfac, guard, eta, eps;
 };
 void launch(double* d, int* iv, const Params& p, cudaStream_t st);
+// The right half-step after the adjoint's reduction, fused (ctl_kernels.cu
+// k_right_tail): partial mode's axpy + norms, R_A, local second pass, R_B,
+// then cgs2 (gated) with CG_MID / CG_END and R_END -- one cluster launch for
+// n <= kTailMaxN, the unfused kernels' bits. V: n x (s + 1), ld n. Returns
+// false (nothing enqueued) when it does not apply; the caller then enqueues
+// the unfused sequence.
+constexpr int64_t kTailMaxN = 16 * 256 * 4;
+struct TailArgs {
+  double* d;
+  int* iv;
+  Params p;  // ctl_params(o, OP_R_B, s)
+  const double* V;
+  double* z;
+  int64_t n;
+  unsigned long long* tlog = nullptr;  // GKB_RTAIL_TLOG: per-phase SM cycles of CTA 0 (debug)
+};
+bool right_tail(const TailArgs& a, cudaStream_t st);
 // A light decision (OP_L_A, OP_R_A, OP_CG_MID: ctl_ops.cuh) handed to the
 // reduction that produces its inputs: its last CTA runs it after the finalize
 // (block 0 when the reduction is gated off), saving the ctl launch. Only where

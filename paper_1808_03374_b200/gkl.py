@@ -158,6 +158,7 @@ class SvdlStats:  # gkl.hpp:170-180
     err_history: List[np.ndarray] = field(default_factory=list)
     device_seconds: float = 0.0
     host_syncs: int = 0
+    fused_tails: int = 0  # right half-steps run as one fused launch (device path)
 
 
 @dataclass
@@ -495,7 +496,8 @@ def svdl(op: LinearOperator, opts: GklOptions) -> SvdlResult:
     st = SvdlStats(mvps=r.mvps, steps=r.steps, restarts=r.restarts,
                    reorth_count=r.reorth_count, deflations=r.deflations,
                    converged=bool(r.all_converged), wall_seconds=r.wall_seconds,
-                   device_seconds=r.device_seconds, host_syncs=r.host_syncs)
+                   device_seconds=r.device_seconds, host_syncs=r.host_syncs,
+                   fused_tails=r.fused_tails)
     if r.history_len > 0:
         k = int(opts.k)
         h = arr(r.ritz_history, r.history_len * k).reshape(r.history_len, k)

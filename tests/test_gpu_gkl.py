@@ -319,8 +319,31 @@ def test_device_step_control_is_bitwise_host_step(gkb, orc, monkeypatch, cfg, sc
         monkeypatch.delenv("GKB_HOST_STEP")
         b = gkb.svdl(op, opts)
         _same_solve(a, b)
-        if opts.restart == gkb.RestartMode.kThick:
+        assert a.stats.fused_tails == 0
+        if opts.restart == gkb.RestartMode.kThick:  # the device-controlled steps
+            # n <= 16,384 in partial mode: the fused right tail ran
+            assert (b.stats.fused_tails > 0) == (opts.reorth == gkb.ReorthMode.kPartial)
             assert b.stats.host_syncs < a.stats.host_syncs
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_fused_right_tail_is_bitwise_unfused(gkb, monkeypatch, cfg):
+    """The right half-step's tail as one cluster launch (k_right_tail, partial
+    reorthogonalization) must give the unfused kernels' bits -- full-size
+    configs 1 and 2 (n = 2,000 and 10,000), all option variants -- and must
+    actually have run where it applies."""
+    from paper_1808_03374_b200 import synth
+    op = gkb.GenotypeOperator.from_synth(synth.config_spec(cfg), scheme=gkb.ScalingScheme.kHwe)
+    for opts in _opts_variants(gkb, synth.config_options(cfg)):
+        monkeypatch.setenv("GKB_NO_RTAIL", "1")
+        a = gkb.svdl(op, opts)
+        monkeypatch.delenv("GKB_NO_RTAIL")
+        b = gkb.svdl(op, opts)
+        _same_solve(a, b)
+        assert a.stats.fused_tails == 0
+        assert (b.stats.fused_tails > 0) == (opts.restart == gkb.RestartMode.kThick
+                                             and opts.reorth == gkb.ReorthMode.kPartial)
+    op.close()
 
 
 def test_device_step_control_breakdowns(gkb, monkeypatch):
