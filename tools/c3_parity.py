@@ -1,0 +1,66 @@
+"""One-off svdl parity at the FULL config-3 size (n = 50,000 x p = 500,000,
+6.25 GB packed; BASELINE options: partial reorth, thick restart 40/20, k = 10):
+the GPU solve against the CPU oracle's solve on the same seeded .bed bytes and
+scaling, with the protocol of tests/test_gpu_parity_full.py (per-sigma 1e-9,
+principal angles < 1e-6, restarts +-1). Too slow for the test suite (the
+oracle needs ~15 min on 16 cores); run on the GPU box, result committed under
+profiles/.
+
+usage: c3_parity.py OUT.json
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+
+import numpy as np  # noqa: E402
+
+import oracle as orc  # noqa: E402
+import paper_1808_03374_b200 as gkb  # noqa: E402
+from conftest import principal_angles, sigma_rel_err  # noqa: E402
+from paper_1808_03374_b200 import synth  # noqa: E402
+
+out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/c3_parity.json"
+cfg = 3
+spec = synth.config_spec(cfg)
+opts = synth.config_options(cfg)
+op = gkb.GenotypeOperator.from_synth(spec, scheme=gkb.ScalingScheme.kHwe)
+mu, inv_s = op.scaling()
+t0 = time.perf_counter()
+g = gkb.svdl(op, opts)
+t_gpu = time.perf_counter() - t0
+op.close()
+t0 = time.perf_counter()
+payload = orc.synth_bed(spec)
+t_gen = time.perf_counter() - t0
+nt = os.cpu_count() or 1
+t0 = time.perf_counter()
+o = orc.svdl(orc.GenoOracle(payload, spec.p, spec.n, mu, inv_s, nthreads=nt),
+             orc.Options.from_gkl(opts))
+t_cpu = time.perf_counter() - t0
+res = dict(
+    config=synth.CONFIG_TEXT[cfg] if hasattr(synth, "CONFIG_TEXT") else cfg,
+    options=synth.OPTIONS_TEXT[cfg] if hasattr(synth, "OPTIONS_TEXT") else "",
+    k=int(opts.k),
+    sigma_gpu=[float(x) for x in g.singvals],
+    sigma_oracle=[float(x) for x in o.singvals],
+    sigma_rel_err_max=float(sigma_rel_err(g.singvals, o.singvals)),
+    angle_U=float(principal_angles(g.U, o.U)),
+    angle_V=float(principal_angles(g.V, o.V)),
+    mvps_gpu=int(g.stats.mvps), mvps_oracle=int(o.mvps),
+    restarts_gpu=int(g.stats.restarts), restarts_oracle=int(o.restarts),
+    converged_gpu=bool(g.stats.converged), converged_oracle=bool(o.all_converged),
+    seconds_gpu=round(t_gpu, 3), seconds_oracle=round(t_cpu, 1), oracle_threads=nt,
+    seconds_oracle_generate=round(t_gen, 1),
+    thresholds=dict(sigma_rel=1e-9, angle=1e-6, restarts=1),
+)
+res["pass"] = (res["sigma_rel_err_max"] <= 1e-9 and res["angle_U"] < 1e-6 and res["angle_V"] < 1e-6
+               and abs(res["restarts_gpu"] - res["restarts_oracle"]) <= 1
+               and res["converged_gpu"] == res["converged_oracle"])
+os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+with open(out, "w") as f:
+    json.dump(res, f, indent=1)
+print(json.dumps(res))
