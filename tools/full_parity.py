@@ -1,12 +1,11 @@
-"""One-off svdl parity at the FULL config-3 size (n = 50,000 x p = 500,000,
-6.25 GB packed; BASELINE options: partial reorth, thick restart 40/20, k = 10):
-the GPU solve against the CPU oracle's solve on the same seeded .bed bytes and
-scaling, with the protocol of tests/test_gpu_parity_full.py (per-sigma 1e-9,
-principal angles < 1e-6, restarts +-1). Too slow for the test suite (the
-oracle needs ~15 min on 16 cores); run on the GPU box, result committed under
-profiles/.
+"""One-off svdl parity at a FULL BASELINE config size (config 3: 6.25 GB,
+~15 min of oracle on 16 cores; config 4: 12.5 GB, ~2 h) with the BASELINE
+options: the GPU solve against the CPU oracle's solve on the same seeded .bed
+bytes and scaling, with the protocol of tests/test_gpu_parity_full.py
+(per-sigma 1e-9, principal angles < 1e-6, restarts +-1). Too slow for the
+test suite; run on the GPU box, result committed under profiles/.
 
-usage: c3_parity.py OUT.json
+usage: full_parity.py CONFIG OUT.json
 """
 import json
 import os
@@ -23,8 +22,8 @@ import paper_1808_03374_b200 as gkb  # noqa: E402
 from conftest import principal_angles, sigma_rel_err  # noqa: E402
 from paper_1808_03374_b200 import synth  # noqa: E402
 
-out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/c3_parity.json"
-cfg = 3
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+out = sys.argv[2] if len(sys.argv) > 2 else f"gpurun_out/c{cfg}_parity.json"
 spec = synth.config_spec(cfg)
 opts = synth.config_options(cfg)
 op = gkb.GenotypeOperator.from_synth(spec, scheme=gkb.ScalingScheme.kHwe)
