@@ -524,9 +524,9 @@ __global__ void __launch_bounds__(kTT) k_right_tail(TailArgs a) {
     tail_gemv_t(a.V, n, ncols, (int)ncols + 1, zr, cta, CL, nblk, spart[ph], ws);
     clk.mark(6);  // gemv_t partials
     cluster_sync_all();
-    clk.mark(7);
+    clk.mark(7);  // cluster barrier
     tail_finalize(spart[ph], nblk, (int)ncols + 1, fin, seg);
-    clk.mark(9);
+    clk.mark(9);  // finalize
     ph ^= 1;
     if (cta == 0)
       for (int64_t k = t; k <= ncols; k += kTT) res[R_CG + k] = fin[k];
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(kTT) k_right_tail(TailArgs a) {
     clk.mark(10);  // gemv_n
     cluster_sync_all();
     tail_finalize(spart[ph], nblk, 2, fin, seg);
-    clk.mark(11);
+    clk.mark(11);  // cluster barrier + finalize
     ph ^= 1;
     const double na = sqrt(fin[1]);
     const bool gre2 = na < p.eta * nb;  // CG_MID
