@@ -140,3 +140,59 @@ def test_two_process_spmd_equals_single_process(gkb, monkeypatch, host_step, env
         assert a["sub_mvps"] == b["sub_mvps"]
     for key in (env or {}):
         monkeypatch.delenv(key, raising=False)
+
+
+def _nccl_worker(q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["GKB_NCCL_FORCE"] = "1"
+    try:
+        import paper_1808_03374_b200 as gkb
+        from paper_1808_03374_b200 import synth
+        uid = gkb.Context.nccl_unique_id()
+        ctx = gkb.Context(nccl=(0, uid, 1, 0))
+        spec = synth.config_spec(2, scale=0.05)
+        op = gkb.GenotypeOperator.from_synth(spec, ctx=ctx, scheme=gkb.ScalingScheme.kHwe)
+        x = np.random.default_rng(2).standard_normal(spec.n)
+        y = op.apply(x)
+        z = op.apply_adjoint(y)
+        res = gkb.svdl(op, synth.config_options(2))
+        q.put(dict(y=y.copy(), z=z.copy(), s=res.singvals.copy(), U=np.array(res.U),
+                   V=np.array(res.V), mvps=res.stats.mvps, mu=op.scaling()[0].copy()))
+        op.close()
+        ctx.close()
+    except BaseException:
+        import traceback
+        traceback.print_exc()
+        q.put(None)
+        raise
+
+
+@pytest.mark.timeout(300)
+def test_nccl_one_rank_equals_default_context(gkb):
+    """A one-rank NCCL context (gkb_init_nccl) with GKB_NCCL_FORCE=1 sends
+    every allreduce of the SPMD branches through ncclAllReduce (an identity
+    for one rank): the solve must be bitwise the default context's. This runs
+    the NCCL plumbing (comm init, allreduces enqueued on the library's stream)
+    on a one-GPU box; sums across ranks are covered by the host-comm tests."""
+    import torch.multiprocessing as mp
+    from paper_1808_03374_b200 import synth
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_nccl_worker, args=(q,))
+    pr.start()
+    got = q.get(timeout=280)
+    pr.join(timeout=60)
+    assert got is not None and pr.exitcode == 0
+    spec = synth.config_spec(2, scale=0.05)
+    op = gkb.GenotypeOperator.from_synth(spec, scheme=gkb.ScalingScheme.kHwe)
+    x = np.random.default_rng(2).standard_normal(spec.n)
+    assert np.array_equal(got["mu"], op.scaling()[0])
+    assert np.array_equal(got["y"], op.apply(x))
+    assert np.array_equal(got["z"], op.apply_adjoint(got["y"]))
+    res = gkb.svdl(op, synth.config_options(2))
+    assert np.array_equal(got["s"], res.singvals)
+    assert np.array_equal(got["U"], np.array(res.U)) and np.array_equal(got["V"], np.array(res.V))
+    assert got["mvps"] == res.stats.mvps
+    op.close()
