@@ -265,10 +265,10 @@ __global__ void k_layout_to_bed(const uint32_t* __restrict__ lay, int64_t KT, in
 
 // ---------------------------------------------------------------- missing lists
 // Per-CTA missing lists: block b = kc * grid_x + bx
-// covers rows [256 bx, 256 bx + 256) x columns [2048 kc, 2048 kc + 2048) of a
+// covers rows [256 bx, 256 bx + 256) x columns [128 kt_cta kc, 128 kt_cta (kc + 1)) of a
 // tile layout -- exactly one k_pm_main CTA. Row r of the block owns
 //   ent[base[b] + off[b*257 + r] .. base[b] + off[b*257 + r + 1])
-// = the block-local column indices (< 2048, ascending) of its missing entries.
+// = the block-local column indices (< 128 kt_cta = 1792 by default, ascending) of its missing entries.
 // Count pass (kFill = false) writes cnt[b*256 + r]; fill pass writes ent.
 template <bool kFill>
 __global__ void __launch_bounds__(kRowsPerCta) k_miss_tiles(const uint32_t* __restrict__ lay, int64_t KT,
@@ -1972,8 +1972,17 @@ __global__ void k1_reduce(const double* __restrict__ part, int nkc, int64_t rows
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   pdl_wait();
   if (j >= p_loc) return;
+  const double* p = part + j;
   double acc = 0.0;
-  for (int c = 0; c < nkc; ++c) acc += part[(int64_t)c * rows_pad + j];
+  int c = 0;
+  for (; c + 8 <= nkc; c += 8) {  // 8 loads in flight, added in range order
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __ldcs(p + (int64_t)(c + i) * rows_pad);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc += v[i];
+  }
+  for (; c < nkc; ++c) acc += __ldcs(p + (int64_t)c * rows_pad);
   y[j] = inv_s[j] * acc;
 }
 
@@ -1998,6 +2007,44 @@ __global__ void __launch_bounds__(1024) k2_reduce(const double* __restrict__ par
     for (int w = 0; w < 32; ++w) t += ps[w][lane];
     z[s] = t;
   }
+}
+
+// K2 finish for tall sample counts (n >= kK2SeqMin): thread per sample, the
+// ranges in order (as k1_reduce), 8 coalesced loads in flight per thread.
+// The 32-warp block above keeps short vectors spread over the SMs; here there
+// are enough samples, and its one-or-two loads per thread with a block
+// barrier ran at ~2.2 TB/s on config 4 (n = 500,000: 224 MB of partials).
+constexpr int64_t kK2SeqMin = 65536;
+__global__ void __launch_bounds__(256) k2_reduce_seq(const double* __restrict__ part, int nkc,
+                                                     int64_t rows_pad, int64_t n,
+                                                     double* __restrict__ z) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
+  if (s >= n) return;
+  const double* p = part + s;
+  double acc = 0.0;
+  int c = 0;
+  for (; c + 8 <= nkc; c += 8) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __ldcs(p + (int64_t)(c + i) * rows_pad);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc += v[i];
+  }
+  for (; c < nkc; ++c) acc += __ldcs(p + (int64_t)c * rows_pad);
+  z[s] = acc;
+}
+
+// every K2 finish (two-layout, single-layout, block products) goes through
+// here, so a given (n, nkc) always sums its partials in the same order
+void launch_k2_reduce(const double* part, int nkc, int64_t rows_pad, int64_t n, double* z,
+                      cudaStream_t s) {
+  if (n >= kK2SeqMin)
+    launch_pdl(k2_reduce_seq, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, true, part, nkc,
+               rows_pad, n, z);
+  else
+    launch_pdl(k2_reduce, dim3((unsigned)((n + 31) / 32)), dim3(1024), 0, s, true, part, nkc,
+               rows_pad, n, z);
 }
 
 int grid_for(int64_t work, int threads, int cap = 148 * 16) {
@@ -2244,8 +2291,7 @@ void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s, c
   if (g.single) {  // K2 from layout 1
     digitize_l1t(g, y, s, di);
     launch_adj_l1(g, s, true);
-    launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
-               (const double*)g.s2.part, (int)g.l1t_nkc, g.l1t_rows_pad, g.n, z);
+    launch_k2_reduce((const double*)g.s2.part, (int)g.l1t_nkc, g.l1t_rows_pad, g.n, z, s);
     return;
   }
   k2_digitize(g, y, s, di);
@@ -2255,8 +2301,7 @@ void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s, c
   } else {
     launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, true);
   }
-  launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
-             (const double*)g.s2.part, g.pl2.nkc, g.pl2.rows_pad, g.n, z);
+  launch_k2_reduce((const double*)g.s2.part, g.pl2.nkc, g.pl2.rows_pad, g.n, z, s);
 }
 
 // ---- tcgen05 block products ------------------------------------------------
@@ -2316,9 +2361,8 @@ void k2_adjoint_tc(const GenoView& g, const TcScratch& t, const double* Yin, int
              (const double*)g.mean, g.p_loc, kTcSpan, t.dig, t.dig2, t.dexp, t.dexp2, t.dsum);
   launch_tc<1>(g, pl, g.lt2, t, k, s);
   for (int v = 0; v < k; ++v)
-    launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
-               (const double*)(t.part + (size_t)v * nkc * pl.rows_pad), nkc, pl.rows_pad, g.n,
-               Z + (size_t)v * ldz);
+    launch_k2_reduce((const double*)(t.part + (size_t)v * nkc * pl.rows_pad), nkc, pl.rows_pad, g.n,
+               Z + (size_t)v * ldz, s);
 }
 
 // ---- two vectors per pass (block products) ------------------------------
@@ -2396,9 +2440,8 @@ void k2_adjoint2(const GenoView& g, const PMScratch& sb, const double* y0, const
   digitize_into<1>(g, g.pl2, y1, sb, s, true);
   launch_main2<1>(g, g.pl2, g.lt2, g.s2, sb, g.s2.cm, sb.cm, g.m2, s);
   for (int v = 0; v < 2; ++v)
-    launch_pdl(k2_reduce, dim3((unsigned)((g.n + 31) / 32)), dim3(1024), 0, s, true,
-               (const double*)(v ? sb.part : g.s2.part), g.pl2.nkc, g.pl2.rows_pad, g.n,
-               v ? z1 : z0);
+    launch_k2_reduce((const double*)(v ? sb.part : g.s2.part), g.pl2.nkc, g.pl2.rows_pad, g.n,
+               v ? z1 : z0, s);
 }
 
 void marker_scan(const GenoView& g, const double* P, int64_t ldp, int K, const double* Ainv,
