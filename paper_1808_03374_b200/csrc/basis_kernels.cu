@@ -156,6 +156,11 @@ __device__ __forceinline__ Chunk chunk(int64_t len, int64_t rpb) {
 // covers row chunk bx and partial columns [kCB by, kCB by + kCB): kCB x kBatch
 // independent loads per thread in flight, warp sums per column, then the
 // kWarps warp sums in order into partial[bx * K + k].
+// kBatchT rows per thread per batch (x kCB columns of loads in flight): a
+// thread visits the same rows in the same order for any batch size, so the
+// sums do not depend on it -- 4 for one-group calls (few columns), else 2
+// (registers: 76 instead of 116).
+template <int kBatchT>
 __global__ void __launch_bounds__(kT) k_gemv_t(const double* __restrict__ Q, int64_t ld,
                                                int64_t len, int64_t ncols,
                                                const double* __restrict__ v, int with_norm,
@@ -172,26 +177,37 @@ __global__ void __launch_bounds__(kT) k_gemv_t(const double* __restrict__ Q, int
   double acc[kCB];
 #pragma unroll
   for (int k = 0; k < kCB; ++k) acc[k] = 0.0;
-  for (int64_t rb = ch.r0 + threadIdx.x; rb < ch.r1; rb += (int64_t)kT * kBatch) {
-    double vr[kBatch];
+  for (int64_t rb = ch.r0 + threadIdx.x; rb < ch.r1; rb += (int64_t)kT * kBatchT) {
+    double vr[kBatchT];
 #pragma unroll
-    for (int i = 0; i < kBatch; ++i) {
+    for (int i = 0; i < kBatchT; ++i) {
       const int64_t r = rb + (int64_t)i * kT;
       vr[i] = r < ch.r1 ? v[r] : 0.0;
+    }
+    // all kCB x kBatchT loads issued before the FMAs (as in k_gemv_n): the
+    // FMA order per column is unchanged, so are the bits
+    double q[kCB][kBatchT];
+#pragma unroll
+    for (int k = 0; k < kCB; ++k) {
+      const int64_t c = c0 + k;
+#pragma unroll
+      for (int i = 0; i < kBatchT; ++i) {
+        const int64_t r = rb + (int64_t)i * kT;
+        q[k][i] = (c < ncols && r < ch.r1) ? Q[c * ld + r] : 0.0;
+      }
     }
 #pragma unroll
     for (int k = 0; k < kCB; ++k) {
       const int64_t c = c0 + k;
       if (c < ncols) {
-        const double* q = Q + c * ld;
 #pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
+        for (int i = 0; i < kBatchT; ++i) {
           const int64_t r = rb + (int64_t)i * kT;
-          if (r < ch.r1) acc[k] = __fma_rn(q[r], vr[i], acc[k]);
+          if (r < ch.r1) acc[k] = __fma_rn(q[k][i], vr[i], acc[k]);
         }
       } else if (c == ncols && with_norm) {
 #pragma unroll
-        for (int i = 0; i < kBatch; ++i) acc[k] = __fma_rn(vr[i], vr[i], acc[k]);
+        for (int i = 0; i < kBatchT; ++i) acc[k] = __fma_rn(vr[i], vr[i], acc[k]);
       }
     }
   }
@@ -572,8 +588,8 @@ void gemv_t(const double* Q, int64_t ld, int64_t len, int64_t ncols, const doubl
   const int64_t rpb = rpb_target(len, "GKB_GT_BLOCKS", 296);
   const int64_t nb = std::max<int64_t>(1, (len + rpb - 1) / rpb);
   const dim3 grid((unsigned)nb, (unsigned)((K + kCB - 1) / kCB));
-  launch_pdl(k_gemv_t, grid, dim3(kT), 0, s, true, Q, ld, len, ncols, v, with_norm ? 1 : 0, rpb,
-             K, rs.partial, out, rs.ticket, gate);
+  launch_pdl(K <= 4 ? k_gemv_t<4> : k_gemv_t<2>, grid, dim3(kT), 0, s, true, Q, ld, len, ncols, v,
+             with_norm ? 1 : 0, rpb, K, rs.partial, out, rs.ticket, gate);
 }
 
 void gemv_n(const double* Q, int64_t ld, int64_t len, int64_t ncols, const double* c, double* v,
