@@ -509,6 +509,26 @@ __device__ __forceinline__ double walk_list(const uint16_t* __restrict__ ent, ui
   return corr;
 }
 
+// walk_list in one loop of chunks of four with the chunk's loads and adds
+// predicated on the run's end (each entry still added in order: same bits),
+// so a warp's lanes do not diverge between a chunk loop and a tail loop
+__device__ __forceinline__ double walk_list_u(const uint16_t* __restrict__ ent, uint32_t k0,
+                                              uint32_t ke, const double* __restrict__ cv) {
+  double corr = 0.0;
+  const uint32_t n = ke - k0;
+#pragma unroll 1
+  for (uint32_t i = 0; i < n; i += 4) {
+    double x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u < n) x[u] = cv[ent[k0 + i + u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u < n) corr += x[u];
+  }
+  return corr;
+}
+
 // walk_list over two runs at once: each sum in its own sequential order (the
 // bits of two walk_list calls), the two runs' load latencies overlapped
 __device__ __forceinline__ void walk_list_pair(const uint16_t* __restrict__ ent, uint32_t ka,
@@ -553,6 +573,44 @@ __device__ __forceinline__ void walk_list_pair(const uint16_t* __restrict__ ent,
   for (; ka < kea || kb < keb; ++ka, ++kb) {
     if (ka < kea) sa += cv[ent[ka]];
     if (kb < keb) sb += cv[ent[kb]];
+  }
+  ca = sa;
+  cb = sb;
+}
+
+// walk_list_pair as ONE loop over both runs in chunks of four: past a run's
+// end a lane reads the zero slot cv[-1] = +0.0 instead. A sum that starts at
+// +0.0 never becomes -0.0, so adding +0.0 leaves it unchanged and each run's
+// sum keeps walk_list's bits -- without the remainder and tail loops, between
+// which a warp's lanes diverged (the epilogue's largest instruction cost).
+#ifndef GKB_WALK_UNIFORM
+#define GKB_WALK_UNIFORM 1
+#endif
+__device__ __forceinline__ void walk_list_pair_u(const uint16_t* __restrict__ ent, uint32_t ka,
+                                                 uint32_t kea, uint32_t kb, uint32_t keb,
+                                                 const double* __restrict__ cv, double& ca,
+                                                 double& cb) {
+  double sa = 0.0, sb = 0.0;
+  const uint32_t na = kea - ka, nb = keb - kb, n = max(na, nb);
+#pragma unroll 1
+  for (uint32_t i = 0; i < n; i += 4) {
+    int a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = i + u < na ? (int)ent[ka + i + u] : -1;
+      b[u] = i + u < nb ? (int)ent[kb + i + u] : -1;
+    }
+    double x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[u] = cv[a[u]];
+      y[u] = cv[b[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      sa += x[u];
+      sb += y[u];
+    }
   }
   ca = sa;
   cb = sb;
@@ -677,6 +735,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
   } else if (cbulk && (ncol & 1) && threadIdx.x == kThreads - 1) {
     cvs[ncol - 1] = csrc[ncol - 1];
   }
+  if (threadIdx.x == kThreads - 2) cvs[-1] = 0.0;  // walk_list_pair_u's zero slot (staging pad)
   __syncthreads();  // the mbarriers' init, the plain copies
   mbar_wait(&sbar[0], 0);
 #else
@@ -813,14 +872,19 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     if (ent_shift >= 0) {  // shared-memory runs (pointer derived from the smem array: LDS)
       const uint16_t* ent = reinterpret_cast<const uint16_t*>(stage + kOffBytes) + ent_shift;
       if (kStripsPerWarp == 2)  // both strips' runs walked together (latencies overlap)
+#if GKB_WALK_UNIFORM
+        walk_list_pair_u(ent, k0[0], ke[0], k0[kStripsPerWarp - 1], ke[kStripsPerWarp - 1], cvs,
+                         corr[0], corr[kStripsPerWarp - 1]);
+#else
         walk_list_pair(ent, k0[0], ke[0], k0[kStripsPerWarp - 1], ke[kStripsPerWarp - 1], cvs,
                        corr[0], corr[kStripsPerWarp - 1]);
+#endif
       else
 #pragma unroll
-        for (int r = 0; r < kStripsPerWarp; ++r) corr[r] = walk_list(ent, k0[r], ke[r], cvs);
+        for (int r = 0; r < kStripsPerWarp; ++r) corr[r] = walk_list_u(ent, k0[r], ke[r], cvs);
     } else {
 #pragma unroll
-      for (int r = 0; r < kStripsPerWarp; ++r) corr[r] = walk_list(m_ent + eb, k0[r], ke[r], cvs);
+      for (int r = 0; r < kStripsPerWarp; ++r) corr[r] = walk_list_u(m_ent + eb, k0[r], ke[r], cvs);
     }
 #pragma unroll
     for (int r = 0; r < kStripsPerWarp; ++r)  // both halves, commutative -> same bits
@@ -1094,9 +1158,9 @@ __global__ void __launch_bounds__(kThreads, GKB_L1T_MINB) k_pm_adj_l1(
     if (m_off) {
       const uint32_t e0 = offs[rl], e1 = offs[rl + 1];
       corr = ent_shift >= 0
-                 ? walk_list(reinterpret_cast<const uint16_t*>(stage + kL1tOffBytes) + ent_shift,
+                 ? walk_list_u(reinterpret_cast<const uint16_t*>(stage + kL1tOffBytes) + ent_shift,
                              e0, e1, cvs)
-                 : walk_list(m_ent + eb, e0, e1, cvs);
+                 : walk_list_u(m_ent + eb, e0, e1, cvs);
     }
     const double val = scale2(S[q], E - 62 - 2 * q);
     part[(int64_t)kc * rows_pad + (int64_t)bx * kL1tRows + rl] = val - rsum - corr;
@@ -1367,6 +1431,34 @@ __device__ __forceinline__ void walk_list2(const uint16_t* __restrict__ ent, uin
   cb = sb;
 }
 
+// walk_list2 in one predicated chunk loop (as walk_list_u; same bits)
+__device__ __forceinline__ void walk_list2_u(const uint16_t* __restrict__ ent, uint32_t k0,
+                                             uint32_t ke, const double* __restrict__ cva,
+                                             const double* __restrict__ cvb, double& ca,
+                                             double& cb) {
+  double sa = 0.0, sb = 0.0;
+  const uint32_t n = ke - k0;
+#pragma unroll 1
+  for (uint32_t i = 0; i < n; i += 4) {
+    double x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u < n) {
+        const int c = ent[k0 + i + u];
+        x[u] = cva[c];
+        y[u] = cvb[c];
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u < n) sa += x[u];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u < n) sb += y[u];
+  }
+  ca = sa;
+  cb = sb;
+}
+
 size_t pm2_smem_bytes(int kt_cta) {
   return 2 * (size_t)kt_cta * 64 * 16 + kOffBytes + 2 * kEntCap + 16 + 2 * (size_t)kt_cta * 128 * 8;
 }
@@ -1559,10 +1651,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_main2(
       const uint32_t e0 = offs[rl], e1 = offs[rl + 1], mid = e0 + (e1 - e0) / 2;
       const uint32_t k0 = (tid >> 1) ? mid : e0, ke = (tid >> 1) ? e1 : mid;
       if (ent_shift >= 0)
-        walk_list2(reinterpret_cast<const uint16_t*>(stage + kOffBytes) + ent_shift, k0, ke, cvs0,
-                   cvs1, c0, c1);
+        walk_list2_u(reinterpret_cast<const uint16_t*>(stage + kOffBytes) + ent_shift, k0, ke,
+                     cvs0, cvs1, c0, c1);
       else
-        walk_list2(m_ent + eb, k0, ke, cvs0, cvs1, c0, c1);
+        walk_list2_u(m_ent + eb, k0, ke, cvs0, cvs1, c0, c1);
       c0 += __shfl_xor_sync(0xffffffffu, c0, 2);
       c1 += __shfl_xor_sync(0xffffffffu, c1, 2);
     }
