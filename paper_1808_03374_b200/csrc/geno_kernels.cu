@@ -1240,6 +1240,28 @@ __device__ __forceinline__ uint4 miss_ind(const uint4 w) {
   return t;
 }
 
+// mma_tile of the missing indicators of w: the group-q register is
+// w & (w >> 1) & (0x01010101 << 2q) -- one shift per word and one LOP3 per
+// register (the same values as miss_ind(w) & (0x03030303 << 2q))
+__device__ __forceinline__ uint32_t and3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;  // one LOP3 (the compiler would share a & b and spend two per register)
+  asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ void mma_tile_ind(int (&acc)[4], const uint4 w, const uint4 b01,
+                                             const uint4 b23) {
+  const uint32_t m0 = 0x01010101u, m1 = m0 << 2, m2 = m0 << 4, m3 = m0 << 6;
+  const uint32_t sx = w.x >> 1, sy = w.y >> 1, sz = w.z >> 1, sw = w.w >> 1;
+  mma_u8s8(acc, and3(w.x, sx, m0), and3(w.y, sy, m0), and3(w.x, sx, m1), and3(w.y, sy, m1),
+           b01.x, b01.y);
+  mma_u8s8(acc, and3(w.x, sx, m2), and3(w.y, sy, m2), and3(w.x, sx, m3), and3(w.y, sy, m3),
+           b01.z, b01.w);
+  mma_u8s8(acc, and3(w.z, sz, m0), and3(w.w, sw, m0), and3(w.z, sz, m1), and3(w.w, sw, m1),
+           b23.x, b23.y);
+  mma_u8s8(acc, and3(w.z, sz, m2), and3(w.w, sw, m2), and3(w.z, sz, m3), and3(w.w, sw, m3),
+           b23.z, b23.w);
+}
+
 size_t pmi_smem_bytes(int kt_cta, int mode) {
   return (size_t)kt_cta * 64 * 16 * (mode ? 2 : 1);
 }
@@ -1297,7 +1319,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_ind(
       DST[r] = ld_stream(nxt[r]);                                          \
       nxt[r] += adv ? 32 : 0;                                              \
       mma_tile(acc[r], CUR[r], b01, b23);                                  \
-      mma_tile(accm[r], miss_ind(CUR[r]), c01, c23);                       \
+      mma_tile_ind(accm[r], CUR[r], c01, c23);                       \
     }                                                                      \
     bp += 64;                                                              \
     ++t;                                                                   \
@@ -1317,7 +1339,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pm_ind(
       }                                                                    \
       _Pragma("unroll") for (int r = 0; r < kStripsPerWarp; ++r) {         \
         mma_tile(acc[r], CUR[r], b01, b23);                                \
-        mma_tile(accm[r], miss_ind(CUR[r]), c01, c23);                     \
+        mma_tile_ind(accm[r], CUR[r], c01, c23);                     \
       }                                                                    \
     }
     static_assert(kStripsPerWarp == 2, "the unrolled loop prefetches strips 0 and 1");
