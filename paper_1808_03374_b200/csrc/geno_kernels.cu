@@ -338,12 +338,21 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
                                                    double* __restrict__ cm,
                                                    const double* __restrict__ div,
                                                    double* __restrict__ store,
-                                                   const int* __restrict__ gate) {
-  extern __shared__ uint4 dsm[];  // kt_cta * 64 uint4 (digits), then kt_cta * 128 doubles
+                                                   const int* __restrict__ gate,
+                                                   uint4* __restrict__ dig2 = nullptr,
+                                                   int* __restrict__ dexp2 = nullptr) {
+  // kt_cta * 64 uint4 (digits), then kt_cta * 128 doubles; with dig2 (MODE 1,
+  // dense-missing mode: the digits of cm as k_digitize<0> would make them from
+  // the stored cm, in the same launch) another kt_cta * 64 uint4 + kt_cta * 128 doubles
+  extern __shared__ uint4 dsm[];
   __shared__ double red[33];
   __shared__ int redi[33];
   double* vals = reinterpret_cast<double*>(dsm + kt_cta * 64);
   uint8_t* db = reinterpret_cast<uint8_t*>(dsm);
+  const bool two = MODE == 1 && dig2 != nullptr;
+  uint4* dsm2 = dsm + kt_cta * 64 + kt_cta * 64;  // after vals (kt_cta * 128 doubles)
+  double* cvals = reinterpret_cast<double*>(dsm2 + kt_cta * 64);
+  int emax2 = -1100;
   // trigger only after the wait: the main kernel's early reads of the lists and
   // layout then follow the completion of every kernel before this one
   pdl_wait();
@@ -372,14 +381,35 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
       } else {  // MODE 1 and 2: the adjoint's coefficients
         v = inv_s[c] * x;
         part += v * mu[c];
-        cm[c] = v * (3.0 - mean[c]);  // a missing entry holds the imputed mean (genio.cpp:144)
+        const double cmc = v * (3.0 - mean[c]);  // a missing entry holds the imputed mean (genio.cpp:144)
+        cm[c] = cmc;
+        if (two) {
+          cvals[t] = cmc;
+          emax2 = max(emax2, exp_of(cmc));
+        }
       }
+    } else if (two) {
+      cvals[t] = 0.0;
     }
     emax = max(emax, exp_of(v));
     vals[t] = v;
   }
   const int E = block_max_int(emax, redi);
   const double s = block_sum(part, red);
+  const int E2 = two ? block_max_int(emax2, redi) : 0;
+  if (two) {  // k_digitize<0>'s digits of cm (group-q prescale, swizzled slots)
+    uint8_t* db2 = reinterpret_cast<uint8_t*>(dsm2);
+    for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
+      const int wc = t >> 4, k = t & 15, q = k & 3, e = k >> 2;
+      long long M = __double2ll_rn(scale2(cvals[t], 62 - E2 - 2 * q));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int d = (int)(signed char)(M & 0xFF);
+        M = (M - d) >> 8;
+        db2[(wc * 8 + (i ^ (2 * (wc & 3)))) * 16 + 4 * q + e] = (uint8_t)d;
+      }
+    }
+  }
   for (int t = threadIdx.x; t < ncol; t += blockDim.x) {
     if (MODE == 2) {
       // K2 from layout 1 (k_pm_adj_l1): no column prescale (the 4^q scale sits
@@ -408,9 +438,14 @@ __global__ void __launch_bounds__(1024) k_digitize(const double* __restrict__ v_
   __syncthreads();
   uint4* out = dig + (int64_t)kc * kt_cta * 64;
   for (int t = threadIdx.x; t < kt_cta * 64; t += blockDim.x) out[t] = dsm[t];
+  if (two) {
+    uint4* out2 = dig2 + (int64_t)kc * kt_cta * 64;
+    for (int t = threadIdx.x; t < kt_cta * 64; t += blockDim.x) out2[t] = dsm2[t];
+  }
   if (threadIdx.x == 0) {
     dexp[kc] = E;
     dsum[kc] = s;
+    if (two) dexp2[kc] = E2;
   }
 }
 
@@ -1267,7 +1302,8 @@ size_t pmi_smem_bytes(int kt_cta, int mode) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 3) k_pm_ind(
+// CTAs per SM: K1 fits 64 registers (4), K2's second digit set does not (3)
+__global__ void __launch_bounds__(kThreads, MODE == 0 ? 4 : 3) k_pm_ind(
     const uint4* __restrict__ lay, int64_t KT, int kt_cta, const uint4* __restrict__ dig,
     const int* __restrict__ dexp, const double* __restrict__ dsum,
     const uint4* __restrict__ dig2, const int* __restrict__ dexp2,
@@ -2276,15 +2312,18 @@ void k1_digitize(const GenoView& g, const double* x, cudaStream_t s, const DivIn
   allow_smem(k_digitize<0>, pl.dig_smem);
   launch_pdl(k_digitize<0>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, true, x,
              (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, g.n, pl.kt_cta,
-             g.s1.dig, g.s1.dexp, g.s1.dsum, (double*)nullptr, di.div, di.store, di.gate);
+             g.s1.dig, g.s1.dexp, g.s1.dsum, (double*)nullptr, di.div, di.store, di.gate, (uint4*)nullptr, (int*)nullptr);
 }
 
 void k2_digitize(const GenoView& g, const double* y, cudaStream_t s, const DivIn& di) {
   const PMPlan& pl = g.pl2;
-  allow_smem(k_digitize<1>, pl.dig_smem);
-  launch_pdl(k_digitize<1>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, true, y,
+  // dense-missing mode: the cm digits (k_pm_ind's second digit set) in the same launch
+  const size_t smem = g.ind ? 2 * pl.dig_smem : pl.dig_smem;
+  allow_smem(k_digitize<1>, smem);
+  launch_pdl(k_digitize<1>, dim3((unsigned)pl.nkc), dim3(1024), smem, s, true, y,
              (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc,
-             pl.kt_cta, g.s2.dig, g.s2.dexp, g.s2.dsum, g.s2.cm, di.div, di.store, di.gate);
+             pl.kt_cta, g.s2.dig, g.s2.dexp, g.s2.dsum, g.s2.cm, di.div, di.store, di.gate,
+             g.ind ? g.s2m.dig : (uint4*)nullptr, g.ind ? g.s2m.dexp : (int*)nullptr);
 }
 
 namespace {
@@ -2319,15 +2358,6 @@ void launch_ind(const GenoView& g, const PMPlan& pl, const uint4* lay, const PMS
              (const double*)sc.dsum, (const uint4*)g.s2m.dig, (const int*)g.s2m.dexp,
              (const double*)g.mu, (const double*)g.mean, pl.rows_pad, sc.part);
 }
-// digits of cm_j = c_j (3 - m_j) (written by k_digitize<1>) for the K2 indicator MMA
-void digitize_cm(const GenoView& g, cudaStream_t s, bool pdl) {
-  const PMPlan& pl = g.pl2;
-  allow_smem(k_digitize<0>, pl.dig_smem);
-  launch_pdl(k_digitize<0>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, pdl,
-             (const double*)g.s2.cm, (const double*)nullptr, (const double*)nullptr,
-             (const double*)nullptr, g.p_loc, pl.kt_cta, g.s2m.dig, g.s2m.dexp, g.s2m.dsum,
-             (double*)nullptr, (const double*)nullptr, (double*)nullptr, (const int*)nullptr);
-}
 }  // namespace
 
 namespace {
@@ -2337,7 +2367,7 @@ void digitize_l1t(const GenoView& g, const double* y, cudaStream_t s, const DivI
   allow_smem(k_digitize<2>, smem);
   launch_pdl(k_digitize<2>, dim3((unsigned)g.l1t_nkc), dim3(1024), smem, s, true, y,
              (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc, 14,
-             g.s2.dig, g.s2.dexp, g.s2.dsum, g.s2.cm, di.div, di.store, di.gate);
+             g.s2.dig, g.s2.dexp, g.s2.dsum, g.s2.cm, di.div, di.store, di.gate, (uint4*)nullptr, (int*)nullptr);
 }
 void launch_adj_l1(const GenoView& g, cudaStream_t s, bool pdl) {
   const size_t smem = l1t_smem_bytes();
@@ -2408,9 +2438,8 @@ void k2_adjoint(const GenoView& g, const double* y, double* z, cudaStream_t s, c
     launch_k2_reduce((const double*)g.s2.part, (int)g.l1t_nkc, g.l1t_rows_pad, g.n, z, s);
     return;
   }
-  k2_digitize(g, y, s, di);
+  k2_digitize(g, y, s, di);  // (+ the cm digits in dense-missing mode)
   if (g.ind) {
-    digitize_cm(g, s, true);
     launch_ind<1>(g, g.pl2, g.lt2, g.s2, s, true);
   } else {
     launch_main<1>(g, g.pl2, g.lt2, g.s2, g.s2.cm, g.m2, s, true);
@@ -2489,12 +2518,12 @@ void digitize_into(const GenoView& g, const PMPlan& pl, const double* v, const P
     launch_pdl(k_digitize<0>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, pdl, v,
                (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, g.n,
                pl.kt_cta, sc.dig, sc.dexp, sc.dsum, (double*)nullptr, (const double*)nullptr,
-               (double*)nullptr, (const int*)nullptr);
+               (double*)nullptr, (const int*)nullptr, (uint4*)nullptr, (int*)nullptr);
   else
     launch_pdl(k_digitize<1>, dim3((unsigned)pl.nkc), dim3(1024), pl.dig_smem, s, pdl, v,
                (const double*)g.inv_s, (const double*)g.mu, (const double*)g.mean, g.p_loc,
                pl.kt_cta, sc.dig, sc.dexp, sc.dsum, sc.cm, (const double*)nullptr, (double*)nullptr,
-               (const int*)nullptr);
+               (const int*)nullptr, (uint4*)nullptr, (int*)nullptr);
 }
 
 template <int MODE>
