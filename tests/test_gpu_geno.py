@@ -30,7 +30,9 @@ def random_payload(p, n, seed, missing=0.02, special_rows=True):
 SHAPES = [(1, 1), (4, 16), (5, 17), (7, 3), (33, 100), (130, 257), (257, 1000), (1031, 2049),
           (64, 4099),
           # column-range boundaries (14 tiles = 1792 columns; the unrolled full-range loop)
-          (5, 1792), (5, 1793), (1792, 3), (1793, 1791)]
+          (5, 1792), (5, 1793), (1792, 3), (1793, 1791),
+          # >= 65,536 samples: the adjoint's thread-per-sample finish (k2_reduce_seq)
+          (37, 70001)]
 
 
 @pytest.mark.parametrize("p,n", SHAPES)
@@ -72,6 +74,24 @@ def test_apply_and_adjoint_vs_oracle(gkb, orc, p, n, missing):
             1e-13 * scale * np.sqrt(n) * (np.max(inv_s) * 2.0 + 1.0)
         assert np.max(np.abs(za - zo)) <= 1e-12 * max(1e-300, np.max(np.abs(zo))) + \
             1e-13 * scale * np.sqrt(p) * (np.max(inv_s) * 2.0 + 1.0)
+
+
+@pytest.mark.parametrize("missing", [0.01, 0.013])
+def test_tall_sample_count_lists_vs_oracle(gkb, orc, missing):
+    """n >= 65,536 with per-CTA missing lists (list mode): K2's partials are
+    summed by the thread-per-sample finish, K1's and K2's list walks take the
+    uniform chunk loop; both against the oracle."""
+    p, n = 41, 70003
+    payload, _ = random_payload(p, n, seed=91, missing=missing)
+    op = gkb.GenotypeOperator.from_bed_payload(payload, p, n, scheme=gkb.ScalingScheme.kHwe)
+    mu, inv_s = op.scaling()
+    ref = orc.GenoOracle(payload, p, n, mu, inv_s)
+    rng = np.random.default_rng(5)
+    x, y = rng.standard_normal(n), rng.standard_normal(p)
+    ya, yo = op.apply(x), ref.apply(x)
+    za, zo = op.apply_adjoint(y), ref.apply_adjoint(y)
+    assert np.max(np.abs(ya - yo)) <= 1e-12 * np.max(np.abs(yo))
+    assert np.max(np.abs(za - zo)) <= 1e-12 * np.max(np.abs(zo))
 
 
 def test_edge_rows_are_zero(gkb, orc):
