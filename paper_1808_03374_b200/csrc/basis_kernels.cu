@@ -585,7 +585,10 @@ void gemv_t(const double* Q, int64_t ld, int64_t len, int64_t ncols, const doubl
     }
     return;
   }
-  const int64_t rpb = rpb_target(len, "GKB_GT_BLOCKS", 296);
+  // row chunks: ~74 (below 300k rows) / 148 (basis_bench sweep: 100k x 50
+  // 14.4 -> 10.6 us, 500k x 50 46.7 -> 43.3 us against 296); at most 18,944
+  // rows stay 256-row chunks (the fused right tail reduces like these CTAs)
+  const int64_t rpb = rpb_target(len, "GKB_GT_BLOCKS", len < 300000 ? 74 : 148);
   const int64_t nb = std::max<int64_t>(1, (len + rpb - 1) / rpb);
   const dim3 grid((unsigned)nb, (unsigned)((K + kCB - 1) / kCB));
   launch_pdl(K <= 4 ? k_gemv_t<4> : k_gemv_t<2>, grid, dim3(kT), 0, s, true, Q, ld, len, ncols, v,
@@ -596,7 +599,8 @@ void gemv_n(const double* Q, int64_t ld, int64_t len, int64_t ncols, const doubl
             double beta, double sign, bool norms, RedScratch& rs, double* out, cudaStream_t s,
             const int* gate, const ctl::Post* post) {
   if (len == 0 && !norms) return;
-  const int64_t rpb = rpb_target(len, "GKB_GN_BLOCKS", 296);
+  // ~148 row chunks below 300k rows (100k x 50: 9.9 -> 8.5 us), 296 above
+  const int64_t rpb = rpb_target(len, "GKB_GN_BLOCKS", len < 300000 ? 148 : 296);
   const int64_t nb = std::max<int64_t>(1, (len + rpb - 1) / rpb);
   launch_pdl(k_gemv_n, dim3((unsigned)nb), dim3(kT), 0, s, true, Q, ld, len, ncols, c, v, beta,
              sign, norms ? 1 : 0, rpb, rs.partial, out, rs.ticket, gate, post_of(post));
