@@ -526,25 +526,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-// sum_{k in [k0, ke)} cv[ent[k]] in order, 4 independent loads in flight
-__device__ __forceinline__ double walk_list(const uint16_t* __restrict__ ent, uint32_t k0,
-                                            uint32_t ke, const double* __restrict__ cv) {
-  double corr = 0.0;
-  uint32_t k = k0;
-#pragma unroll 1
-  for (; k + 4 <= ke; k += 4) {
-    const int c0 = ent[k], c1 = ent[k + 1], c2 = ent[k + 2], c3 = ent[k + 3];
-    corr += cv[c0];
-    corr += cv[c1];
-    corr += cv[c2];
-    corr += cv[c3];
-  }
-#pragma unroll 1
-  for (; k < ke; ++k) corr += cv[ent[k]];
-  return corr;
-}
-
-// walk_list in one loop of chunks of four with the chunk's loads and adds
+// sum_{k in [k0, ke)} cv[ent[k]] in order, in one loop of chunks of four with the chunk's loads and adds
 // predicated on the run's end (each entry still added in order: same bits),
 // so a warp's lanes do not diverge between a chunk loop and a tail loop
 __device__ __forceinline__ double walk_list_u(const uint16_t* __restrict__ ent, uint32_t k0,
@@ -564,63 +546,11 @@ __device__ __forceinline__ double walk_list_u(const uint16_t* __restrict__ ent, 
   return corr;
 }
 
-// walk_list over two runs at once: each sum in its own sequential order (the
-// bits of two walk_list calls), the two runs' load latencies overlapped
-__device__ __forceinline__ void walk_list_pair(const uint16_t* __restrict__ ent, uint32_t ka,
-                                               uint32_t kea, uint32_t kb, uint32_t keb,
-                                               const double* __restrict__ cv, double& ca,
-                                               double& cb) {
-  double sa = 0.0, sb = 0.0;
-#pragma unroll 1
-  for (; ka + 4 <= kea && kb + 4 <= keb; ka += 4, kb += 4) {
-    const int a0 = ent[ka], a1 = ent[ka + 1], a2 = ent[ka + 2], a3 = ent[ka + 3];
-    const int b0 = ent[kb], b1 = ent[kb + 1], b2 = ent[kb + 2], b3 = ent[kb + 3];
-    const double x0 = cv[a0], x1 = cv[a1], x2 = cv[a2], x3 = cv[a3];
-    const double y0 = cv[b0], y1 = cv[b1], y2 = cv[b2], y3 = cv[b3];
-    sa += x0;
-    sb += y0;
-    sa += x1;
-    sb += y1;
-    sa += x2;
-    sb += y2;
-    sa += x3;
-    sb += y3;
-  }
-  // the rest of each run as walk_list continues it
-#pragma unroll 1
-  for (; ka + 4 <= kea; ka += 4) {
-    const int c0 = ent[ka], c1 = ent[ka + 1], c2 = ent[ka + 2], c3 = ent[ka + 3];
-    sa += cv[c0];
-    sa += cv[c1];
-    sa += cv[c2];
-    sa += cv[c3];
-  }
-#pragma unroll 1
-  for (; kb + 4 <= keb; kb += 4) {
-    const int c0 = ent[kb], c1 = ent[kb + 1], c2 = ent[kb + 2], c3 = ent[kb + 3];
-    sb += cv[c0];
-    sb += cv[c1];
-    sb += cv[c2];
-    sb += cv[c3];
-  }
-  // tails (< 4 each) interleaved
-#pragma unroll 1
-  for (; ka < kea || kb < keb; ++ka, ++kb) {
-    if (ka < kea) sa += cv[ent[ka]];
-    if (kb < keb) sb += cv[ent[kb]];
-  }
-  ca = sa;
-  cb = sb;
-}
-
-// walk_list_pair as ONE loop over both runs in chunks of four: past a run's
+// two runs (a warp's two strips) in ONE loop of chunks of four: past a run's
 // end a lane reads the zero slot cv[-1] = +0.0 instead. A sum that starts at
 // +0.0 never becomes -0.0, so adding +0.0 leaves it unchanged and each run's
-// sum keeps walk_list's bits -- without the remainder and tail loops, between
+// sum is the in-order sum -- without the remainder and tail loops, between
 // which a warp's lanes diverged (the epilogue's largest instruction cost).
-#ifndef GKB_WALK_UNIFORM
-#define GKB_WALK_UNIFORM 1
-#endif
 __device__ __forceinline__ void walk_list_pair_u(const uint16_t* __restrict__ ent, uint32_t ka,
                                                  uint32_t kea, uint32_t kb, uint32_t keb,
                                                  const double* __restrict__ cv, double& ca,
@@ -907,13 +837,8 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
     if (ent_shift >= 0) {  // shared-memory runs (pointer derived from the smem array: LDS)
       const uint16_t* ent = reinterpret_cast<const uint16_t*>(stage + kOffBytes) + ent_shift;
       if (kStripsPerWarp == 2)  // both strips' runs walked together (latencies overlap)
-#if GKB_WALK_UNIFORM
         walk_list_pair_u(ent, k0[0], ke[0], k0[kStripsPerWarp - 1], ke[kStripsPerWarp - 1], cvs,
                          corr[0], corr[kStripsPerWarp - 1]);
-#else
-        walk_list_pair(ent, k0[0], ke[0], k0[kStripsPerWarp - 1], ke[kStripsPerWarp - 1], cvs,
-                       corr[0], corr[kStripsPerWarp - 1]);
-#endif
       else
 #pragma unroll
         for (int r = 0; r < kStripsPerWarp; ++r) corr[r] = walk_list_u(ent, k0[r], ke[r], cvs);
@@ -1458,35 +1383,6 @@ __device__ __forceinline__ void mma_tile2(int (&a0)[4], int (&a1)[4], const uint
   p0 = w.z & m2; p1 = w.w & m2; p2 = w.z & m3; p3 = w.w & m3;
   mma_u8s8(a0, p0, p1, p2, p3, b23a.z, b23a.w);
   mma_u8s8(a1, p0, p1, p2, p3, b23b.z, b23b.w);
-}
-
-// walk_list for two coefficient vectors (same entries, same order per vector)
-__device__ __forceinline__ void walk_list2(const uint16_t* __restrict__ ent, uint32_t k0,
-                                           uint32_t ke, const double* __restrict__ cva,
-                                           const double* __restrict__ cvb, double& ca,
-                                           double& cb) {
-  double sa = 0.0, sb = 0.0;
-  uint32_t k = k0;
-#pragma unroll 1
-  for (; k + 4 <= ke; k += 4) {
-    const int c0 = ent[k], c1 = ent[k + 1], c2 = ent[k + 2], c3 = ent[k + 3];
-    sa += cva[c0];
-    sa += cva[c1];
-    sa += cva[c2];
-    sa += cva[c3];
-    sb += cvb[c0];
-    sb += cvb[c1];
-    sb += cvb[c2];
-    sb += cvb[c3];
-  }
-#pragma unroll 1
-  for (; k < ke; ++k) {
-    const int c = ent[k];
-    sa += cva[c];
-    sb += cvb[c];
-  }
-  ca = sa;
-  cb = sb;
 }
 
 // walk_list2 in one predicated chunk loop (as walk_list_u; same bits)
