@@ -595,7 +595,7 @@ size_t pm_smem_bytes(int kt_cta) {
 // exact partial (MODE 0: K1, MODE 1: K2 -- see the header) to part[kc][row].
 // The CTA's missing list (offsets + entries) and the range's correction
 // coefficients cval (K1: x, K2: c_j (3 - mu_j)) are staged into shared memory
-// by cp.async in the prologue, so the epilogue walk never touches global
+// by bulk copies in the prologue (below), so the epilogue walk never touches global
 // memory (random 8-byte gathers from L2 cost ~30% of the kernel otherwise).
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, kMinCtas) k_pm_main(
