@@ -5,7 +5,12 @@ bytes and scaling, with the protocol of tests/test_gpu_parity_full.py
 (per-sigma 1e-9, principal angles < 1e-6, restarts +-1). Too slow for the
 test suite; run on the GPU box, result committed under profiles/.
 
-usage: full_parity.py CONFIG OUT.json
+usage: full_parity.py CONFIG OUT.json [MAX_MVPS]
+
+MAX_MVPS caps both solves at the same mvp budget (GklOptions::max_mvps): the
+GPU and the oracle then run the same truncated trajectory, which is how config
+4's full size fits the GPU box's one-hour call limit (the uncapped oracle solve
+takes ~2 h on 16 cores).
 """
 import json
 import os
@@ -26,6 +31,9 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 out = sys.argv[2] if len(sys.argv) > 2 else f"gpurun_out/c{cfg}_parity.json"
 spec = synth.config_spec(cfg)
 opts = synth.config_options(cfg)
+max_mvps = int(sys.argv[3]) if len(sys.argv) > 3 else None
+if max_mvps:
+    opts.max_mvps = max_mvps
 op = gkb.GenotypeOperator.from_synth(spec, scheme=gkb.ScalingScheme.kHwe)
 mu, inv_s = op.scaling()
 t0 = time.perf_counter()
@@ -44,6 +52,8 @@ res = dict(
     config=synth.CONFIG_TEXT[cfg] if hasattr(synth, "CONFIG_TEXT") else cfg,
     options=synth.OPTIONS_TEXT[cfg] if hasattr(synth, "OPTIONS_TEXT") else "",
     k=int(opts.k),
+    max_mvps=max_mvps,
+    sigma_rel_err_each=[float(abs(a - b) / abs(b)) for a, b in zip(g.singvals, o.singvals)],
     sigma_gpu=[float(x) for x in g.singvals],
     sigma_oracle=[float(x) for x in o.singvals],
     sigma_rel_err_max=float(sigma_rel_err(g.singvals, o.singvals)),
