@@ -1124,8 +1124,9 @@ static void gather_left(Context* ctx, DevOp* op, const std::vector<double*>& src
   if (ctx->spmd_mode && ctx->nshards_total > 1) {
     ctx->set_device(0);
     Shard& s = ctx->shards[0];
-    double* full = nullptr;
-    GKB_CUDA(cudaMalloc(&full, sizeof(double) * (size_t)(m * ncols)));
+    DevScratch fhold;  // RAII: freed if the allreduce or a copy throws
+    GKB_CUDA(cudaMalloc(&fhold.p, sizeof(double) * (size_t)(m * ncols)));
+    double* full = fhold.as<double>();
     GKB_CUDA(cudaMemsetAsync(full, 0, sizeof(double) * (size_t)(m * ncols), s.stream));
     const int64_t r = op->rows(0);
     if (r > 0)
@@ -1136,7 +1137,6 @@ static void gather_left(Context* ctx, DevOp* op, const std::vector<double*>& src
     GKB_CUDA(cudaMemcpyAsync(host, full, sizeof(double) * (size_t)(m * ncols),
                              cudaMemcpyDeviceToHost, s.stream));
     GKB_CUDA(cudaStreamSynchronize(s.stream));
-    cudaFree(full);
     return;
   }
   if (L == 1) {  // rows(0) == m: one contiguous block

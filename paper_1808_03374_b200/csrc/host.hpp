@@ -35,6 +35,17 @@ struct DevScratch {
   template <class T>
   T* as() const { return static_cast<T*>(p); }
 };
+struct PinnedScratch {  // cudaMallocHost'd staging buffer
+  void* p = nullptr;
+  PinnedScratch() = default;
+  PinnedScratch(const PinnedScratch&) = delete;
+  PinnedScratch& operator=(const PinnedScratch&) = delete;
+  ~PinnedScratch() {
+    if (p) cudaFreeHost(p);
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
 struct EventHolder {
   cudaEvent_t e = nullptr;
   EventHolder() = default;

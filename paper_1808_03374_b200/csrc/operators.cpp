@@ -554,10 +554,12 @@ void GenoOp::build_from_payload(const uint8_t* payload, int64_t p, int64_t nn) {
     Shard& sh = ctx->shards[i];
     ctx->set_device(i);
     const int64_t br = staging_rows(stride, 64ll << 20, pr);
-    uint8_t* dstage = nullptr;
-    uint8_t* hstage = nullptr;
-    GKB_CUDA(cudaMalloc(&dstage, (size_t)(br * stride)));
-    GKB_CUDA(cudaMallocHost(&hstage, (size_t)(br * stride)));
+    DevScratch dhold;  // RAII: a throw below must not leak the staging buffers
+    PinnedScratch hhold;
+    GKB_CUDA(cudaMalloc(&dhold.p, (size_t)(br * stride)));
+    GKB_CUDA(cudaMallocHost(&hhold.p, (size_t)(br * stride)));
+    uint8_t* dstage = dhold.as<uint8_t>();
+    uint8_t* hstage = hhold.as<uint8_t>();
     for (int64_t b0 = 0; b0 < pr; b0 += br) {
       const int64_t rb = std::min(br, pr - b0);
       GKB_CUDA(cudaStreamSynchronize(sh.stream));  // hstage free again
@@ -570,8 +572,6 @@ void GenoOp::build_from_payload(const uint8_t* payload, int64_t p, int64_t nn) {
       GKB_LAUNCH_CHECK();
     }
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
-    cudaFree(dstage);
-    cudaFreeHost(hstage);
   }
   finish_build();
 }
@@ -753,34 +753,39 @@ void GenoOp::build_from_synth(const dev::SynthDev& sp_in, const gkb_synth_spec* 
     Shard& sh = ctx->shards[i];
     ctx->set_device(i);
     // device copies of the spec arrays
+    DevScratch hfreq, hpop, hadmix, hcopy, dhold;  // RAII: freed on a throw too
     double* dfreq = nullptr;
     int32_t* dpop = nullptr;
     double* dadmix = nullptr;
     int32_t* dcopy = nullptr;
-    GKB_CUDA(cudaMalloc(&dfreq, sizeof(double) * (size_t)(spec->npop * p)));
+    GKB_CUDA(cudaMalloc(&hfreq.p, sizeof(double) * (size_t)(spec->npop * p)));
+    dfreq = hfreq.as<double>();
     // stream-ordered copies: a synchronous cudaMemcpy from pageable memory may
     // return before its DMA lands, and the shard stream does not wait for it
     GKB_CUDA(cudaMemcpyAsync(dfreq, spec->freq, sizeof(double) * (size_t)(spec->npop * p),
                              cudaMemcpyHostToDevice, sh.stream));
     if (spec->pop) {
-      GKB_CUDA(cudaMalloc(&dpop, sizeof(int32_t) * (size_t)nn));
+      GKB_CUDA(cudaMalloc(&hpop.p, sizeof(int32_t) * (size_t)nn));
+      dpop = hpop.as<int32_t>();
       GKB_CUDA(cudaMemcpyAsync(dpop, spec->pop, sizeof(int32_t) * (size_t)nn,
                                cudaMemcpyHostToDevice, sh.stream));
     } else {
-      GKB_CUDA(cudaMalloc(&dadmix, sizeof(double) * (size_t)(nn * spec->npop)));
+      GKB_CUDA(cudaMalloc(&hadmix.p, sizeof(double) * (size_t)(nn * spec->npop)));
+      dadmix = hadmix.as<double>();
       GKB_CUDA(cudaMemcpyAsync(dadmix, spec->admix, sizeof(double) * (size_t)(nn * spec->npop),
                                cudaMemcpyHostToDevice, sh.stream));
     }
     if (spec->copy_from) {
-      GKB_CUDA(cudaMalloc(&dcopy, sizeof(int32_t) * (size_t)nn));
+      GKB_CUDA(cudaMalloc(&hcopy.p, sizeof(int32_t) * (size_t)nn));
+      dcopy = hcopy.as<int32_t>();
       GKB_CUDA(cudaMemcpyAsync(dcopy, spec->copy_from, sizeof(int32_t) * (size_t)nn,
                                cudaMemcpyHostToDevice, sh.stream));
     }
     dev::SynthDev sd{p, nn, spec->seed, spec->npop, dfreq, dpop, dadmix, spec->missing_rate, dcopy,
                      spec->copy_prob};
     const int64_t br = staging_rows(stride, 256ll << 20, pr);
-    uint8_t* dstage = nullptr;
-    GKB_CUDA(cudaMalloc(&dstage, (size_t)(br * stride)));
+    GKB_CUDA(cudaMalloc(&dhold.p, (size_t)(br * stride)));
+    uint8_t* dstage = dhold.as<uint8_t>();
     for (int64_t b0 = 0; b0 < pr; b0 += br) {
       const int64_t rb = std::min(br, pr - b0);
       dev::synth_bed(sd, r0 + b0, rb, dstage, sh.stream);
@@ -791,11 +796,6 @@ void GenoOp::build_from_synth(const dev::SynthDev& sp_in, const gkb_synth_spec* 
       GKB_LAUNCH_CHECK();
     }
     GKB_CUDA(cudaStreamSynchronize(sh.stream));
-    cudaFree(dstage);
-    cudaFree(dfreq);
-    if (dpop) cudaFree(dpop);
-    if (dadmix) cudaFree(dadmix);
-    if (dcopy) cudaFree(dcopy);
   }
   finish_build();
 }
