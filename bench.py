@@ -47,8 +47,7 @@ import numpy as np  # noqa: E402
 DEFAULT_CFG = 4
 METRIC = "packed genotype matvec HBM GB/s (A·v+Aᵀ·u); seconds to top-k singular triplets"
 # ncu --set full captures of the main kernels per config (tools/ncu_summary.py)
-NCU_CAPTURE = {4: "r2c_ncu_full_config4.json", 3: "r2_ncu_full_config3.json",
-               2: "r1j_ncu_full_config2.json"}
+NCU_CAPTURE = {4: "r2d_ncu_full_config4.json", 2: "r1j_ncu_full_config2.json"}
 
 
 def load_workloads():
