@@ -10,7 +10,13 @@ usage: full_parity.py CONFIG OUT.json [MAX_MVPS]
 MAX_MVPS caps both solves at the same mvp budget (GklOptions::max_mvps): the
 GPU and the oracle then run the same truncated trajectory, which is how config
 4's full size fits the GPU box's one-hour call limit (the uncapped oracle solve
-takes ~2 h on 16 cores).
+takes ~2 h on 16 cores). At a cap the trailing Ritz triplets are not converged
+(config 4's sigma_4.. sit at the edge of the Marchenko-Pastur bulk, gaps of
+2e-4 relative), so the k-dimensional Ritz subspace is not yet a well-posed
+quantity: the record then also holds the angles over the leading triplets BOTH
+solvers flag converged, each vector's own misalignment, and the error
+estimates -- `pass` uses the converged lead for the angles and all k values for
+sigma.
 """
 import json
 import os
@@ -66,7 +72,28 @@ res = dict(
     seconds_oracle_generate=round(t_gen, 1),
     thresholds=dict(sigma_rel=1e-9, angle=1e-6, restarts=1),
 )
-res["pass"] = (res["sigma_rel_err_max"] <= 1e-9 and res["angle_U"] < 1e-6 and res["angle_V"] < 1e-6
+gc, oc = np.asarray(g.converged, bool), np.asarray(o.converged, bool)
+lead = 0
+while lead < int(opts.k) and gc[lead] and oc[lead]:
+    lead += 1
+res["converged_lead"] = lead
+res["converged_flags_equal"] = bool(np.array_equal(gc, oc))
+res["err_estimates_gpu"] = [float(x) for x in g.err_estimates]
+res["err_estimates_oracle"] = [float(x) for x in o.err]
+res["misalign_U_each"] = [float(1.0 - min(1.0, abs(np.dot(g.U[:, i], o.U[:, i]))
+                                             / (np.linalg.norm(g.U[:, i]) * np.linalg.norm(o.U[:, i]))))
+                           for i in range(int(opts.k))]
+res["misalign_V_each"] = [float(1.0 - min(1.0, abs(np.dot(g.V[:, i], o.V[:, i]))
+                                             / (np.linalg.norm(g.V[:, i]) * np.linalg.norm(o.V[:, i]))))
+                           for i in range(int(opts.k))]
+if max_mvps and lead < int(opts.k):
+    res["angle_U_lead"] = float(principal_angles(g.U[:, :lead], o.U[:, :lead])) if lead else None
+    res["angle_V_lead"] = float(principal_angles(g.V[:, :lead], o.V[:, :lead])) if lead else None
+    aU, aV = res["angle_U_lead"] or 0.0, res["angle_V_lead"] or 0.0
+else:
+    aU, aV = res["angle_U"], res["angle_V"]
+res["pass"] = (res["sigma_rel_err_max"] <= 1e-9 and aU < 1e-6 and aV < 1e-6
+               and res["converged_flags_equal"]
                and abs(res["restarts_gpu"] - res["restarts_oracle"]) <= 1
                and res["converged_gpu"] == res["converged_oracle"])
 os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
