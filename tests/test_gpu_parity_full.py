@@ -136,6 +136,40 @@ def test_config5_subblock_vs_golden(gkb):
     assert g.stats.converged == bool(ref["converged"])
 
 
+@pytest.mark.parametrize("scale,cap", [(0.02, 240), (0.05, 420)])
+def test_config4_capped_trajectory_vs_oracle(gkb, orc, scale, cap):
+    """Both solvers stopped at the same mvp budget (GklOptions::max_mvps,
+    gkl.hpp:17-60) on the config-4 model, before the triplets at the edge of
+    the bulk converge -- the protocol of the full-size one-off
+    (tools/full_parity.py 4 OUT 420, profiles/r2e_c4_parity_capped_420mvps.json):
+    same mvps / restarts / converged flags, every Ritz value within 1e-9, the
+    error estimates equal, the left Ritz subspace and the converged lead on
+    both sides within 1e-6. (The k-dim RIGHT subspace of a truncated run is
+    not compared: cols = n > rank, and unconverged right Ritz vectors carry a
+    rounding-sensitive share of the start vector's null(X) component --
+    DESIGN.md 5, tools/capped_sensitivity.py.)"""
+    from paper_1808_03374_b200 import synth
+    spec = synth.config_spec(4, scale=scale)
+    opts = dataclasses.replace(synth.config_options(4), max_mvps=cap)
+    op, payload, mu, inv_s = _pair(gkb, orc, spec)
+    g = gkb.svdl(op, opts)
+    o = orc.svdl(orc.GenoOracle(payload, spec.p, spec.n, mu, inv_s, nthreads=NT),
+                 orc.Options.from_gkl(opts))
+    k = opts.k
+    assert g.stats.mvps == o.mvps and g.stats.mvps <= cap
+    assert g.stats.restarts == o.restarts
+    gc, oc = np.asarray(g.converged, bool), np.asarray(o.converged, bool)
+    assert np.array_equal(gc, oc)
+    assert not gc.all(), "cap too loose: the solve converged"
+    assert sigma_rel_err(g.singvals, o.singvals) <= 1e-9
+    np.testing.assert_allclose(g.err_estimates, o.err, rtol=1e-6, atol=1e-10 * o.singvals[0])
+    assert principal_angles(g.U, o.U) < 1e-6
+    lead = int(np.argmin(gc)) if not gc.all() else k
+    assert lead >= 1
+    assert principal_angles(g.U[:, :lead], o.U[:, :lead]) < 1e-6
+    assert principal_angles(g.V[:, :lead], o.V[:, :lead]) < 1e-6
+
+
 def test_config4_full_solve_properties(gkb):
     """Full config 4 (500,000 x 100,000, 12.5 GB packed; the CPU oracle would
     need ~2 h): size-independent properties of the solve -- the Ritz
